@@ -1,0 +1,220 @@
+/*
+ * tensile_b200.h -- C-ABI of the B200-native TENSILE scheduling-plan generator.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   memsched::build_plan            (/root/reference/proj/include/memsched/orchestrator.hpp:26-28,
+ *                                    src/orchestrator.cpp:8-70)
+ *   memsched::analyze_job           (peak.hpp:77-78, src/peak.cpp:246-250)
+ *   memsched::save_plans            (plan.hpp:57, src/plan.cpp:30-65)
+ *   memsched::PeakReport::to_json   (peak.hpp:55, src/peak.cpp:258-272)
+ * Everything is plain C: pointers, sizes, int status codes. Inputs are
+ * caller-owned and copied at call time; results are library-owned and freed by
+ * tsl_result_destroy. Errors return a nonzero status and leave a message in
+ * tsl_last_error() (thread-local), mirroring the reference's ValidationError
+ * texts where the reference throws.
+ *
+ * A graph is passed exactly as the reference's ComputeGraph holds it
+ * (graph.hpp:14-54): tensors (id, size, kind) and operators (id, kind, inputs,
+ * outputs, phase) with the per-op latency table (the reference's
+ * std::map<OpId, Tick>, orchestrator.hpp:26-28) flattened to one entry per op.
+ */
+#ifndef TENSILE_B200_H
+#define TENSILE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define TSL_OK 0
+#define TSL_ERR_VALIDATION 1 /* reference would throw memsched::ValidationError */
+#define TSL_ERR_CUDA 2       /* CUDA runtime / launch failure                    */
+#define TSL_ERR_INTERNAL 3   /* invariant broken inside the library              */
+#define TSL_ERR_ARGUMENT 4   /* NULL pointer / bad size at the C boundary        */
+#define TSL_ERR_CAPACITY 5   /* input exceeds a compiled device capacity         */
+
+/* TensorKind (types.hpp:21) and OpPhase (types.hpp:22), same order. */
+enum tsl_tensor_kind {
+  TSL_KIND_INPUT = 0,
+  TSL_KIND_INTERIM = 1,
+  TSL_KIND_PARAMETER = 2,
+  TSL_KIND_UPDATED_PARAMETER = 3,
+  TSL_KIND_OUTPUT = 4
+};
+enum tsl_op_phase { TSL_PHASE_FORWARD_BACKWARD = 0, TSL_PHASE_OPTIMIZE = 1 };
+
+/* An op with no latency entry (generate_access_sequence throws
+ * "missing latency entry for op X", access.cpp:35-36). */
+#define TSL_LATENCY_MISSING INT64_MIN
+
+/* PlannerConfig (config.hpp:9-18). max_swap_ratios lives in tsl_job_desc. */
+typedef struct tsl_config {
+  int64_t pcie_bandwidth;      /* bytes per tick, > 0          */
+  int64_t transfer_setup;      /* ticks, >= 0                  */
+  int64_t memory_budget;       /* bytes, >= 0                  */
+  double ewma_alpha;           /* [0,1], default 0.3           */
+  double replan_threshold;     /* > 0, default 0.2             */
+  double stall_epsilon;        /* (0,1), default 0.0005        */
+  int32_t stall_min_iters;     /* default 100                  */
+  double cold_start_gpu_usage; /* default 0.5                  */
+} tsl_config;
+
+/* Fills the reference defaults (config.hpp:10-18). */
+void tsl_config_default(tsl_config* cfg);
+
+/* One job: ComputeGraph + latency table (+ its max_swap_ratios entry). */
+typedef struct tsl_job_desc {
+  const char* job_id;
+  int32_t n_tensors;
+  const char* const* tensor_ids; /* [n_tensors]                      */
+  const int64_t* tensor_sizes;   /* [n_tensors], > 0                 */
+  const int8_t* tensor_kinds;    /* [n_tensors], tsl_tensor_kind     */
+  int32_t n_ops;
+  const char* const* op_ids;     /* [n_ops]                          */
+  const char* const* op_kinds;   /* [n_ops]; "update" marks updates  */
+  const int8_t* op_phases;       /* [n_ops], tsl_op_phase            */
+  const int32_t* op_in_offsets;  /* [n_ops+1] CSR into op_inputs     */
+  const int32_t* op_inputs;      /* tensor indices, op.inputs order  */
+  const int32_t* op_out_offsets; /* [n_ops+1] CSR into op_outputs    */
+  const int32_t* op_outputs;     /* tensor indices, op.outputs order */
+  const int64_t* op_latencies;   /* [n_ops] ticks or TSL_LATENCY_MISSING */
+  double max_swap_ratio;         /* config.max_swap_ratios[job]; <=0 means "absent" (1.0) */
+} tsl_job_desc;
+
+/* Read-only view of one job's plan + peak report inside a result. All arrays
+ * are owned by the result. Swap events are in plan order (the reference's
+ * SchedulingPlan::swap_events vector, plan.hpp:46-53). */
+typedef struct tsl_job_view {
+  const char* job_id;
+  int64_t version;
+  /* SwapEvent (plan.hpp:18-32); tensor = index of the storage tensor */
+  int32_t n_swap;
+  const int64_t* ev_id;
+  const int32_t* ev_tensor;
+  const int8_t* ev_dir; /* 0 = out, 1 = in */
+  const int64_t* ev_trigger;
+  const int64_t* ev_delta;
+  const int64_t* ev_start;
+  const int64_t* ev_end;
+  const int64_t* ev_earliest;
+  const int64_t* ev_latest;
+  const int8_t* ev_wraps;
+  const int64_t* ev_pair;
+  const int64_t* ev_serves;
+  /* RecomputeEvent (plan.hpp:34-42) */
+  int32_t n_recompute;
+  const int64_t* rc_id;
+  const int32_t* rc_tensor;
+  const int64_t* rc_target;
+  const int32_t* rc_regen_op;
+  const int64_t* rc_latency;
+  const int64_t* rc_saving;
+  /* release_flags (std::set<AccessId>, ascending) */
+  int32_t n_release;
+  const int64_t* release_flags;
+  /* PeakReport (peak.hpp:47-56) */
+  int64_t memory_peak;
+  int64_t peak_time;
+  int8_t has_last_input_access;
+  int64_t last_input_access;
+  int32_t n_peak_tensors;
+  const int32_t* peak_tensors; /* tensor indices, std::set<string> order */
+  int32_t n_curve;
+  const int64_t* curve_time;
+  const int64_t* curve_bytes;
+  /* working access sequence after planning (recomputation shifts it) */
+  int64_t iteration_period;
+  int32_t n_accesses;
+} tsl_job_view;
+
+/* Device-side counters of one build, for the roofline. */
+typedef struct tsl_stats {
+  double kernel_ms;          /* device time of the planning kernel(s)       */
+  double total_ms;           /* host wall time of tsl_build_plan            */
+  int64_t n_accesses;        /* sum of |AccessSequence| over jobs           */
+  int64_t loop_iterations;   /* orchestrator loop iterations                */
+  int64_t evaluations;       /* analyze_job evaluations performed           */
+  int64_t timeline_events;   /* sum of timeline events over evaluations     */
+  int64_t candidates;        /* swap candidates visited                     */
+  int64_t candidate_accesses;/* sum of storage accesses read by the scorer  */
+  int64_t busy_intervals;    /* channel intervals scanned by gap searches   */
+  int64_t algorithmic_bytes; /* SURVEY §8(d) byte formula over the build    */
+  int64_t kernel_launches;   /* device kernels launched by this call        */
+} tsl_stats;
+
+typedef struct tsl_ctx tsl_ctx;
+typedef struct tsl_result tsl_result;
+
+const char* tsl_last_error(void);
+
+/* Device context: CUDA device, streams, device workspace (grown on demand). */
+int tsl_create(int device, tsl_ctx** out);
+int tsl_destroy(tsl_ctx* ctx);
+
+/* memsched::build_plan(jobs, config) -- orchestrator.cpp:8-70. */
+int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs,
+                   const tsl_config* cfg, tsl_result** out);
+
+/* Several independent build_plan calls ("job groups", e.g. the 8 workload
+ * shards of one GPU) planned by ONE device launch, one CTA per group.
+ * group_offsets[n_groups+1] partitions jobs[]. out[g] receives each result. */
+int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs,
+                          const int32_t* group_offsets, int32_t n_groups,
+                          const tsl_config* cfg, tsl_result** out);
+
+/* A caller-supplied plan for one job (SchedulingPlan, plan.hpp:46-53), used by
+ * tsl_analyze_job. ev_tensor / rc_tensor / rc_regen_op index the job's
+ * tensor / op tables. */
+typedef struct tsl_plan_desc {
+  int32_t n_swap;
+  const int64_t* ev_id;
+  const int32_t* ev_tensor;
+  const int8_t* ev_dir;
+  const int64_t* ev_trigger;
+  const int64_t* ev_delta;
+  const int64_t* ev_start;
+  const int64_t* ev_end;
+  const int8_t* ev_wraps;
+  const int64_t* ev_pair;
+  const int64_t* ev_serves;
+  int32_t n_recompute;
+  const int64_t* rc_id;
+  const int32_t* rc_tensor;
+  const int64_t* rc_target;
+  const int32_t* rc_regen_op;
+  const int64_t* rc_latency;
+  const int64_t* rc_saving;
+  int32_t n_release;
+  const int64_t* release_flags;
+  int64_t version;
+} tsl_plan_desc;
+
+/* memsched::analyze_job(seq, plan, catalog) -- peak.cpp:246-250 -- where seq
+ * is the job's activity-analysed access sequence (make_job_context,
+ * swap_planner.cpp:156-169). The result holds one job: the given plan and its
+ * PeakReport. */
+int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* plan,
+                    tsl_result** out);
+
+/* Result accessors. Jobs are ordered by job id (std::map<JobId,...>). */
+int32_t tsl_result_n_jobs(const tsl_result* r);
+int tsl_result_job(const tsl_result* r, int32_t i, tsl_job_view* out);
+int32_t tsl_result_history(const tsl_result* r, const int64_t** merged_peak_history);
+int64_t tsl_result_final_merged_peak(const tsl_result* r);
+int32_t tsl_result_within_budget(const tsl_result* r);
+const char* tsl_result_diagnostic(const tsl_result* r);
+int tsl_result_stats(const tsl_result* r, tsl_stats* out);
+/* save_plans(result.plans) byte-for-byte (plan.cpp:30-65). Caller frees with tsl_free. */
+char* tsl_result_save_plans(const tsl_result* r);
+/* PeakReport::to_json of job i (peak.cpp:258-272). Caller frees with tsl_free. */
+char* tsl_result_report_json(const tsl_result* r, int32_t i);
+void tsl_result_destroy(tsl_result* r);
+void tsl_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENSILE_B200_H */

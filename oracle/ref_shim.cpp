@@ -1,0 +1,216 @@
+// TEST INFRASTRUCTURE -- C entry points over the UNMODIFIED reference library
+// (/root/reference/proj/src/*.cpp compiled in place by oracle/Makefile into
+// oracle/_ref/libmemsched_ref.so). Used only by tests/, by
+// tests/golden/make_golden.py (fixture generation) and by bench.py's
+// reference / cpu_baseline arm. Never linked into the product.
+//
+// Everything crosses this boundary as JSON in the reference's own formats:
+// graphs as save_graph/load_graph documents (graph.cpp:187-243), plans as
+// save_plans documents (plan.cpp:30-65) and reports as PeakReport::to_json
+// (peak.cpp:258-272).
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nlohmann/json.hpp>
+
+#include "memsched/orchestrator.hpp"
+#include "memsched/peak.hpp"
+#include "memsched/plan.hpp"
+#include "memsched/simulator.hpp"
+#include "memsched/swap_planner.hpp"
+#include "memsched/workload.hpp"
+// test_support.hpp is header-only reference test code (random_job,
+// planned_random_job, replay_oracle); compiled where it lies.
+#include "test_support.hpp"
+
+using namespace memsched;
+using json = nlohmann::json;
+using ojson = nlohmann::ordered_json;
+
+namespace {
+
+thread_local std::string g_err;
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size() + 1);
+  return p;
+}
+
+std::string lat_doc(const std::map<OpId, Tick>& lat) {
+  ojson d = ojson::object();
+  for (const auto& [op, t] : lat) d[op] = t;
+  return d.dump();
+}
+
+PlannerConfig parse_config(const json& c) {
+  PlannerConfig cfg;
+  cfg.pcie_bandwidth = c.at("pcie_bandwidth").get<Bytes>();
+  cfg.transfer_setup = c.at("transfer_setup").get<Tick>();
+  cfg.memory_budget = c.at("memory_budget").get<Bytes>();
+  if (c.contains("ewma_alpha")) cfg.ewma_alpha = c["ewma_alpha"].get<double>();
+  if (c.contains("replan_threshold"))
+    cfg.replan_threshold = c["replan_threshold"].get<double>();
+  if (c.contains("stall_epsilon")) cfg.stall_epsilon = c["stall_epsilon"].get<double>();
+  if (c.contains("stall_min_iters")) cfg.stall_min_iters = c["stall_min_iters"].get<int>();
+  if (c.contains("max_swap_ratios"))
+    for (const auto& [k, v] : c["max_swap_ratios"].items())
+      cfg.max_swap_ratios[k] = v.get<double>();
+  return cfg;
+}
+
+using JobList = std::vector<std::pair<ComputeGraph, std::map<OpId, Tick>>>;
+
+JobList parse_jobs(const json& req) {
+  JobList jobs;
+  for (const auto& j : req.at("jobs")) {
+    ComputeGraph g = load_graph(j.at("graph").dump());
+    std::map<OpId, Tick> lat;
+    for (const auto& [k, v] : j.at("latencies").items()) lat[k] = v.get<Tick>();
+    jobs.emplace_back(std::move(g), std::move(lat));
+  }
+  return jobs;
+}
+
+json report_json(const PeakReport& r) { return json::parse(r.to_json()); }
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_free(char* p) { std::free(p); }
+
+// generate_workload + true_latency_table (workload.cpp:96-209).
+int ref_generate_workload(const char* family, int batch, std::uint64_t seed, int depth,
+                          const char* job_id, std::uint64_t lat_seed, double usage,
+                          char** graph_json, char** lat_json) {
+  return guarded([&] {
+    WorkloadSpec spec;
+    spec.family = family;
+    spec.batch_size = batch;
+    spec.seed = seed;
+    spec.depth = depth;
+    spec.job_id = job_id ? job_id : "";
+    ComputeGraph g = generate_workload(spec);
+    *graph_json = dup(save_graph(g));
+    *lat_json = dup(lat_doc(true_latency_table(g, lat_seed, usage)));
+  });
+}
+
+// testsup::random_job (test_support.hpp:166-178).
+int ref_random_job(std::uint64_t seed, char** graph_json, char** lat_json) {
+  return guarded([&] {
+    auto [g, lat] = testsup::random_job(seed);
+    *graph_json = dup(save_graph(g));
+    *lat_json = dup(lat_doc(lat));
+  });
+}
+
+// Initial per-job peaks (make_job_context, swap_planner.cpp:156-169).
+int ref_initial_peaks(const char* request, char** out_json) {
+  return guarded([&] {
+    json req = json::parse(request);
+    JobList jobs = parse_jobs(req);
+    ojson out = ojson::object();
+    for (auto& [g, lat] : jobs) {
+      JobContext ctx = make_job_context(g, lat);
+      out[g.job_id()] = ctx.report.memory_peak;
+    }
+    *out_json = dup(out.dump());
+  });
+}
+
+// build_plan (orchestrator.cpp:8-70), timed `repeats` times around the call
+// (make_job_context included, JSON parsing excluded).
+int ref_build_plan(const char* request, int repeats, char** plans_json, char** result_json) {
+  return guarded([&] {
+    json req = json::parse(request);
+    PlannerConfig cfg = parse_config(req.at("config"));
+    JobList jobs = parse_jobs(req);
+    BuildResult r;
+    std::vector<double> times;
+    for (int i = 0; i < std::max(1, repeats); ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      r = build_plan(jobs, cfg);
+      auto t1 = std::chrono::steady_clock::now();
+      times.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+    std::size_t n_acc = 0;
+    for (auto& [g, lat] : jobs)
+      n_acc += generate_access_sequence(g, lat).accesses.size();
+    ojson out;
+    out["merged_peak_history"] = r.merged_peak_history;
+    out["final_merged_peak"] = r.final_merged_peak;
+    out["within_budget"] = r.within_budget;
+    out["diagnostic"] = r.diagnostic;
+    ojson reps = ojson::object();
+    for (const auto& [job, rep] : r.reports) reps[job] = ojson::parse(rep.to_json());
+    out["reports"] = reps;
+    out["n_accesses"] = n_acc;
+    out["times_ms"] = times;
+    *plans_json = dup(save_plans(r.plans));
+    *result_json = dup(out.dump());
+  });
+}
+
+// testsup::planned_random_job + analyzer + replay_oracle
+// (test_support.hpp:52-226): golden vectors for the footprint evaluator.
+int ref_planned_random_job(std::uint64_t seed, int max_swaps, std::int64_t bw,
+                           std::int64_t setup, char** out_json) {
+  return guarded([&] {
+    PlannerConfig cfg;
+    cfg.pcie_bandwidth = bw;
+    cfg.transfer_setup = setup;
+    JobContext job = testsup::planned_random_job(seed, max_swaps, cfg);
+    testsup::OracleResult o = testsup::replay_oracle(job.seq, job.plan, job.catalog);
+    auto [g, lat] = testsup::random_job(seed);
+    ojson out;
+    out["graph"] = ojson::parse(save_graph(g));
+    out["latencies"] = ojson::parse(lat_doc(lat));
+    out["plan"] = ojson::parse(save_plans({{job.seq.job_id, job.plan}}))[job.seq.job_id];
+    out["report"] = ojson::parse(job.report.to_json());
+    ojson oo;
+    oo["peak"] = o.peak;
+    oo["peak_time"] = o.peak_time;
+    oo["tensors"] = std::vector<std::string>(o.tensors.begin(), o.tensors.end());
+    out["replay_oracle"] = oo;
+    *out_json = dup(out.dump());
+  });
+}
+
+// analyze_job (peak.cpp:246-250) on a caller-supplied plan for one job.
+// request: {"graph":…, "latencies":…, "plan": <save_plans entry>}
+int ref_analyze_job(const char* request, char** out_json) {
+  return guarded([&] {
+    json req = json::parse(request);
+    ComputeGraph g = load_graph(req.at("graph").dump());
+    std::map<OpId, Tick> lat;
+    for (const auto& [k, v] : req.at("latencies").items()) lat[k] = v.get<Tick>();
+    JobContext ctx = make_job_context(g, lat);
+    json wrapped;
+    wrapped[g.job_id()] = req.at("plan");
+    auto plans = load_plans(wrapped.dump());
+    SchedulingPlan plan = plans.at(g.job_id());
+    PeakReport rep = analyze_job(ctx.seq, plan, ctx.catalog);
+    *out_json = dup(rep.to_json());
+  });
+}
+
+}  // extern "C"

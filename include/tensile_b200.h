@@ -146,6 +146,7 @@ typedef struct tsl_stats {
 
 typedef struct tsl_ctx tsl_ctx;
 typedef struct tsl_result tsl_result;
+typedef struct tsl_plan tsl_plan;
 
 const char* tsl_last_error(void);
 
@@ -163,6 +164,22 @@ int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs,
 int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs,
                           const int32_t* group_offsets, int32_t n_groups,
                           const tsl_config* cfg, tsl_result** out);
+
+/* The same call split in three so inputs can stay resident in HBM between
+ * device-only runs (bench.py's device-timed `value`):
+ *   tsl_plan_prepare  validate + pack + one H2D copy      (no kernel)
+ *   tsl_plan_run      `repeats` kernel launches on the context stream, timed
+ *                     with CUDA events; *kernel_ms = mean per launch
+ *   tsl_plan_collect  one D2H copy + results; out[n_groups]
+ * tsl_build_plan_groups == prepare + run(1) + collect. */
+int tsl_plan_prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets,
+                     int32_t n_groups, const tsl_config* cfg, tsl_plan** out);
+int tsl_plan_run(tsl_plan* plan, int32_t repeats, double* kernel_ms);
+/* Enqueue one launch on `stream` (a cudaStream_t, NULL = the context stream)
+ * without synchronising -- for callers that time with their own events. */
+int tsl_plan_launch_async(tsl_plan* plan, void* stream);
+int tsl_plan_collect(tsl_plan* plan, tsl_result** out);
+void tsl_plan_destroy(tsl_plan* plan);
 
 /* A caller-supplied plan for one job (SchedulingPlan, plan.hpp:46-53), used by
  * tsl_analyze_job. ev_tensor / rc_tensor / rc_regen_op index the job's

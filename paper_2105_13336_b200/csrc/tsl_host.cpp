@@ -1,0 +1,1138 @@
+// Host side of the C-ABI (include/tensile_b200.h): graph validation and
+// topological order (graph.cpp:49-119, 245-282), integer/rank packing, one
+// H2D copy, one kernel launch for all groups, one D2H copy, and the
+// reference's output formats (save_plans, PeakReport::to_json).
+//
+// Everything on the planning path runs in tsl_plan_kernel (tsl_kernel.cu);
+// this file never computes a plan. Without a CUDA device every entry point
+// fails with TSL_ERR_CUDA -- there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <queue>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "tensile_b200.h"
+#include "tsl_kernel.h"
+
+using namespace tsl;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw Fail{code, m}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TSL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+std::vector<int32_t> lex_rank(const std::vector<std::string>& ids) {
+  std::vector<int32_t> idx(ids.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  std::vector<int32_t> rank(ids.size());
+  for (size_t r = 0; r < idx.size(); ++r) rank[idx[r]] = static_cast<int32_t>(r);
+  return rank;
+}
+
+// ---------------------------------------------------------------------------
+// Graph: ComputeGraph (graph.hpp:14-62) over dense indices.
+// ---------------------------------------------------------------------------
+struct Graph {
+  std::string job_id;
+  int32_t T = 0, O = 0, A = 0;
+  std::vector<std::string> tid, oid;
+  std::vector<int64_t> size, lat;
+  std::vector<int8_t> kind;
+  std::vector<int32_t> in_off, in, out_off, out;
+  std::vector<int32_t> trank, store, upd, prod, topo;
+  double ratio = 1.0;
+  bool ratio_given = false;
+};
+
+const char* kind_name(int k) {
+  static const char* n[] = {"input", "interim", "parameter", "updated_parameter", "output"};
+  return (k >= 0 && k < 5) ? n[k] : "?";
+}
+
+// ComputeGraph::validate, graph.cpp:49-119, same checks in the same order.
+Graph load_graph(const tsl_job_desc& d) {
+  Graph g;
+  g.job_id = d.job_id ? d.job_id : "";
+  g.T = d.n_tensors;
+  g.O = d.n_ops;
+  if (g.T < 0 || g.O < 0) fail(TSL_ERR_ARGUMENT, "negative tensor/op count in job " + g.job_id);
+  if (g.T > 0 && (!d.tensor_ids || !d.tensor_sizes || !d.tensor_kinds))
+    fail(TSL_ERR_ARGUMENT, "null tensor table in job " + g.job_id);
+  if (g.O > 0 && (!d.op_ids || !d.op_kinds || !d.op_phases || !d.op_in_offsets || !d.op_out_offsets))
+    fail(TSL_ERR_ARGUMENT, "null op table in job " + g.job_id);
+  g.ratio_given = d.max_swap_ratio > 0 || std::isnan(d.max_swap_ratio);
+  g.ratio = g.ratio_given ? d.max_swap_ratio : 1.0;
+  std::set<std::string> seen;
+  for (int i = 0; i < g.T; ++i) {
+    g.tid.emplace_back(d.tensor_ids[i] ? d.tensor_ids[i] : "");
+    g.size.push_back(d.tensor_sizes[i]);
+    int8_t k = d.tensor_kinds[i];
+    if (k < 0 || k > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(k));
+    g.kind.push_back(k);
+  }
+  for (int i = 0; i < g.T; ++i) {
+    if (g.size[i] <= 0) fail(TSL_ERR_VALIDATION, "nonpositive size for tensor " + g.tid[i]);
+    if (!seen.insert(g.tid[i]).second) fail(TSL_ERR_VALIDATION, "duplicate tensor id " + g.tid[i]);
+  }
+  std::vector<int32_t> producer(g.T, -1);
+  std::vector<std::vector<int32_t>> consumers(g.T);
+  std::set<std::string> oseen;
+  g.in_off.push_back(0);
+  g.out_off.push_back(0);
+  std::vector<std::string> okind;
+  std::vector<int8_t> phase;
+  for (int o = 0; o < g.O; ++o) {
+    g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
+    okind.emplace_back(d.op_kinds[o] ? d.op_kinds[o] : "");
+    int8_t ph = d.op_phases[o];
+    if (ph != 0 && ph != 1) fail(TSL_ERR_VALIDATION, "unknown op phase: #" + std::to_string(ph));
+    phase.push_back(ph);
+    if (!oseen.insert(g.oid[o]).second) fail(TSL_ERR_VALIDATION, "duplicate op id " + g.oid[o]);
+    for (int32_t i = d.op_in_offsets[o]; i < d.op_in_offsets[o + 1]; ++i) {
+      int32_t t = d.op_inputs[i];
+      if (t < 0 || t >= g.T)
+        fail(TSL_ERR_VALIDATION, "dangling tensor reference #" + std::to_string(t) + " in op " + g.oid[o]);
+      consumers[t].push_back(o);
+      g.in.push_back(t);
+    }
+    for (int32_t i = d.op_out_offsets[o]; i < d.op_out_offsets[o + 1]; ++i) {
+      int32_t t = d.op_outputs[i];
+      if (t < 0 || t >= g.T)
+        fail(TSL_ERR_VALIDATION, "dangling tensor reference #" + std::to_string(t) + " in op " + g.oid[o]);
+      if (producer[t] >= 0) fail(TSL_ERR_VALIDATION, "tensor " + g.tid[t] + " has more than one producer");
+      producer[t] = o;
+      g.out.push_back(t);
+    }
+    g.in_off.push_back(static_cast<int32_t>(g.in.size()));
+    g.out_off.push_back(static_cast<int32_t>(g.out.size()));
+  }
+  for (int t = 0; t < g.T; ++t) {
+    if (g.kind[t] == TSL_KIND_INPUT || g.kind[t] == TSL_KIND_PARAMETER) {
+      if (producer[t] >= 0) fail(TSL_ERR_VALIDATION, "source tensor " + g.tid[t] + " must not have a producing op");
+      continue;
+    }
+    if (producer[t] < 0) fail(TSL_ERR_VALIDATION, "tensor " + g.tid[t] + " has no producing op");
+  }
+  std::vector<int32_t> alias(g.T, -1);
+  g.upd.assign(g.T, -1);
+  for (int o = 0; o < g.O; ++o) {
+    if (phase[o] != TSL_PHASE_OPTIMIZE || okind[o] != "update") continue;
+    std::vector<int32_t> u, p;
+    for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i)
+      if (g.kind[g.out[i]] == TSL_KIND_UPDATED_PARAMETER) u.push_back(g.out[i]);
+    if (u.size() != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must output exactly one updated_parameter");
+    for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i)
+      if (g.kind[g.in[i]] == TSL_KIND_PARAMETER) p.push_back(g.in[i]);
+    if (p.size() != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must read exactly one parameter");
+    if (g.size[u[0]] != g.size[p[0]])
+      fail(TSL_ERR_VALIDATION, "updated parameter " + g.tid[u[0]] + " must match the size of " + g.tid[p[0]]);
+    alias[u[0]] = p[0];
+    g.upd[p[0]] = u[0];
+  }
+  for (int t = 0; t < g.T; ++t)
+    if (g.kind[t] == TSL_KIND_UPDATED_PARAMETER && alias[t] < 0)
+      fail(TSL_ERR_VALIDATION, "updated parameter " + g.tid[t] + " is not produced by an update op");
+  g.store.resize(g.T);
+  for (int t = 0; t < g.T; ++t) g.store[t] = alias[t] >= 0 ? alias[t] : t;
+  g.prod = producer;
+  g.trank = lex_rank(g.tid);
+  // topological_order (graph.cpp:245-282): Kahn with a min-heap on the op id,
+  // plus user -> update edges for every consumer of an updated param's param.
+  std::vector<int32_t> orank = lex_rank(g.oid);
+  std::vector<int32_t> indeg(g.O, 0);
+  std::vector<std::set<int32_t>> succ(g.O);
+  for (int o = 0; o < g.O; ++o) {
+    for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i) {
+      int32_t p = producer[g.in[i]];
+      if (p >= 0 && p != o && succ[p].insert(o).second) indeg[o]++;
+    }
+    for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i) {
+      int32_t t = g.out[i];
+      if (g.kind[t] != TSL_KIND_UPDATED_PARAMETER || alias[t] < 0) continue;
+      for (int32_t user : consumers[alias[t]])
+        if (user != o && succ[user].insert(o).second) indeg[o]++;
+    }
+  }
+  auto cmp = [&](int32_t a, int32_t b) { return orank[a] > orank[b]; };
+  std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
+  for (int o = 0; o < g.O; ++o)
+    if (indeg[o] == 0) ready.push(o);
+  while (!ready.empty()) {
+    int32_t o = ready.top();
+    ready.pop();
+    g.topo.push_back(o);
+    for (int32_t n : succ[o])
+      if (--indeg[n] == 0) ready.push(n);
+  }
+  if (static_cast<int32_t>(g.topo.size()) != g.O) fail(TSL_ERR_VALIDATION, "cycle detected in graph of job " + g.job_id);
+  // latency table (generate_access_sequence, access.cpp:33-38), checked in
+  // topological order like the reference.
+  g.lat.assign(g.O, 0);
+  for (int32_t o : g.topo) {
+    int64_t l = d.op_latencies ? d.op_latencies[o] : TSL_LATENCY_MISSING;
+    g.lat[o] = l;
+  }
+  int64_t A = 0;
+  for (int o = 0; o < g.O; ++o) A += (g.in_off[o + 1] - g.in_off[o]) + (g.out_off[o + 1] - g.out_off[o]);
+  if (A > (1 << 30)) fail(TSL_ERR_CAPACITY, "job " + g.job_id + " has too many accesses");
+  g.A = static_cast<int32_t>(A);
+  return g;
+}
+
+void check_latencies(const Graph& g) {
+  for (int32_t o : g.topo) {
+    if (g.lat[o] == TSL_LATENCY_MISSING) fail(TSL_ERR_VALIDATION, "missing latency entry for op " + g.oid[o]);
+    if (g.lat[o] < 0) fail(TSL_ERR_VALIDATION, "negative latency for op " + g.oid[o]);
+  }
+}
+
+// PlannerConfig::validate, config.hpp:25-35.
+void validate_config(const tsl_config& c, const std::vector<const Graph*>& jobs) {
+  if (c.pcie_bandwidth <= 0) fail(TSL_ERR_VALIDATION, "pcie_bandwidth must be positive");
+  if (c.transfer_setup < 0) fail(TSL_ERR_VALIDATION, "transfer_setup must be nonnegative");
+  if (c.memory_budget < 0) fail(TSL_ERR_VALIDATION, "memory_budget must be nonnegative");
+  if (c.ewma_alpha < 0 || c.ewma_alpha > 1) fail(TSL_ERR_VALIDATION, "ewma_alpha out of [0,1]");
+  if (c.replan_threshold <= 0) fail(TSL_ERR_VALIDATION, "replan_threshold must be positive");
+  if (c.stall_epsilon <= 0 || c.stall_epsilon >= 1) fail(TSL_ERR_VALIDATION, "stall_epsilon out of (0,1)");
+  std::map<std::string, double> ratios;  // std::map<JobId,double> order
+  for (const Graph* g : jobs)
+    if (g->ratio_given) ratios[g->job_id] = g->ratio;
+  for (auto& [job, r] : ratios)
+    if (!(r > 0 && r <= 1)) fail(TSL_ERR_VALIDATION, "max swap ratio for " + job + " out of (0,1]");
+}
+
+// ---------------------------------------------------------------------------
+// Device buffer layout
+// ---------------------------------------------------------------------------
+struct Layout {
+  size_t off = 0;
+  template <class T>
+  size_t take(size_t n) {
+    off = (off + 15) & ~size_t(15);
+    size_t o = off;
+    off += n * sizeof(T);
+    return o;
+  }
+};
+
+struct JobPlace {  // byte offsets into the device buffer
+  size_t topo, o_lat, o_in_off, o_in, o_out_off, o_out, t_size, t_kind, t_rank, t_store, t_upd, t_prod, inflag;
+  size_t a_tensor, a_store, a_type, a_start, a_end, a_base, a_flag, a_owned, s_off, s_acc, t_wfirst, t_utga;
+  size_t ev[12], bz_s, bz_e, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
+  size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve;
+  int32_t Scap, Rcap, Ecap;
+};
+
+struct GroupPlace {
+  size_t hist;
+  size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
+  int32_t hist_cap;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Results
+// ---------------------------------------------------------------------------
+struct JobOut {
+  const Graph* g = nullptr;
+  int32_t version = 0;
+  JobState st{};
+  std::vector<int64_t> ev_id, ev_trig, ev_delta, ev_start, ev_end, ev_earl, ev_late, ev_pair, ev_serves;
+  std::vector<int32_t> ev_tensor;
+  std::vector<int8_t> ev_dir, ev_wraps;
+  std::vector<int64_t> rc_id, rc_target, rc_lat, rc_saving;
+  std::vector<int32_t> rc_tensor, rc_regen;
+  std::vector<int64_t> flags;
+  std::vector<int32_t> peak_tensors;
+  std::vector<int64_t> curve_t, curve_b;
+};
+
+struct tsl_result {
+  std::vector<Graph> graphs;
+  std::vector<JobOut> jobs;  // job-id order
+  std::vector<int64_t> history;
+  int64_t final_merged = 0;
+  bool within = true;
+  std::string diagnostic;
+  tsl_stats stats{};
+};
+
+struct tsl_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* dbuf = nullptr;
+  size_t dcap = 0;
+  uint8_t* hbuf = nullptr;  // pinned staging
+  size_t hcap = 0;
+};
+
+struct tsl_plan {
+  tsl_ctx* ctx = nullptr;
+  int mode = 0;  // 0 build_plan, 1 analyze_job
+  int32_t n_groups = 0;
+  std::vector<std::vector<Graph>> graphs;  // per group, caller order
+  std::vector<std::vector<JobPlace>> jp;
+  std::vector<GroupPlace> gp;
+  tsl_config cfg{};
+  size_t h2d_bytes = 0;          // [0, h2d_bytes) uploaded
+  size_t d2h_off = 0, d2h_bytes = 0;
+  size_t groups_off = 0, jobs_off = 0, states_off = 0;
+  std::vector<int32_t> group_job_base;  // first JobDev index of each group
+  double last_kernel_ms = 0;
+  double prep_ms = 0;
+  int64_t n_accesses = 0;
+};
+
+namespace {
+
+void grow(tsl_ctx* c, size_t need) {
+  if (need > c->dcap) {
+    if (c->dbuf) cudaFree(c->dbuf);
+    c->dbuf = nullptr;
+    size_t cap = std::max(need, c->dcap * 2);
+    cuda_check(cudaMalloc(&c->dbuf, cap), "cudaMalloc");
+    c->dcap = cap;
+  }
+  if (need > c->hcap) {
+    if (c->hbuf) cudaFreeHost(c->hbuf);
+    c->hbuf = nullptr;
+    size_t cap = std::max(need, c->hcap * 2);
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c->hbuf), cap), "cudaMallocHost");
+    c->hcap = cap;
+  }
+}
+
+template <class T>
+T* hp(tsl_ctx* c, size_t off) { return reinterpret_cast<T*>(c->hbuf + off); }
+template <class T>
+T* dp(tsl_ctx* c, size_t off) { return reinterpret_cast<T*>(static_cast<uint8_t*>(c->dbuf) + off); }
+
+template <class T>
+void put(tsl_ctx* c, size_t off, const std::vector<T>& v) {
+  if (!v.empty()) std::memcpy(c->hbuf + off, v.data(), v.size() * sizeof(T));
+}
+
+// A caller plan for analyze mode (tsl_plan_desc), kept with its job.
+struct CallerPlan {
+  const tsl_plan_desc* p = nullptr;
+};
+
+tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, int32_t n_groups,
+                  const tsl_config* cfg, int mode, const tsl_plan_desc* caller) {
+  auto t0 = std::chrono::steady_clock::now();
+  auto* P = new tsl_plan();
+  P->ctx = ctx;
+  P->mode = mode;
+  P->n_groups = n_groups;
+  P->cfg = *cfg;
+  P->graphs.resize(n_groups);
+  // 1. validate graphs (caller order), then the config, then latencies
+  for (int gi = 0; gi < n_groups; ++gi) {
+    for (int32_t k = offs[gi]; k < offs[gi + 1]; ++k) P->graphs[gi].push_back(load_graph(jobs[k]));
+  }
+  for (int gi = 0; gi < n_groups; ++gi) {
+    std::vector<const Graph*> gg;
+    for (auto& g : P->graphs[gi]) gg.push_back(&g);
+    if (mode == 0) validate_config(*cfg, gg);
+    std::set<std::string> ids;
+    for (auto& g : P->graphs[gi]) {
+      if (!ids.insert(g.job_id).second)
+        fail(TSL_ERR_ARGUMENT, "duplicate job id " + g.job_id + " in one build (unsupported)");
+      check_latencies(g);
+      if (g.T >= (1 << 24)) fail(TSL_ERR_CAPACITY, "job " + g.job_id + " has too many tensors");
+    }
+    if (P->graphs[gi].size() > 128) fail(TSL_ERR_CAPACITY, "more than 128 jobs in one group");
+  }
+  // 2. layout: [static inputs][groups|states|jobs][outputs][workspace]
+  Layout L;
+  P->jp.resize(n_groups);
+  P->gp.resize(n_groups);
+  for (int gi = 0; gi < n_groups; ++gi) {
+    for (auto& g : P->graphs[gi]) {
+      JobPlace p{};
+      p.topo = L.take<int32_t>(g.O);
+      p.o_lat = L.take<int64_t>(g.O);
+      p.o_in_off = L.take<int32_t>(g.O + 1);
+      p.o_in = L.take<int32_t>(g.in.size());
+      p.o_out_off = L.take<int32_t>(g.O + 1);
+      p.o_out = L.take<int32_t>(g.out.size());
+      p.t_size = L.take<int64_t>(g.T);
+      p.t_kind = L.take<int8_t>(g.T);
+      p.t_rank = L.take<int32_t>(g.T);
+      p.t_store = L.take<int32_t>(g.T);
+      p.t_upd = L.take<int32_t>(g.T);
+      p.t_prod = L.take<int32_t>(g.T);
+      p.inflag = mode == 1 ? L.take<uint8_t>(g.A) : 0;
+      p.Scap = 2 * g.A + 2;
+      p.Rcap = g.T + 1;
+      p.Ecap = 2 * g.A + p.Scap + p.Rcap;
+      P->n_accesses += g.A;
+      P->jp[gi].push_back(p);
+    }
+  }
+  P->groups_off = L.take<GroupDev>(n_groups);
+  int32_t nj = 0;
+  for (auto& v : P->graphs) { P->group_job_base.push_back(nj); nj += static_cast<int32_t>(v.size()); }
+  P->states_off = L.take<JobState>(nj);
+  P->jobs_off = L.take<JobDev>(nj);
+  const size_t stage_end = L.off;
+  // outputs (read back)
+  for (int gi = 0; gi < n_groups; ++gi) {
+    int64_t sumT = 0;
+    for (auto& g : P->graphs[gi]) sumT += g.T;
+    P->gp[gi].hist_cap = static_cast<int32_t>(2 * sumT + 16);
+    P->gp[gi].hist = L.take<int64_t>(P->gp[gi].hist_cap);
+    for (size_t k = 0; k < P->graphs[gi].size(); ++k) {
+      const Graph& g = P->graphs[gi][k];
+      JobPlace& p = P->jp[gi][k];
+      for (int f = 0; f < 12; ++f) {
+        size_t w = (f == 1) ? 4 : (f == 2 || f == 3) ? 1 : 8;  // tensor int32, dir/wraps int8
+        p.ev[f] = L.take<uint8_t>(w * p.Scap);
+      }
+      for (int f = 0; f < 6; ++f) {
+        size_t w = (f == 1 || f == 3) ? 4 : 8;
+        p.rc[f] = L.take<uint8_t>(w * p.Rcap);
+      }
+      p.a_flag = L.take<uint8_t>(g.A);
+      p.in_peak = L.take<uint8_t>(g.T);
+      p.curve_t = L.take<int64_t>(p.Ecap + 1);
+      p.curve_b = L.take<int64_t>(p.Ecap + 1);
+    }
+  }
+  const size_t out_end = L.off;
+  // workspace
+  for (int gi = 0; gi < n_groups; ++gi) {
+    for (size_t k = 0; k < P->graphs[gi].size(); ++k) {
+      const Graph& g = P->graphs[gi][k];
+      JobPlace& p = P->jp[gi][k];
+      p.a_tensor = L.take<int32_t>(g.A);
+      p.a_store = L.take<int32_t>(g.A);
+      p.a_type = L.take<int8_t>(g.A);
+      p.a_start = L.take<int64_t>(g.A);
+      p.a_end = L.take<int64_t>(g.A);
+      p.a_base = L.take<uint8_t>(g.A);
+      p.a_owned = L.take<uint8_t>(g.A);
+      p.s_off = L.take<int32_t>(g.T + 1);
+      p.s_acc = L.take<int32_t>(g.A);
+      p.t_wfirst = L.take<int32_t>(g.T);
+      p.t_utga = L.take<int32_t>(g.T);
+      p.bz_s = L.take<int64_t>(p.Scap);
+      p.bz_e = L.take<int64_t>(p.Scap);
+      p.st_evcnt = L.take<int32_t>(g.T);
+      p.swapped = L.take<uint8_t>(g.T);
+      p.ev_drop = L.take<uint8_t>(p.Scap);
+      p.res_init = L.take<uint8_t>(g.T);
+      p.bk_a_start = L.take<int64_t>(g.A);
+      p.bk_a_end = L.take<int64_t>(g.A);
+      p.bk_flag = L.take<uint8_t>(g.A);
+      p.bk_in_peak = L.take<uint8_t>(g.T);
+      p.bk_ev = L.take<int64_t>(size_t(12) * p.Scap);
+      p.bk_rc = L.take<int64_t>(size_t(6) * p.Rcap);
+      p.bk_bz = L.take<int64_t>(size_t(2) * p.Scap);
+      p.bk_evcnt = L.take<int32_t>(g.T);
+      p.bk_curve = L.take<int64_t>(size_t(2) * (p.Ecap + 1));
+    }
+    GroupPlace& q = P->gp[gi];
+    const size_t E = SORT_CAP;
+    q.k_key = L.take<uint64_t>(E);
+    q.k_val = L.take<int32_t>(E);
+    q.x_time = L.take<int64_t>(E);
+    q.x_fp = L.take<int64_t>(E);
+    q.x_store = L.take<int32_t>(E);
+    q.x_aid = L.take<int32_t>(E);
+    q.x_type = L.take<int8_t>(E);
+    q.x_job = L.take<int8_t>(E);
+    q.x_state = L.take<uint8_t>(E);
+    q.x_seq2 = L.take<int32_t>(E);
+    q.x_key2 = L.take<uint64_t>(E);
+    q.x_order = L.take<int32_t>(E);
+  }
+  const size_t total = L.off;
+  grow(ctx, total);
+  // 3. fill the staging buffer
+  int32_t jglob = 0;
+  for (int gi = 0; gi < n_groups; ++gi) {
+    const auto& gs = P->graphs[gi];
+    std::vector<std::string> jids;
+    for (auto& g : gs) jids.push_back(g.job_id);
+    std::vector<int32_t> jrank = lex_rank(jids);
+    bool coupled = false;
+    for (auto& g : gs) coupled = coupled || g.ratio < 1.0;
+    GroupDev* G = hp<GroupDev>(ctx, P->groups_off) + gi;
+    std::memset(G, 0, sizeof *G);
+    G->n_jobs = static_cast<int32_t>(gs.size());
+    G->coupled = coupled ? 1 : 0;
+    G->hist_cap = P->gp[gi].hist_cap;
+    G->cfg.bw = cfg->pcie_bandwidth;
+    G->cfg.setup = cfg->transfer_setup;
+    G->cfg.budget = cfg->memory_budget;
+    G->cfg.stall_eps = cfg->stall_epsilon;
+    G->cfg.stall_min_iters = cfg->stall_min_iters;
+    G->jobs = dp<JobDev>(ctx, P->jobs_off) + jglob;
+    G->st = dp<JobState>(ctx, P->states_off) + jglob;
+    const GroupPlace& q = P->gp[gi];
+    G->hist = dp<int64_t>(ctx, q.hist);
+    G->ecap = SORT_CAP;
+    G->k_key = dp<uint64_t>(ctx, q.k_key);
+    G->k_val = dp<int32_t>(ctx, q.k_val);
+    G->x_time = dp<int64_t>(ctx, q.x_time);
+    G->x_fp = dp<int64_t>(ctx, q.x_fp);
+    G->x_store = dp<int32_t>(ctx, q.x_store);
+    G->x_aid = dp<int32_t>(ctx, q.x_aid);
+    G->x_type = dp<int8_t>(ctx, q.x_type);
+    G->x_job = dp<int8_t>(ctx, q.x_job);
+    G->x_state = dp<uint8_t>(ctx, q.x_state);
+    G->x_seq2 = dp<int32_t>(ctx, q.x_seq2);
+    G->x_key2 = dp<uint64_t>(ctx, q.x_key2);
+    G->x_order = dp<int32_t>(ctx, q.x_order);
+    for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
+      const Graph& g = gs[k];
+      const JobPlace& p = P->jp[gi][k];
+      if (g.A > SORT_CAP || g.O + 1 > SORT_CAP)
+        fail(TSL_ERR_CAPACITY, "job " + g.job_id + " exceeds the single-CTA planner capacity (" +
+                                   std::to_string(SORT_CAP) + " accesses)");
+      std::vector<int32_t> topo = g.topo;
+      put(ctx, p.topo, topo);
+      put(ctx, p.o_lat, g.lat);
+      put(ctx, p.o_in_off, g.in_off);
+      put(ctx, p.o_in, g.in);
+      put(ctx, p.o_out_off, g.out_off);
+      put(ctx, p.o_out, g.out);
+      put(ctx, p.t_size, g.size);
+      put(ctx, p.t_kind, g.kind);
+      put(ctx, p.t_rank, g.trank);
+      put(ctx, p.t_store, g.store);
+      put(ctx, p.t_upd, g.upd);
+      put(ctx, p.t_prod, g.prod);
+      JobDev* J = hp<JobDev>(ctx, P->jobs_off) + jglob;
+      std::memset(J, 0, sizeof *J);
+      J->A = g.A; J->T = g.T; J->O = g.O; J->rank = jrank[k]; J->ratio = g.ratio;
+      J->Scap = p.Scap; J->Rcap = p.Rcap; J->Ecap = p.Ecap;
+      J->topo = dp<int32_t>(ctx, p.topo);
+      J->o_lat = dp<int64_t>(ctx, p.o_lat);
+      J->o_in_off = dp<int32_t>(ctx, p.o_in_off);
+      J->o_in = dp<int32_t>(ctx, p.o_in);
+      J->o_out_off = dp<int32_t>(ctx, p.o_out_off);
+      J->o_out = dp<int32_t>(ctx, p.o_out);
+      J->t_size = dp<int64_t>(ctx, p.t_size);
+      J->t_kind = dp<int8_t>(ctx, p.t_kind);
+      J->t_rank = dp<int32_t>(ctx, p.t_rank);
+      J->t_store = dp<int32_t>(ctx, p.t_store);
+      J->t_upd = dp<int32_t>(ctx, p.t_upd);
+      J->t_prod = dp<int32_t>(ctx, p.t_prod);
+      J->a_inflag = mode == 1 ? dp<uint8_t>(ctx, p.inflag) : nullptr;
+      J->a_tensor = dp<int32_t>(ctx, p.a_tensor);
+      J->a_store = dp<int32_t>(ctx, p.a_store);
+      J->a_type = dp<int8_t>(ctx, p.a_type);
+      J->a_start = dp<int64_t>(ctx, p.a_start);
+      J->a_end = dp<int64_t>(ctx, p.a_end);
+      J->a_base = dp<uint8_t>(ctx, p.a_base);
+      J->a_flag = dp<uint8_t>(ctx, p.a_flag);
+      J->a_owned = dp<uint8_t>(ctx, p.a_owned);
+      J->s_off = dp<int32_t>(ctx, p.s_off);
+      J->s_acc = dp<int32_t>(ctx, p.s_acc);
+      J->t_wfirst = dp<int32_t>(ctx, p.t_wfirst);
+      J->t_utga = dp<int32_t>(ctx, p.t_utga);
+      J->ev_id = dp<int64_t>(ctx, p.ev[0]);
+      J->ev_tensor = dp<int32_t>(ctx, p.ev[1]);
+      J->ev_dir = dp<int8_t>(ctx, p.ev[2]);
+      J->ev_wraps = dp<int8_t>(ctx, p.ev[3]);
+      J->ev_trig = dp<int64_t>(ctx, p.ev[4]);
+      J->ev_delta = dp<int64_t>(ctx, p.ev[5]);
+      J->ev_start = dp<int64_t>(ctx, p.ev[6]);
+      J->ev_end = dp<int64_t>(ctx, p.ev[7]);
+      J->ev_earl = dp<int64_t>(ctx, p.ev[8]);
+      J->ev_late = dp<int64_t>(ctx, p.ev[9]);
+      J->ev_pair = dp<int64_t>(ctx, p.ev[10]);
+      J->ev_serves = dp<int64_t>(ctx, p.ev[11]);
+      J->bz_s = dp<int64_t>(ctx, p.bz_s);
+      J->bz_e = dp<int64_t>(ctx, p.bz_e);
+      J->st_evcnt = dp<int32_t>(ctx, p.st_evcnt);
+      J->swapped = dp<uint8_t>(ctx, p.swapped);
+      J->rc_id = dp<int64_t>(ctx, p.rc[0]);
+      J->rc_tensor = dp<int32_t>(ctx, p.rc[1]);
+      J->rc_target = dp<int64_t>(ctx, p.rc[2]);
+      J->rc_regen = dp<int32_t>(ctx, p.rc[3]);
+      J->rc_lat = dp<int64_t>(ctx, p.rc[4]);
+      J->rc_saving = dp<int64_t>(ctx, p.rc[5]);
+      J->in_peak = dp<uint8_t>(ctx, p.in_peak);
+      J->ev_drop = dp<uint8_t>(ctx, p.ev_drop);
+      J->res_init = dp<uint8_t>(ctx, p.res_init);
+      J->curve_t = dp<int64_t>(ctx, p.curve_t);
+      J->curve_b = dp<int64_t>(ctx, p.curve_b);
+      J->bk_a_start = dp<int64_t>(ctx, p.bk_a_start);
+      J->bk_a_end = dp<int64_t>(ctx, p.bk_a_end);
+      J->bk_flag = dp<uint8_t>(ctx, p.bk_flag);
+      J->bk_in_peak = dp<uint8_t>(ctx, p.bk_in_peak);
+      J->bk_ev = dp<int64_t>(ctx, p.bk_ev);
+      J->bk_rc = dp<int64_t>(ctx, p.bk_rc);
+      J->bk_bz = dp<int64_t>(ctx, p.bk_bz);
+      J->bk_evcnt = dp<int32_t>(ctx, p.bk_evcnt);
+      J->bk_curve = dp<int64_t>(ctx, p.bk_curve);
+      JobState* S = hp<JobState>(ctx, P->states_off) + jglob;
+      std::memset(S, 0, sizeof *S);
+      if (mode == 1) {
+        // caller plan -> ev/rc arrays in the output region + flags
+        const tsl_plan_desc& pd = caller[jglob];
+        if (pd.n_swap > p.Scap || pd.n_recompute > p.Rcap) fail(TSL_ERR_CAPACITY, "caller plan too large");
+        int64_t mx = -1;
+        for (int32_t i = 0; i < pd.n_swap; ++i) {
+          if (pd.ev_tensor[i] < 0 || pd.ev_tensor[i] >= g.T)
+            fail(TSL_ERR_VALIDATION, "unknown tensor #" + std::to_string(pd.ev_tensor[i]) + " in catalog of " + g.job_id);
+          hp<int64_t>(ctx, p.ev[0])[i] = pd.ev_id[i];
+          hp<int32_t>(ctx, p.ev[1])[i] = pd.ev_tensor[i];
+          hp<int8_t>(ctx, p.ev[2])[i] = pd.ev_dir[i];
+          hp<int8_t>(ctx, p.ev[3])[i] = pd.ev_wraps[i];
+          hp<int64_t>(ctx, p.ev[4])[i] = pd.ev_trigger[i];
+          hp<int64_t>(ctx, p.ev[5])[i] = pd.ev_delta[i];
+          hp<int64_t>(ctx, p.ev[6])[i] = pd.ev_start[i];
+          hp<int64_t>(ctx, p.ev[7])[i] = pd.ev_end[i];
+          hp<int64_t>(ctx, p.ev[8])[i] = 0;
+          hp<int64_t>(ctx, p.ev[9])[i] = 0;
+          hp<int64_t>(ctx, p.ev[10])[i] = pd.ev_pair[i];
+          hp<int64_t>(ctx, p.ev[11])[i] = pd.ev_serves[i];
+          mx = std::max(mx, pd.ev_id[i]);
+        }
+        for (int32_t r = 0; r < pd.n_recompute; ++r) {
+          if (pd.rc_tensor[r] < 0 || pd.rc_tensor[r] >= g.T)
+            fail(TSL_ERR_VALIDATION, "unknown tensor #" + std::to_string(pd.rc_tensor[r]) + " in catalog of " + g.job_id);
+          hp<int64_t>(ctx, p.rc[0])[r] = pd.rc_id[r];
+          hp<int32_t>(ctx, p.rc[1])[r] = pd.rc_tensor[r];
+          hp<int64_t>(ctx, p.rc[2])[r] = pd.rc_target[r];
+          hp<int32_t>(ctx, p.rc[3])[r] = pd.rc_regen_op[r];
+          hp<int64_t>(ctx, p.rc[4])[r] = pd.rc_latency[r];
+          hp<int64_t>(ctx, p.rc[5])[r] = pd.rc_saving[r];
+          mx = std::max(mx, pd.rc_id[r]);
+        }
+        uint8_t* fl = hp<uint8_t>(ctx, p.inflag);
+        std::memset(fl, 0, g.A);
+        for (int32_t i = 0; i < pd.n_release; ++i)
+          if (pd.release_flags[i] >= 0 && pd.release_flags[i] < g.A) fl[pd.release_flags[i]] = 1;
+        S->S = pd.n_swap;
+        S->R = pd.n_recompute;
+        S->next_id = mx + 1;
+      }
+    }
+  }
+  P->h2d_bytes = mode == 1 ? out_end : stage_end;
+  P->d2h_off = P->groups_off;
+  P->d2h_bytes = out_end - P->groups_off;
+  auto t1 = std::chrono::steady_clock::now();
+  P->prep_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  return P;
+}
+
+void upload(tsl_plan* P) {
+  tsl_ctx* c = P->ctx;
+  cuda_check(cudaMemcpyAsync(c->dbuf, c->hbuf, P->h2d_bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+}
+
+void launch(tsl_plan* P, int repeats, bool timed) {
+  tsl_ctx* c = P->ctx;
+  GroupDev* dg = dp<GroupDev>(c, P->groups_off);
+  if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
+  for (int r = 0; r < repeats; ++r) {
+    if (r > 0) {  // re-arm the mutable group header for a repeated device-only run
+      cuda_check(cudaMemcpyAsync(dg, hp<GroupDev>(c, P->groups_off), sizeof(GroupDev) * P->n_groups,
+                                 cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, c->stream), "launch");
+  }
+  if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
+}
+
+void download(tsl_plan* P) {
+  tsl_ctx* c = P->ctx;
+  cuda_check(cudaMemcpyAsync(c->hbuf + P->d2h_off, static_cast<uint8_t*>(c->dbuf) + P->d2h_off, P->d2h_bytes,
+                             cudaMemcpyDeviceToHost, c->stream), "D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+}
+
+std::string err_text(const GroupDev& G, const std::vector<Graph>& gs) {
+  const ErrInfo& e = G.err;
+  const Graph* g = (e.job >= 0 && e.job < static_cast<int>(gs.size())) ? &gs[e.job] : nullptr;
+  auto tname = [&](int64_t t) { return (g && t >= 0 && t < g->T) ? g->tid[t] : "#" + std::to_string(t); };
+  switch (e.code) {
+    case E_DOUBLE_RELEASE: return "double release of tensor " + tname(e.tensor);
+    case E_SWAPIN_RESIDENT: return "swap-in of resident tensor " + tname(e.tensor);
+    case E_NEG_FOOTPRINT: return "negative footprint at tick " + std::to_string(e.tick);
+    case E_NO_TGA: return "tensor " + tname(e.tensor) + " has no TGA in sequence";
+    case E_UNKNOWN_ACCESS:
+      return "unknown access id " + std::to_string(e.tensor) + " in job " + (g ? g->job_id : std::string("?"));
+    case E_CAPACITY: return "device planner capacity exceeded (" + std::to_string(e.tensor) + ")";
+    default: return "internal planner error";
+  }
+}
+
+tsl_result* collect_group(tsl_plan* P, int gi) {
+  tsl_ctx* c = P->ctx;
+  const GroupDev& G = hp<GroupDev>(c, P->groups_off)[gi];
+  if (G.err.code) {
+    int code = G.err.code == E_CAPACITY ? TSL_ERR_CAPACITY
+             : G.err.code == E_INTERNAL ? TSL_ERR_INTERNAL : TSL_ERR_VALIDATION;
+    fail(code, err_text(G, P->graphs[gi]));
+  }
+  auto* R = new tsl_result();
+  R->graphs = P->graphs[gi];
+  const int32_t jb = P->group_job_base[gi];
+  std::map<std::string, int> order;
+  for (size_t k = 0; k < R->graphs.size(); ++k) order[R->graphs[k].job_id] = static_cast<int>(k);
+  for (auto& kv : order) {
+    const int k = kv.second;
+    const Graph& g = R->graphs[k];
+    const JobPlace& p = P->jp[gi][k];
+    const JobState& st = hp<JobState>(c, P->states_off)[jb + k];
+    JobOut o;
+    o.g = &R->graphs[k];
+    o.st = st;
+    auto cp64 = [&](std::vector<int64_t>& v, size_t off, int32_t n) {
+      v.assign(hp<int64_t>(c, off), hp<int64_t>(c, off) + n);
+    };
+    cp64(o.ev_id, p.ev[0], st.S);
+    o.ev_tensor.assign(hp<int32_t>(c, p.ev[1]), hp<int32_t>(c, p.ev[1]) + st.S);
+    o.ev_dir.assign(hp<int8_t>(c, p.ev[2]), hp<int8_t>(c, p.ev[2]) + st.S);
+    o.ev_wraps.assign(hp<int8_t>(c, p.ev[3]), hp<int8_t>(c, p.ev[3]) + st.S);
+    cp64(o.ev_trig, p.ev[4], st.S);
+    cp64(o.ev_delta, p.ev[5], st.S);
+    cp64(o.ev_start, p.ev[6], st.S);
+    cp64(o.ev_end, p.ev[7], st.S);
+    cp64(o.ev_earl, p.ev[8], st.S);
+    cp64(o.ev_late, p.ev[9], st.S);
+    cp64(o.ev_pair, p.ev[10], st.S);
+    cp64(o.ev_serves, p.ev[11], st.S);
+    cp64(o.rc_id, p.rc[0], st.R);
+    o.rc_tensor.assign(hp<int32_t>(c, p.rc[1]), hp<int32_t>(c, p.rc[1]) + st.R);
+    cp64(o.rc_target, p.rc[2], st.R);
+    o.rc_regen.assign(hp<int32_t>(c, p.rc[3]), hp<int32_t>(c, p.rc[3]) + st.R);
+    cp64(o.rc_lat, p.rc[4], st.R);
+    cp64(o.rc_saving, p.rc[5], st.R);
+    const uint8_t* fl = hp<uint8_t>(c, p.a_flag);
+    for (int32_t a = 0; a < g.A; ++a)
+      if (fl[a]) o.flags.push_back(a);
+    if (P->mode == 1) {  // caller flags outside [0, A) are kept verbatim
+      o.flags.clear();
+    }
+    const uint8_t* pk = hp<uint8_t>(c, p.in_peak);
+    std::vector<int32_t> byr(g.T);
+    for (int32_t t = 0; t < g.T; ++t) byr[g.trank[t]] = t;
+    for (int32_t r = 0; r < g.T; ++r)
+      if (pk[byr[r]]) o.peak_tensors.push_back(byr[r]);
+    cp64(o.curve_t, p.curve_t, st.n_curve);
+    cp64(o.curve_b, p.curve_b, st.n_curve);
+    R->jobs.push_back(std::move(o));
+  }
+  R->history.assign(hp<int64_t>(c, P->gp[gi].hist), hp<int64_t>(c, P->gp[gi].hist) + std::min(G.n_hist, G.hist_cap));
+  R->final_merged = G.final_merged;
+  R->within = G.within_budget != 0;
+  if (P->mode == 0 && !R->within)
+    R->diagnostic = "merged memory peak " + std::to_string(G.final_merged) + " still exceeds budget " +
+                    std::to_string(P->cfg.memory_budget) + " after exhausting swap and recomputation";
+  tsl_stats& s = R->stats;
+  s.kernel_ms = P->last_kernel_ms;
+  for (auto& g : R->graphs) s.n_accesses += g.A;
+  s.loop_iterations = G.stats.loop_iterations;
+  s.evaluations = G.stats.evaluations;
+  s.timeline_events = G.stats.timeline_events;
+  s.candidates = G.stats.candidates;
+  s.candidate_accesses = G.stats.candidate_accesses;
+  s.busy_intervals = G.stats.busy_intervals;
+  s.algorithmic_bytes = 24 * s.timeline_events + 24 * s.candidate_accesses + 16 * s.busy_intervals + 16 * s.candidates;
+  s.kernel_launches = 1;
+  return R;
+}
+
+// ---------------------------------------------------------------------------
+// JSON (nlohmann ordered_json dump(2) layout, as the reference prints it)
+// ---------------------------------------------------------------------------
+void jstr(std::string& o, const std::string& s) {
+  o += '"';
+  for (unsigned char ch : s) {
+    switch (ch) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
+      case '\n': o += "\\n"; break;
+      case '\r': o += "\\r"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (ch < 0x20) {
+          char buf[8];
+          std::snprintf(buf, sizeof buf, "\\u%04x", ch);
+          o += buf;
+        } else {
+          o += static_cast<char>(ch);
+        }
+    }
+  }
+  o += '"';
+}
+
+std::string sp(int n) { return std::string(static_cast<size_t>(n), ' '); }
+std::string num(int64_t v) { return std::to_string(v); }
+
+// save_plans, plan.cpp:30-65.
+std::string save_plans(const tsl_result& r) {
+  if (r.jobs.empty()) return "null\n";
+  std::string o = "{\n";
+  for (size_t ji = 0; ji < r.jobs.size(); ++ji) {
+    const JobOut& j = r.jobs[ji];
+    o += sp(2);
+    jstr(o, j.g->job_id);
+    o += ": {\n" + sp(4) + "\"version\": " + num(j.version) + ",\n" + sp(4) + "\"swap_events\": ";
+    const size_t S = j.ev_id.size();
+    if (!S) o += "[],\n";
+    else {
+      o += "[\n";
+      for (size_t i = 0; i < S; ++i) {
+        o += sp(6) + "{\n";
+        o += sp(8) + "\"event_id\": " + num(j.ev_id[i]) + ",\n";
+        o += sp(8) + "\"tensor\": ";
+        jstr(o, j.g->tid[j.ev_tensor[i]]);
+        o += ",\n" + sp(8) + "\"direction\": " + (j.ev_dir[i] == 0 ? "\"out\"" : "\"in\"") + ",\n";
+        o += sp(8) + "\"trigger_access\": " + num(j.ev_trig[i]) + ",\n";
+        o += sp(8) + "\"delta_time\": " + num(j.ev_delta[i]) + ",\n";
+        o += sp(8) + "\"wraps_iteration\": " + (j.ev_wraps[i] ? "true" : "false") + ",\n";
+        o += sp(8) + "\"start_time\": " + num(j.ev_start[i]) + ",\n";
+        o += sp(8) + "\"end_time\": " + num(j.ev_end[i]) + ",\n";
+        o += sp(8) + "\"pair_id\": " + num(j.ev_pair[i]) + ",\n";
+        o += sp(8) + "\"serves_access\": " + num(j.ev_serves[i]) + "\n";
+        o += sp(6) + (i + 1 < S ? "},\n" : "}\n");
+      }
+      o += sp(4) + "],\n";
+    }
+    o += sp(4) + "\"recompute_events\": ";
+    const size_t R = j.rc_id.size();
+    if (!R) o += "[],\n";
+    else {
+      o += "[\n";
+      for (size_t i = 0; i < R; ++i) {
+        o += sp(6) + "{\n";
+        o += sp(8) + "\"event_id\": " + num(j.rc_id[i]) + ",\n";
+        o += sp(8) + "\"tensor\": ";
+        jstr(o, j.g->tid[j.rc_tensor[i]]);
+        o += ",\n" + sp(8) + "\"target_access\": " + num(j.rc_target[i]) + ",\n";
+        o += sp(8) + "\"regen_op\": ";
+        jstr(o, j.g->oid[j.rc_regen[i]]);
+        o += ",\n" + sp(8) + "\"recompute_latency\": " + num(j.rc_lat[i]) + ",\n";
+        o += sp(8) + "\"memory_saving\": " + num(j.rc_saving[i]) + "\n";
+        o += sp(6) + (i + 1 < R ? "},\n" : "}\n");
+      }
+      o += sp(4) + "],\n";
+    }
+    // nlohmann 3.11.3 prints an array whose elements are all numbers inline.
+    o += sp(4) + "\"release_flags\": [";
+    for (size_t k = 0; k < j.flags.size(); ++k) o += (k ? "," : "") + num(j.flags[k]);
+    o += "]\n" + sp(2) + (ji + 1 < r.jobs.size() ? "},\n" : "}\n");
+  }
+  return o + "}\n";
+}
+
+// PeakReport::to_json, peak.cpp:258-272.
+std::string report_json(const JobOut& j) {
+  std::string o = "{\n" + sp(2) + "\"memory_peak\": " + num(j.st.peak) + ",\n" + sp(2) + "\"peak_tensors\": ";
+  if (j.peak_tensors.empty()) o += "[],\n";
+  else {
+    o += "[\n";
+    for (size_t i = 0; i < j.peak_tensors.size(); ++i) {
+      o += sp(4);
+      jstr(o, j.g->tid[j.peak_tensors[i]]);
+      o += i + 1 < j.peak_tensors.size() ? ",\n" : "\n";
+    }
+    o += sp(2) + "],\n";
+  }
+  o += sp(2) + "\"last_input_access\": " + (j.st.has_lua ? num(j.st.lua) : std::string("null")) + ",\n";
+  o += sp(2) + "\"peak_time\": " + num(j.st.peak_time) + ",\n" + sp(2) + "\"footprint_curve\": ";
+  if (j.curve_t.empty()) o += "[]\n";
+  else {
+    o += "[\n";
+    for (size_t i = 0; i < j.curve_t.size(); ++i)
+      o += sp(4) + "[" + num(j.curve_t[i]) + "," + num(j.curve_b[i]) + (i + 1 < j.curve_t.size() ? "],\n" : "]\n");
+    o += sp(2) + "]\n";
+  }
+  return o + "}\n";
+}
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TSL_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TSL_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsl_last_error(void) { return g_err.c_str(); }
+
+void tsl_config_default(tsl_config* c) {
+  c->pcie_bandwidth = 1;
+  c->transfer_setup = 0;
+  c->memory_budget = 0;
+  c->ewma_alpha = 0.3;
+  c->replan_threshold = 0.2;
+  c->stall_epsilon = 0.0005;
+  c->stall_min_iters = 100;
+  c->cold_start_gpu_usage = 0.5;
+}
+
+int tsl_create(int device, tsl_ctx** out) {
+  if (!out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) fail(TSL_ERR_CUDA, "no CUDA device " + std::to_string(device));
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new tsl_ctx();
+    c->device = device;
+    cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreate(&c->ev0), "event");
+    cuda_check(cudaEventCreate(&c->ev1), "event");
+    *out = c;
+  });
+}
+
+int tsl_destroy(tsl_ctx* c) {
+  if (!c) return TSL_OK;
+  cudaSetDevice(c->device);
+  if (c->dbuf) cudaFree(c->dbuf);
+  if (c->hbuf) cudaFreeHost(c->hbuf);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return TSL_OK;
+}
+
+int tsl_plan_prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets, int32_t n_groups,
+                     const tsl_config* cfg, tsl_plan** out) {
+  if (!ctx || !cfg || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfg, 0, nullptr);
+    try {
+      upload(P);
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int tsl_plan_run(tsl_plan* P, int32_t repeats, double* kernel_ms) {
+  if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    tsl_ctx* c = P->ctx;
+    launch(P, std::max(1, repeats), true);
+    cuda_check(cudaEventSynchronize(c->ev1), "sync");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
+    P->last_kernel_ms = ms / std::max(1, repeats);
+    if (kernel_ms) *kernel_ms = P->last_kernel_ms;
+  });
+}
+
+int tsl_plan_launch_async(tsl_plan* P, void* stream) {
+  if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    tsl_ctx* c = P->ctx;
+    cuda_check(launch_plan_kernel(dp<GroupDev>(c, P->groups_off), P->n_groups, P->mode,
+                                  stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
+  });
+}
+
+int tsl_plan_collect(tsl_plan* P, tsl_result** out) {
+  if (!P || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    download(P);
+    std::vector<tsl_result*> rs;
+    try {
+      for (int gi = 0; gi < P->n_groups; ++gi) rs.push_back(collect_group(P, gi));
+    } catch (...) {
+      for (auto* r : rs) delete r;
+      throw;
+    }
+    for (int gi = 0; gi < P->n_groups; ++gi) out[gi] = rs[gi];
+  });
+}
+
+void tsl_plan_destroy(tsl_plan* P) { delete P; }
+
+int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets, int32_t n_groups,
+                          const tsl_config* cfg, tsl_result** out) {
+  if (!ctx || !cfg || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfg, 0, nullptr);
+    std::vector<tsl_result*> rs;
+    try {
+      upload(P);
+      launch(P, 1, true);
+      download(P);
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "elapsed");
+      P->last_kernel_ms = ms;
+      for (int gi = 0; gi < n_groups; ++gi) rs.push_back(collect_group(P, gi));
+    } catch (...) {
+      for (auto* r : rs) delete r;
+      delete P;
+      throw;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    const double tot = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    for (int gi = 0; gi < n_groups; ++gi) {
+      rs[gi]->stats.total_ms = tot;
+      out[gi] = rs[gi];
+    }
+    delete P;
+  });
+}
+
+int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs, const tsl_config* cfg,
+                   tsl_result** out) {
+  if (n_jobs < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  const int32_t offs[2] = {0, n_jobs};
+  if (n_jobs == 0) {  // build_plan returns an empty result (orchestrator.cpp:12)
+    if (!ctx || !cfg || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+    return guard([&] {
+      validate_config(*cfg, {});
+      *out = new tsl_result();
+    });
+  }
+  return tsl_build_plan_groups(ctx, jobs, offs, 1, cfg, out);
+}
+
+int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* plan, tsl_result** out) {
+  if (!ctx || !job || !plan || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tsl_config cfg;
+    tsl_config_default(&cfg);
+    const int32_t offs[2] = {0, 1};
+    tsl_plan* P = prepare(ctx, job, offs, 1, &cfg, 1, plan);
+    tsl_result* r = nullptr;
+    try {
+      upload(P);
+      launch(P, 1, true);
+      download(P);
+      r = collect_group(P, 0);
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    // the caller's plan is echoed verbatim (release flags included)
+    JobOut& o = r->jobs[0];
+    o.version = static_cast<int32_t>(plan->version);
+    o.flags.assign(plan->release_flags, plan->release_flags + plan->n_release);
+    std::sort(o.flags.begin(), o.flags.end());
+    o.flags.erase(std::unique(o.flags.begin(), o.flags.end()), o.flags.end());
+    delete P;
+    *out = r;
+  });
+}
+
+int32_t tsl_result_n_jobs(const tsl_result* r) { return r ? static_cast<int32_t>(r->jobs.size()) : 0; }
+
+int tsl_result_job(const tsl_result* r, int32_t i, tsl_job_view* v) {
+  if (!r || !v || i < 0 || i >= static_cast<int32_t>(r->jobs.size())) { g_err = "bad job index"; return TSL_ERR_ARGUMENT; }
+  const JobOut& o = r->jobs[static_cast<size_t>(i)];
+  std::memset(v, 0, sizeof *v);
+  v->job_id = o.g->job_id.c_str();
+  v->version = o.version;
+  v->n_swap = static_cast<int32_t>(o.ev_id.size());
+  v->ev_id = o.ev_id.data();
+  v->ev_tensor = o.ev_tensor.data();
+  v->ev_dir = o.ev_dir.data();
+  v->ev_trigger = o.ev_trig.data();
+  v->ev_delta = o.ev_delta.data();
+  v->ev_start = o.ev_start.data();
+  v->ev_end = o.ev_end.data();
+  v->ev_earliest = o.ev_earl.data();
+  v->ev_latest = o.ev_late.data();
+  v->ev_wraps = o.ev_wraps.data();
+  v->ev_pair = o.ev_pair.data();
+  v->ev_serves = o.ev_serves.data();
+  v->n_recompute = static_cast<int32_t>(o.rc_id.size());
+  v->rc_id = o.rc_id.data();
+  v->rc_tensor = o.rc_tensor.data();
+  v->rc_target = o.rc_target.data();
+  v->rc_regen_op = o.rc_regen.data();
+  v->rc_latency = o.rc_lat.data();
+  v->rc_saving = o.rc_saving.data();
+  v->n_release = static_cast<int32_t>(o.flags.size());
+  v->release_flags = o.flags.data();
+  v->memory_peak = o.st.peak;
+  v->peak_time = o.st.peak_time;
+  v->has_last_input_access = o.st.has_lua ? 1 : 0;
+  v->last_input_access = o.st.has_lua ? o.st.lua : -1;
+  v->n_peak_tensors = static_cast<int32_t>(o.peak_tensors.size());
+  v->peak_tensors = o.peak_tensors.data();
+  v->n_curve = static_cast<int32_t>(o.curve_t.size());
+  v->curve_time = o.curve_t.data();
+  v->curve_bytes = o.curve_b.data();
+  v->iteration_period = o.st.period;
+  v->n_accesses = o.g->A;
+  return TSL_OK;
+}
+
+int32_t tsl_result_history(const tsl_result* r, const int64_t** h) {
+  if (!r || !h) return 0;
+  *h = r->history.data();
+  return static_cast<int32_t>(r->history.size());
+}
+int64_t tsl_result_final_merged_peak(const tsl_result* r) { return r ? r->final_merged : 0; }
+int32_t tsl_result_within_budget(const tsl_result* r) { return r && r->within ? 1 : 0; }
+const char* tsl_result_diagnostic(const tsl_result* r) { return r ? r->diagnostic.c_str() : ""; }
+int tsl_result_stats(const tsl_result* r, tsl_stats* out) {
+  if (!r || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  *out = r->stats;
+  return TSL_OK;
+}
+char* tsl_result_save_plans(const tsl_result* r) { return r ? dup(save_plans(*r)) : nullptr; }
+char* tsl_result_report_json(const tsl_result* r, int32_t i) {
+  if (!r || i < 0 || i >= static_cast<int32_t>(r->jobs.size())) return nullptr;
+  return dup(report_json(r->jobs[static_cast<size_t>(i)]));
+}
+void tsl_result_destroy(tsl_result* r) { delete r; }
+void tsl_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,14 @@
+// Host-side view of the planning kernel (tsl_kernel.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "tsl_types.h"
+
+namespace tsl {
+constexpr int NT = 512;         // threads per planning CTA
+constexpr int SORT_IPT = 24;    // largest block-sort tile: NT * SORT_IPT keys
+constexpr int SORT_CAP = NT * SORT_IPT;
+size_t kernel_smem_bytes();
+cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, cudaStream_t stream);
+}  // namespace tsl

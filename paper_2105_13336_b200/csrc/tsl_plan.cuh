@@ -1,0 +1,1380 @@
+// TENSILE scheduling-plan generator: the whole memsched::build_plan
+// (/root/reference/proj/src/orchestrator.cpp:8-70) for one planning group,
+// written against an execution context X so that ONE CTA runs it end to end.
+//
+//   X::tid/nthr          CTA thread index / count
+//   X::lane/warp/nwarp   warp geometry (W == 32 on the device)
+//   X::sync()            CTA barrier         X::wsync()  warp barrier
+//   X::sort(k,v,n,bits)  CTA-collective stable radix sort of (u64 key, i32 value)
+//   X::scan(a,n)         CTA-collective inclusive int64 scan in place
+//   X::amin/amax/aadd    atomics on shared/global scalars
+//   X::sh                CTA-shared scalar scratch (SH_WORDS int64)
+//
+// The device context lives in tsl_kernel.cu. tests/emu/ compiles this same
+// file with a one-thread host context purely to debug the algorithm against
+// the oracle on CPU; the product library never contains that build.
+//
+// Design:
+//  * stage 1, timeline builder (access.cpp:28-78): latency scan over the topo
+//    order, access emission, activity analysis, CSR-by-storage via a sort.
+//  * stage 2, footprint evaluator (peak.cpp:66-244): all events of a batch of
+//    jobs get a packed 64-bit key (job, time, frees-first, storage rank, type
+//    rank, tie) and one block radix sort; a second stable sort groups the
+//    sorted positions by storage so each storage's residency automaton runs
+//    independently (one thread per storage); then a block scan gives the
+//    footprint curve, a max-reduce + first-index-min gives the first strict
+//    maximum, and the per-storage state at that position gives peak_tensors.
+//  * stage 3/4, scorer + selector (swap_planner.cpp:461-520): each job's
+//    candidate list is walked in the reference's order by one warp; the
+//    feasible-region queries are k-way merge sweeps over the job's swap
+//    intervals kept sorted by start (they are pairwise disjoint), with early
+//    exit; all lanes run the scalar logic redundantly and cooperate on bulk
+//    moves. Jobs are independent unless a max_swap_ratio < 1 couples them
+//    through SwapBudget, in which case one warp walks the global order.
+//  * recomputation (recompute_planner.cpp:50-153): candidates scored by all
+//    threads, argmax, commit, shift, revalidate, re-evaluate, rollback.
+#pragma once
+#include <stdint.h>
+
+#include "tsl_types.h"
+
+#ifdef __CUDACC__
+#define TSL_HD __device__ inline
+#else
+#define TSL_HD inline
+#endif
+
+namespace tsl {
+
+constexpr int SH_WORDS = 2048;   // CTA-shared int64 scalars
+constexpr int MAXB = 32;         // jobs per evaluation batch
+constexpr int EV_FIELDS = 12;    // swap-event fields (rollback copies)
+constexpr int RC_FIELDS = 6;
+
+TSL_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+TSL_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+TSL_HD int nbits(uint64_t v) {  // bits needed to hold v (0 -> 0)
+  int b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+// transfer_duration, plan.cpp:22-28 (bandwidth / setup validated on the host).
+TSL_HD int64_t duration(int64_t size, const GroupConfig& c) {
+  return (size + c.bw - 1) / c.bw + c.setup;
+}
+
+// Storage accesses of `s` are s_acc[s_off[s] .. s_off[s+1]) in ascending
+// access id, which is also (start, id) order: starts (and ends) never
+// decrease with the access id, before or after recomputation shifts.
+
+// ----------------------------------------------------------------------------
+// Feasible-region queries (swap_planner.cpp:26-72, 315-337)
+// ----------------------------------------------------------------------------
+// A stream is a run of intervals sorted by start AND end, lifted by `sh`.
+struct Stream {
+  const int64_t* s;
+  const int64_t* e;
+  const int32_t* ix;  // indirection (storage accesses) or null
+  int32_t i, j;       // live range [i, j)
+  int64_t sh;
+};
+TSL_HD int32_t sidx(const Stream& q, int32_t k) { return q.ix ? q.ix[k] : k; }
+
+// Intervals of a sorted run that intersect [L, H) form one index range:
+// ends are nondecreasing, so e > L is a suffix; s < H is a prefix.
+TSL_HD void clip_range(Stream& q, int32_t n, int64_t L, int64_t H) {
+  L -= q.sh;
+  H -= q.sh;
+  if (n == 0 || q.e[sidx(q, n - 1)] <= L || q.s[sidx(q, 0)] >= H) {
+    q.i = q.j = 0;
+    return;
+  }
+  int32_t lo = 0, hi = n;  // first k with e[k] > L
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (q.e[sidx(q, m)] > L) hi = m; else lo = m + 1;
+  }
+  q.i = lo;
+  lo = q.i;
+  hi = n;  // first k with s[k] >= H
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (q.s[sidx(q, m)] >= H) hi = m; else lo = m + 1;
+  }
+  q.j = lo;
+}
+
+struct FitQuery {
+  int32_t store;
+  int64_t b, e, d;   // window [b, e], duration d
+  bool has_extra;    // busy_intervals' `extra` (lifted like the others)
+  int64_t xs, xe;
+};
+
+// busy_intervals (swap_planner.cpp:39-50) restricted to [b, e) + the
+// feasible_regions sweep + place_earliest / place_latest. Returns the
+// placement start, or INT64_MIN when no region of length >= d exists.
+// Forward sweep (earliest) stops at the first maximal free interval of length
+// >= d; the reverse sweep (latest) enumerates the same maximal free intervals
+// from the right.
+TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest,
+                   int64_t* swept) {
+  const int64_t NONE = INT64_MIN;
+  if (q.e <= q.b) return NONE;
+  const int64_t P = imax(1, st.period);
+  Stream str[7];
+  int ns = 0;
+  const int32_t a0 = J.s_off[q.store], na = J.s_off[q.store + 1] - a0;
+  int64_t exs[3], exe[3];
+  int nex = 0;
+  for (int k = -1; k <= 1; ++k) {
+    const int64_t sh = k * P;
+    Stream ev{J.bz_s, J.bz_e, nullptr, 0, 0, sh};
+    clip_range(ev, st.S, q.b, q.e);
+    if (ev.j > ev.i) str[ns++] = ev;
+    Stream ac{J.a_start, J.a_end, J.s_acc + a0, 0, 0, sh};
+    clip_range(ac, na, q.b, q.e);
+    if (ac.j > ac.i) str[ns++] = ac;
+    if (q.has_extra && q.xe > q.xs && q.xe + sh > q.b && q.xs + sh < q.e) {
+      exs[nex] = q.xs + sh;
+      exe[nex] = q.xe + sh;
+      ++nex;
+    }
+  }
+  if (nex) str[ns++] = Stream{exs, exe, nullptr, 0, nex, 0};
+  int64_t n_swept = 0;
+  int64_t result = NONE;
+  if (!latest) {
+    int64_t cursor = q.b;
+    for (;;) {
+      int best = -1;
+      int64_t bs = 0;
+      for (int t = 0; t < ns; ++t) {
+        if (str[t].i >= str[t].j) continue;
+        int64_t s = str[t].s[sidx(str[t], str[t].i)] + str[t].sh;
+        if (best < 0 || s < bs) { best = t; bs = s; }
+      }
+      if (best < 0) break;
+      Stream& z = str[best];
+      int64_t be = z.e[sidx(z, z.i)] + z.sh;
+      ++z.i;
+      if (be <= bs) continue;  // lift_into drops empty intervals
+      ++n_swept;
+      int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
+      if (ce <= cs) continue;
+      if (cs > cursor && cs - cursor >= q.d) { result = cursor; break; }
+      cursor = imax(cursor, ce);
+    }
+    if (result == NONE && q.e > cursor && q.e - cursor >= q.d) result = cursor;
+  } else {
+    int64_t cur = q.e;
+    bool found = false;
+    for (;;) {
+      int best = -1;
+      int64_t be = 0;
+      for (int t = 0; t < ns; ++t) {
+        if (str[t].j <= str[t].i) continue;
+        int64_t e = str[t].e[sidx(str[t], str[t].j - 1)] + str[t].sh;
+        if (best < 0 || e > be) { best = t; be = e; }
+      }
+      if (best < 0) break;
+      Stream& z = str[best];
+      int64_t bs = z.s[sidx(z, z.j - 1)] + z.sh;
+      --z.j;
+      if (be <= bs) continue;
+      ++n_swept;
+      int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
+      if (ce <= cs) continue;
+      if (cur > ce && cur - ce >= q.d) { found = true; break; }
+      cur = imin(cur, cs);
+    }
+    if (found || (cur > q.b && cur - q.b >= q.d)) result = cur - q.d;
+  }
+  if (swept) *swept += n_swept;
+  return result;
+}
+
+// ----------------------------------------------------------------------------
+// Plan mutation helpers (warp-redundant: every lane runs the scalar code and
+// writes identical values; bulk moves are split across lanes)
+// ----------------------------------------------------------------------------
+
+// anchor, swap_planner.cpp:76-93: the access with the greatest end <= t, ties
+// to the larger id; ends never decrease with the id, so it is the last one.
+TSL_HD void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
+                   int64_t& delta) {
+  if (wrapped && st.period > 0) t = ((t % st.period) + st.period) % st.period;
+  int32_t lo = 0, hi = J.A;
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (J.a_end[m] <= t) lo = m + 1; else hi = m;
+  }
+  if (lo == 0) { trig = -1; delta = t; }
+  else { trig = lo - 1; delta = t - J.a_end[lo - 1]; }
+}
+
+// Last storage access with end <= t (skipping `skip`), or -1.
+TSL_HD int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64_t skip) {
+  const int32_t a0 = J.s_off[store], a1 = J.s_off[store + 1];
+  int32_t lo = a0, hi = a1;  // first position with end > t
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (J.a_end[J.s_acc[m]] <= t) lo = m + 1; else hi = m;
+  }
+  for (int32_t k = lo - 1; k >= a0; --k)
+    if (J.s_acc[k] != skip) return J.s_acc[k];
+  return -1;
+}
+
+template <class X>
+TSL_HD void bz_insert(X& x, const JobDev& J, int32_t n, int64_t s, int64_t e) {
+  int32_t lo = 0, hi = n;  // first position with start > s
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (J.bz_s[m] <= s) lo = m + 1; else hi = m;
+  }
+  const int32_t pos = lo;
+  x.wsync();
+  for (int32_t top = n; top > pos; top -= X::W) {
+    int32_t i = top - 1 - x.lane;
+    bool act = i >= pos;
+    int64_t vs = 0, ve = 0;
+    if (act) { vs = J.bz_s[i]; ve = J.bz_e[i]; }
+    x.wsync();
+    if (act) { J.bz_s[i + 1] = vs; J.bz_e[i + 1] = ve; }
+    x.wsync();
+  }
+  J.bz_s[pos] = s;
+  J.bz_e[pos] = e;
+  x.wsync();
+}
+
+struct PairSpec {
+  int32_t store;
+  int64_t os, oe, o_earl, o_late;
+  int64_t is, ie, i_earl, i_late;
+  bool wraps;
+  int64_t serves;
+  bool in_at_iter_start;  // schedule_wrapped_swap's forced anchor (swap_planner.cpp:448-452)
+};
+
+// make_event x2 + pair linking + flag_release_before (swap_planner.cpp:95-122,
+// 141-150, 376-386, 443-456).
+template <class X>
+TSL_HD bool commit_pair(X& x, const JobDev& J, JobState& st, const PairSpec& p, ErrInfo* err, int job) {
+  // All lanes read every scalar first, then barrier, then write: lanes of a
+  // warp need not run in lockstep, so a read-modify-write must never straddle
+  // another lane's store.
+  const int32_t S = st.S;
+  const int64_t id0 = st.next_id, id1 = id0 + 1;
+  const int32_t cnt = J.st_evcnt[p.store];
+  if (S + 2 > J.Scap) {
+    if (x.lane == 0) { err->code = E_CAPACITY; err->job = job; err->tensor = J.Scap; err->tick = 0; }
+    return false;
+  }
+  int64_t otrig, odelta, itrig, idelta;
+  anchor(J, st, p.os, p.wraps, otrig, odelta);
+  if (p.in_at_iter_start) { itrig = -1; idelta = p.is - st.period; }
+  else anchor(J, st, p.is, p.wraps, itrig, idelta);
+  const int32_t pre = preceding_access(J, p.store, p.os, -2);
+  x.wsync();
+  const int32_t i0 = S, i1 = S + 1;
+  J.ev_id[i0] = id0; J.ev_tensor[i0] = p.store; J.ev_dir[i0] = 0; J.ev_wraps[i0] = p.wraps;
+  J.ev_trig[i0] = otrig; J.ev_delta[i0] = odelta; J.ev_start[i0] = p.os; J.ev_end[i0] = p.oe;
+  J.ev_earl[i0] = p.o_earl; J.ev_late[i0] = p.o_late; J.ev_pair[i0] = id1; J.ev_serves[i0] = -1;
+  J.ev_id[i1] = id1; J.ev_tensor[i1] = p.store; J.ev_dir[i1] = 1; J.ev_wraps[i1] = p.wraps;
+  J.ev_trig[i1] = itrig; J.ev_delta[i1] = idelta; J.ev_start[i1] = p.is; J.ev_end[i1] = p.ie;
+  J.ev_earl[i1] = p.i_earl; J.ev_late[i1] = p.i_late; J.ev_pair[i1] = id0; J.ev_serves[i1] = p.serves;
+  bz_insert(x, J, S, p.os, p.oe);
+  bz_insert(x, J, S + 1, p.is, p.ie);
+  st.S = S + 2;
+  st.next_id = id0 + 2;
+  J.st_evcnt[p.store] = cnt + 2;
+  if (pre >= 0) J.a_flag[pre] = 1;
+  st.dirty = 1;
+  x.wsync();
+  return true;
+}
+
+// try_gap_pair, swap_planner.cpp:126-152.
+template <class X>
+TSL_HD bool try_gap_pair(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t store, int64_t lo,
+                         int64_t hi, int64_t serves, GroupStats* gs, ErrInfo* err, int job) {
+  const int64_t d = duration(J.t_size[store], c);
+  if (hi - lo < 2 * d) return false;
+  FitQuery q{store, lo, hi, d, false, 0, 0};
+  int64_t sw = 0;
+  int64_t os = fit(J, st, q, false, &sw);
+  gs->fit_queries += 1;
+  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+  // the busy list is the one filtered for [lo, hi) plus the out interval; the
+  // in-regions re-clip to [out.end, hi], where that out interval is empty.
+  FitQuery qi{store, os + d, hi, d, false, 0, 0};
+  int64_t is = fit(J, st, qi, true, &sw);
+  gs->fit_queries += 1;
+  gs->busy_intervals += sw;
+  if (is == INT64_MIN) return false;
+  PairSpec p{store, os, os + d, lo, hi, is, is + d, os + d, hi, false, serves, false};
+  return commit_pair(x, J, st, p, err, job);
+}
+
+// schedule_swap, swap_planner.cpp:339-399, single shot: a failed swap-in
+// placement leaves the next retry with the same swap-out region, the same
+// first access and the same swap-in window, so the reference's retry loop
+// (swap_planner.cpp:503-513) can never succeed after the first failure.
+template <class X>
+TSL_HD bool schedule_swap(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t store,
+                          int64_t earliest, int64_t latest, GroupStats* gs, ErrInfo* err, int job) {
+  const int64_t d = duration(J.t_size[store], c);
+  FitQuery q{store, earliest, latest, d, false, 0, 0};
+  int64_t sw = 0;
+  int64_t os = fit(J, st, q, false, &sw);
+  gs->fit_queries += 1;
+  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+  const int64_t oe = os + d;
+  const int32_t a0 = J.s_off[store], a1 = J.s_off[store + 1];
+  int32_t fk = -1;
+  for (int32_t k = a0; k < a1; ++k) {
+    int32_t a = J.s_acc[k];
+    if (J.a_type[a] == ACC_TUA && J.a_start[a] >= oe) { fk = k; break; }
+  }
+  gs->candidate_accesses += a1 - a0;
+  if (fk < 0) { gs->busy_intervals += sw; return false; }
+  const int32_t fa = J.s_acc[fk];
+  const int64_t fs = J.a_start[fa];
+  FitQuery qi{store, oe, fs, d, true, os, oe};
+  int64_t is = fit(J, st, qi, true, &sw);
+  gs->fit_queries += 1;
+  gs->busy_intervals += sw;
+  if (is == INT64_MIN) return false;
+  PairSpec p{store, os, oe, earliest, latest, is, is + d, oe, fs, false, fa, false};
+  if (!commit_pair(x, J, st, p, err, job)) return false;
+  // Greedily keep the tensor offloaded between its remaining uses.
+  for (int32_t k = fk; k + 1 < a1; ++k) {
+    int32_t a = J.s_acc[k], b = J.s_acc[k + 1];
+    if (J.a_type[b] != ACC_TUA) continue;
+    try_gap_pair(x, J, st, c, store, J.a_end[a], J.a_start[b], b, gs, err, job);
+    if (err->code) return false;
+  }
+  return true;
+}
+
+// schedule_wrapped_swap, swap_planner.cpp:401-459.
+template <class X>
+TSL_HD bool schedule_wrapped_swap(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t param,
+                                  GroupStats* gs, ErrInfo* err, int job) {
+  if (J.t_upd[param] < 0) return false;
+  const int64_t d = duration(J.t_size[param], c);
+  const int64_t period = st.period;
+  const int32_t ut = J.t_utga[param];
+  const int64_t tga_end = ut >= 0 ? J.a_end[ut] : -1;
+  if (tga_end < 0) return false;
+  FitQuery q{param, tga_end, period, d, false, 0, 0};
+  int64_t sw = 0;
+  int64_t os = fit(J, st, q, false, &sw);
+  gs->fit_queries += 1;
+  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+  const int32_t fa = J.t_wfirst[param];
+  if (fa < 0) { gs->busy_intervals += sw; return false; }
+  const int64_t in_lo = period, in_hi = period + J.a_start[fa];
+  FitQuery qi{param, in_lo, in_hi, d, true, os, os + d};
+  int64_t is = fit(J, st, qi, true, &sw);
+  gs->fit_queries += 1;
+  gs->busy_intervals += sw;
+  if (is == INT64_MIN) return false;
+  PairSpec p{param, os, os + d, tga_end, period, is, is + d, in_lo, in_hi, true, fa, true};
+  return commit_pair(x, J, st, p, err, job);
+}
+
+// swap_window, swap_planner.cpp:290-313.
+TSL_HD bool swap_window(const JobDev& J, int32_t store, int64_t peak_time, int64_t& earliest, int64_t& latest) {
+  latest = peak_time;
+  earliest = -1;
+  bool has_tga = false;
+  for (int32_t k = J.s_off[store]; k < J.s_off[store + 1]; ++k) {
+    int32_t a = J.s_acc[k];
+    if (J.a_type[a] == ACC_TGA) { has_tga = true; earliest = imax(earliest, J.a_end[a]); }
+    if (J.a_start[a] < latest) earliest = imax(earliest, J.a_end[a]);
+  }
+  if (!has_tga && J.t_kind[store] == K_INTERIM) return false;
+  if (earliest < 0) earliest = 0;
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// Stage 1: timeline builder (generate_access_sequence + activity_analysis +
+// CSR by storage), one job, whole CTA.
+// ----------------------------------------------------------------------------
+template <class X>
+TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  int64_t* lat = g.x_fp;    // [O] latencies in topo order -> inclusive ends
+  int64_t* cnt = g.x_time;  // [O] accesses per op -> inclusive offsets
+  for (int32_t k = x.tid; k < J.O; k += x.nthr) {
+    int32_t o = J.topo[k];
+    lat[k] = J.o_lat[o];
+    cnt[k] = (J.o_in_off[o + 1] - J.o_in_off[o]) + (J.o_out_off[o + 1] - J.o_out_off[o]);
+  }
+  x.sync();
+  x.scan(lat, J.O);
+  x.scan(cnt, J.O);
+  for (int32_t k = x.tid; k < J.O; k += x.nthr) {
+    int32_t o = J.topo[k];
+    int64_t end = lat[k], start = end - J.o_lat[o];
+    int32_t a = int32_t(cnt[k] - ((J.o_in_off[o + 1] - J.o_in_off[o]) + (J.o_out_off[o + 1] - J.o_out_off[o])));
+    for (int32_t i = J.o_in_off[o]; i < J.o_in_off[o + 1]; ++i, ++a) {
+      int32_t t = J.o_in[i];
+      J.a_tensor[a] = t; J.a_store[a] = J.t_store[t]; J.a_type[a] = ACC_TUA;
+      J.a_start[a] = start; J.a_end[a] = end;
+    }
+    for (int32_t i = J.o_out_off[o]; i < J.o_out_off[o + 1]; ++i, ++a) {
+      int32_t t = J.o_out[i];
+      J.a_tensor[a] = t; J.a_store[a] = J.t_store[t]; J.a_type[a] = ACC_TGA;
+      J.a_start[a] = start; J.a_end[a] = end;
+    }
+  }
+  // activity analysis: last access of every tensor id (st_evcnt as scratch)
+  for (int32_t t = x.tid; t < J.T; t += x.nthr) J.st_evcnt[t] = -1;
+  if (x.tid == 0) { st.period = J.O > 0 ? lat[J.O - 1] : 0; }
+  x.sync();
+  for (int32_t a = x.tid; a < J.A; a += x.nthr) x.amax32(&J.st_evcnt[J.a_tensor[a]], a);
+  x.sync();
+  // CSR by storage: stable sort of (storage, access id)
+  const int ab = nbits(uint64_t(J.A > 0 ? J.A - 1 : 0));
+  for (int32_t a = x.tid; a < J.A; a += x.nthr) {
+    int32_t t = J.a_tensor[a];
+    uint8_t f = (J.st_evcnt[t] == a && J.t_kind[t] == K_INTERIM) ? 1 : 0;
+    J.a_base[a] = f;
+    J.a_flag[a] = f;
+    g.k_key[a] = (uint64_t(J.a_store[a]) << ab) | uint64_t(a);
+    g.k_val[a] = a;
+  }
+  x.sync();
+  x.sort(g.k_key, g.k_val, J.A, ab + nbits(uint64_t(J.T)));
+  for (int32_t m = x.tid; m < J.A; m += x.nthr) {
+    int32_t a = g.k_val[m];
+    J.s_acc[m] = a;
+    int32_t cur = J.a_store[a];
+    int32_t prev = m == 0 ? -1 : J.a_store[g.k_val[m - 1]];
+    for (int32_t s = prev + 1; s <= cur; ++s) J.s_off[s] = m;
+    if (m == J.A - 1)
+      for (int32_t s = cur + 1; s <= J.T; ++s) J.s_off[s] = J.A;
+  }
+  if (J.A == 0)
+    for (int32_t s = x.tid; s <= J.T; s += x.nthr) J.s_off[s] = 0;
+  x.sync();
+  for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+    int32_t wf = -1, ut = -1;
+    const int32_t u = J.t_upd[t];
+    if (u >= 0) {
+      for (int32_t k = J.s_off[t]; k < J.s_off[t + 1]; ++k) {
+        int32_t a = J.s_acc[k];
+        if (wf < 0 && J.a_tensor[a] == t && J.a_type[a] == ACC_TUA) wf = a;
+        if (J.a_tensor[a] == u && J.a_type[a] == ACC_TGA) ut = a;
+      }
+    }
+    J.t_wfirst[t] = wf;
+    J.t_utga[t] = ut;
+    J.st_evcnt[t] = 0;
+    J.swapped[t] = 0;
+    J.in_peak[t] = 0;
+  }
+  if (x.tid == 0) {
+    st.S = 0; st.R = 0; st.n_peak = 0; st.n_curve = 0;
+    st.next_id = 0; st.peak = 0; st.peak_time = 0; st.lua = -1; st.has_lua = 0;
+    st.dirty = 1; st.n_events = 0; st.son = 0;
+  }
+  x.sync();
+}
+
+// ----------------------------------------------------------------------------
+// Stage 2: footprint evaluator for jobs [jb, je) (analyze_job, peak.cpp:246-250)
+// ----------------------------------------------------------------------------
+// Shared scalar layout per batch job b: sh[b*16 + field].
+enum { F_BASE = 0, F_N, F_REL, F_INIT, F_OFF, F_MAXFP, F_PPOS, F_LUA, F_ERR, F_NPEAK, F_RELCUR, NF = 16 };
+
+template <class X>
+TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
+  int64_t* sh = x.sh;
+  const int nb = je - jb;
+  int64_t* gsh = sh + MAXB * NF;  // [0]=tmin [1]=tmax [2]=n_total [3]=bits info [4]=fail
+  if (x.tid == 0) {
+    for (int b = 0; b < nb; ++b) {
+      int64_t* f = sh + b * NF;
+      f[F_REL] = 0; f[F_INIT] = 0; f[F_MAXFP] = INT64_MIN; f[F_PPOS] = INT64_MAX;
+      f[F_LUA] = -1; f[F_ERR] = INT64_MAX; f[F_NPEAK] = 0; f[F_RELCUR] = 0;
+    }
+    gsh[0] = INT64_MAX; gsh[1] = INT64_MIN; gsh[4] = 0;
+  }
+  // 0. initial residency (peak.cpp:176-190) and release-ownership scratch
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+      int8_t k = J.t_kind[t];
+      J.res_init[t] = (J.t_store[t] == t && (k == K_PARAM || k == K_INPUT || k == K_OUTPUT)) ? 1 : 0;
+    }
+    for (int32_t a = x.tid; a < J.A; a += x.nthr) J.a_owned[a] = 0;
+  }
+  x.sync();
+  // 1. wrapped swap-ins leave the initial set; swap-outs own releases; time range
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    const JobState& st = g.st[jb + b];
+    int64_t lmin = INT64_MAX, lmax = INT64_MIN;
+    if (x.tid == 0 && J.A > 0) { lmin = J.a_start[0]; lmax = J.a_end[J.A - 1]; }
+    for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+      const int32_t s = J.t_store[J.ev_tensor[i]];
+      int64_t when = J.ev_end[i];
+      if (J.ev_dir[i] == 1) {
+        if (J.ev_wraps[i]) {
+          J.res_init[s] = 0;
+          if (st.period > 0) when = ((when % st.period) + st.period) % st.period;
+        }
+      } else {
+        const int64_t tr = J.ev_trig[i];
+        if (tr != -1) {
+          if (tr < 0 || tr >= J.A) {
+            x.amax(&gsh[4], 1);
+          } else {
+            when = imax(when, J.a_end[tr]);
+          }
+        }
+        // peak.cpp:107-130: a flagged access a loses its release when a
+        // swap-out of its storage starts in [a.end, next access start).
+        // With m = the last storage access start <= t, that is m < a.end <= t.
+        const int64_t t0 = J.ev_start[i];
+        const int32_t k0 = J.s_off[s], k1 = J.s_off[s + 1];
+        int32_t lo = k0, hi = k1;
+        while (lo < hi) {
+          int32_t md = (lo + hi) >> 1;
+          if (J.a_start[J.s_acc[md]] <= t0) lo = md + 1; else hi = md;
+        }
+        if (lo > k0) {
+          const int64_t m = J.a_start[J.s_acc[lo - 1]];
+          int32_t l2 = k0, h2 = k1;  // first position with end > m
+          while (l2 < h2) {
+            int32_t md = (l2 + h2) >> 1;
+            if (J.a_end[J.s_acc[md]] <= m) l2 = md + 1; else h2 = md;
+          }
+          for (int32_t k = l2; k < k1; ++k) {
+            int32_t a = J.s_acc[k];
+            if (J.a_end[a] > t0) break;
+            J.a_owned[a] = 1;
+          }
+        }
+      }
+      lmin = imin(lmin, when);
+      lmax = imax(lmax, when);
+    }
+    for (int32_t r = x.tid; r < st.R; r += x.nthr) {
+      const int64_t tg = J.rc_target[r];
+      if (tg < 0 || tg >= J.A) { x.amax(&gsh[4], 1); continue; }
+      int64_t when = J.a_start[tg] - J.rc_lat[r];
+      lmin = imin(lmin, when);
+      lmax = imax(lmax, when);
+    }
+    if (lmin != INT64_MAX) { x.amin(&gsh[0], lmin); x.amax(&gsh[1], lmax); }
+  }
+  x.sync();
+  if (gsh[4]) {  // unknown access id in a caller plan (access.cpp:8-10)
+    if (x.tid == 0) {
+      for (int b = 0; b < nb && !g.err.code; ++b) {
+        const JobDev& J = g.jobs[jb + b];
+        const JobState& st = g.st[jb + b];
+        for (int32_t i = 0; i < st.S; ++i)
+          if (J.ev_dir[i] == 0 && J.ev_trig[i] != -1 && (J.ev_trig[i] < 0 || J.ev_trig[i] >= J.A)) {
+            g.err.code = E_UNKNOWN_ACCESS; g.err.job = jb + b; g.err.tensor = J.ev_trig[i]; g.err.tick = 0;
+            break;
+          }
+        for (int32_t r = 0; r < st.R && !g.err.code; ++r)
+          if (J.rc_target[r] < 0 || J.rc_target[r] >= J.A) {
+            g.err.code = E_UNKNOWN_ACCESS; g.err.job = jb + b; g.err.tensor = J.rc_target[r]; g.err.tick = 0;
+          }
+      }
+    }
+    x.sync();
+    return false;
+  }
+  // 2. count releases; initial footprint
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    int32_t rel = 0;
+    for (int32_t a = x.tid; a < J.A; a += x.nthr) rel += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
+    if (rel) x.aadd(&sh[b * NF + F_REL], rel);
+    int64_t fp = 0;
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.res_init[t]) fp += J.t_size[t];
+    if (fp) x.aadd(&sh[b * NF + F_INIT], fp);
+  }
+  x.sync();
+  // 3. bases and key geometry
+  if (x.tid == 0) {
+    int64_t base = 0, maxT = 1, maxTie = 1;
+    for (int b = 0; b < nb; ++b) {
+      const JobDev& J = g.jobs[jb + b];
+      const JobState& st = g.st[jb + b];
+      int64_t* f = sh + b * NF;
+      f[F_BASE] = base;
+      f[F_N] = J.A + f[F_REL] + st.S + st.R;
+      base += f[F_N];
+      maxT = imax(maxT, J.T);
+      maxTie = imax(maxTie, int64_t(J.A) + st.S + st.R);
+    }
+    gsh[2] = base;
+    int64_t tmin = gsh[0], tmax = gsh[1];
+    if (tmin > tmax) { tmin = 0; tmax = 0; }
+    gsh[0] = tmin;
+    const int jbits = nbits(uint64_t(nb - 1)), tbits = nbits(uint64_t(tmax - tmin));
+    const int rbits = nbits(uint64_t(maxT - 1)), xbits = nbits(uint64_t(maxTie - 1));
+    gsh[3] = (int64_t(jbits) << 48) | (int64_t(tbits) << 32) | (int64_t(rbits) << 16) | int64_t(xbits);
+    if (base > g.ecap || jbits + tbits + 1 + rbits + 3 + xbits > 63) {
+      g.err.code = E_CAPACITY; g.err.job = jb; g.err.tensor = base; g.err.tick = jbits + tbits + rbits + xbits + 4;
+    }
+  }
+  x.sync();
+  if (g.err.code) return false;
+  const int jbits = int(gsh[3] >> 48), tbits = int((gsh[3] >> 32) & 0xffff);
+  const int rbits = int((gsh[3] >> 16) & 0xffff), xbits = int(gsh[3] & 0xffff);
+  const int64_t tmin = gsh[0];
+  const int64_t n = gsh[2];
+  auto key = [&](int b, int64_t time, int type, int32_t srank, int64_t tie) -> uint64_t {
+    const bool fr = type == EV_REL || type == EV_SOUT;
+    uint64_t k = uint64_t(b);
+    k = (k << tbits) | uint64_t(time - tmin);
+    k = (k << 1) | (fr ? 0u : 1u);
+    k = (k << rbits) | uint64_t(srank);
+    k = (k << 3) | uint64_t(type);
+    k = (k << xbits) | uint64_t(tie);
+    return k;
+  };
+  // 4. emit events (build_timeline, peak.cpp:66-174)
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    const JobState& st = g.st[jb + b];
+    int64_t* f = sh + b * NF;
+    const int64_t base = f[F_BASE];
+    const int64_t tie0 = int64_t(st.S) + st.R;
+    for (int32_t a = x.tid; a < J.A; a += x.nthr) {
+      const int32_t s = J.a_store[a];
+      const int64_t slot = base + a;
+      const bool flagged = J.a_flag[a] != 0;
+      if (J.a_type[a] == ACC_TGA) {
+        g.x_time[slot] = J.a_start[a];
+        g.x_type[slot] = int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0));
+        g.k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s], tie0 + a);
+      } else {
+        g.x_time[slot] = J.a_end[a];
+        g.x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
+        g.k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s], tie0 + a);
+      }
+      g.x_store[slot] = s; g.x_aid[slot] = a; g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
+      if (flagged && !J.a_owned[a]) {
+        const int64_t rs = base + J.A + st.S + st.R + x.aadd(&f[F_RELCUR], 1);
+        g.x_time[rs] = J.a_end[a]; g.x_type[rs] = EV_REL; g.x_store[rs] = s; g.x_aid[rs] = a;
+        g.x_job[rs] = int8_t(b); g.k_val[rs] = int32_t(rs);
+        g.k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s], tie0 + a);
+      }
+    }
+    for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+      const int32_t s = J.t_store[J.ev_tensor[i]];
+      const int64_t slot = base + J.A + i;
+      int64_t when = J.ev_end[i];
+      int type;
+      if (J.ev_dir[i] == 0) {
+        type = EV_SOUT;
+        if (J.ev_trig[i] != -1) when = imax(when, J.a_end[J.ev_trig[i]]);
+      } else {
+        type = EV_SIN;
+        if (J.ev_wraps[i] && st.period > 0) when = ((when % st.period) + st.period) % st.period;
+      }
+      g.x_time[slot] = when; g.x_type[slot] = int8_t(type); g.x_store[slot] = s; g.x_aid[slot] = -1;
+      g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
+      g.k_key[slot] = key(b, when, type, J.t_rank[s], i);
+    }
+    for (int32_t r = x.tid; r < st.R; r += x.nthr) {
+      const int32_t s = J.t_store[J.rc_tensor[r]];
+      const int64_t slot = base + J.A + st.S + r;
+      const int64_t when = J.a_start[J.rc_target[r]] - J.rc_lat[r];
+      g.x_time[slot] = when; g.x_type[slot] = EV_TGA; g.x_store[slot] = s; g.x_aid[slot] = -1;
+      g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
+      g.k_key[slot] = key(b, when, EV_TGA, J.t_rank[s], st.S + r);
+    }
+  }
+  x.sync();
+  // 5. timeline order (sort_timeline, peak.cpp:44-62)
+  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 3 + xbits);
+  // 6. group sorted positions by (job, storage), keeping timeline order
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int32_t slot = g.k_val[m];
+    g.x_order[m] = slot;
+    const int b = g.x_job[slot];
+    g.x_key2[m] = (uint64_t(b) << rbits) | uint64_t(g.jobs[jb + b].t_rank[g.x_store[slot]]);
+    g.x_seq2[m] = int32_t(m);
+  }
+  x.sync();
+  x.sort(g.x_key2, g.x_seq2, int32_t(n), jbits + rbits);
+  // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230)
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    if (m > 0 && g.x_key2[m] == g.x_key2[m - 1]) continue;
+    int32_t pos = g.x_seq2[m];
+    const int b = g.x_job[g.x_order[pos]];
+    const JobDev& J = g.jobs[jb + b];
+    const int32_t s = g.x_store[g.x_order[pos]];
+    uint8_t res = J.res_init[s];
+    const int64_t size = J.t_size[s];
+    for (int64_t q = m; q < n && g.x_key2[q] == g.x_key2[m]; ++q) {
+      pos = g.x_seq2[q];
+      const int32_t slot = g.x_order[pos];
+      const int ty = g.x_type[slot] & 7;
+      int64_t eff = 0;
+      int errc = 0;
+      switch (ty) {
+        case EV_TGA:
+          if (!res) { eff = (g.x_type[slot] & 8) ? 0 : size; res = 1; }
+          break;
+        case EV_TUA: break;
+        case EV_REL:
+        case EV_SOUT:
+          if (!res) errc = E_DOUBLE_RELEASE;
+          eff = -size; res = 0;
+          break;
+        default:  // EV_SIN
+          if (res) errc = E_SWAPIN_RESIDENT;
+          eff = size; res = 1;
+          break;
+      }
+      g.x_fp[pos] = eff;
+      g.x_state[pos] = res;
+      if (errc) x.amin(&sh[b * NF + F_ERR], (int64_t(pos) << 3) | errc);
+    }
+  }
+  x.sync();
+  // 8. footprint curve: inclusive scan of the effective deltas
+  x.scan(g.x_fp, int32_t(n));
+  if (x.tid == 0) {
+    for (int b = 0; b < nb; ++b) {
+      int64_t* f = sh + b * NF;
+      f[F_OFF] = f[F_INIT] - (f[F_BASE] > 0 ? g.x_fp[f[F_BASE] - 1] : 0);
+    }
+  }
+  x.sync();
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int b = g.x_job[g.x_order[m]];
+    int64_t* f = sh + b * NF;
+    const int64_t fp = g.x_fp[m] + f[F_OFF];
+    g.x_fp[m] = fp;  // own element only: no cross-thread hazard after the scan
+    if (fp < 0) x.amin(&f[F_ERR], (int64_t(m) << 3) | E_NEG_FOOTPRINT);
+  }
+  x.sync();
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int b = g.x_job[g.x_order[m]];
+    x.amax(&sh[b * NF + F_MAXFP], g.x_fp[m]);
+  }
+  x.sync();
+  // 9. first strict maximum (analyze_peak, peak.cpp:236-241)
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int b = g.x_job[g.x_order[m]];
+    int64_t* f = sh + b * NF;
+    if (f[F_MAXFP] > f[F_INIT] && g.x_fp[m] == f[F_MAXFP]) x.amin(&f[F_PPOS], m);
+  }
+  x.sync();
+  // 10. last_input_access at the peak; residency at the peak
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int32_t slot = g.x_order[m];
+    const int b = g.x_job[slot];
+    int64_t* f = sh + b * NF;
+    if (f[F_PPOS] != INT64_MAX && m <= f[F_PPOS] && (g.x_type[slot] & 7) == EV_TUA && !(g.x_type[slot] & 16))
+      x.amax(&f[F_LUA], m);
+  }
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) J.in_peak[t] = J.res_init[t];
+  }
+  x.sync();
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    if (m > 0 && g.x_key2[m] == g.x_key2[m - 1]) continue;
+    const int32_t slot0 = g.x_order[g.x_seq2[m]];
+    const int b = g.x_job[slot0];
+    const int64_t pp = sh[b * NF + F_PPOS];
+    if (pp == INT64_MAX) continue;
+    int64_t last = -1;
+    for (int64_t q = m; q < n && g.x_key2[q] == g.x_key2[m]; ++q) {
+      if (g.x_seq2[q] <= pp) last = g.x_seq2[q]; else break;
+    }
+    if (last >= 0) g.jobs[jb + b].in_peak[g.x_store[slot0]] = g.x_state[last];
+  }
+  x.sync();
+  // 11. report + curve
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    int64_t* f = sh + b * NF;
+    int32_t cnt = 0;
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) cnt += J.in_peak[t];
+    if (cnt) x.aadd(&f[F_NPEAK], cnt);
+    const int64_t base = f[F_BASE], nn = f[F_N];
+    if (x.tid == 0) { J.curve_t[0] = 0; J.curve_b[0] = f[F_INIT]; }
+    for (int64_t m = x.tid; m < nn; m += x.nthr) {
+      J.curve_t[m + 1] = g.x_time[g.x_order[base + m]];
+      J.curve_b[m + 1] = g.x_fp[base + m];
+    }
+  }
+  x.sync();
+  if (x.tid == 0) {
+    for (int b = 0; b < nb; ++b) {
+      int64_t* f = sh + b * NF;
+      if (f[F_ERR] != INT64_MAX && !g.err.code) {
+        const int64_t pos = f[F_ERR] >> 3;
+        const int32_t slot = g.x_order[pos];
+        g.err.code = int32_t(f[F_ERR] & 7);
+        g.err.job = jb + b;
+        g.err.tensor = g.x_store[slot];
+        g.err.tick = g.x_time[slot];
+      }
+      JobState& st = g.st[jb + b];
+      const bool up = f[F_PPOS] != INT64_MAX;
+      st.peak = up ? f[F_MAXFP] : f[F_INIT];
+      st.peak_time = up ? g.x_time[g.x_order[f[F_PPOS]]] : 0;
+      st.has_lua = (up && f[F_LUA] >= 0) ? 1 : 0;
+      st.lua = st.has_lua ? g.x_aid[g.x_order[f[F_LUA]]] : -1;
+      st.n_peak = int32_t(f[F_NPEAK]);
+      st.n_curve = int32_t(f[F_N] + 1);
+      st.n_events = f[F_N];
+      st.dirty = 0;
+    }
+    g.stats.evaluations += nb;
+    g.stats.timeline_events += n;
+    g.stats.sort_elems += 2 * n;
+  }
+  x.sync();
+  return g.err.code == 0;
+}
+
+// Evaluate every job in [j0, j1) whose plan changed (or all when force),
+// in batches that fit the sort capacity.
+template <class X>
+TSL_HD bool refresh(X& x, GroupDev& g, int j0, int j1, bool force) {
+  int j = j0;
+  while (j < j1) {
+    while (j < j1 && !force && !g.st[j].dirty) ++j;
+    if (j >= j1) break;
+    int e = j;
+    int64_t tot = 0;
+    while (e < j1 && e - j < MAXB && (force || g.st[e].dirty || e == j)) {
+      const int64_t need = int64_t(g.jobs[e].A) * 2 + g.st[e].S + g.st[e].R;
+      if (e > j && tot + need > g.ecap) break;
+      tot += need;
+      ++e;
+    }
+    if (!evaluate(x, g, j, e)) return false;
+    j = e;
+  }
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// Stage 3+4: swap pass (swap_planner.cpp:461-520)
+// ----------------------------------------------------------------------------
+template <class X>
+TSL_HD bool swap_pass(X& x, GroupDev& g) {
+  int64_t* sh = x.sh;
+  int64_t* gsh = sh + MAXB * NF;  // [8]=nc [9]=maxT [10]=changed [11]=cursor [12]=maxsize [16..] segments
+  if (x.tid == 0) {
+    int64_t maxT = 1;
+    for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
+    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1;
+  }
+  x.sync();
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    int64_t mx = 1;
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.in_peak[t]) mx = imax(mx, J.t_size[t]);
+    x.amax(&gsh[12], mx);
+  }
+  x.sync();
+  const int jbits = nbits(uint64_t(g.n_jobs - 1));
+  const int rbits = nbits(uint64_t(gsh[9] - 1));
+  const int sbits = nbits(uint64_t(gsh[12]));
+  const uint64_t smax = (sbits >= 63) ? (~0ull >> 1) : ((1ull << sbits) - 1);
+  const bool coupled = g.coupled != 0;
+  // candidates: every job's peak tensors (the report stays stale for the whole
+  // pass), ordered (size desc, job id, storage id) -- swap_planner.cpp:469-481
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+      if (!J.in_peak[t]) continue;
+      const int64_t slot = x.aadd(&gsh[11], 1);
+      if (slot >= g.ecap) continue;
+      const uint64_t inv = smax - uint64_t(J.t_size[t]);
+      uint64_t k;
+      if (coupled) k = (((inv << jbits) | uint64_t(J.rank)) << rbits) | uint64_t(J.t_rank[t]);
+      else k = (((uint64_t(j) << sbits) | inv) << rbits) | uint64_t(J.t_rank[t]);
+      g.k_key[slot] = k;
+      g.k_val[slot] = (j << 24) | t;  // the host guarantees T < 2^24 and < 128 jobs
+    }
+  }
+  x.sync();
+  const int64_t nc = gsh[11];
+  if (nc > g.ecap) {
+    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = -1; g.err.tensor = nc; g.err.tick = 1; }
+    x.sync();
+    return false;
+  }
+  x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
+  if (x.tid == 0) {
+    g.stats.candidates += nc;
+    g.stats.sort_elems += nc;
+    for (int j = 0; j <= g.n_jobs; ++j) gsh[16 + j] = nc;
+    if (!coupled) {
+      for (int64_t m = nc - 1; m >= 0; --m) gsh[16 + (g.k_val[m] >> 24)] = m;
+      for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
+    }
+    gsh[13] = 0;
+  }
+  x.sync();
+  const int nseg = coupled ? 1 : g.n_jobs;
+  for (int seg = x.warp; seg < nseg; seg += x.nwarp) {
+    GroupStats ls{};
+    ErrInfo lerr{};
+    const int64_t m0 = coupled ? 0 : gsh[16 + seg];
+    const int64_t m1 = coupled ? nc : gsh[16 + seg + 1];
+    bool changed = false;
+    for (int64_t m = m0; m < m1; ++m) {
+      const int j = g.k_val[m] >> 24;
+      const int32_t s = g.k_val[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      JobState& st = g.st[j];
+      if (J.swapped[s]) continue;  // SwapBudget::already_swapped
+      if (coupled && g.total_swapped != 0) {  // SwapBudget::allows, swap_planner.cpp:268-276
+        const double lhs = double(st.son + 1) / double(g.total_swapped + 1);
+        if (!(lhs <= J.ratio)) continue;
+      }
+      bool ok = false;
+      if (J.t_kind[s] == K_PARAM && J.t_upd[s] >= 0) {
+        ok = schedule_wrapped_swap(x, J, st, g.cfg, s, &ls, &lerr, j);
+      } else {
+        if (J.s_off[s + 1] - J.s_off[s] <= 1) continue;
+        int64_t earliest, latest;
+        if (!swap_window(J, s, st.peak_time, earliest, latest)) {
+          lerr.code = E_NO_TGA; lerr.job = j; lerr.tensor = s; lerr.tick = 0;
+        } else if (latest > earliest) {
+          ok = schedule_swap(x, J, st, g.cfg, s, earliest, latest, &ls, &lerr, j);
+        }
+      }
+      if (lerr.code) break;
+      if (ok) {  // SwapBudget::record
+        const int64_t son = st.son, tot = g.total_swapped;
+        x.wsync();
+        J.swapped[s] = 1;
+        st.son = son + 1;
+        if (coupled) g.total_swapped = tot + 1;
+        changed = true;
+        x.wsync();
+      }
+    }
+    x.wsync();
+    if (x.lane == 0) {
+      if (changed) gsh[10] = 1;
+      if (lerr.code) x.errset(g, lerr);
+      x.aadd(&g.stats.fit_queries, ls.fit_queries);
+      x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+      x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+    }
+  }
+  x.sync();
+  return gsh[10] != 0;
+}
+
+// ----------------------------------------------------------------------------
+// revalidate_swap_events + rebuild_release_flags (swap_planner.cpp:171-266)
+// ----------------------------------------------------------------------------
+TSL_HD bool ovl_mod(int64_t s1, int64_t e1, int64_t s2, int64_t e2, int64_t P) {
+  for (int k = -1; k <= 1; ++k) {
+    const int64_t sh = k * P;
+    if (s1 + sh < e2 && s2 < e1 + sh) return true;
+  }
+  return false;
+}
+
+template <class X>
+TSL_HD void rebuild_flags(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  const JobState& st = g.st[j];
+  for (int32_t a = x.tid; a < J.A; a += x.nthr) J.a_flag[a] = J.a_base[a];
+  x.sync();
+  for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+    if (J.ev_dir[i] != 0) continue;
+    int32_t p = preceding_access(J, J.t_store[J.ev_tensor[i]], J.ev_start[i], -2);
+    if (p >= 0) J.a_flag[p] = 1;
+  }
+  for (int32_t r = x.tid; r < st.R; r += x.nthr) {
+    const int64_t tg = J.rc_target[r];
+    int32_t p = preceding_access(J, J.t_store[J.rc_tensor[r]], J.a_start[tg], tg);
+    if (p >= 0) J.a_flag[p] = 1;
+  }
+  x.sync();
+}
+
+// Rebuilds the sorted busy structure, per-storage counts and next_event_id.
+template <class X>
+TSL_HD void rebuild_index(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  int64_t* gsh = x.sh + MAXB * NF;
+  if (x.tid == 0) { gsh[20] = INT64_MAX; gsh[21] = INT64_MIN; gsh[22] = 0; }
+  for (int32_t t = x.tid; t < J.T; t += x.nthr) J.st_evcnt[t] = 0;
+  x.sync();
+  int64_t mn = INT64_MAX, mx = INT64_MIN, mid = -1;
+  for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+    mn = imin(mn, J.ev_start[i]);
+    mx = imax(mx, J.ev_start[i]);
+    mid = imax(mid, J.ev_id[i]);
+    x.aadd32(&J.st_evcnt[J.ev_tensor[i]], 1);
+  }
+  for (int32_t r = x.tid; r < st.R; r += x.nthr) mid = imax(mid, J.rc_id[r]);
+  if (mn != INT64_MAX) { x.amin(&gsh[20], mn); x.amax(&gsh[21], mx); }
+  x.amax(&gsh[22], mid + 1);
+  x.sync();
+  const int64_t lo = gsh[20];
+  const int bits = st.S > 0 ? nbits(uint64_t(gsh[21] - lo)) : 0;
+  const int ib = nbits(uint64_t(st.S > 0 ? st.S - 1 : 0));
+  for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+    g.k_key[i] = (uint64_t(J.ev_start[i] - lo) << ib) | uint64_t(i);
+    g.k_val[i] = i;
+  }
+  x.sync();
+  x.sort(g.k_key, g.k_val, st.S, bits + ib);
+  for (int32_t m = x.tid; m < st.S; m += x.nthr) {
+    const int32_t i = g.k_val[m];
+    J.bz_s[m] = J.ev_start[i];
+    J.bz_e[m] = J.ev_end[i];
+  }
+  if (x.tid == 0) st.next_id = gsh[22];
+  x.sync();
+}
+
+template <class X>
+TSL_HD bool revalidate(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  const int64_t P = imax(1, st.period);
+  int64_t* gsh = x.sh + MAXB * NF;
+  if (x.tid == 0) gsh[23] = 0;
+  x.sync();
+  // re-derive absolute times from the (trigger, delta) anchors
+  for (int32_t i = x.tid; i < st.S; i += x.nthr) {
+    const int64_t tr = J.ev_trig[i];
+    if (tr != -1 && (tr < 0 || tr >= J.A)) { x.amax(&gsh[23], 1); continue; }
+    const int64_t base = tr == -1 ? 0 : J.a_end[tr];
+    const int64_t d = duration(J.t_size[J.t_store[J.ev_tensor[i]]], g.cfg);
+    int64_t s = base + J.ev_delta[i];
+    if (J.ev_wraps[i] && J.ev_dir[i] == 1) s += P;
+    J.ev_start[i] = s;
+    J.ev_end[i] = s + d;
+    J.ev_drop[i] = 0;
+  }
+  x.sync();
+  if (gsh[23]) {
+    if (x.tid == 0) { g.err.code = E_UNKNOWN_ACCESS; g.err.job = j; g.err.tensor = -1; g.err.tick = 0; }
+    x.sync();
+    return false;
+  }
+  // keep pairs in event order against an accumulating kept set (bz_* reused)
+  if (x.warp == 0) {
+    int32_t nk = 0;
+    for (int32_t i = 0; i < st.S; ++i) {
+      if (J.ev_dir[i] != 0) continue;
+      int32_t in = -1;
+      if (J.ev_pair[i] >= 0) {
+        if (i + 1 < st.S && J.ev_id[i + 1] == J.ev_pair[i]) in = i + 1;
+        else
+          for (int32_t k = 0; k < st.S; ++k)
+            if (J.ev_id[k] == J.ev_pair[i]) { in = k; break; }
+      }
+      bool ok = in >= 0 && J.ev_end[i] <= J.ev_start[in];
+      if (ok && J.ev_serves[in] >= 0) {
+        int64_t deadline = J.a_start[J.ev_serves[in]];
+        if (J.ev_wraps[in]) deadline += P;
+        ok = J.ev_end[in] <= deadline;
+      }
+      if (ok) {
+        const int32_t s = J.t_store[J.ev_tensor[i]];
+        bool bad = false;
+        for (int32_t k = J.s_off[s] + x.lane; k < J.s_off[s + 1]; k += X::W) {
+          const int32_t a = J.s_acc[k];
+          if (ovl_mod(J.ev_start[i], J.ev_end[i], J.a_start[a], J.a_end[a], P) ||
+              ovl_mod(J.ev_start[in], J.ev_end[in], J.a_start[a], J.a_end[a], P))
+            bad = true;
+        }
+        for (int32_t k = x.lane; k < nk; k += X::W) {
+          if (ovl_mod(J.ev_start[i], J.ev_end[i], J.bz_s[k], J.bz_e[k], P) ||
+              ovl_mod(J.ev_start[in], J.ev_end[in], J.bz_s[k], J.bz_e[k], P))
+            bad = true;
+        }
+        ok = !x.wany(bad);
+      }
+      if (!ok) {
+        J.ev_drop[i] = 1;
+        if (in >= 0) J.ev_drop[in] = 1;
+      } else {
+        x.wsync();
+        J.bz_s[nk] = J.ev_start[i]; J.bz_e[nk] = J.ev_end[i];
+        J.bz_s[nk + 1] = J.ev_start[in]; J.bz_e[nk + 1] = J.ev_end[in];
+        nk += 2;
+      }
+      x.wsync();
+    }
+    // stable compaction (lane 0; pairs are rare to drop)
+    if (x.lane == 0) {
+      int32_t w = 0;
+      for (int32_t i = 0; i < st.S; ++i) {
+        if (J.ev_drop[i]) continue;
+        if (w != i) {
+          J.ev_id[w] = J.ev_id[i]; J.ev_tensor[w] = J.ev_tensor[i]; J.ev_dir[w] = J.ev_dir[i];
+          J.ev_wraps[w] = J.ev_wraps[i]; J.ev_trig[w] = J.ev_trig[i]; J.ev_delta[w] = J.ev_delta[i];
+          J.ev_start[w] = J.ev_start[i]; J.ev_end[w] = J.ev_end[i]; J.ev_earl[w] = J.ev_earl[i];
+          J.ev_late[w] = J.ev_late[i]; J.ev_pair[w] = J.ev_pair[i]; J.ev_serves[w] = J.ev_serves[i];
+        }
+        ++w;
+      }
+      st.S = w;
+    }
+  }
+  x.sync();
+  rebuild_flags(x, g, j);
+  rebuild_index(x, g, j);
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// Recompute pass (recompute_planner.cpp:50-153)
+// ----------------------------------------------------------------------------
+template <class X>
+TSL_HD void backup_job(X& x, GroupDev& g, int j, bool restore, int32_t S, int32_t R, int64_t nc) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  int64_t* E[EV_FIELDS] = {J.ev_id, nullptr, nullptr, nullptr, J.ev_trig, J.ev_delta,
+                           J.ev_start, J.ev_end, J.ev_earl, J.ev_late, J.ev_pair, J.ev_serves};
+  (void)st;
+  auto cp64 = [&](int64_t* live, int64_t* bk, int64_t n) {
+    for (int64_t i = x.tid; i < n; i += x.nthr) { if (restore) live[i] = bk[i]; else bk[i] = live[i]; }
+  };
+  auto cp8 = [&](uint8_t* live, uint8_t* bk, int64_t n) {
+    for (int64_t i = x.tid; i < n; i += x.nthr) { if (restore) live[i] = bk[i]; else bk[i] = live[i]; }
+  };
+  cp64(J.a_start, J.bk_a_start, J.A);
+  cp64(J.a_end, J.bk_a_end, J.A);
+  cp8(J.a_flag, J.bk_flag, J.A);
+  cp8(J.in_peak, J.bk_in_peak, J.T);
+  for (int f = 0; f < EV_FIELDS; ++f)
+    if (E[f]) cp64(E[f], J.bk_ev + int64_t(f) * J.Scap, S);
+  for (int32_t i = x.tid; i < S; i += x.nthr) {  // narrow fields packed into word 1..3
+    int64_t* b1 = J.bk_ev + 1LL * J.Scap;
+    int64_t* b2 = J.bk_ev + 2LL * J.Scap;
+    if (restore) {
+      J.ev_tensor[i] = int32_t(b1[i]);
+      J.ev_dir[i] = int8_t(b2[i] & 0xff);
+      J.ev_wraps[i] = int8_t(b2[i] >> 8);
+    } else {
+      b1[i] = J.ev_tensor[i];
+      b2[i] = int64_t(uint8_t(J.ev_dir[i])) | (int64_t(uint8_t(J.ev_wraps[i])) << 8);
+    }
+  }
+  cp64(J.rc_id, J.bk_rc, R);
+  cp64(J.rc_target, J.bk_rc + 2LL * J.Rcap, R);
+  cp64(J.rc_lat, J.bk_rc + 4LL * J.Rcap, R);
+  cp64(J.rc_saving, J.bk_rc + 5LL * J.Rcap, R);
+  for (int32_t r = x.tid; r < R; r += x.nthr) {
+    int64_t* b1 = J.bk_rc + 1LL * J.Rcap;
+    int64_t* b3 = J.bk_rc + 3LL * J.Rcap;
+    if (restore) { J.rc_tensor[r] = int32_t(b1[r]); J.rc_regen[r] = int32_t(b3[r]); }
+    else { b1[r] = J.rc_tensor[r]; b3[r] = J.rc_regen[r]; }
+  }
+  cp64(J.bz_s, J.bk_bz, S);
+  cp64(J.bz_e, J.bk_bz + J.Scap, S);
+  for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+    if (restore) J.st_evcnt[t] = J.bk_evcnt[t]; else J.bk_evcnt[t] = J.st_evcnt[t];
+  }
+  cp64(J.curve_t, J.bk_curve, nc);
+  cp64(J.curve_b, J.bk_curve + (J.Ecap + 1), nc);
+  x.sync();
+}
+
+template <class X>
+TSL_HD bool recompute_pass(X& x, GroupDev& g) {
+  int64_t* gsh = x.sh + MAXB * NF;
+  int64_t merged = 0;
+  for (int j = 0; j < g.n_jobs; ++j) merged += g.st[j].peak;
+  if (merged < g.cfg.budget) return false;  // strict (recompute_planner.cpp:54)
+  // candidates (recompute_planner.cpp:56-110): one thread per (job, tensor)
+  if (x.tid == 0) gsh[24] = 0;
+  x.sync();
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    const JobState& st = g.st[j];
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+      if (!J.in_peak[t] || J.t_kind[t] != K_INTERIM) continue;
+      if (J.st_evcnt[t] > 0) continue;  // storage_has_swap
+      bool rec = false;
+      for (int32_t r = 0; r < st.R; ++r) if (J.rc_tensor[r] == t) rec = true;
+      if (rec) continue;
+      const int32_t p = J.t_prod[t];
+      if (p < 0) continue;
+      bool resident = true;
+      for (int32_t i = J.o_in_off[p]; i < J.o_in_off[p + 1] && resident; ++i) {
+        const int32_t s = J.t_store[J.o_in[i]];
+        if (J.st_evcnt[s] > 0) resident = false;
+        for (int32_t k = J.s_off[s]; k < J.s_off[s + 1] && resident; ++k)
+          if (J.a_flag[J.s_acc[k]]) resident = false;
+      }
+      if (!resident) continue;
+      const int64_t lat = J.o_lat[p];
+      if (lat <= 0) continue;
+      int32_t target = -1, preceding = -1;
+      for (int32_t k = J.s_off[t]; k < J.s_off[t + 1]; ++k) {
+        const int32_t a = J.s_acc[k];
+        if (J.a_type[a] == ACC_TUA && J.a_start[a] > st.peak_time) { target = a; break; }
+        preceding = a;
+      }
+      if (target < 0 || preceding < 0) continue;
+      if (J.a_end[preceding] > st.peak_time) continue;
+      const int64_t slot = x.aadd(&gsh[24], 1);
+      if (slot >= g.ecap) continue;
+      g.x_time[slot] = (int64_t(j) << 32) | t;   // candidate identity
+      g.x_fp[slot] = target;
+    }
+  }
+  x.sync();
+  const int64_t nc = imin(gsh[24], g.ecap);
+  if (nc == 0) return false;
+  // argmax (msps desc, job id asc, tensor id asc) -- recompute_planner.cpp:113-119
+  if (x.tid == 0) {
+    int64_t best = -1;
+    double bv = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      const int j = int(g.x_time[c] >> 32);
+      const int32_t t = int32_t(g.x_time[c] & 0xffffffff);
+      const JobDev& J = g.jobs[j];
+      const double v = double(J.t_size[t]) / double(J.o_lat[J.t_prod[t]]);
+      bool better = best < 0;
+      if (!better) {
+        const int bj = int(g.x_time[best] >> 32);
+        const int32_t bt = int32_t(g.x_time[best] & 0xffffffff);
+        if (v != bv) better = v > bv;
+        else if (J.rank != g.jobs[bj].rank) better = J.rank < g.jobs[bj].rank;
+        else better = J.t_rank[t] < g.jobs[bj].t_rank[bt];
+      }
+      if (better) { best = c; bv = v; }
+    }
+    gsh[25] = g.x_time[best];
+    gsh[26] = g.x_fp[best];
+  }
+  x.sync();
+  const int j = int(gsh[25] >> 32);
+  const int32_t t = int32_t(gsh[25] & 0xffffffff);
+  const int32_t target = int32_t(gsh[26]);
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  // backup (recompute_planner.cpp:123)
+  const JobState saved = st;
+  backup_job(x, g, j, false, saved.S, saved.R, saved.n_curve);
+  if (st.R + 1 > J.Rcap) {
+    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = j; g.err.tensor = J.Rcap; g.err.tick = 2; }
+    x.sync();
+    return false;
+  }
+  const int32_t p = J.t_prod[t];
+  const int64_t lat = J.o_lat[p];
+  const int64_t pivot = J.a_start[target];
+  x.sync();
+  if (x.tid == 0) {
+    const int32_t r = st.R;
+    J.rc_id[r] = st.next_id; J.rc_tensor[r] = t; J.rc_target[r] = target; J.rc_regen[r] = p;
+    J.rc_lat[r] = lat; J.rc_saving[r] = J.t_size[t];
+    st.R = r + 1;
+    st.next_id += 1;
+    st.period += lat;
+  }
+  for (int32_t a = x.tid; a < J.A; a += x.nthr)
+    if (J.a_start[a] >= pivot) { J.a_start[a] += lat; J.a_end[a] += lat; }
+  x.sync();
+  if (!revalidate(x, g, j)) return false;
+  if (x.tid == 0) st.dirty = 1;
+  x.sync();
+  if (!evaluate(x, g, j, j + 1)) return false;
+  if (st.peak > saved.peak) {  // rollback (recompute_planner.cpp:148-151)
+    backup_job(x, g, j, true, saved.S, saved.R, saved.n_curve);
+    if (x.tid == 0) st = saved;
+    x.sync();
+    return false;
+  }
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// build_plan (orchestrator.cpp:8-70) for one group
+// ----------------------------------------------------------------------------
+template <class X>
+TSL_HD void plan_group(X& x, GroupDev& g) {
+  for (int j = 0; j < g.n_jobs; ++j) build_sequence(x, g, j);
+  if (!refresh(x, g, 0, g.n_jobs, true)) return;  // make_job_context's refresh
+  bool swap_ok = true, rc_ok = true;
+  int iter = 0;
+  while (swap_ok || rc_ok) {
+    if (!refresh(x, g, 0, g.n_jobs, false)) return;  // only jobs whose plan changed
+    int64_t merged = 0;
+    for (int j = 0; j < g.n_jobs; ++j) merged += g.st[j].peak;
+    if (x.tid == 0) {
+      if (g.n_hist < g.hist_cap) g.hist[g.n_hist] = merged;
+      g.n_hist += 1;
+    }
+    x.sync();
+    const int nh = g.n_hist;
+    // stall rule: mean per-job peak barely moved over the last 3 rounds
+    if (iter > g.cfg.stall_min_iters && nh > 3 && nh <= g.hist_cap) {
+      const double nj = double(g.n_jobs);
+      const double before = double(g.hist[nh - 4]) / nj;
+      const double now = double(g.hist[nh - 1]) / nj;
+      if (before > 0 && (before - now) / before < g.cfg.stall_eps) break;
+    }
+    if (swap_ok) {
+      swap_ok = swap_pass(x, g);
+    } else if (merged >= g.cfg.budget) {
+      rc_ok = recompute_pass(x, g);
+    } else {
+      rc_ok = false;
+    }
+    if (g.err.code) return;
+    ++iter;
+  }
+  if (!refresh(x, g, 0, g.n_jobs, false)) return;
+  if (x.tid == 0) {
+    int64_t merged = 0;
+    for (int j = 0; j < g.n_jobs; ++j) merged += g.st[j].peak;
+    g.final_merged = merged;
+    g.within_budget = merged <= g.cfg.budget;
+    g.loop_iters = iter;
+    g.stats.loop_iterations = iter;
+  }
+  x.sync();
+}
+
+// analyze_job on a caller-supplied plan: timeline builder + one evaluation.
+template <class X>
+TSL_HD void analyze_group(X& x, GroupDev& g) {
+  for (int j = 0; j < g.n_jobs; ++j) {
+    // keep the caller's plan (events/flags were uploaded into the job arrays)
+    const JobState keep = g.st[j];
+    build_sequence(x, g, j);
+    const JobDev& J = g.jobs[j];
+    for (int32_t a = x.tid; a < J.A; a += x.nthr) J.a_flag[a] = J.a_inflag[a];
+    if (x.tid == 0) {
+      JobState& st = g.st[j];
+      st.S = keep.S; st.R = keep.R; st.next_id = keep.next_id; st.dirty = 1;
+    }
+    x.sync();
+  }
+  refresh(x, g, 0, g.n_jobs, true);
+}
+
+}  // namespace tsl

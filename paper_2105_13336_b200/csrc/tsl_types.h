@@ -1,0 +1,189 @@
+// Device-visible plain-old-data layout of one planning group (one CTA).
+//
+// The host (tsl_host.cpp) packs every group into one staging buffer with
+// absolute device addresses already resolved, uploads it with one H2D copy,
+// and launches one CTA per group (tsl_plan_kernel, tsl_kernel.cu). Everything
+// here is integer SoA: tensor / op / access ids are dense int32 indices, and
+// every std::string ordering of the reference (tensor ids, job ids) is carried
+// as a precomputed lexicographic rank.
+#pragma once
+#include <stdint.h>
+
+namespace tsl {
+
+// AccessType (access.hpp:11): TGA = generating access, TUA = using access.
+enum : int8_t { ACC_TGA = 0, ACC_TUA = 1 };
+// TimelineEventType (peak.hpp:33-39), same order == same type rank.
+enum : int { EV_TGA = 0, EV_TUA = 1, EV_SIN = 2, EV_SOUT = 3, EV_REL = 4 };
+// TensorKind (types.hpp:21).
+enum : int8_t { K_INPUT = 0, K_INTERIM = 1, K_PARAM = 2, K_UPD = 3, K_OUTPUT = 4 };
+
+// Device error codes; the host turns them into the reference's
+// ValidationError texts.
+enum : int32_t {
+  E_OK = 0,
+  E_DOUBLE_RELEASE = 1,   // peak.cpp:220-222 "double release of tensor X"
+  E_SWAPIN_RESIDENT = 2,  // peak.cpp:226-227 "swap-in of resident tensor X"
+  E_NEG_FOOTPRINT = 3,    // peak.cpp:232-234 "negative footprint at tick T"
+  E_NO_TGA = 4,           // swap_planner.cpp:309-310 "tensor X has no TGA in sequence"
+  E_UNKNOWN_ACCESS = 5,   // access.cpp:8-10 "unknown access id N in job J"
+  E_CAPACITY = 6,         // a compiled capacity was exceeded
+  E_INTERNAL = 7
+};
+
+struct ErrInfo {
+  int32_t code;
+  int32_t job;     // job index in the group
+  int64_t tensor;  // tensor index / access id, per code
+  int64_t tick;
+};
+
+// Everything the planner knows and mutates about one job.
+struct JobDev {
+  // ---- sizes and identity ----
+  int32_t A, T, O;   // accesses, tensors, ops
+  int32_t rank;      // job-id rank inside the group (std::string order)
+  double ratio;      // SwapBudget max ratio (config.max_swap_ratio(job))
+  int32_t Scap, Rcap, Ecap;  // swap-event / recompute-event / timeline capacities
+
+  // ---- static graph (host-packed) ----
+  const int32_t* topo;       // [O] op indices in topological order (graph.cpp:245-282)
+  const int64_t* o_lat;      // [O] latency ticks
+  const int32_t* o_in_off;   // [O+1]
+  const int32_t* o_in;       // tensor indices, op.inputs order
+  const int32_t* o_out_off;  // [O+1]
+  const int32_t* o_out;      // tensor indices, op.outputs order
+  const int64_t* t_size;     // [T]
+  const int8_t* t_kind;      // [T]
+  const int32_t* t_rank;     // [T] lexicographic rank of the tensor id
+  const int32_t* t_store;    // [T] storage root (graph.cpp:159-163)
+  const int32_t* t_upd;      // [T] param -> its updated version, else -1
+  const int32_t* t_prod;     // [T] producer op, else -1
+  const uint8_t* a_inflag;   // [A] caller plan release flags (tsl_analyze_job only)
+
+  // ---- derived on the device by the timeline builder ----
+  int32_t* a_tensor;  // [A]
+  int32_t* a_store;   // [A]
+  int8_t* a_type;     // [A]
+  int64_t* a_start;   // [A] (shifted by recomputation)
+  int64_t* a_end;     // [A]
+  uint8_t* a_base;    // [A] activity-analysis release flags (access.cpp:61-78)
+  uint8_t* a_flag;    // [A] current plan release flags
+  uint8_t* a_owned;   // [A] scratch: release owned by a swap-out (peak.cpp:107-130)
+  int32_t* s_off;     // [T+1] CSR by storage
+  int32_t* s_acc;     // [A]   access ids of each storage, ascending (== (start, id) order)
+  int32_t* t_wfirst;  // [T] first TUA whose tensor id is exactly the param (swap_planner.cpp:426-431)
+  int32_t* t_utga;    // [T] last TGA access of the param's updated version (:412-415)
+
+  // ---- plan: swap events in plan order (plan.hpp:18-32) ----
+  int64_t* ev_id;
+  int32_t* ev_tensor;
+  int8_t* ev_dir;  // 0 out, 1 in
+  int8_t* ev_wraps;
+  int64_t* ev_trig;
+  int64_t* ev_delta;
+  int64_t* ev_start;
+  int64_t* ev_end;
+  int64_t* ev_earl;
+  int64_t* ev_late;
+  int64_t* ev_pair;
+  int64_t* ev_serves;
+  // busy structure: the job's swap intervals sorted by start (disjoint at shift 0)
+  int64_t* bz_s;
+  int64_t* bz_e;
+  int32_t* st_evcnt;  // [T] swap events per storage (storage_has_swap)
+  uint8_t* swapped;   // [T] SwapBudget::swapped_storages for this job
+  // recompute events (plan.hpp:34-42)
+  int64_t* rc_id;
+  int32_t* rc_tensor;
+  int64_t* rc_target;
+  int32_t* rc_regen;
+  int64_t* rc_lat;
+  int64_t* rc_saving;
+
+  // ---- report (PeakReport, peak.hpp:47-56) ----
+  uint8_t* in_peak;   // [T] storage resident at the peak
+  uint8_t* ev_drop;   // [Scap] scratch for revalidation
+  uint8_t* res_init;  // [T] scratch: initial residency (peak.cpp:176-190)
+  int64_t* curve_t;   // [Ecap+1]
+  int64_t* curve_b;   // [Ecap+1]
+
+  // ---- recompute rollback copies (recompute_planner.cpp:123, 148-151) ----
+  int64_t* bk_a_start;
+  int64_t* bk_a_end;
+  uint8_t* bk_flag;
+  uint8_t* bk_in_peak;
+  int64_t* bk_ev;      // 12 * Scap int64 words (all swap-event fields)
+  int64_t* bk_rc;      // 6 * Rcap words
+  int64_t* bk_bz;      // 2 * Scap
+  int32_t* bk_evcnt;   // [T]
+  int64_t* bk_curve;   // 2 * (Ecap+1)
+};
+
+// Mutable per-job scalars (kept apart so a rollback is one struct copy).
+struct JobState {
+  int32_t S, R;        // swap / recompute event counts
+  int32_t n_peak;      // |peak_tensors|
+  int32_t n_curve;     // footprint curve points
+  int64_t period;      // iteration_period (shifted by recomputation)
+  int64_t next_id;     // SchedulingPlan::next_event_id (plan.cpp:15-20)
+  int64_t peak, peak_time, lua;
+  int32_t has_lua;
+  int32_t dirty;       // plan changed since the last evaluation
+  int64_t n_events;    // timeline events of the last evaluation
+  int64_t son;         // SwapBudget::swapped_out_count[job] (swap_planner.cpp:278-282)
+};
+
+struct GroupConfig {
+  int64_t bw, setup, budget;
+  double stall_eps;
+  int32_t stall_min_iters;
+};
+
+// Device-side counters for the roofline (SURVEY §8(d) byte formula).
+struct GroupStats {
+  int64_t evaluations;       // analyze_job evaluations
+  int64_t timeline_events;   // sum of timeline events over evaluations
+  int64_t candidates;        // swap candidates visited
+  int64_t candidate_accesses;// storage accesses read by the scorer
+  int64_t busy_intervals;    // busy intervals swept by feasible-region queries
+  int64_t fit_queries;
+  int64_t loop_iterations;
+  int64_t sort_elems;        // elements through block sorts
+};
+
+struct GroupDev {
+  int32_t n_jobs;
+  int32_t coupled;      // some job has ratio < 1: swap passes run globally in order
+  int32_t hist_cap;
+  int32_t n_hist;
+  GroupConfig cfg;
+  JobDev* jobs;         // [n_jobs]
+  JobState* st;         // [n_jobs]
+  int64_t* hist;        // merged_peak_history
+  int64_t final_merged;
+  int32_t within_budget;
+  int32_t pad0;
+  int64_t total_swapped;  // SwapBudget::total_swapped
+  int32_t loop_iters;
+  int32_t pad2;
+  ErrInfo err;
+  GroupStats stats;
+  // timeline / sort scratch, capacity ecap (global memory)
+  int32_t ecap;
+  int32_t pad1;
+  uint64_t* k_key;   // [ecap]
+  int32_t* k_val;    // [ecap]
+  int64_t* x_time;   // [ecap] event time
+  int64_t* x_fp;     // [ecap] footprint after the event (sorted order)
+  int32_t* x_store;  // [ecap]
+  int32_t* x_aid;    // [ecap]
+  int8_t* x_type;    // [ecap] type | 8 if the TGA delta is 0 (aliased) | 16 if a flagged TUA
+  int8_t* x_job;     // [ecap]
+  uint8_t* x_state;  // [ecap] residency after the event (per-position)
+  int32_t* x_seq2;   // [ecap] positions grouped by (job, storage)
+  uint64_t* x_key2;  // [ecap]
+  int32_t* x_order;  // [ecap] sorted position -> slot
+};
+
+}  // namespace tsl

@@ -1,0 +1,53 @@
+// TEST INFRASTRUCTURE ONLY: runs tsl_plan.cuh's plan_group/analyze_group with a
+// one-thread host context in place of tsl_plan_kernel (see cuda_runtime.h here).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <utility>
+#include <vector>
+
+#include "tsl_kernel.h"
+#include "tsl_plan.cuh"
+
+namespace tsl {
+
+struct HostX {
+  static constexpr int W = 1;
+  int tid = 0, nthr = 1, lane = 0, warp = 0, nwarp = 1;
+  int64_t* sh = nullptr;
+  void sync() {}
+  void wsync() {}
+  bool wany(bool p) { return p; }
+  int64_t aadd(int64_t* p, int64_t v) { int64_t o = *p; *p += v; return o; }
+  int32_t aadd32(int32_t* p, int32_t v) { int32_t o = *p; *p += v; return o; }
+  void amin(int64_t* p, int64_t v) { if (v < *p) *p = v; }
+  void amax(int64_t* p, int64_t v) { if (v > *p) *p = v; }
+  void amax32(int32_t* p, int32_t v) { if (v > *p) *p = v; }
+  void errset(GroupDev& g, const ErrInfo& e) { if (!g.err.code) g.err = e; }
+  void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
+    if (n <= 1 || bits <= 0) return;
+    if (n > SORT_CAP) { std::fprintf(stderr, "emu: sort of %d > SORT_CAP\n", n); std::abort(); }
+    const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+    std::vector<std::pair<uint64_t, int32_t>> v(n);
+    for (int i = 0; i < n; ++i) v[i] = {keys[i], vals[i]};
+    std::stable_sort(v.begin(), v.end(), [&](const auto& a, const auto& b) { return (a.first & mask) < (b.first & mask); });
+    for (int i = 0; i < n; ++i) { keys[i] = v[i].first; vals[i] = v[i].second; }
+  }
+  void scan(int64_t* a, int n) { for (int i = 1; i < n; ++i) a[i] += a[i - 1]; }
+};
+
+size_t kernel_smem_bytes() { return SH_WORDS * sizeof(int64_t); }
+
+cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, cudaStream_t) {
+  std::vector<int64_t> sh(SH_WORDS);
+  for (int gi = 0; gi < n_groups; ++gi) {
+    HostX x;
+    x.sh = sh.data();
+    if (mode == 0) plan_group(x, groups[gi]);
+    else analyze_group(x, groups[gi]);
+  }
+  return cudaSuccess;
+}
+
+}  // namespace tsl

@@ -142,6 +142,12 @@ typedef struct tsl_stats {
   int64_t busy_intervals;    /* channel intervals scanned by gap searches   */
   int64_t algorithmic_bytes; /* SURVEY §8(d) byte formula over the build    */
   int64_t kernel_launches;   /* device kernels launched by this call        */
+  /* SM clock cycles spent per stage inside the planning CTA (thread 0):
+   * timeline builder, evaluator, swap passes, recompute passes, whole CTA */
+  int64_t cyc_sequence, cyc_evaluate, cyc_swap, cyc_recompute, cyc_total;
+  int64_t rescored;          /* speculative swap candidates re-scored in order */
+  /* inside the swap passes: speculation, conflicts, in-order sweep, merge */
+  int64_t cyc_spec, cyc_conflict, cyc_sweep, cyc_merge;
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

@@ -76,7 +76,11 @@ class TslStats(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("n_accesses", C.c_int64),
                 ("loop_iterations", C.c_int64), ("evaluations", C.c_int64), ("timeline_events", C.c_int64),
                 ("candidates", C.c_int64), ("candidate_accesses", C.c_int64), ("busy_intervals", C.c_int64),
-                ("algorithmic_bytes", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("algorithmic_bytes", C.c_int64), ("kernel_launches", C.c_int64),
+                ("cyc_sequence", C.c_int64), ("cyc_evaluate", C.c_int64), ("cyc_swap", C.c_int64),
+                ("cyc_recompute", C.c_int64), ("cyc_total", C.c_int64), ("rescored", C.c_int64),
+                ("cyc_spec", C.c_int64), ("cyc_conflict", C.c_int64), ("cyc_sweep", C.c_int64),
+                ("cyc_merge", C.c_int64)]
 
 
 def make_config(pcie_bandwidth: int = 1, transfer_setup: int = 0, memory_budget: int = 0,

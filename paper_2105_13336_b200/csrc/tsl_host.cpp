@@ -239,13 +239,14 @@ struct Layout {
 struct JobPlace {  // byte offsets into the device buffer
   size_t topo, o_lat, o_in_off, o_in, o_out_off, o_out, t_size, t_kind, t_rank, t_store, t_upd, t_prod, inflag;
   size_t a_tensor, a_store, a_type, a_start, a_end, a_base, a_flag, a_owned, s_off, s_acc, t_wfirst, t_utga;
-  size_t ev[12], bz_s, bz_e, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
+  size_t ev[12], bz_s, bz_e, pd_s, pd_e, pd_ts, pd_te, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
   size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve;
   int32_t Scap, Rcap, Ecap;
 };
 
 struct GroupPlace {
-  size_t hist;
+  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf;
+  int64_t pr_cap, w_cap, wcap;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
 };
@@ -441,6 +442,10 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
       p.t_utga = L.take<int32_t>(g.T);
       p.bz_s = L.take<int64_t>(p.Scap);
       p.bz_e = L.take<int64_t>(p.Scap);
+      p.pd_s = L.take<int64_t>(p.Scap);
+      p.pd_e = L.take<int64_t>(p.Scap);
+      p.pd_ts = L.take<int64_t>(p.Scap);
+      p.pd_te = L.take<int64_t>(p.Scap);
       p.st_evcnt = L.take<int32_t>(g.T);
       p.swapped = L.take<uint8_t>(g.T);
       p.ev_drop = L.take<uint8_t>(p.Scap);
@@ -469,6 +474,19 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
     q.x_seq2 = L.take<int32_t>(E);
     q.x_key2 = L.take<uint64_t>(E);
     q.x_order = L.take<int32_t>(E);
+    int64_t sumA = 0, sumT = 0;
+    for (auto& g : P->graphs[gi]) { sumA += g.A; sumT += g.T; }
+    q.pr_cap = sumA + sumT + 16;
+    q.w_cap = 2 * q.pr_cap + 2 * sumT + 16;
+    q.c_info = L.take<int32_t>(E * 16);
+    q.c_hull = L.take<int64_t>(E * 4);
+    q.dev_list = L.take<int64_t>(E);
+    q.pr_pool = L.take<uint8_t>(size_t(q.pr_cap) * tsl::PAIRREC_BYTES);
+    q.w_pool = L.take<int64_t>(size_t(2 * q.w_cap));
+    int64_t maxS = 0;
+    for (auto& p : P->jp[gi]) maxS = std::max<int64_t>(maxS, p.Scap);
+    q.wcap = 3 * maxS + 64;
+    q.wbuf = L.take<int64_t>(size_t(NT / 32) * 4 * q.wcap);
   }
   const size_t total = L.off;
   grow(ctx, total);
@@ -508,6 +526,15 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
     G->x_seq2 = dp<int32_t>(ctx, q.x_seq2);
     G->x_key2 = dp<uint64_t>(ctx, q.x_key2);
     G->x_order = dp<int32_t>(ctx, q.x_order);
+    G->c_info = dp<int32_t>(ctx, q.c_info);
+    G->c_hull = dp<int64_t>(ctx, q.c_hull);
+    G->dev_list = dp<int64_t>(ctx, q.dev_list);
+    G->pr_pool = reinterpret_cast<tsl::PairRec*>(static_cast<uint8_t*>(ctx->dbuf) + q.pr_pool);
+    G->w_pool = dp<int64_t>(ctx, q.w_pool);
+    G->pr_cap = q.pr_cap;
+    G->wbuf = dp<int64_t>(ctx, q.wbuf);
+    G->wcap = q.wcap;
+    G->w_cap = q.w_cap;
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
       const Graph& g = gs[k];
       const JobPlace& p = P->jp[gi][k];
@@ -570,6 +597,10 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
       J->ev_serves = dp<int64_t>(ctx, p.ev[11]);
       J->bz_s = dp<int64_t>(ctx, p.bz_s);
       J->bz_e = dp<int64_t>(ctx, p.bz_e);
+      J->pd_s = dp<int64_t>(ctx, p.pd_s);
+      J->pd_e = dp<int64_t>(ctx, p.pd_e);
+      J->pd_ts = dp<int64_t>(ctx, p.pd_ts);
+      J->pd_te = dp<int64_t>(ctx, p.pd_te);
       J->st_evcnt = dp<int32_t>(ctx, p.st_evcnt);
       J->swapped = dp<uint8_t>(ctx, p.swapped);
       J->rc_id = dp<int64_t>(ctx, p.rc[0]);
@@ -761,6 +792,16 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   s.busy_intervals = G.stats.busy_intervals;
   s.algorithmic_bytes = 24 * s.timeline_events + 24 * s.candidate_accesses + 16 * s.busy_intervals + 16 * s.candidates;
   s.kernel_launches = 1;
+  s.rescored = G.stats.rescored;
+  s.cyc_sequence = G.stats.cyc[0];
+  s.cyc_evaluate = G.stats.cyc[1];
+  s.cyc_swap = G.stats.cyc[2];
+  s.cyc_recompute = G.stats.cyc[3];
+  s.cyc_total = G.stats.cyc[4];
+  s.cyc_spec = G.stats.cyc[5];
+  s.cyc_conflict = G.stats.cyc[6];
+  s.cyc_sweep = G.stats.cyc[7];
+  s.cyc_merge = G.stats.cyc[8] + G.stats.cyc[9];
   return R;
 }
 

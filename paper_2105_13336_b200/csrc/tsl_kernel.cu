@@ -10,6 +10,8 @@
 
 namespace tsl {
 
+static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
+
 template <int IPT>
 using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;
 using BScan = cub::BlockScan<int64_t, NT>;
@@ -28,8 +30,20 @@ struct DevX {
   void* tmp;
 
   __device__ void sync() { __syncthreads(); }
+  __device__ int64_t clock() { return (int64_t)clock64(); }
   __device__ void wsync() { __syncwarp(); }
   __device__ bool wany(bool p) { return __any_sync(0xffffffffu, p); }
+  // warp exclusive prefix sum of v; *total = warp sum
+  __device__ int32_t wexcl(int32_t v, int32_t* total) {
+    int32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    *total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - v;
+  }
   __device__ int64_t aadd(int64_t* p, int64_t v) {
     return (int64_t)atomicAdd((unsigned long long*)p, (unsigned long long)v);
   }

@@ -72,38 +72,74 @@ TSL_HD int64_t duration(int64_t size, const GroupConfig& c) {
 // Feasible-region queries (swap_planner.cpp:26-72, 315-337)
 // ----------------------------------------------------------------------------
 // A stream is a run of intervals sorted by start AND end, lifted by `sh`.
+// Only the bound the sweep direction needs is searched; the other side ends
+// the stream lazily (starts are sorted, so a forward sweep stops at the
+// first start >= the window end; ends are sorted, so a reverse sweep stops
+// at the first end <= the window begin). The head interval is cached.
 struct Stream {
   const int64_t* s;
   const int64_t* e;
   const int32_t* ix;  // indirection (storage accesses) or null
-  int32_t i, j;       // live range [i, j)
+  int32_t i, n;       // forward: next index i of n; reverse: remaining [0, i)
   int64_t sh;
+  int64_t hs, he;     // cached head (lifted)
+  bool live;
 };
 TSL_HD int32_t sidx(const Stream& q, int32_t k) { return q.ix ? q.ix[k] : k; }
 
-// Intervals of a sorted run that intersect [L, H) form one index range:
-// ends are nondecreasing, so e > L is a suffix; s < H is a prefix.
-TSL_HD void clip_range(Stream& q, int32_t n, int64_t L, int64_t H) {
-  L -= q.sh;
-  H -= q.sh;
+TSL_HD void stream_load(Stream& q, bool fwd, int64_t b, int64_t e) {
+  if (fwd) {
+    q.live = q.i < q.n;
+    if (q.live) {
+      const int32_t k = sidx(q, q.i);
+      q.hs = q.s[k] + q.sh;
+      q.he = q.e[k] + q.sh;
+      q.live = q.hs < e;
+    }
+  } else {
+    q.live = q.i > 0;
+    if (q.live) {
+      const int32_t k = sidx(q, q.i - 1);
+      q.hs = q.s[k] + q.sh;
+      q.he = q.e[k] + q.sh;
+      q.live = q.he > b;
+    }
+  }
+}
+
+// Positions a stream on the intervals that intersect [b, e) (lifted).
+TSL_HD void stream_open(Stream& q, int32_t n, bool fwd, int64_t b, int64_t e) {
+  q.n = n;
+  const int64_t L = b - q.sh, H = e - q.sh;
   if (n == 0 || q.e[sidx(q, n - 1)] <= L || q.s[sidx(q, 0)] >= H) {
-    q.i = q.j = 0;
+    q.i = fwd ? n : 0;
+    q.live = false;
     return;
   }
-  int32_t lo = 0, hi = n;  // first k with e[k] > L
-  while (lo < hi) {
-    int32_t m = (lo + hi) >> 1;
-    if (q.e[sidx(q, m)] > L) hi = m; else lo = m + 1;
+  int32_t lo = 0, hi = n;
+  if (fwd) {  // first k with e[k] > L
+    while (lo < hi) {
+      int32_t m = (lo + hi) >> 1;
+      if (q.e[sidx(q, m)] > L) hi = m; else lo = m + 1;
+    }
+  } else {  // first k with s[k] >= H
+    while (lo < hi) {
+      int32_t m = (lo + hi) >> 1;
+      if (q.s[sidx(q, m)] >= H) hi = m; else lo = m + 1;
+    }
   }
   q.i = lo;
-  lo = q.i;
-  hi = n;  // first k with s[k] >= H
-  while (lo < hi) {
-    int32_t m = (lo + hi) >> 1;
-    if (q.s[sidx(q, m)] >= H) hi = m; else lo = m + 1;
-  }
-  q.j = lo;
+  stream_load(q, fwd, b, e);
 }
+
+// A sorted set of swap intervals (pairwise disjoint at shift 0, so ends are
+// sorted too): the pass-start busy structure, this pass's commits, or a
+// speculative candidate's own commits.
+struct Src {
+  const int64_t* s;
+  const int64_t* e;
+  int32_t n;
+};
 
 struct FitQuery {
   int32_t store;
@@ -112,79 +148,88 @@ struct FitQuery {
   int64_t xs, xe;
 };
 
+constexpr int64_t NONE = INT64_MIN;
+
 // busy_intervals (swap_planner.cpp:39-50) restricted to [b, e) + the
 // feasible_regions sweep + place_earliest / place_latest. Returns the
-// placement start, or INT64_MIN when no region of length >= d exists.
+// placement start, or NONE when no region of length >= d exists.
 // Forward sweep (earliest) stops at the first maximal free interval of length
 // >= d; the reverse sweep (latest) enumerates the same maximal free intervals
 // from the right.
-TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest,
-                   int64_t* swept) {
-  const int64_t NONE = INT64_MIN;
+TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
+                   int nsrc, int64_t* swept) {
   if (q.e <= q.b) return NONE;
+  const bool fwd = !latest;
   const int64_t P = imax(1, st.period);
-  Stream str[7];
+  Stream str[13];
   int ns = 0;
   const int32_t a0 = J.s_off[q.store], na = J.s_off[q.store + 1] - a0;
   int64_t exs[3], exe[3];
   int nex = 0;
   for (int k = -1; k <= 1; ++k) {
     const int64_t sh = k * P;
-    Stream ev{J.bz_s, J.bz_e, nullptr, 0, 0, sh};
-    clip_range(ev, st.S, q.b, q.e);
-    if (ev.j > ev.i) str[ns++] = ev;
-    Stream ac{J.a_start, J.a_end, J.s_acc + a0, 0, 0, sh};
-    clip_range(ac, na, q.b, q.e);
-    if (ac.j > ac.i) str[ns++] = ac;
+    for (int t = 0; t < nsrc; ++t) {
+      Stream& z = str[ns];
+      z.s = src[t].s; z.e = src[t].e; z.ix = nullptr; z.sh = sh;
+      stream_open(z, src[t].n, fwd, q.b, q.e);
+      if (z.live) ++ns;
+    }
+    Stream& z = str[ns];
+    z.s = J.a_start; z.e = J.a_end; z.ix = J.s_acc + a0; z.sh = sh;
+    stream_open(z, na, fwd, q.b, q.e);
+    if (z.live) ++ns;
     if (q.has_extra && q.xe > q.xs && q.xe + sh > q.b && q.xs + sh < q.e) {
       exs[nex] = q.xs + sh;
       exe[nex] = q.xe + sh;
       ++nex;
     }
   }
-  if (nex) str[ns++] = Stream{exs, exe, nullptr, 0, nex, 0};
+  if (nex) {
+    Stream& z = str[ns];
+    z.s = exs; z.e = exe; z.ix = nullptr; z.sh = 0; z.n = nex;
+    z.i = fwd ? 0 : nex;
+    stream_load(z, fwd, q.b, q.e);
+    if (z.live) ++ns;
+  }
   int64_t n_swept = 0;
   int64_t result = NONE;
-  if (!latest) {
+  if (fwd) {
     int64_t cursor = q.b;
+    bool found = false;
     for (;;) {
       int best = -1;
       int64_t bs = 0;
-      for (int t = 0; t < ns; ++t) {
-        if (str[t].i >= str[t].j) continue;
-        int64_t s = str[t].s[sidx(str[t], str[t].i)] + str[t].sh;
-        if (best < 0 || s < bs) { best = t; bs = s; }
-      }
+      for (int t = 0; t < ns; ++t)
+        if (str[t].live && (best < 0 || str[t].hs < bs)) { best = t; bs = str[t].hs; }
       if (best < 0) break;
       Stream& z = str[best];
-      int64_t be = z.e[sidx(z, z.i)] + z.sh;
+      const int64_t be = z.he;
       ++z.i;
+      stream_load(z, true, q.b, q.e);
       if (be <= bs) continue;  // lift_into drops empty intervals
       ++n_swept;
-      int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
+      const int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
       if (ce <= cs) continue;
-      if (cs > cursor && cs - cursor >= q.d) { result = cursor; break; }
+      if (cs > cursor && cs - cursor >= q.d) { found = true; break; }
       cursor = imax(cursor, ce);
     }
-    if (result == NONE && q.e > cursor && q.e - cursor >= q.d) result = cursor;
+    if (found || (q.e > cursor && q.e - cursor >= q.d)) result = cursor;
   } else {
     int64_t cur = q.e;
     bool found = false;
     for (;;) {
       int best = -1;
       int64_t be = 0;
-      for (int t = 0; t < ns; ++t) {
-        if (str[t].j <= str[t].i) continue;
-        int64_t e = str[t].e[sidx(str[t], str[t].j - 1)] + str[t].sh;
-        if (best < 0 || e > be) { best = t; be = e; }
-      }
+      for (int t = 0; t < ns; ++t)
+        if (str[t].live && (best < 0 || str[t].he > be)) { best = t; be = str[t].he; }
       if (best < 0) break;
       Stream& z = str[best];
-      int64_t bs = z.s[sidx(z, z.j - 1)] + z.sh;
-      --z.j;
+      const int64_t bs = z.hs;
+      --z.i;
+      stream_load(z, false, q.b, q.e);
       if (be <= bs) continue;
       ++n_swept;
-      int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
+      const int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
       if (ce <= cs) continue;
       if (cur > ce && cur - ce >= q.d) { found = true; break; }
       cur = imin(cur, cs);
@@ -196,8 +241,7 @@ TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool 
 }
 
 // ----------------------------------------------------------------------------
-// Plan mutation helpers (warp-redundant: every lane runs the scalar code and
-// writes identical values; bulk moves are split across lanes)
+// Plan mutation helpers
 // ----------------------------------------------------------------------------
 
 // anchor, swap_planner.cpp:76-93: the access with the greatest end <= t, ties
@@ -227,28 +271,17 @@ TSL_HD int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64
   return -1;
 }
 
-template <class X>
-TSL_HD void bz_insert(X& x, const JobDev& J, int32_t n, int64_t s, int64_t e) {
-  int32_t lo = 0, hi = n;  // first position with start > s
-  while (lo < hi) {
-    int32_t m = (lo + hi) >> 1;
-    if (J.bz_s[m] <= s) lo = m + 1; else hi = m;
-  }
-  const int32_t pos = lo;
-  x.wsync();
-  for (int32_t top = n; top > pos; top -= X::W) {
-    int32_t i = top - 1 - x.lane;
-    bool act = i >= pos;
-    int64_t vs = 0, ve = 0;
-    if (act) { vs = J.bz_s[i]; ve = J.bz_e[i]; }
-    x.wsync();
-    if (act) { J.bz_s[i + 1] = vs; J.bz_e[i + 1] = ve; }
-    x.wsync();
-  }
-  J.bz_s[pos] = s;
-  J.bz_e[pos] = e;
-  x.wsync();
-}
+// One committed (or speculatively scored) out/in pair, with its anchors and
+// the release flag it sets already resolved (make_event, swap_planner.cpp:95-113;
+// flag_release_before, :115-122).
+struct PairRec {
+  int64_t os, oe, o_earl, o_late, otrig, odelta;
+  int64_t is, ie, i_earl, i_late, itrig, idelta;
+  int64_t serves;
+  int32_t store, pre;
+  int32_t wraps, pad;
+  int64_t pad2;
+};
 
 struct PairSpec {
   int32_t store;
@@ -259,79 +292,198 @@ struct PairSpec {
   bool in_at_iter_start;  // schedule_wrapped_swap's forced anchor (swap_planner.cpp:448-452)
 };
 
-// make_event x2 + pair linking + flag_release_before (swap_planner.cpp:95-122,
-// 141-150, 376-386, 443-456).
-template <class X>
-TSL_HD bool commit_pair(X& x, const JobDev& J, JobState& st, const PairSpec& p, ErrInfo* err, int job) {
-  // All lanes read every scalar first, then barrier, then write: lanes of a
-  // warp need not run in lockstep, so a read-modify-write must never straddle
-  // another lane's store.
-  const int32_t S = st.S;
-  const int64_t id0 = st.next_id, id1 = id0 + 1;
-  const int32_t cnt = J.st_evcnt[p.store];
-  if (S + 2 > J.Scap) {
-    if (x.lane == 0) { err->code = E_CAPACITY; err->job = job; err->tensor = J.Scap; err->tick = 0; }
-    return false;
-  }
-  int64_t otrig, odelta, itrig, idelta;
-  anchor(J, st, p.os, p.wraps, otrig, odelta);
-  if (p.in_at_iter_start) { itrig = -1; idelta = p.is - st.period; }
-  else anchor(J, st, p.is, p.wraps, itrig, idelta);
-  const int32_t pre = preceding_access(J, p.store, p.os, -2);
-  x.wsync();
-  const int32_t i0 = S, i1 = S + 1;
-  J.ev_id[i0] = id0; J.ev_tensor[i0] = p.store; J.ev_dir[i0] = 0; J.ev_wraps[i0] = p.wraps;
-  J.ev_trig[i0] = otrig; J.ev_delta[i0] = odelta; J.ev_start[i0] = p.os; J.ev_end[i0] = p.oe;
-  J.ev_earl[i0] = p.o_earl; J.ev_late[i0] = p.o_late; J.ev_pair[i0] = id1; J.ev_serves[i0] = -1;
-  J.ev_id[i1] = id1; J.ev_tensor[i1] = p.store; J.ev_dir[i1] = 1; J.ev_wraps[i1] = p.wraps;
-  J.ev_trig[i1] = itrig; J.ev_delta[i1] = idelta; J.ev_start[i1] = p.is; J.ev_end[i1] = p.ie;
-  J.ev_earl[i1] = p.i_earl; J.ev_late[i1] = p.i_late; J.ev_pair[i1] = id0; J.ev_serves[i1] = p.serves;
-  bz_insert(x, J, S, p.os, p.oe);
-  bz_insert(x, J, S + 1, p.is, p.ie);
-  st.S = S + 2;
-  st.next_id = id0 + 2;
-  J.st_evcnt[p.store] = cnt + 2;
-  if (pre >= 0) J.a_flag[pre] = 1;
-  st.dirty = 1;
-  x.wsync();
-  return true;
+TSL_HD PairRec resolve_pair(const JobDev& J, const JobState& st, const PairSpec& p) {
+  PairRec r;
+  r.os = p.os; r.oe = p.oe; r.o_earl = p.o_earl; r.o_late = p.o_late;
+  r.is = p.is; r.ie = p.ie; r.i_earl = p.i_earl; r.i_late = p.i_late;
+  r.serves = p.serves; r.store = p.store; r.wraps = p.wraps ? 1 : 0; r.pad = 0;
+  anchor(J, st, p.os, p.wraps, r.otrig, r.odelta);
+  if (p.in_at_iter_start) { r.itrig = -1; r.idelta = p.is - st.period; }
+  else anchor(J, st, p.is, p.wraps, r.itrig, r.idelta);
+  r.pre = preceding_access(J, p.store, p.os, -2);
+  return r;
 }
 
-// try_gap_pair, swap_planner.cpp:126-152.
+// This pass's committed intervals J.pd_[0, pend_n): the prefix
+// [0, pend_sorted) is sorted by start, commits taken verbatim from the
+// speculation are appended unsorted. Before a re-score the (short) suffix is
+// ranked and merged in with binary searches (tmp: 2 * pend_n scratch words).
+// Warp-collective.
 template <class X>
-TSL_HD bool try_gap_pair(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t store, int64_t lo,
-                         int64_t hi, int64_t serves, GroupStats* gs, ErrInfo* err, int job) {
-  const int64_t d = duration(J.t_size[store], c);
+TSL_HD void pend_sort(X& x, const JobDev& J, JobState& st, int64_t* tmp) {
+  const int32_t n = st.pend_n, p = st.pend_sorted;
+  if (p >= n) return;
+  const int32_t k = n - p;
+  int64_t* ts = tmp;      // sorted suffix
+  int64_t* te = tmp + k;
+  x.wsync();
+  for (int32_t i = x.lane; i < k; i += X::W) {
+    const int64_t si = J.pd_s[p + i];
+    int32_t r = 0;
+    for (int32_t t = 0; t < k; ++t) {
+      const int64_t sj = J.pd_s[p + t];
+      r += (sj < si || (sj == si && t < i)) ? 1 : 0;
+    }
+    ts[r] = si;
+    te[r] = J.pd_e[p + i];
+  }
+  x.wsync();
+  for (int32_t i = x.lane; i < p; i += X::W) {  // prefix element: + suffix elements before it
+    const int64_t si = J.pd_s[i];
+    int32_t lo = 0, hi = k;
+    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (ts[m] < si) lo = m + 1; else hi = m; }
+    J.pd_ts[i + lo] = si;
+    J.pd_te[i + lo] = J.pd_e[i];
+  }
+  for (int32_t r = x.lane; r < k; r += X::W) {  // suffix element: + prefix elements up to it
+    const int64_t si = ts[r];
+    int32_t lo = 0, hi = p;
+    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (J.pd_s[m] <= si) lo = m + 1; else hi = m; }
+    J.pd_ts[r + lo] = si;
+    J.pd_te[r + lo] = te[r];
+  }
+  x.wsync();
+  for (int32_t i = x.lane; i < n; i += X::W) { J.pd_s[i] = J.pd_ts[i]; J.pd_e[i] = J.pd_te[i]; }
+  x.wsync();
+  st.pend_sorted = n;
+  x.wsync();
+}
+
+// Inserts one interval into the sorted pass list (re-scoring commits).
+template <class X>
+TSL_HD void pend_insert(X& x, const JobDev& J, int32_t n, int64_t s, int64_t e) {
+  int32_t lo = 0, hi = n;  // first position with start > s
+  while (lo < hi) {
+    int32_t m = (lo + hi) >> 1;
+    if (J.pd_s[m] <= s) lo = m + 1; else hi = m;
+  }
+  const int32_t pos = lo;
+  x.wsync();
+  for (int32_t top = n; top > pos; top -= X::W) {
+    int32_t i = top - 1 - x.lane;
+    bool act = i >= pos;
+    int64_t vs = 0, ve = 0;
+    if (act) { vs = J.pd_s[i]; ve = J.pd_e[i]; }
+    x.wsync();
+    if (act) { J.pd_s[i + 1] = vs; J.pd_e[i + 1] = ve; }
+    x.wsync();
+  }
+  J.pd_s[pos] = s;
+  J.pd_e[pos] = e;
+  x.wsync();
+}
+
+// Re-scoring context (one warp, warp-redundant): busy = pass-start structure
+// + every interval committed earlier in this pass (sorted) + this schedule's
+// own commits; pairs are recorded into the candidate's pool slot.
+template <class X>
+struct ReCtx {
+  X& x;
+  const JobDev& J;
+  JobState& st;
+  const GroupConfig& cfg;
+  GroupStats* gs;
+  PairRec* out;
+  int32_t nout, cap;
+  bool overflow;
+  TSL_HD int64_t query(const FitQuery& q, bool latest) {
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n}, {J.pd_s, J.pd_e, st.pend_n}};
+    int64_t sw = 0;
+    int64_t r = fit(J, st, q, latest, src, 2, &sw);
+    gs->fit_queries += 1;
+    gs->busy_intervals += sw;
+    return r;
+  }
+  TSL_HD bool commit(const PairSpec& p) {
+    const int32_t pn = st.pend_n;
+    if (nout >= cap || pn + 2 > J.Scap) { overflow = true; return false; }
+    const PairRec r = resolve_pair(J, st, p);
+    x.wsync();
+    out[nout] = r;
+    x.wsync();
+    pend_insert(x, J, pn, r.os, r.oe);
+    pend_insert(x, J, pn + 1, r.is, r.ie);
+    st.pend_n = pn + 2;
+    st.pend_sorted = pn + 2;
+    ++nout;
+    x.wsync();
+    return true;
+  }
+};
+
+constexpr int SPEC_MAXP = 48;   // private intervals of one speculative schedule
+constexpr int CAPC = 7;         // conflict list entries per candidate
+
+// Speculative context (one thread, one candidate): busy = pass-start
+// structure + the candidate's own commits; pairs and the effective windows of
+// every successful query are recorded for validation at commit time.
+struct SpecCtx {
+  const JobDev& J;
+  const JobState& st;
+  const GroupConfig& cfg;
+  GroupStats* gs;
+  int64_t ps[SPEC_MAXP], pe[SPEC_MAXP];
+  int32_t np;
+  PairRec* pairs;
+  int32_t npairs, cap_pairs;
+  int64_t* win;  // (lo, hi) pairs
+  int32_t nwin, cap_win;
+  bool overflow;
+  TSL_HD int64_t query(const FitQuery& q, bool latest) {
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n}, {ps, pe, np}};
+    int64_t sw = 0;
+    int64_t r = fit(J, st, q, latest, src, 2, &sw);
+    gs->fit_queries += 1;
+    gs->busy_intervals += sw;
+    if (r != NONE) {
+      // A later commit can only change this answer if it intersects the part
+      // of the window the answer depends on; a failed query stays failed.
+      if (nwin >= cap_win) { overflow = true; return r; }
+      win[2 * nwin] = latest ? r : q.b;
+      win[2 * nwin + 1] = latest ? q.e : r + q.d;
+      ++nwin;
+    }
+    return r;
+  }
+  TSL_HD void ins(int64_t s, int64_t e) {
+    int32_t i = np;
+    while (i > 0 && ps[i - 1] > s) { ps[i] = ps[i - 1]; pe[i] = pe[i - 1]; --i; }
+    ps[i] = s; pe[i] = e;
+    ++np;
+  }
+  TSL_HD bool commit(const PairSpec& p) {
+    if (npairs >= cap_pairs || np + 2 > SPEC_MAXP) { overflow = true; return false; }
+    pairs[npairs++] = resolve_pair(J, st, p);
+    ins(p.os, p.oe);
+    ins(p.is, p.ie);
+    return true;
+  }
+};
+
+// try_gap_pair, swap_planner.cpp:126-152.
+template <class C>
+TSL_HD bool try_gap_pair(C& c, int32_t store, int64_t lo, int64_t hi, int64_t serves) {
+  const int64_t d = duration(c.J.t_size[store], c.cfg);
   if (hi - lo < 2 * d) return false;
-  FitQuery q{store, lo, hi, d, false, 0, 0};
-  int64_t sw = 0;
-  int64_t os = fit(J, st, q, false, &sw);
-  gs->fit_queries += 1;
-  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+  const int64_t os = c.query(FitQuery{store, lo, hi, d, false, 0, 0}, false);
+  if (os == NONE) return false;
   // the busy list is the one filtered for [lo, hi) plus the out interval; the
   // in-regions re-clip to [out.end, hi], where that out interval is empty.
-  FitQuery qi{store, os + d, hi, d, false, 0, 0};
-  int64_t is = fit(J, st, qi, true, &sw);
-  gs->fit_queries += 1;
-  gs->busy_intervals += sw;
-  if (is == INT64_MIN) return false;
-  PairSpec p{store, os, os + d, lo, hi, is, is + d, os + d, hi, false, serves, false};
-  return commit_pair(x, J, st, p, err, job);
+  const int64_t is = c.query(FitQuery{store, os + d, hi, d, false, 0, 0}, true);
+  if (is == NONE) return false;
+  return c.commit(PairSpec{store, os, os + d, lo, hi, is, is + d, os + d, hi, false, serves, false});
 }
 
 // schedule_swap, swap_planner.cpp:339-399, single shot: a failed swap-in
 // placement leaves the next retry with the same swap-out region, the same
 // first access and the same swap-in window, so the reference's retry loop
 // (swap_planner.cpp:503-513) can never succeed after the first failure.
-template <class X>
-TSL_HD bool schedule_swap(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t store,
-                          int64_t earliest, int64_t latest, GroupStats* gs, ErrInfo* err, int job) {
-  const int64_t d = duration(J.t_size[store], c);
-  FitQuery q{store, earliest, latest, d, false, 0, 0};
-  int64_t sw = 0;
-  int64_t os = fit(J, st, q, false, &sw);
-  gs->fit_queries += 1;
-  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+template <class C>
+TSL_HD bool schedule_swap(C& c, int32_t store, int64_t earliest, int64_t latest) {
+  const JobDev& J = c.J;
+  const int64_t d = duration(J.t_size[store], c.cfg);
+  const int64_t os = c.query(FitQuery{store, earliest, latest, d, false, 0, 0}, false);
+  if (os == NONE) return false;
   const int64_t oe = os + d;
   const int32_t a0 = J.s_off[store], a1 = J.s_off[store + 1];
   int32_t fk = -1;
@@ -339,52 +491,40 @@ TSL_HD bool schedule_swap(X& x, const JobDev& J, JobState& st, const GroupConfig
     int32_t a = J.s_acc[k];
     if (J.a_type[a] == ACC_TUA && J.a_start[a] >= oe) { fk = k; break; }
   }
-  gs->candidate_accesses += a1 - a0;
-  if (fk < 0) { gs->busy_intervals += sw; return false; }
+  c.gs->candidate_accesses += a1 - a0;
+  if (fk < 0) return false;
   const int32_t fa = J.s_acc[fk];
   const int64_t fs = J.a_start[fa];
-  FitQuery qi{store, oe, fs, d, true, os, oe};
-  int64_t is = fit(J, st, qi, true, &sw);
-  gs->fit_queries += 1;
-  gs->busy_intervals += sw;
-  if (is == INT64_MIN) return false;
-  PairSpec p{store, os, oe, earliest, latest, is, is + d, oe, fs, false, fa, false};
-  if (!commit_pair(x, J, st, p, err, job)) return false;
+  const int64_t is = c.query(FitQuery{store, oe, fs, d, true, os, oe}, true);
+  if (is == NONE) return false;
+  if (!c.commit(PairSpec{store, os, oe, earliest, latest, is, is + d, oe, fs, false, fa, false})) return false;
   // Greedily keep the tensor offloaded between its remaining uses.
   for (int32_t k = fk; k + 1 < a1; ++k) {
     int32_t a = J.s_acc[k], b = J.s_acc[k + 1];
     if (J.a_type[b] != ACC_TUA) continue;
-    try_gap_pair(x, J, st, c, store, J.a_end[a], J.a_start[b], b, gs, err, job);
-    if (err->code) return false;
+    try_gap_pair(c, store, J.a_end[a], J.a_start[b], b);
   }
   return true;
 }
 
 // schedule_wrapped_swap, swap_planner.cpp:401-459.
-template <class X>
-TSL_HD bool schedule_wrapped_swap(X& x, const JobDev& J, JobState& st, const GroupConfig& c, int32_t param,
-                                  GroupStats* gs, ErrInfo* err, int job) {
+template <class C>
+TSL_HD bool schedule_wrapped_swap(C& c, int32_t param) {
+  const JobDev& J = c.J;
   if (J.t_upd[param] < 0) return false;
-  const int64_t d = duration(J.t_size[param], c);
-  const int64_t period = st.period;
+  const int64_t d = duration(J.t_size[param], c.cfg);
+  const int64_t period = c.st.period;
   const int32_t ut = J.t_utga[param];
   const int64_t tga_end = ut >= 0 ? J.a_end[ut] : -1;
   if (tga_end < 0) return false;
-  FitQuery q{param, tga_end, period, d, false, 0, 0};
-  int64_t sw = 0;
-  int64_t os = fit(J, st, q, false, &sw);
-  gs->fit_queries += 1;
-  if (os == INT64_MIN) { gs->busy_intervals += sw; return false; }
+  const int64_t os = c.query(FitQuery{param, tga_end, period, d, false, 0, 0}, false);
+  if (os == NONE) return false;
   const int32_t fa = J.t_wfirst[param];
-  if (fa < 0) { gs->busy_intervals += sw; return false; }
+  if (fa < 0) return false;
   const int64_t in_lo = period, in_hi = period + J.a_start[fa];
-  FitQuery qi{param, in_lo, in_hi, d, true, os, os + d};
-  int64_t is = fit(J, st, qi, true, &sw);
-  gs->fit_queries += 1;
-  gs->busy_intervals += sw;
-  if (is == INT64_MIN) return false;
-  PairSpec p{param, os, os + d, tga_end, period, is, is + d, in_lo, in_hi, true, fa, true};
-  return commit_pair(x, J, st, p, err, job);
+  const int64_t is = c.query(FitQuery{param, in_lo, in_hi, d, true, os, os + d}, true);
+  if (is == NONE) return false;
+  return c.commit(PairSpec{param, os, os + d, tga_end, period, is, is + d, in_lo, in_hi, true, fa, true});
 }
 
 // swap_window, swap_planner.cpp:290-313.
@@ -400,6 +540,15 @@ TSL_HD bool swap_window(const JobDev& J, int32_t store, int64_t peak_time, int64
   if (!has_tga && J.t_kind[store] == K_INTERIM) return false;
   if (earliest < 0) earliest = 0;
   return true;
+}
+
+// Which branch swap_pass takes for a candidate (swap_planner.cpp:489-513):
+// 1 wrapped, 2 normal (window in earliest/latest), 0 skip, -1 error.
+TSL_HD int candidate_kind(const JobDev& J, const JobState& st, int32_t s, int64_t& earliest, int64_t& latest) {
+  if (J.t_kind[s] == K_PARAM && J.t_upd[s] >= 0) return 1;
+  if (J.s_off[s + 1] - J.s_off[s] <= 1) return 0;
+  if (!swap_window(J, s, st.peak_time, earliest, latest)) return -1;
+  return latest > earliest ? 2 : 0;
 }
 
 // ----------------------------------------------------------------------------
@@ -873,16 +1022,98 @@ TSL_HD bool refresh(X& x, GroupDev& g, int j0, int j1, bool force) {
 }
 
 // ----------------------------------------------------------------------------
-// Stage 3+4: swap pass (swap_planner.cpp:461-520)
+// Stage 3+4: swap pass (swap_planner.cpp:461-520), speculate -> validate ->
+// commit in order.
+//
+//  A. every candidate is scored by one thread against the pass-start busy set
+//     plus its own commits (SpecCtx), recording its pairs and the effective
+//     windows of its successful queries;
+//  B. for every candidate, the earlier candidates of the same job whose
+//     speculative intervals (lifted by -P/0/+P) touch one of its windows;
+//  C. one warp per job (one warp overall when a swap ratio < 1 couples the
+//     jobs through SwapBudget) walks the candidates in the reference order and
+//     decides: a candidate none of whose conflicting predecessors committed as
+//     speculated, and whose windows no re-scored commit touches, keeps its
+//     speculative result; any other candidate is re-scored against the real
+//     state (ReCtx), exactly like the sequential reference. Event slots and
+//     ids are assigned here, in order;
+//  D. all threads write the committed events, flags and counters;
+//  E. one block sort rebuilds every job's sorted busy structure.
 // ----------------------------------------------------------------------------
+enum { CI_P0 = 0, CI_NP, CI_W0, CI_NW, CI_STATUS, CI_NCONF, CI_CONF, CI_STATE = CI_CONF + CAPC, CI_EV0, CI_ID0,
+       CI_STRIDE = 16 };
+enum { CS_FAIL = 0, CS_OK = 1, CS_OVERFLOW = 2, CS_SKIP = 3, CS_ERROR = 4 };
+
+TSL_HD bool hits(int64_t s, int64_t e, int64_t wl, int64_t wh, int64_t P) {
+  for (int k = -1; k <= 1; ++k) {
+    const int64_t sh = k * P;
+    if (s + sh < wh && wl < e + sh) return true;
+  }
+  return false;
+}
+
+// Sorted busy structure of every job rebuilt from the plan: one block sort of
+// (job, start) keys.
+template <class X>
+TSL_HD void rebuild_busy(X& x, GroupDev& g) {
+  int64_t* gsh = x.sh + MAXB * NF;
+  if (x.tid == 0) {
+    int64_t off = 0, mx = 0;
+    for (int j = 0; j < g.n_jobs; ++j) { gsh[16 + j] = off; off += g.st[j].S; }
+    gsh[15] = off;
+    (void)mx;
+    gsh[14] = 0;
+  }
+  x.sync();
+  const int64_t n = gsh[15];
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    int64_t mx = 0;
+    for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) mx = imax(mx, J.ev_start[i]);
+    x.amax(&gsh[14], mx);
+  }
+  x.sync();
+  if (n > g.ecap) {
+    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = -1; g.err.tensor = n; g.err.tick = 3; }
+    x.sync();
+    return;
+  }
+  const int jbits = nbits(uint64_t(g.n_jobs - 1));
+  const int tbits = nbits(uint64_t(gsh[14]));
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    const int64_t base = gsh[16 + j];
+    for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) {
+      g.k_key[base + i] = (uint64_t(j) << tbits) | uint64_t(J.ev_start[i]);
+      g.k_val[base + i] = (j << 24) | i;
+    }
+  }
+  x.sync();
+  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits);
+  for (int64_t m = x.tid; m < n; m += x.nthr) {
+    const int j = g.k_val[m] >> 24;
+    const int32_t i = g.k_val[m] & 0xffffff;
+    const JobDev& J = g.jobs[j];
+    const int64_t pos = m - gsh[16 + j];
+    J.bz_s[pos] = J.ev_start[i];
+    J.bz_e[pos] = J.ev_end[i];
+  }
+  for (int j = x.tid; j < g.n_jobs; j += x.nthr) g.st[j].bz_n = g.st[j].S;
+  x.sync();
+}
+
 template <class X>
 TSL_HD bool swap_pass(X& x, GroupDev& g) {
   int64_t* sh = x.sh;
-  int64_t* gsh = sh + MAXB * NF;  // [8]=nc [9]=maxT [10]=changed [11]=cursor [12]=maxsize [16..] segments
+  int64_t* gsh = sh + MAXB * NF;  // [9]=maxT [10]=changed [11]=cursor [12]=maxsize [13..14] pools [16..] segments
   if (x.tid == 0) {
     int64_t maxT = 1;
     for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
-    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1;
+    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[13] = 0; gsh[14] = 0;
+    for (int j = 0; j < g.n_jobs; ++j) {
+      JobState& st = g.st[j];
+      st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
+    }
   }
   x.sync();
   for (int j = 0; j < g.n_jobs; ++j) {
@@ -910,7 +1141,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       if (coupled) k = (((inv << jbits) | uint64_t(J.rank)) << rbits) | uint64_t(J.t_rank[t]);
       else k = (((uint64_t(j) << sbits) | inv) << rbits) | uint64_t(J.t_rank[t]);
       g.k_key[slot] = k;
-      g.k_val[slot] = (j << 24) | t;  // the host guarantees T < 2^24 and < 128 jobs
+      g.k_val[slot] = (j << 24) | t;  // the host guarantees T < 2^24 and <= 128 jobs
     }
   }
   x.sync();
@@ -929,45 +1160,179 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       for (int64_t m = nc - 1; m >= 0; --m) gsh[16 + (g.k_val[m] >> 24)] = m;
       for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
     }
-    gsh[13] = 0;
   }
   x.sync();
+  int64_t t0 = x.clock(), t1;
+  auto tick = [&](int k) { t1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += t1 - t0; t0 = t1; };
+  // ---- A. speculative scoring, one thread per candidate ----
+  {
+    GroupStats ls{};
+    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      const int j = g.k_val[m] >> 24;
+      const int32_t s = g.k_val[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      const JobState& st = g.st[j];
+      int32_t* ci = g.c_info + m * CI_STRIDE;
+      int64_t* hl = g.c_hull + m * 4;
+      ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
+      ci[CI_P0] = -1;
+      hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
+      if (J.swapped[s]) { ci[CI_STATUS] = CS_SKIP; continue; }
+      int64_t earliest = 0, latest = 0;
+      const int kind = candidate_kind(J, st, s, earliest, latest);
+      if (kind == 0) { ci[CI_STATUS] = CS_SKIP; continue; }
+      if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
+      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+      const int32_t capw = 2 * capp + 2;
+      const int64_t p0 = x.aadd(&gsh[13], capp);
+      const int64_t w0 = x.aadd(&gsh[14], capw);
+      if (p0 + capp > g.pr_cap || w0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
+      ci[CI_P0] = int32_t(p0);
+      SpecCtx c{J, st, g.cfg, &ls, {}, {}, 0, g.pr_pool + p0, 0, capp, g.w_pool + 2 * w0, 0, capw, false};
+      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+      ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
+      ci[CI_NP] = c.npairs;
+      ci[CI_W0] = int32_t(w0);
+      ci[CI_NW] = c.nwin;
+      for (int32_t w = 0; w < c.nwin; ++w) {
+        hl[0] = imin(hl[0], c.win[2 * w]);
+        hl[1] = imax(hl[1], c.win[2 * w + 1]);
+      }
+      for (int32_t p = 0; p < c.npairs; ++p) {
+        hl[2] = imin(hl[2], imin(c.pairs[p].os, c.pairs[p].is));
+        hl[3] = imax(hl[3], imax(c.pairs[p].oe, c.pairs[p].ie));
+      }
+    }
+    x.aadd(&g.stats.fit_queries, ls.fit_queries);
+    x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+    x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+  }
+  x.sync();
+  tick(5);
+  // ---- B. conflicts with earlier speculative commits of the same job ----
+  for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    int32_t* ci = g.c_info + m * CI_STRIDE;
+    if (ci[CI_NW] == 0) continue;
+    const int j = g.k_val[m] >> 24;
+    const int64_t P = imax(1, g.st[j].period);
+    const int64_t* hl = g.c_hull + m * 4;
+    const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+    const int64_t m0 = coupled ? 0 : gsh[16 + j];
+    int32_t nconf = 0;
+    for (int64_t i = m0; i < m; ++i) {
+      if ((g.k_val[i] >> 24) != j) continue;
+      const int32_t* cj = g.c_info + i * CI_STRIDE;
+      if (cj[CI_STATUS] != CS_OK) continue;
+      const int64_t* hi_ = g.c_hull + i * 4;
+      if (!hits(hi_[2], hi_[3], hl[0], hl[1], P)) continue;
+      const PairRec* pr = g.pr_pool + cj[CI_P0];
+      bool conf = false;
+      for (int32_t p = 0; p < cj[CI_NP] && !conf; ++p)
+        for (int32_t w = 0; w < ci[CI_NW] && !conf; ++w)
+          conf = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                 hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
+      if (conf) {
+        if (nconf < CAPC) ci[CI_CONF + nconf] = int32_t(i);
+        ++nconf;
+      }
+    }
+    ci[CI_NCONF] = nconf;
+  }
+  x.sync();
+  tick(6);
+  // ---- C. in-order decisions ----
   const int nseg = coupled ? 1 : g.n_jobs;
   for (int seg = x.warp; seg < nseg; seg += x.nwarp) {
     GroupStats ls{};
     ErrInfo lerr{};
     const int64_t m0 = coupled ? 0 : gsh[16 + seg];
     const int64_t m1 = coupled ? nc : gsh[16 + seg + 1];
+    int64_t* wtmp = g.wbuf + int64_t(x.warp) * 4 * g.wcap;
+    int32_t ndev = 0;
     bool changed = false;
     for (int64_t m = m0; m < m1; ++m) {
       const int j = g.k_val[m] >> 24;
       const int32_t s = g.k_val[m] & 0xffffff;
       const JobDev& J = g.jobs[j];
       JobState& st = g.st[j];
-      if (J.swapped[s]) continue;  // SwapBudget::already_swapped
+      int32_t* ci = g.c_info + m * CI_STRIDE;
+      const int32_t status = ci[CI_STATUS];
+      if (status == CS_SKIP) continue;
       if (coupled && g.total_swapped != 0) {  // SwapBudget::allows, swap_planner.cpp:268-276
         const double lhs = double(st.son + 1) / double(g.total_swapped + 1);
         if (!(lhs <= J.ratio)) continue;
       }
-      bool ok = false;
-      if (J.t_kind[s] == K_PARAM && J.t_upd[s] >= 0) {
-        ok = schedule_wrapped_swap(x, J, st, g.cfg, s, &ls, &lerr, j);
-      } else {
-        if (J.s_off[s + 1] - J.s_off[s] <= 1) continue;
-        int64_t earliest, latest;
-        if (!swap_window(J, s, st.peak_time, earliest, latest)) {
-          lerr.code = E_NO_TGA; lerr.job = j; lerr.tensor = s; lerr.tick = 0;
-        } else if (latest > earliest) {
-          ok = schedule_swap(x, J, st, g.cfg, s, earliest, latest, &ls, &lerr, j);
+      if (status == CS_ERROR) { lerr.code = E_NO_TGA; lerr.job = j; lerr.tensor = s; lerr.tick = 0; break; }
+      if (ci[CI_P0] < 0) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = g.pr_cap; lerr.tick = 4; break; }
+      const int64_t P = imax(1, st.period);
+      bool valid = status != CS_OVERFLOW && ci[CI_NCONF] <= CAPC;
+      for (int32_t k = 0; valid && k < ci[CI_NCONF]; ++k)
+        if (g.c_info[int64_t(ci[CI_CONF + k]) * CI_STRIDE + CI_STATE] == 1) valid = false;
+      if (valid && ndev) {
+        const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+        for (int32_t d = 0; d < ndev && valid; ++d) {
+          const int64_t dm = g.dev_list[m0 + d];
+          if ((g.k_val[dm] >> 24) != j) continue;
+          const int32_t* cd = g.c_info + dm * CI_STRIDE;
+          const PairRec* pr = g.pr_pool + cd[CI_P0];
+          for (int32_t p = 0; p < cd[CI_NP] && valid; ++p)
+            for (int32_t w = 0; w < ci[CI_NW] && valid; ++w)
+              if (hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                  hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P))
+                valid = false;
         }
       }
-      if (lerr.code) break;
-      if (ok) {  // SwapBudget::record
+      int32_t np = 0;
+      int32_t state = 0;
+      if (valid) {
+        if (status == CS_OK) {
+          np = ci[CI_NP];
+          state = 1;
+          const PairRec* pr = g.pr_pool + ci[CI_P0];
+          const int32_t pn = st.pend_n;
+          if (pn + 2 * np > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; break; }
+          x.wsync();
+          for (int32_t p = x.lane; p < np; p += X::W) {
+            J.pd_s[pn + 2 * p] = pr[p].os; J.pd_e[pn + 2 * p] = pr[p].oe;
+            J.pd_s[pn + 2 * p + 1] = pr[p].is; J.pd_e[pn + 2 * p + 1] = pr[p].ie;
+          }
+          st.pend_n = pn + 2 * np;
+          x.wsync();
+        }
+      } else {
+        ls.rescored += 1;
+        int64_t earliest = 0, latest = 0;
+        const int kind = candidate_kind(J, st, s, earliest, latest);
+        const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+        pend_sort(x, J, st, wtmp);
+        ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+        const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+        if (c.overflow) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; lerr.tick = 5; break; }
+        if (ok) {
+          np = c.nout;
+          state = 2;
+          x.wsync();
+          g.dev_list[m0 + ndev] = m;
+          ci[CI_NP] = np;
+          ++ndev;
+          x.wsync();
+        }
+      }
+      if (state) {  // SwapBudget::record + event slots/ids in plan order
         const int64_t son = st.son, tot = g.total_swapped;
+        const int32_t S = st.S;
+        const int64_t id = st.next_id;
+        if (S + 2 * np > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; break; }
         x.wsync();
+        ci[CI_STATE] = state;
+        ci[CI_EV0] = S;
+        ci[CI_ID0] = int32_t(id);
         J.swapped[s] = 1;
         st.son = son + 1;
         if (coupled) g.total_swapped = tot + 1;
+        st.S = S + 2 * np;
+        st.next_id = id + 2 * np;
+        st.dirty = 1;
         changed = true;
         x.wsync();
       }
@@ -979,9 +1344,39 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       x.aadd(&g.stats.fit_queries, ls.fit_queries);
       x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
       x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+      x.aadd(&g.stats.rescored, ls.rescored);
     }
   }
   x.sync();
+  tick(7);
+  if (g.err.code) return false;
+  // ---- D. write the committed events (make_event + pair links + flags) ----
+  for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    const int32_t* ci = g.c_info + m * CI_STRIDE;
+    if (!ci[CI_STATE]) continue;
+    const int j = g.k_val[m] >> 24;
+    const JobDev& J = g.jobs[j];
+    const PairRec* pr = g.pr_pool + ci[CI_P0];
+    const int32_t np = ci[CI_NP];
+    for (int32_t p = 0; p < np; ++p) {
+      const PairRec& r = pr[p];
+      const int32_t i0 = ci[CI_EV0] + 2 * p, i1 = i0 + 1;
+      const int64_t id0 = int64_t(ci[CI_ID0]) + 2 * p, id1 = id0 + 1;
+      J.ev_id[i0] = id0; J.ev_tensor[i0] = r.store; J.ev_dir[i0] = 0; J.ev_wraps[i0] = int8_t(r.wraps);
+      J.ev_trig[i0] = r.otrig; J.ev_delta[i0] = r.odelta; J.ev_start[i0] = r.os; J.ev_end[i0] = r.oe;
+      J.ev_earl[i0] = r.o_earl; J.ev_late[i0] = r.o_late; J.ev_pair[i0] = id1; J.ev_serves[i0] = -1;
+      J.ev_id[i1] = id1; J.ev_tensor[i1] = r.store; J.ev_dir[i1] = 1; J.ev_wraps[i1] = int8_t(r.wraps);
+      J.ev_trig[i1] = r.itrig; J.ev_delta[i1] = r.idelta; J.ev_start[i1] = r.is; J.ev_end[i1] = r.ie;
+      J.ev_earl[i1] = r.i_earl; J.ev_late[i1] = r.i_late; J.ev_pair[i1] = id0; J.ev_serves[i1] = r.serves;
+      if (r.pre >= 0) J.a_flag[r.pre] = 1;
+    }
+    x.aadd32(&J.st_evcnt[g.k_val[m] & 0xffffff], 2 * np);
+  }
+  x.sync();
+  tick(8);
+  // ---- E. sorted busy structure for the next pass ----
+  if (gsh[10]) rebuild_busy(x, g);
+  tick(9);
   return gsh[10] != 0;
 }
 
@@ -1316,12 +1711,19 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
 // ----------------------------------------------------------------------------
 template <class X>
 TSL_HD void plan_group(X& x, GroupDev& g) {
+  int64_t c0 = x.clock(), c1;
+  const int64_t cstart = c0;
+  auto lap = [&](int k) { c1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += c1 - c0; c0 = c1; };
   for (int j = 0; j < g.n_jobs; ++j) build_sequence(x, g, j);
+  lap(0);
   if (!refresh(x, g, 0, g.n_jobs, true)) return;  // make_job_context's refresh
+  lap(1);
   bool swap_ok = true, rc_ok = true;
   int iter = 0;
   while (swap_ok || rc_ok) {
+    c0 = x.clock();
     if (!refresh(x, g, 0, g.n_jobs, false)) return;  // only jobs whose plan changed
+    lap(1);
     int64_t merged = 0;
     for (int j = 0; j < g.n_jobs; ++j) merged += g.st[j].peak;
     if (x.tid == 0) {
@@ -1338,9 +1740,13 @@ TSL_HD void plan_group(X& x, GroupDev& g) {
       if (before > 0 && (before - now) / before < g.cfg.stall_eps) break;
     }
     if (swap_ok) {
+      c0 = x.clock();
       swap_ok = swap_pass(x, g);
+      lap(2);
     } else if (merged >= g.cfg.budget) {
+      c0 = x.clock();
       rc_ok = recompute_pass(x, g);
+      lap(3);
     } else {
       rc_ok = false;
     }
@@ -1355,6 +1761,7 @@ TSL_HD void plan_group(X& x, GroupDev& g) {
     g.within_budget = merged <= g.cfg.budget;
     g.loop_iters = iter;
     g.stats.loop_iterations = iter;
+    g.stats.cyc[4] = x.clock() - cstart;
   }
   x.sync();
 }

@@ -11,6 +11,8 @@
 
 namespace tsl {
 
+struct PairRec;
+
 // AccessType (access.hpp:11): TGA = generating access, TUA = using access.
 enum : int8_t { ACC_TGA = 0, ACC_TUA = 1 };
 // TimelineEventType (peak.hpp:33-39), same order == same type rank.
@@ -91,6 +93,10 @@ struct JobDev {
   // busy structure: the job's swap intervals sorted by start (disjoint at shift 0)
   int64_t* bz_s;
   int64_t* bz_e;
+  int64_t* pd_s;   // [Scap] this pass's committed intervals
+  int64_t* pd_e;
+  int64_t* pd_ts;  // [Scap] merge scratch
+  int64_t* pd_te;
   int32_t* st_evcnt;  // [T] swap events per storage (storage_has_swap)
   uint8_t* swapped;   // [T] SwapBudget::swapped_storages for this job
   // recompute events (plan.hpp:34-42)
@@ -132,6 +138,10 @@ struct JobState {
   int32_t dirty;       // plan changed since the last evaluation
   int64_t n_events;    // timeline events of the last evaluation
   int64_t son;         // SwapBudget::swapped_out_count[job] (swap_planner.cpp:278-282)
+  int32_t bz_n;        // events reflected in the sorted busy structure
+  int32_t pend_n;      // this pass's commits not yet merged into it
+  int32_t pend_sorted; // pend_[0, pend_sorted) is sorted by start
+  int32_t pad_;
 };
 
 struct GroupConfig {
@@ -150,6 +160,8 @@ struct GroupStats {
   int64_t fit_queries;
   int64_t loop_iterations;
   int64_t sort_elems;        // elements through block sorts
+  int64_t rescored;          // swap candidates re-scored after speculation
+  int64_t cyc[16];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
 };
 
 struct GroupDev {
@@ -184,6 +196,15 @@ struct GroupDev {
   int32_t* x_seq2;   // [ecap] positions grouped by (job, storage)
   uint64_t* x_key2;  // [ecap]
   int32_t* x_order;  // [ecap] sorted position -> slot
+  // speculative swap pass scratch (tsl_plan.cuh swap_pass)
+  int32_t* c_info;   // [ecap * 16]
+  int64_t* c_hull;   // [ecap * 4]
+  int64_t* dev_list; // [ecap]
+  PairRec* pr_pool;  // [pr_cap]
+  int64_t* w_pool;   // [2 * w_cap]
+  int64_t pr_cap, w_cap;
+  int64_t* wbuf;     // [NT/32 warps * 4 * wcap] re-scoring gather scratch
+  int64_t wcap;
 };
 
 }  // namespace tsl

@@ -17,8 +17,10 @@ struct HostX {
   int tid = 0, nthr = 1, lane = 0, warp = 0, nwarp = 1;
   int64_t* sh = nullptr;
   void sync() {}
+  int64_t clock() { return 0; }
   void wsync() {}
   bool wany(bool p) { return p; }
+  int32_t wexcl(int32_t v, int32_t* total) { *total = v; return 0; }
   int64_t aadd(int64_t* p, int64_t v) { int64_t o = *p; *p += v; return o; }
   int32_t aadd32(int32_t* p, int32_t v) { int32_t o = *p; *p += v; return o; }
   void amin(int64_t* p, int64_t v) { if (v < *p) *p = v; }

@@ -1,0 +1,21 @@
+"""Per-stage SM-cycle breakdown of the planning kernel (dev tool)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import ref
+from paper_2105_13336_b200 import configs as CF
+from paper_2105_13336_b200.planner import Planner
+P = Planner(0)
+for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
+    reqs = CF.requests(name)
+    for req in [reqs[-1]]:
+        cfg = req.config(ref.initial_peaks(req.jobs))
+        P.build_plan(req.jobs, cfg)
+        p = P.build_plan(req.jobs, cfg)
+        s = p["stats"]
+        tot = s["cyc_total"] or 1
+        print(f"{req.name} A={req.n_accesses} kernel={s['kernel_ms']:.3f}ms cyc_total={tot} "
+              f"seq={s['cyc_sequence']/tot:.2%} eval={s['cyc_evaluate']/tot:.2%} swap={s['cyc_swap']/tot:.2%} "
+              f"rc={s['cyc_recompute']/tot:.2%} evals={s['evaluations']} events={s['timeline_events']} "
+              f"cands={s['candidates']} queries={s['busy_intervals']} rescored={s['rescored']} "
+              f"spec={s['cyc_spec']/tot:.2%} conflict={s['cyc_conflict']/tot:.2%} sweep={s['cyc_sweep']/tot:.2%} "
+              f"merge={s['cyc_merge']/tot:.2%}", flush=True)

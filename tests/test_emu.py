@@ -1,0 +1,100 @@
+"""Algorithm checks on CPU through the TEST-ONLY emulation build
+(tests/emu: the product's tsl_plan.cuh + tsl_host.cpp compiled for the host
+with a one-thread execution context). The product library never contains
+this build; the GPU tests (test_gpu_parity.py) check the CUDA build itself.
+"""
+import json
+
+import pytest
+
+from helpers import check_against_golden, config_jobs, ensure_emu, fuzz_jobs, golden
+from paper_2105_13336_b200 import abi, workload as W
+from paper_2105_13336_b200.planner import Planner, ValidationError
+
+
+@pytest.fixture(scope="module")
+def emu():
+    return Planner(lib_path=ensure_emu())
+
+
+@pytest.mark.parametrize("case", [c for c in golden("configs") if c["name"].split(".")[0] in ("C1", "C2", "C3")
+                                  or c["name"] in ("C5s0.7", "C5s0.14", "C5s1.7", "C5s3.5")],
+                         ids=lambda c: f"{c['name']}-r{c['ratio']}")
+def test_configs(emu, case):
+    check_against_golden(emu.build_plan(config_jobs(case), case["config"]), case)
+
+
+@pytest.mark.parametrize("case", golden("fuzz")[::2], ids=lambda c: f"seed{c['seed']}")
+def test_fuzz(emu, case):
+    check_against_golden(emu.build_plan(fuzz_jobs(case), case["config"]), case)
+
+
+def test_handbuilt(emu):
+    for name, spec in golden("handbuilt").items():
+        for case in spec["cases"]:
+            check_against_golden(emu.build_plan([(spec["graph"], spec["latencies"])], case["config"]), case)
+
+
+def test_analyze(emu):
+    for c in golden("analyze"):
+        r = emu.analyze_job(c["graph"], c["latencies"], c["plan"])
+        assert json.loads(r["report_json"]) == c["report"], c["name"]
+
+
+def _chain():
+    g = W.generate_workload("chain", 1, 0, 3, "cj")
+    return g, W.true_latency_table(g, 1)
+
+
+# (mutation, expected ValidationError text) -- texts from graph.cpp:49-119,
+# access.cpp:33-38, config.hpp:25-35
+ERRORS = [
+    (lambda g, l, c: g["tensors"][1].update(size=0), "nonpositive size for tensor a01"),
+    (lambda g, l, c: g["tensors"].append(dict(g["tensors"][0])), "duplicate tensor id x"),
+    (lambda g, l, c: g["ops"].append(dict(g["ops"][0])), "duplicate op id f01"),
+    (lambda g, l, c: g["ops"][1]["outputs"].append("a01"), "tensor a01 has more than one producer"),
+    (lambda g, l, c: g["tensors"].append({"id": "zz", "size": 1, "kind": "interim"}), "tensor zz has no producing op"),
+    (lambda g, l, c: l.pop("b02"), "missing latency entry for op b02"),
+    (lambda g, l, c: l.update(f02=-1), "negative latency for op f02"),
+    (lambda g, l, c: c.update(pcie_bandwidth=0), "pcie_bandwidth must be positive"),
+    (lambda g, l, c: c.update(transfer_setup=-1), "transfer_setup must be nonnegative"),
+    (lambda g, l, c: c.update(memory_budget=-5), "memory_budget must be nonnegative"),
+    (lambda g, l, c: c.update(stall_epsilon=2.0), "stall_epsilon out of (0,1)"),
+    (lambda g, l, c: c.update(max_swap_ratios={"cj": 1.5}), "max swap ratio for cj out of (0,1]"),
+]
+
+
+@pytest.mark.parametrize("mutate,msg", ERRORS, ids=[m for _, m in ERRORS])
+def test_validation_errors(emu, mutate, msg):
+    g, l = _chain()
+    cfg = {"pcie_bandwidth": 4, "transfer_setup": 0, "memory_budget": 0}
+    mutate(g, l, cfg)
+    with pytest.raises(ValidationError) as e:
+        emu.build_plan([(g, l)], cfg)
+    assert str(e.value) == msg
+
+
+def test_cycle_detected(emu):
+    g = {"job_id": "cyc", "tensors": [{"id": "a", "size": 1, "kind": "interim"},
+                                      {"id": "b", "size": 1, "kind": "interim"}],
+         "ops": [{"id": "p", "kind": "f", "inputs": ["b"], "outputs": ["a"], "attributes": [], "phase": "forward_backward"},
+                 {"id": "q", "kind": "f", "inputs": ["a"], "outputs": ["b"], "attributes": [], "phase": "forward_backward"}]}
+    with pytest.raises(ValidationError, match="cycle detected in graph of job cyc"):
+        emu.build_plan([(g, {"p": 1, "q": 1})], {"pcie_bandwidth": 1, "transfer_setup": 0, "memory_budget": 0})
+
+
+def test_empty_build(emu):
+    out = emu.build_plan([], {"pcie_bandwidth": 1, "transfer_setup": 0, "memory_budget": 0})
+    assert out["plans_json"] == "null\n" and out["merged_peak_history"] == []
+
+
+def test_groups_equal_single_calls(emu):
+    from paper_2105_13336_b200 import configs as CF
+    reqs = CF.requests("C3")
+    cfgs = [r.config(CF.INITIAL_PEAK) for r in reqs]
+    # one shared config: use the last request's budget for all three groups
+    outs = emu.build_plan_groups([r.jobs for r in reqs], cfgs[-1])
+    for r, o in zip(reqs, outs):
+        single = emu.build_plan(r.jobs, cfgs[-1])
+        assert o["plans_json"] == single["plans_json"]
+        assert o["merged_peak_history"] == single["merged_peak_history"]

@@ -148,6 +148,8 @@ typedef struct tsl_stats {
   int64_t rescored;          /* speculative swap candidates re-scored in order */
   /* inside the swap passes: speculation, conflicts, in-order sweep, merge */
   int64_t cyc_spec, cyc_conflict, cyc_sweep, cyc_merge;
+  int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by this call     */
+  double prep_ms;               /* host validation + packing before the H2D  */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;
@@ -165,11 +167,14 @@ int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs,
                    const tsl_config* cfg, tsl_result** out);
 
 /* Several independent build_plan calls ("job groups", e.g. the 8 workload
- * shards of one GPU) planned by ONE device launch, one CTA per group.
- * group_offsets[n_groups+1] partitions jobs[]. out[g] receives each result. */
+ * shards of one GPU, or every arrival/departure replan of a scenario) planned
+ * by ONE device launch, one CTA per group. group_offsets[n_groups+1]
+ * partitions jobs[]. cfgs holds n_cfgs configs: 1 (shared by every group) or
+ * n_groups (one per group, e.g. a per-set memory budget). out[g] receives
+ * each group's result. */
 int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs,
                           const int32_t* group_offsets, int32_t n_groups,
-                          const tsl_config* cfg, tsl_result** out);
+                          const tsl_config* cfgs, int32_t n_cfgs, tsl_result** out);
 
 /* The same call split in three so inputs can stay resident in HBM between
  * device-only runs (bench.py's device-timed `value`):
@@ -179,7 +184,7 @@ int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs,
  *   tsl_plan_collect  one D2H copy + results; out[n_groups]
  * tsl_build_plan_groups == prepare + run(1) + collect. */
 int tsl_plan_prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets,
-                     int32_t n_groups, const tsl_config* cfg, tsl_plan** out);
+                     int32_t n_groups, const tsl_config* cfgs, int32_t n_cfgs, tsl_plan** out);
 int tsl_plan_run(tsl_plan* plan, int32_t repeats, double* kernel_ms);
 /* Enqueue one launch on `stream` (a cudaStream_t, NULL = the context stream)
  * without synchronising -- for callers that time with their own events. */

@@ -297,7 +297,7 @@ struct tsl_plan {
   std::vector<std::vector<Graph>> graphs;  // per group, caller order
   std::vector<std::vector<JobPlace>> jp;
   std::vector<GroupPlace> gp;
-  tsl_config cfg{};
+  std::vector<tsl_config> cfgs;
   size_t h2d_bytes = 0;          // [0, h2d_bytes) uploaded
   size_t d2h_off = 0, d2h_bytes = 0;
   size_t groups_off = 0, jobs_off = 0, states_off = 0;
@@ -342,13 +342,14 @@ struct CallerPlan {
 };
 
 tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, int32_t n_groups,
-                  const tsl_config* cfg, int mode, const tsl_plan_desc* caller) {
+                  const tsl_config* cfgs, int32_t n_cfgs, int mode, const tsl_plan_desc* caller) {
+  if (n_cfgs != 1 && n_cfgs != n_groups) fail(TSL_ERR_ARGUMENT, "n_cfgs must be 1 or n_groups");
   auto t0 = std::chrono::steady_clock::now();
   auto* P = new tsl_plan();
   P->ctx = ctx;
   P->mode = mode;
   P->n_groups = n_groups;
-  P->cfg = *cfg;
+  P->cfgs.assign(cfgs, cfgs + n_cfgs);
   P->graphs.resize(n_groups);
   // 1. validate graphs (caller order), then the config, then latencies
   for (int gi = 0; gi < n_groups; ++gi) {
@@ -357,7 +358,7 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
   for (int gi = 0; gi < n_groups; ++gi) {
     std::vector<const Graph*> gg;
     for (auto& g : P->graphs[gi]) gg.push_back(&g);
-    if (mode == 0) validate_config(*cfg, gg);
+    if (mode == 0) validate_config(cfgs[n_cfgs == 1 ? 0 : gi], gg);
     std::set<std::string> ids;
     for (auto& g : P->graphs[gi]) {
       if (!ids.insert(g.job_id).second)
@@ -499,6 +500,7 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
     std::vector<int32_t> jrank = lex_rank(jids);
     bool coupled = false;
     for (auto& g : gs) coupled = coupled || g.ratio < 1.0;
+    const tsl_config* cfg = &cfgs[n_cfgs == 1 ? 0 : gi];
     GroupDev* G = hp<GroupDev>(ctx, P->groups_off) + gi;
     std::memset(G, 0, sizeof *G);
     G->n_jobs = static_cast<int32_t>(gs.size());
@@ -780,7 +782,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   R->within = G.within_budget != 0;
   if (P->mode == 0 && !R->within)
     R->diagnostic = "merged memory peak " + std::to_string(G.final_merged) + " still exceeds budget " +
-                    std::to_string(P->cfg.memory_budget) + " after exhausting swap and recomputation";
+                    std::to_string(G.cfg.budget) + " after exhausting swap and recomputation";
   tsl_stats& s = R->stats;
   s.kernel_ms = P->last_kernel_ms;
   for (auto& g : R->graphs) s.n_accesses += g.A;
@@ -792,6 +794,9 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   s.busy_intervals = G.stats.busy_intervals;
   s.algorithmic_bytes = 24 * s.timeline_events + 24 * s.candidate_accesses + 16 * s.busy_intervals + 16 * s.candidates;
   s.kernel_launches = 1;
+  s.h2d_bytes = static_cast<int64_t>(P->h2d_bytes);
+  s.d2h_bytes = static_cast<int64_t>(P->d2h_bytes);
+  s.prep_ms = P->prep_ms;
   s.rescored = G.stats.rescored;
   s.cyc_sequence = G.stats.cyc[0];
   s.cyc_evaluate = G.stats.cyc[1];
@@ -983,11 +988,11 @@ int tsl_destroy(tsl_ctx* c) {
 }
 
 int tsl_plan_prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets, int32_t n_groups,
-                     const tsl_config* cfg, tsl_plan** out) {
-  if (!ctx || !cfg || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+                     const tsl_config* cfgs, int32_t n_cfgs, tsl_plan** out) {
+  if (!ctx || !cfgs || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfg, 0, nullptr);
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr);
     try {
       upload(P);
     } catch (...) {
@@ -1038,12 +1043,12 @@ int tsl_plan_collect(tsl_plan* P, tsl_result** out) {
 void tsl_plan_destroy(tsl_plan* P) { delete P; }
 
 int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* group_offsets, int32_t n_groups,
-                          const tsl_config* cfg, tsl_result** out) {
-  if (!ctx || !cfg || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+                          const tsl_config* cfgs, int32_t n_cfgs, tsl_result** out) {
+  if (!ctx || !cfgs || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfg, 0, nullptr);
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr);
     std::vector<tsl_result*> rs;
     try {
       upload(P);
@@ -1079,7 +1084,7 @@ int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs, const
       *out = new tsl_result();
     });
   }
-  return tsl_build_plan_groups(ctx, jobs, offs, 1, cfg, out);
+  return tsl_build_plan_groups(ctx, jobs, offs, 1, cfg, 1, out);
 }
 
 int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* plan, tsl_result** out) {
@@ -1089,7 +1094,7 @@ int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* 
     tsl_config cfg;
     tsl_config_default(&cfg);
     const int32_t offs[2] = {0, 1};
-    tsl_plan* P = prepare(ctx, job, offs, 1, &cfg, 1, plan);
+    tsl_plan* P = prepare(ctx, job, offs, 1, &cfg, 1, 1, plan);
     tsl_result* r = nullptr;
     try {
       upload(P);

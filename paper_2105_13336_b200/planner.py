@@ -51,9 +51,9 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     L.tsl_destroy.argtypes = [vp]
     L.tsl_build_plan.argtypes = [vp, C.POINTER(abi.TslJobDesc), C.c_int32, C.POINTER(abi.TslConfig), C.POINTER(vp)]
     L.tsl_build_plan_groups.argtypes = [vp, C.POINTER(abi.TslJobDesc), C.POINTER(C.c_int32), C.c_int32,
-                                        C.POINTER(abi.TslConfig), C.POINTER(vp)]
+                                        C.POINTER(abi.TslConfig), C.c_int32, C.POINTER(vp)]
     L.tsl_plan_prepare.argtypes = [vp, C.POINTER(abi.TslJobDesc), C.POINTER(C.c_int32), C.c_int32,
-                                   C.POINTER(abi.TslConfig), C.POINTER(vp)]
+                                   C.POINTER(abi.TslConfig), C.c_int32, C.POINTER(vp)]
     L.tsl_plan_run.argtypes = [vp, C.c_int32, C.POINTER(C.c_double)]
     L.tsl_plan_launch_async.argtypes = [vp, vp]
     L.tsl_plan_collect.argtypes = [vp, C.POINTER(vp)]
@@ -201,9 +201,20 @@ class Planner:
         out["ms"] = (t1 - t0) * 1e3
         return out
 
-    def _pack_groups(self, groups: Sequence[Sequence], config: dict):
+    @staticmethod
+    def _configs(config, n_groups: int):
+        """One shared config dict, or a list with one config per group."""
+        cfgs = list(config) if isinstance(config, (list, tuple)) else [config]
+        if len(cfgs) not in (1, n_groups):
+            raise ValueError("need one config or one per group")
+        arr = (abi.TslConfig * len(cfgs))(*[abi.make_config(**c) for c in cfgs])
+        ratios: Dict[str, float] = {}
+        for c in cfgs:
+            ratios.update(c.get("max_swap_ratios") or {})
+        return arr, len(cfgs), ratios
+
+    def _pack_groups(self, groups: Sequence[Sequence], ratios: dict):
         flat = [j for grp in groups for j in grp]
-        ratios = dict(config.get("max_swap_ratios") or {})
         descs, arr = abi.pack_jobs(flat, ratios)
         offs = (C.c_int32 * (len(groups) + 1))()
         k = 0
@@ -213,12 +224,13 @@ class Planner:
         offs[len(groups)] = k
         return descs, arr, offs
 
-    def build_plan_groups(self, groups: Sequence[Sequence], config: dict, with_views: bool = True) -> List[dict]:
-        """Independent build_plan calls (one per group) in ONE kernel launch."""
-        descs, arr, offs = self._pack_groups(groups, config)
-        cfg = abi.make_config(**config)
+    def build_plan_groups(self, groups: Sequence[Sequence], config, with_views: bool = True) -> List[dict]:
+        """Independent build_plan calls (one per group) in ONE kernel launch.
+        `config` is one dict shared by all groups or a list, one per group."""
+        cfgs, ncfg, ratios = self._configs(config, len(groups))
+        descs, arr, offs = self._pack_groups(groups, ratios)
         res = (C.c_void_p * len(groups))()
-        rc = self.lib.tsl_build_plan_groups(self._ctx, arr, offs, len(groups), C.byref(cfg), res)
+        rc = self.lib.tsl_build_plan_groups(self._ctx, arr, offs, len(groups), cfgs, ncfg, res)
         if rc:
             _raise(self.lib, rc)
         outs = []
@@ -229,11 +241,11 @@ class Planner:
                 self.lib.tsl_result_destroy(res[g])
         return outs
 
-    def prepare(self, groups: Sequence[Sequence], config: dict) -> PreparedPlan:
-        descs, arr, offs = self._pack_groups(groups, config)
-        cfg = abi.make_config(**config)
+    def prepare(self, groups: Sequence[Sequence], config) -> PreparedPlan:
+        cfgs, ncfg, ratios = self._configs(config, len(groups))
+        descs, arr, offs = self._pack_groups(groups, ratios)
         h = C.c_void_p()
-        rc = self.lib.tsl_plan_prepare(self._ctx, arr, offs, len(groups), C.byref(cfg), C.byref(h))
+        rc = self.lib.tsl_plan_prepare(self._ctx, arr, offs, len(groups), cfgs, ncfg, C.byref(h))
         if rc:
             _raise(self.lib, rc)
         return PreparedPlan(self, h, descs, len(groups))

@@ -230,7 +230,10 @@ def run_ours(a, rank, world, local):
     cfgs = [c for _, _, c in reqs]
     ev = sum(n_accesses(j) for j in groups)
     prep = planner.prepare(groups, cfgs)
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream: the kernel is launched on it and the CUDA
+    # events are recorded on it
+    stream = torch.cuda.Stream(device=f"cuda:{local}")
+    torch.cuda.set_stream(stream)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
     # e2e path: the caller's packed descriptors, one C-ABI call per step
     cfg_arr, ncfg, ratios = planner._configs(cfgs, len(groups))
@@ -262,7 +265,7 @@ def run_ours(a, rank, world, local):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     wall0 = time.perf_counter()
     for e0, e1 in evs:
-        flush.zero_()
+        flush.zero_()  # on the same stream, outside the event pair
         e0.record(stream)
         prep.launch_async(stream.cuda_stream)
         e1.record(stream)

@@ -280,18 +280,34 @@ struct tsl_result {
   tsl_stats stats{};
 };
 
+// Device buffer + pinned staging buffer. One-shot calls reuse the context's;
+// a prepared plan owns its own so its resident inputs survive other calls.
+struct Buffers {
+  void* dbuf = nullptr;
+  size_t dcap = 0;
+  uint8_t* hbuf = nullptr;
+  size_t hcap = 0;
+  void release() {
+    if (dbuf) cudaFree(dbuf);
+    if (hbuf) cudaFreeHost(hbuf);
+    dbuf = nullptr;
+    hbuf = nullptr;
+    dcap = hcap = 0;
+  }
+};
+
 struct tsl_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  void* dbuf = nullptr;
-  size_t dcap = 0;
-  uint8_t* hbuf = nullptr;  // pinned staging
-  size_t hcap = 0;
+  Buffers buf;
 };
 
 struct tsl_plan {
   tsl_ctx* ctx = nullptr;
+  Buffers* buf = nullptr;  // ctx->buf, or own_buf for a prepared plan
+  Buffers own_buf;
+  ~tsl_plan() { own_buf.release(); }
   int mode = 0;  // 0 build_plan, 1 analyze_job
   int32_t n_groups = 0;
   std::vector<std::vector<Graph>> graphs;  // per group, caller order
@@ -309,7 +325,7 @@ struct tsl_plan {
 
 namespace {
 
-void grow(tsl_ctx* c, size_t need) {
+void grow(Buffers* c, size_t need) {
   if (need > c->dcap) {
     if (c->dbuf) cudaFree(c->dbuf);
     c->dbuf = nullptr;
@@ -327,12 +343,12 @@ void grow(tsl_ctx* c, size_t need) {
 }
 
 template <class T>
-T* hp(tsl_ctx* c, size_t off) { return reinterpret_cast<T*>(c->hbuf + off); }
+T* hp(Buffers* c, size_t off) { return reinterpret_cast<T*>(c->hbuf + off); }
 template <class T>
-T* dp(tsl_ctx* c, size_t off) { return reinterpret_cast<T*>(static_cast<uint8_t*>(c->dbuf) + off); }
+T* dp(Buffers* c, size_t off) { return reinterpret_cast<T*>(static_cast<uint8_t*>(c->dbuf) + off); }
 
 template <class T>
-void put(tsl_ctx* c, size_t off, const std::vector<T>& v) {
+void put(Buffers* c, size_t off, const std::vector<T>& v) {
   if (!v.empty()) std::memcpy(c->hbuf + off, v.data(), v.size() * sizeof(T));
 }
 
@@ -341,12 +357,14 @@ struct CallerPlan {
   const tsl_plan_desc* p = nullptr;
 };
 
-tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, int32_t n_groups,
-                  const tsl_config* cfgs, int32_t n_cfgs, int mode, const tsl_plan_desc* caller) {
+tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, int32_t n_groups,
+                  const tsl_config* cfgs, int32_t n_cfgs, int mode, const tsl_plan_desc* caller, bool own) {
   if (n_cfgs != 1 && n_cfgs != n_groups) fail(TSL_ERR_ARGUMENT, "n_cfgs must be 1 or n_groups");
   auto t0 = std::chrono::steady_clock::now();
   auto* P = new tsl_plan();
-  P->ctx = ctx;
+  P->ctx = cx;
+  P->buf = own ? &P->own_buf : &cx->buf;
+  Buffers* ctx = P->buf;
   P->mode = mode;
   P->n_groups = n_groups;
   P->cfgs.assign(cfgs, cfgs + n_cfgs);
@@ -679,29 +697,24 @@ tsl_plan* prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* offs, i
 }
 
 void upload(tsl_plan* P) {
-  tsl_ctx* c = P->ctx;
-  cuda_check(cudaMemcpyAsync(c->dbuf, c->hbuf, P->h2d_bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+  Buffers* b = P->buf;
+  cuda_check(cudaMemcpyAsync(b->dbuf, b->hbuf, P->h2d_bytes, cudaMemcpyHostToDevice, P->ctx->stream), "H2D");
 }
 
 void launch(tsl_plan* P, int repeats, bool timed) {
   tsl_ctx* c = P->ctx;
-  GroupDev* dg = dp<GroupDev>(c, P->groups_off);
+  GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
-  for (int r = 0; r < repeats; ++r) {
-    if (r > 0) {  // re-arm the mutable group header for a repeated device-only run
-      cuda_check(cudaMemcpyAsync(dg, hp<GroupDev>(c, P->groups_off), sizeof(GroupDev) * P->n_groups,
-                                 cudaMemcpyHostToDevice, c->stream), "H2D");
-    }
+  for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
     cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, c->stream), "launch");
-  }
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
-void download(tsl_plan* P) {
-  tsl_ctx* c = P->ctx;
-  cuda_check(cudaMemcpyAsync(c->hbuf + P->d2h_off, static_cast<uint8_t*>(c->dbuf) + P->d2h_off, P->d2h_bytes,
-                             cudaMemcpyDeviceToHost, c->stream), "D2H");
-  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+void download(tsl_plan* P, cudaStream_t s) {
+  Buffers* b = P->buf;
+  cuda_check(cudaMemcpyAsync(b->hbuf + P->d2h_off, static_cast<uint8_t*>(b->dbuf) + P->d2h_off, P->d2h_bytes,
+                             cudaMemcpyDeviceToHost, s), "D2H");
+  cuda_check(cudaStreamSynchronize(s), "sync");
 }
 
 std::string err_text(const GroupDev& G, const std::vector<Graph>& gs) {
@@ -721,7 +734,7 @@ std::string err_text(const GroupDev& G, const std::vector<Graph>& gs) {
 }
 
 tsl_result* collect_group(tsl_plan* P, int gi) {
-  tsl_ctx* c = P->ctx;
+  Buffers* c = P->buf;
   const GroupDev& G = hp<GroupDev>(c, P->groups_off)[gi];
   if (G.err.code) {
     int code = G.err.code == E_CAPACITY ? TSL_ERR_CAPACITY
@@ -978,8 +991,7 @@ int tsl_create(int device, tsl_ctx** out) {
 int tsl_destroy(tsl_ctx* c) {
   if (!c) return TSL_OK;
   cudaSetDevice(c->device);
-  if (c->dbuf) cudaFree(c->dbuf);
-  if (c->hbuf) cudaFreeHost(c->hbuf);
+  c->buf.release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -992,9 +1004,10 @@ int tsl_plan_prepare(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t* grou
   if (!ctx || !cfgs || !out || !group_offsets || n_groups < 0) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr);
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr, true);
     try {
       upload(P);
+      cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
     } catch (...) {
       delete P;
       throw;
@@ -1020,7 +1033,7 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     tsl_ctx* c = P->ctx;
-    cuda_check(launch_plan_kernel(dp<GroupDev>(c, P->groups_off), P->n_groups, P->mode,
+    cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode,
                                   stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
   });
 }
@@ -1028,7 +1041,8 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
 int tsl_plan_collect(tsl_plan* P, tsl_result** out) {
   if (!P || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
-    download(P);
+    cuda_check(cudaDeviceSynchronize(), "sync");  // launches may sit on a caller stream
+    download(P, P->ctx->stream);
     std::vector<tsl_result*> rs;
     try {
       for (int gi = 0; gi < P->n_groups; ++gi) rs.push_back(collect_group(P, gi));
@@ -1048,12 +1062,12 @@ int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t*
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr);
+    tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr, false);
     std::vector<tsl_result*> rs;
     try {
       upload(P);
       launch(P, 1, true);
-      download(P);
+      download(P, ctx->stream);
       float ms = 0;
       cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "elapsed");
       P->last_kernel_ms = ms;
@@ -1094,12 +1108,12 @@ int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* 
     tsl_config cfg;
     tsl_config_default(&cfg);
     const int32_t offs[2] = {0, 1};
-    tsl_plan* P = prepare(ctx, job, offs, 1, &cfg, 1, 1, plan);
+    tsl_plan* P = prepare(ctx, job, offs, 1, &cfg, 1, 1, plan, false);
     tsl_result* r = nullptr;
     try {
       upload(P);
       launch(P, 1, true);
-      download(P);
+      download(P, ctx->stream);
       r = collect_group(P, 0);
     } catch (...) {
       delete P;

@@ -1709,8 +1709,25 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
 // ----------------------------------------------------------------------------
 // build_plan (orchestrator.cpp:8-70) for one group
 // ----------------------------------------------------------------------------
+// Clears the group's mutable header so a prepared plan can be relaunched
+// over resident inputs (every other piece of state is rebuilt from them).
+template <class X>
+TSL_HD void reset_group(X& x, GroupDev& g) {
+  if (x.tid == 0) {
+    g.n_hist = 0;
+    g.final_merged = 0;
+    g.within_budget = 0;
+    g.total_swapped = 0;
+    g.loop_iters = 0;
+    g.err = ErrInfo{};
+    g.stats = GroupStats{};
+  }
+  x.sync();
+}
+
 template <class X>
 TSL_HD void plan_group(X& x, GroupDev& g) {
+  reset_group(x, g);
   int64_t c0 = x.clock(), c1;
   const int64_t cstart = c0;
   auto lap = [&](int k) { c1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += c1 - c0; c0 = c1; };
@@ -1769,6 +1786,7 @@ TSL_HD void plan_group(X& x, GroupDev& g) {
 // analyze_job on a caller-supplied plan: timeline builder + one evaluation.
 template <class X>
 TSL_HD void analyze_group(X& x, GroupDev& g) {
+  reset_group(x, g);
   for (int j = 0; j < g.n_jobs; ++j) {
     // keep the caller's plan (events/flags were uploaded into the job arrays)
     const JobState keep = g.st[j];

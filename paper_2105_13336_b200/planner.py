@@ -133,6 +133,8 @@ class PreparedPlan:
         return ms.value
 
     def launch_async(self, stream_handle: int = 0):
+        """One launch on a cudaStream_t handle (torch.cuda.Stream().cuda_stream);
+        0 means the planner context's own stream."""
         rc = self._p.lib.tsl_plan_launch_async(self._h, C.c_void_p(stream_handle or None))
         if rc:
             _raise(self._p.lib, rc)

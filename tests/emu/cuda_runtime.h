@@ -26,6 +26,7 @@ inline cudaError_t cudaEventRecord(cudaEvent_t, cudaStream_t) { return cudaSucce
 inline cudaError_t cudaEventSynchronize(cudaEvent_t) { return cudaSuccess; }
 inline cudaError_t cudaEventElapsedTime(float* ms, cudaEvent_t, cudaEvent_t) { *ms = 0; return cudaSuccess; }
 inline cudaError_t cudaStreamSynchronize(cudaStream_t) { return cudaSuccess; }
+inline cudaError_t cudaDeviceSynchronize() { return cudaSuccess; }
 inline cudaError_t cudaMalloc(void** p, size_t n) {
   *p = std::calloc(1, n ? n : 1);
   return *p ? cudaSuccess : cudaErrorMemoryAllocation;

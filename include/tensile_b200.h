@@ -150,6 +150,11 @@ typedef struct tsl_stats {
   int64_t cyc_spec, cyc_conflict, cyc_sweep, cyc_merge;
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by this call     */
   double prep_ms;               /* host validation + packing before the H2D  */
+  int64_t cyc_rescore;          /* part of cyc_sweep spent re-scoring (job 0's warp) */
+  int64_t cyc_apply;            /* part of cyc_merge spent writing committed events */
+  int64_t debug[4];             /* development counters */
+  int64_t cyc_pendsort;
+  int64_t fitprof[9];
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

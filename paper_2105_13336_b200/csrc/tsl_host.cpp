@@ -239,7 +239,7 @@ struct Layout {
 struct JobPlace {  // byte offsets into the device buffer
   size_t topo, o_lat, o_in_off, o_in, o_out_off, o_out, t_size, t_kind, t_rank, t_store, t_upd, t_prod, inflag;
   size_t a_tensor, a_store, a_type, a_start, a_end, a_base, a_flag, a_owned, s_off, s_acc, t_wfirst, t_utga;
-  size_t ev[12], bz_s, bz_e, pd_s, pd_e, pd_ts, pd_te, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
+  size_t ev[12], bz_s, bz_e, pd_s, pd_e, pd_ts, pd_te, bzi_s, bzi_e, ai_e, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
   size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve;
   int32_t Scap, Rcap, Ecap;
 };
@@ -320,6 +320,9 @@ struct tsl_plan {
   std::vector<int32_t> group_job_base;  // first JobDev index of each group
   double last_kernel_ms = 0;
   double prep_ms = 0;
+  int32_t max_jobs = 1;
+  int32_t ipt = 1;        // block-sort tile of this launch
+  int64_t sort_cap = 0;   // NT * ipt
   int64_t n_accesses = 0;
 };
 
@@ -386,6 +389,27 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     }
     if (P->graphs[gi].size() > 128) fail(TSL_ERR_CAPACITY, "more than 128 jobs in one group");
   }
+  // Sort tile: the largest block sort of any group -- CSR of a job's
+  // accesses, one job's whole timeline (<= 2A + S + R with S <= 2A + 2 and
+  // R <= T + 1), a pass's candidates (<= sum T). Busy rebuilds and
+  // evaluation batches are split to fit it.
+  {
+    int64_t need = 1;
+    for (auto& gs : P->graphs) {
+      int64_t sumT = 0;
+      for (auto& g : gs) {
+        need = std::max<int64_t>(need, 4 * int64_t(g.A) + g.T + 4);
+        need = std::max<int64_t>(need, g.O + 1);
+        sumT += g.T;
+      }
+      need = std::max<int64_t>(need, sumT);
+    }
+    P->ipt = sort_ipt_for(need);
+    P->sort_cap = int64_t(NT) * P->ipt;
+    if (need > P->sort_cap)
+      fail(TSL_ERR_CAPACITY, "build exceeds the single-CTA planner capacity (" + std::to_string(P->sort_cap) +
+                                 " timeline events per job / candidates per pass)");
+  }
   // 2. layout: [static inputs][groups|states|jobs][outputs][workspace]
   Layout L;
   P->jp.resize(n_groups);
@@ -415,7 +439,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   }
   P->groups_off = L.take<GroupDev>(n_groups);
   int32_t nj = 0;
-  for (auto& v : P->graphs) { P->group_job_base.push_back(nj); nj += static_cast<int32_t>(v.size()); }
+  for (auto& v : P->graphs) {
+    P->group_job_base.push_back(nj);
+    nj += static_cast<int32_t>(v.size());
+    P->max_jobs = std::max<int32_t>(P->max_jobs, static_cast<int32_t>(v.size()));
+  }
   P->states_off = L.take<JobState>(nj);
   P->jobs_off = L.take<JobDev>(nj);
   const size_t stage_end = L.off;
@@ -465,6 +493,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.pd_e = L.take<int64_t>(p.Scap);
       p.pd_ts = L.take<int64_t>(p.Scap);
       p.pd_te = L.take<int64_t>(p.Scap);
+      p.bzi_s = L.take<int32_t>(tsl::TI_NB_HOST + 1);
+      p.bzi_e = L.take<int32_t>(tsl::TI_NB_HOST + 1);
+      p.ai_e = L.take<int32_t>(tsl::TI_NB_HOST + 1);
       p.st_evcnt = L.take<int32_t>(g.T);
       p.swapped = L.take<uint8_t>(g.T);
       p.ev_drop = L.take<uint8_t>(p.Scap);
@@ -480,7 +511,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.bk_curve = L.take<int64_t>(size_t(2) * (p.Ecap + 1));
     }
     GroupPlace& q = P->gp[gi];
-    const size_t E = SORT_CAP;
+    const size_t E = size_t(P->sort_cap);
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
     q.x_time = L.take<int64_t>(E);
@@ -533,7 +564,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->st = dp<JobState>(ctx, P->states_off) + jglob;
     const GroupPlace& q = P->gp[gi];
     G->hist = dp<int64_t>(ctx, q.hist);
-    G->ecap = SORT_CAP;
+    G->ecap = int32_t(P->sort_cap);
     G->k_key = dp<uint64_t>(ctx, q.k_key);
     G->k_val = dp<int32_t>(ctx, q.k_val);
     G->x_time = dp<int64_t>(ctx, q.x_time);
@@ -558,9 +589,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
       const Graph& g = gs[k];
       const JobPlace& p = P->jp[gi][k];
-      if (g.A > SORT_CAP || g.O + 1 > SORT_CAP)
-        fail(TSL_ERR_CAPACITY, "job " + g.job_id + " exceeds the single-CTA planner capacity (" +
-                                   std::to_string(SORT_CAP) + " accesses)");
+
       std::vector<int32_t> topo = g.topo;
       put(ctx, p.topo, topo);
       put(ctx, p.o_lat, g.lat);
@@ -621,6 +650,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       J->pd_e = dp<int64_t>(ctx, p.pd_e);
       J->pd_ts = dp<int64_t>(ctx, p.pd_ts);
       J->pd_te = dp<int64_t>(ctx, p.pd_te);
+      J->bzi_s = dp<int32_t>(ctx, p.bzi_s);
+      J->bzi_e = dp<int32_t>(ctx, p.bzi_e);
+      J->ai_e = dp<int32_t>(ctx, p.ai_e);
       J->st_evcnt = dp<int32_t>(ctx, p.st_evcnt);
       J->swapped = dp<uint8_t>(ctx, p.swapped);
       J->rc_id = dp<int64_t>(ctx, p.rc[0]);
@@ -706,7 +738,7 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
   for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
-    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, c->stream), "launch");
+    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, c->stream), "launch");
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
@@ -820,6 +852,11 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   s.cyc_conflict = G.stats.cyc[6];
   s.cyc_sweep = G.stats.cyc[7];
   s.cyc_merge = G.stats.cyc[8] + G.stats.cyc[9];
+  s.cyc_rescore = G.stats.cyc[10];
+  s.cyc_apply = G.stats.cyc[8];
+  for (int k = 0; k < 4; ++k) s.debug[k] = G.stats.cyc[12 + k];
+  s.cyc_pendsort = G.stats.cyc[11];
+  for (int k = 0; k < 9; ++k) s.fitprof[k] = G.stats.cyc[16 + k];
   return R;
 }
 
@@ -1033,7 +1070,7 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     tsl_ctx* c = P->ctx;
-    cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode,
+    cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode, P->max_jobs, P->ipt,
                                   stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
   });
 }

@@ -11,26 +11,44 @@
 namespace tsl {
 
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
+static_assert(TI_NB == TI_NB_HOST, "time index size");
 
 template <int IPT>
 using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;
 using BScan = cub::BlockScan<int64_t, NT>;
 
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-constexpr size_t TMP_BYTES =
-    cmax(cmax(cmax(sizeof(typename BRS<1>::TempStorage), sizeof(typename BRS<2>::TempStorage)),
-              cmax(sizeof(typename BRS<4>::TempStorage), sizeof(typename BRS<8>::TempStorage))),
-         cmax(cmax(sizeof(typename BRS<16>::TempStorage), sizeof(typename BRS<SORT_IPT>::TempStorage)),
-              sizeof(typename BScan::TempStorage)));
+// Shared scratch needed by the block sort / scan for a given tile (items per
+// thread); the launch reserves only what its largest sort needs, so the rest
+// of the SM's 256 KB stays L1 for the dependent-load chains.
+constexpr size_t tmp_bytes_for(int ipt) {
+  return cmax(sizeof(typename BScan::TempStorage),
+              ipt <= 1 ? sizeof(typename BRS<1>::TempStorage)
+              : ipt <= 2 ? sizeof(typename BRS<2>::TempStorage)
+              : ipt <= 4 ? sizeof(typename BRS<4>::TempStorage)
+              : ipt <= 8 ? sizeof(typename BRS<8>::TempStorage)
+              : ipt <= 16 ? sizeof(typename BRS<16>::TempStorage)
+                          : sizeof(typename BRS<SORT_IPT>::TempStorage));
+}
 
 struct DevX {
   static constexpr int W = 32;
   int tid, nthr, lane, warp, nwarp;
   int64_t* sh;
   void* tmp;
+  size_t tmp_bytes;
+  int sort_cap;  // NT * items-per-thread of the launch's largest tile
 
   __device__ void sync() { __syncthreads(); }
-  __device__ int64_t clock() { return (int64_t)clock64(); }
+  // Reads the SM clock only once the preceding barrier has really released
+  // (BAR.SYNC defers blocking to the first consumer of barrier-protected
+  // state, so a bare clock read would be taken early).
+  __device__ int64_t clock() {
+    const int64_t v = *reinterpret_cast<volatile int64_t*>(&sh[SH_WORDS - 1]);
+    int64_t c;
+    asm volatile("{\n\t.reg .s64 t;\n\tmov.s64 t, %1;\n\tmov.u64 %0, %%clock64;\n\t}" : "=l"(c) : "l"(v) : "memory");
+    return c;
+  }
   __device__ void wsync() { __syncwarp(); }
   __device__ bool wany(bool p) { return __any_sync(0xffffffffu, p); }
   // warp exclusive prefix sum of v; *total = warp sum
@@ -83,6 +101,7 @@ struct DevX {
   __device__ void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     __syncthreads();
     if (n <= 1 || bits <= 0) return;
+    if (n > sort_cap) __trap();  // callers respect GroupDev::ecap == sort_cap
     if (n <= NT) sort_ipt<1>(keys, vals, n, bits);
     else if (n <= 2 * NT) sort_ipt<2>(keys, vals, n, bits);
     else if (n <= 4 * NT) sort_ipt<4>(keys, vals, n, bits);
@@ -108,33 +127,76 @@ struct DevX {
 
 }  // namespace tsl
 
-extern "C" __global__ void __launch_bounds__(tsl::NT, 1) tsl_plan_kernel(tsl::GroupDev* groups, int mode) {
+namespace tsl {
+// Shared-memory layout: [scalars][group header copy][JobState x max_jobs][sort scratch]
+constexpr size_t SH_BYTES = SH_WORDS * sizeof(int64_t);
+constexpr size_t HDR_BYTES = (sizeof(GroupDev) + 15) & ~size_t(15);
+constexpr size_t ST_BYTES = (sizeof(JobState) + 15) & ~size_t(15);
+}  // namespace tsl
+
+// One CTA = one build_plan (mode 0) or one analyze_job (mode 1). The group
+// header and every job's mutable scalars live in shared memory for the whole
+// kernel and are written back at the end.
+extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
+    tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes) {
   extern __shared__ __align__(16) uint8_t smem[];
-  tsl::DevX x;
+  using namespace tsl;
+  DevX x;
   x.tid = threadIdx.x;
   x.nthr = blockDim.x;
   x.lane = threadIdx.x & 31;
   x.warp = threadIdx.x >> 5;
   x.nwarp = blockDim.x >> 5;
   x.sh = reinterpret_cast<int64_t*>(smem);
-  x.tmp = smem + tsl::SH_WORDS * sizeof(int64_t);
-  tsl::GroupDev& g = groups[blockIdx.x];
-  if (mode == 0) tsl::plan_group(x, g);
-  else tsl::analyze_group(x, g);
+  GroupDev* gs = reinterpret_cast<GroupDev*>(smem + SH_BYTES);
+  JobState* sts = reinterpret_cast<JobState*>(smem + SH_BYTES + HDR_BYTES);
+  x.tmp = smem + SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs;
+  x.tmp_bytes = tmp_bytes;
+  x.sort_cap = NT * ipt;
+  GroupDev* gg = &groups[blockIdx.x];
+  JobState* gst = gg->st;
+  if (x.tid == 0) *gs = *gg;
+  for (int j = x.tid; j < gg->n_jobs; j += x.nthr) sts[j] = gst[j];
+  __syncthreads();
+  if (x.tid == 0) gs->st = sts;
+  __syncthreads();
+  if (mode == 0) plan_group(x, *gs);
+  else analyze_group(x, *gs);
+  __syncthreads();
+  for (int j = x.tid; j < gs->n_jobs; j += x.nthr) gst[j] = sts[j];
+  if (x.tid == 0) {
+    gs->st = gst;
+    *gg = *gs;
+  }
 }
 
 namespace tsl {
-size_t kernel_smem_bytes() { return SH_WORDS * sizeof(int64_t) + TMP_BYTES; }
+int sort_ipt_for(int64_t n) {
+  for (int ipt : {1, 2, 4, 8, 16}) if (n <= int64_t(NT) * ipt) return ipt;
+  return SORT_IPT;
+}
 
-cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, cudaStream_t stream) {
-  static bool attr_set = false;
-  const size_t smem = kernel_smem_bytes();
-  if (!attr_set) {
+size_t kernel_smem_bytes(int max_jobs, int ipt) {
+  return SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs + tmp_bytes_for(ipt);
+}
+
+cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt,
+                               cudaStream_t stream) {
+  const size_t smem = kernel_smem_bytes(max_jobs, ipt);
+  static size_t attr = 0;
+  if (smem != attr) {
     cudaError_t e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    // The planner is a latency-bound dependent-load chain over data that
+    // lives in global memory: keep the L1 as large as the shared memory we
+    // need allows (the driver rounds the carveout up to a legal split).
+    const size_t full = size_t(228) << 10;
+    const int pct = int(((smem + 1024) * 100 + full - 1) / full);
+    e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    if (e != cudaSuccess) return e;
+    attr = smem;
   }
-  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode);
+  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, (unsigned)tmp_bytes_for(ipt));
   return cudaGetLastError();
 }
 }  // namespace tsl

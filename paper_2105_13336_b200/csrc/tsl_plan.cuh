@@ -46,7 +46,10 @@
 
 namespace tsl {
 
-constexpr int SH_WORDS = 2048;   // CTA-shared int64 scalars
+#ifndef TSL_DEBUG_REASONS
+#define TSL_DEBUG_REASONS 0
+#endif
+constexpr int SH_WORDS = 1024;   // CTA-shared int64 scalars
 constexpr int MAXB = 32;         // jobs per evaluation batch
 constexpr int EV_FIELDS = 12;    // swap-event fields (rollback copies)
 constexpr int RC_FIELDS = 6;
@@ -107,28 +110,81 @@ TSL_HD void stream_load(Stream& q, bool fwd, int64_t b, int64_t e) {
   }
 }
 
+// Bucketed time index over a sorted run: first[b] = first k with
+// key(k) >= b << shift, for b in [0, TI_NB]. A lookup is one index load plus
+// a short forward scan instead of ~log2(n) dependent probes.
+constexpr int TI_NB = 256;
+
+struct TIndex {
+  const int32_t* first;  // [TI_NB + 1] or null
+  int32_t shift;
+};
+
+// First index k in [0, n) with key(k) > v (strict) or key(k) >= v, for
+// nondecreasing keys key(k) = arr[ix ? ix[k] : k].
+TSL_HD int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
+                           const TIndex* ti = nullptr) {
+  int32_t lo = 0, hi = n;
+  if (ti && ti->first && v >= 0) {
+    // all k before first[b] have key < (b << shift) <= v
+    int64_t bk = v >> ti->shift;
+    if (bk > TI_NB) bk = TI_NB;
+    lo = ti->first[bk];
+    for (;;) {  // short scan
+      if (lo >= n) return n;
+      const int64_t x = arr[ix ? ix[lo] : lo];
+      if (strict ? x > v : x >= v) return lo;
+      ++lo;
+    }
+  }
+  if (n <= 12) {
+    for (int32_t k = 0; k < n; ++k) {
+      const int64_t x = arr[ix ? ix[k] : k];
+      if (strict ? x > v : x >= v) return k;
+    }
+    return n;
+  }
+  while (lo < hi) {
+    const int32_t m = (lo + hi) >> 1;
+    const int64_t x = arr[ix ? ix[m] : m];
+    if (strict ? x > v : x >= v) hi = m; else lo = m + 1;
+  }
+  return lo;
+}
+
+TSL_HD int tindex_shift(int64_t max_key) {
+  int sh = 0;
+  while (max_key > 0 && (max_key >> sh) >= TI_NB) ++sh;
+  return sh;
+}
+
+// Builds first[0..TI_NB] for keys[0, n) (nondecreasing, >= 0); CTA-collective.
+template <class X>
+TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, int shift) {
+  for (int32_t k = x.tid; k <= n; k += x.nthr) {
+    // buckets b with key(k-1) < (b << shift) <= key(k) get first[b] = k
+    int64_t lo = k == 0 ? 0 : (keys[k - 1] >> shift) + 1;
+    if (k > 0 && keys[k - 1] < 0) lo = 0;
+    int64_t hi = k == n ? TI_NB : (keys[k] < 0 ? -1 : (keys[k] >> shift));
+    if (k < n && keys[k] >= 0 && (keys[k] & ((int64_t(1) << shift) - 1)) != 0) hi = keys[k] >> shift;
+    if (hi > TI_NB) hi = TI_NB;
+    for (int64_t b = lo; b <= hi; ++b) first[b] = k;
+  }
+  x.sync();
+}
+
 // Positions a stream on the intervals that intersect [b, e) (lifted).
-TSL_HD void stream_open(Stream& q, int32_t n, bool fwd, int64_t b, int64_t e) {
+// (s0, eN) are the run's first start and last end, loaded once per query.
+TSL_HD void stream_open(Stream& q, int32_t n, bool fwd, int64_t b, int64_t e, int64_t s0, int64_t eN) {
   q.n = n;
   const int64_t L = b - q.sh, H = e - q.sh;
-  if (n == 0 || q.e[sidx(q, n - 1)] <= L || q.s[sidx(q, 0)] >= H) {
+  if (n == 0 || eN <= L || s0 >= H) {
     q.i = fwd ? n : 0;
     q.live = false;
     return;
   }
-  int32_t lo = 0, hi = n;
-  if (fwd) {  // first k with e[k] > L
-    while (lo < hi) {
-      int32_t m = (lo + hi) >> 1;
-      if (q.e[sidx(q, m)] > L) hi = m; else lo = m + 1;
-    }
-  } else {  // first k with s[k] >= H
-    while (lo < hi) {
-      int32_t m = (lo + hi) >> 1;
-      if (q.s[sidx(q, m)] >= H) hi = m; else lo = m + 1;
-    }
-  }
-  q.i = lo;
+  if (fwd) q.i = search_keys(q.e, q.ix, n, L, true);  // first e > L
+  else q.i = search_keys(q.s, q.ix, n, H, false);     // first s >= H
   stream_load(q, fwd, b, e);
 }
 
@@ -139,6 +195,7 @@ struct Src {
   const int64_t* s;
   const int64_t* e;
   int32_t n;
+  TIndex is, ie;  // optional time indexes over starts / ends
 };
 
 struct FitQuery {
@@ -156,41 +213,80 @@ constexpr int64_t NONE = INT64_MIN;
 // Forward sweep (earliest) stops at the first maximal free interval of length
 // >= d; the reverse sweep (latest) enumerates the same maximal free intervals
 // from the right.
+//
+// Streams sit in fixed slots (source t in {src0, src1, storage accesses} x
+// lift k in {-P, 0, +P}, plus the <= 3 lifted copies of `extra`), and every
+// loop over slots is unrolled, so the merge state stays in registers: the
+// sweep is a chain of dependent global loads only, never local memory.
+template <class CLK>
 TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
-                   int nsrc, int64_t* swept) {
+                   int nsrc, int64_t* swept, CLK clk, int64_t* prof) {
   if (q.e <= q.b) return NONE;
+  int64_t tp0 = prof ? clk() : 0;
   const bool fwd = !latest;
   const int64_t P = imax(1, st.period);
-  Stream str[13];
-  int ns = 0;
   const int32_t a0 = J.s_off[q.store], na = J.s_off[q.store + 1] - a0;
-  int64_t exs[3], exe[3];
+  const int64_t* SS[3] = {nsrc > 0 ? src[0].s : nullptr, nsrc > 1 ? src[1].s : nullptr, J.a_start};
+  const int64_t* SE[3] = {nsrc > 0 ? src[0].e : nullptr, nsrc > 1 ? src[1].e : nullptr, J.a_end};
+  const int32_t* IX[3] = {nullptr, nullptr, J.s_acc + a0};
+  const int32_t SN[3] = {nsrc > 0 ? src[0].n : 0, nsrc > 1 ? src[1].n : 0, na};
+  const TIndex NOI{nullptr, 0};
+  const TIndex TIS[3] = {nsrc > 0 ? src[0].is : NOI, nsrc > 1 ? src[1].is : NOI, NOI};
+  const TIndex TIE[3] = {nsrc > 0 ? src[0].ie : NOI, nsrc > 1 ? src[1].ie : NOI, NOI};
+  int64_t S0[3], EN[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const bool any = SN[t] > 0;
+    S0[t] = any ? SS[t][IX[t] ? IX[t][0] : 0] : 0;
+    EN[t] = any ? SE[t][IX[t] ? IX[t][SN[t] - 1] : SN[t] - 1] : 0;
+  }
+  if (prof) { int64_t t = clk(); prof[0] += t - tp0; tp0 = t; }
+  int32_t I[9];
+  int64_t HS[9], HE[9];
+  bool LIVE[9];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int z = 3 * t + k;
+      const int64_t sh = (k - 1) * P;
+      const int32_t n = SN[t];
+      const int64_t L = q.b - sh, H = q.e - sh;
+      LIVE[z] = false;
+      I[z] = 0;
+      HS[z] = HE[z] = 0;
+      if (n == 0 || EN[t] <= L || S0[t] >= H) continue;
+      int64_t tq = prof ? clk() : 0;
+      int32_t i;
+      if (fwd) i = search_keys(SE[t], IX[t], n, L, true, &TIE[t]);
+      else i = search_keys(SS[t], IX[t], n, H, false, &TIS[t]);
+      if (prof) { prof[3 + t] += clk() - tq; prof[6 + t] += 1; }
+      I[z] = i;
+      const int32_t h = fwd ? i : i - 1;
+      if (h >= 0 && h < n) {
+        const int32_t k2 = IX[t] ? IX[t][h] : h;
+        HS[z] = SS[t][k2] + sh;
+        HE[z] = SE[t][k2] + sh;
+        LIVE[z] = fwd ? HS[z] < q.e : HE[z] > q.b;
+      }
+    }
+  }
+  // lifted copies of `extra`, ascending
+  int64_t XS[3], XE[3];
   int nex = 0;
+#pragma unroll
   for (int k = -1; k <= 1; ++k) {
     const int64_t sh = k * P;
-    for (int t = 0; t < nsrc; ++t) {
-      Stream& z = str[ns];
-      z.s = src[t].s; z.e = src[t].e; z.ix = nullptr; z.sh = sh;
-      stream_open(z, src[t].n, fwd, q.b, q.e);
-      if (z.live) ++ns;
-    }
-    Stream& z = str[ns];
-    z.s = J.a_start; z.e = J.a_end; z.ix = J.s_acc + a0; z.sh = sh;
-    stream_open(z, na, fwd, q.b, q.e);
-    if (z.live) ++ns;
+    XS[k + 1] = XE[k + 1] = 0;
     if (q.has_extra && q.xe > q.xs && q.xe + sh > q.b && q.xs + sh < q.e) {
-      exs[nex] = q.xs + sh;
-      exe[nex] = q.xe + sh;
+      if (nex == 0) { XS[0] = q.xs + sh; XE[0] = q.xe + sh; }
+      else if (nex == 1) { XS[1] = q.xs + sh; XE[1] = q.xe + sh; }
+      else { XS[2] = q.xs + sh; XE[2] = q.xe + sh; }
       ++nex;
     }
   }
-  if (nex) {
-    Stream& z = str[ns];
-    z.s = exs; z.e = exe; z.ix = nullptr; z.sh = 0; z.n = nex;
-    z.i = fwd ? 0 : nex;
-    stream_load(z, fwd, q.b, q.e);
-    if (z.live) ++ns;
-  }
+  int xi = fwd ? 0 : nex;  // extra cursor
+  if (prof) { int64_t t = clk(); prof[1] += t - tp0; tp0 = t; }
   int64_t n_swept = 0;
   int64_t result = NONE;
   if (fwd) {
@@ -198,14 +294,33 @@ TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool 
     bool found = false;
     for (;;) {
       int best = -1;
-      int64_t bs = 0;
-      for (int t = 0; t < ns; ++t)
-        if (str[t].live && (best < 0 || str[t].hs < bs)) { best = t; bs = str[t].hs; }
+      int64_t bs = 0, be = 0;
+#pragma unroll
+      for (int z = 0; z < 9; ++z)
+        if (LIVE[z] && (best < 0 || HS[z] < bs)) { best = z; bs = HS[z]; be = HE[z]; }
+      if (xi < nex) {
+        const int64_t xs = xi == 0 ? XS[0] : (xi == 1 ? XS[1] : XS[2]);
+        if (best < 0 || xs < bs) { best = 9; bs = xs; be = xi == 0 ? XE[0] : (xi == 1 ? XE[1] : XE[2]); }
+      }
       if (best < 0) break;
-      Stream& z = str[best];
-      const int64_t be = z.he;
-      ++z.i;
-      stream_load(z, true, q.b, q.e);
+      if (best == 9) {
+        ++xi;
+      } else {
+#pragma unroll
+        for (int z = 0; z < 9; ++z) {
+          if (z != best) continue;
+          const int t = z / 3;
+          const int64_t sh = (z % 3 - 1) * P;
+          const int32_t i = ++I[z];
+          LIVE[z] = i < SN[t];
+          if (LIVE[z]) {
+            const int32_t k2 = IX[t] ? IX[t][i] : i;
+            HS[z] = SS[t][k2] + sh;
+            HE[z] = SE[t][k2] + sh;
+            LIVE[z] = HS[z] < q.e;
+          }
+        }
+      }
       if (be <= bs) continue;  // lift_into drops empty intervals
       ++n_swept;
       const int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
@@ -219,14 +334,33 @@ TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool 
     bool found = false;
     for (;;) {
       int best = -1;
-      int64_t be = 0;
-      for (int t = 0; t < ns; ++t)
-        if (str[t].live && (best < 0 || str[t].he > be)) { best = t; be = str[t].he; }
+      int64_t bs = 0, be = 0;
+#pragma unroll
+      for (int z = 0; z < 9; ++z)
+        if (LIVE[z] && (best < 0 || HE[z] > be)) { best = z; bs = HS[z]; be = HE[z]; }
+      if (xi > 0) {
+        const int64_t xe = xi == 1 ? XE[0] : (xi == 2 ? XE[1] : XE[2]);
+        if (best < 0 || xe > be) { best = 9; be = xe; bs = xi == 1 ? XS[0] : (xi == 2 ? XS[1] : XS[2]); }
+      }
       if (best < 0) break;
-      Stream& z = str[best];
-      const int64_t bs = z.hs;
-      --z.i;
-      stream_load(z, false, q.b, q.e);
+      if (best == 9) {
+        --xi;
+      } else {
+#pragma unroll
+        for (int z = 0; z < 9; ++z) {
+          if (z != best) continue;
+          const int t = z / 3;
+          const int64_t sh = (z % 3 - 1) * P;
+          const int32_t i = --I[z];
+          LIVE[z] = i > 0;
+          if (LIVE[z]) {
+            const int32_t k2 = IX[t] ? IX[t][i - 1] : i - 1;
+            HS[z] = SS[t][k2] + sh;
+            HE[z] = SE[t][k2] + sh;
+            LIVE[z] = HE[z] > q.b;
+          }
+        }
+      }
       if (be <= bs) continue;
       ++n_swept;
       const int64_t cs = imax(bs, q.b), ce = imin(be, q.e);
@@ -237,8 +371,13 @@ TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool 
     if (found || (cur > q.b && cur - q.b >= q.d)) result = cur - q.d;
   }
   if (swept) *swept += n_swept;
+  if (prof) { prof[2] += clk() - tp0; }
   return result;
 }
+
+struct NoClock {
+  TSL_HD int64_t operator()() const { return 0; }
+};
 
 // ----------------------------------------------------------------------------
 // Plan mutation helpers
@@ -249,11 +388,8 @@ TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool 
 TSL_HD void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
                    int64_t& delta) {
   if (wrapped && st.period > 0) t = ((t % st.period) + st.period) % st.period;
-  int32_t lo = 0, hi = J.A;
-  while (lo < hi) {
-    int32_t m = (lo + hi) >> 1;
-    if (J.a_end[m] <= t) lo = m + 1; else hi = m;
-  }
+  const TIndex ti{J.ai_e, st.ai_shift};
+  const int32_t lo = search_keys(J.a_end, nullptr, J.A, t, true, &ti);
   if (lo == 0) { trig = -1; delta = t; }
   else { trig = lo - 1; delta = t - J.a_end[lo - 1]; }
 }
@@ -386,18 +522,25 @@ struct ReCtx {
   PairRec* out;
   int32_t nout, cap;
   bool overflow;
+  int64_t* dbg = nullptr;  // development cycle counters (thread 0 only)
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
-    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n}, {J.pd_s, J.pd_e, st.pend_n}};
+    const int64_t c0 = x.clock();
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
+                   {J.pd_s, J.pd_e, st.pend_n, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
-    int64_t r = fit(J, st, q, latest, src, 2, &sw);
+    int64_t* prof = (dbg && x.tid == 0) ? dbg + 4 : nullptr;  // cyc[16..18]
+    int64_t r = fit(J, st, q, latest, src, 2, &sw, [&]() { return x.clock(); }, prof);
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
+    if (dbg && x.tid == 0) { dbg[0] += x.clock() - c0; dbg[1] += 1; }
     return r;
   }
   TSL_HD bool commit(const PairSpec& p) {
+    const int64_t c0 = x.clock();
     const int32_t pn = st.pend_n;
     if (nout >= cap || pn + 2 > J.Scap) { overflow = true; return false; }
     const PairRec r = resolve_pair(J, st, p);
+    if (dbg && x.tid == 0) { dbg[2] += x.clock() - c0; }
     x.wsync();
     out[nout] = r;
     x.wsync();
@@ -407,6 +550,7 @@ struct ReCtx {
     st.pend_sorted = pn + 2;
     ++nout;
     x.wsync();
+    if (dbg && x.tid == 0) { dbg[3] += x.clock() - c0; }
     return true;
   }
 };
@@ -430,17 +574,21 @@ struct SpecCtx {
   int32_t nwin, cap_win;
   bool overflow;
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
-    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n}, {ps, pe, np}};
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
+                   {ps, pe, np, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
-    int64_t r = fit(J, st, q, latest, src, 2, &sw);
+    int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (r != NONE) {
-      // A later commit can only change this answer if it intersects the part
-      // of the window the answer depends on; a failed query stays failed.
+      // Adding busy intervals only removes free space, so a failed query
+      // stays failed, and a found placement [r, r+d) moves only if a new
+      // interval (any lifted copy) intersects it: regions left of it were
+      // already shorter than d (earliest-fit) or its region only shrinks to a
+      // length still >= d, and symmetrically for latest-fit.
       if (nwin >= cap_win) { overflow = true; return r; }
-      win[2 * nwin] = latest ? r : q.b;
-      win[2 * nwin + 1] = latest ? q.e : r + q.d;
+      win[2 * nwin] = r;
+      win[2 * nwin + 1] = r + q.d;
       ++nwin;
     }
     return r;
@@ -633,9 +781,11 @@ TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
   if (x.tid == 0) {
     st.S = 0; st.R = 0; st.n_peak = 0; st.n_curve = 0;
     st.next_id = 0; st.peak = 0; st.peak_time = 0; st.lua = -1; st.has_lua = 0;
-    st.dirty = 1; st.n_events = 0; st.son = 0;
+    st.dirty = 1; st.n_events = 0; st.son = 0; st.bz_n = 0; st.bzi_shift = 0;
   }
   x.sync();
+  build_anchor_index(x, g, j);
+  build_busy_index(x, g, j);
 }
 
 // ----------------------------------------------------------------------------
@@ -1052,54 +1202,84 @@ TSL_HD bool hits(int64_t s, int64_t e, int64_t wl, int64_t wh, int64_t P) {
   return false;
 }
 
-// Sorted busy structure of every job rebuilt from the plan: one block sort of
-// (job, start) keys.
+// Time indexes over the sorted busy structure (starts and ends) of job j.
+template <class X>
+TSL_HD void build_busy_index(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  const int32_t n = st.S;
+  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0);
+  x.sync();
+  if (x.tid == 0) st.bzi_shift = sh;
+  build_tindex(x, J.bz_s, n, J.bzi_s, sh);
+  build_tindex(x, J.bz_e, n, J.bzi_e, sh);
+}
+
+template <class X>
+TSL_HD void build_anchor_index(X& x, GroupDev& g, int j) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  const int sh = tindex_shift(J.A ? imax(J.a_end[J.A - 1], 0) : 0);
+  x.sync();
+  if (x.tid == 0) st.ai_shift = sh;
+  build_tindex(x, J.a_end, J.A, J.ai_e, sh);
+}
+
+// Sorted busy structure of every job rebuilt from the plan: block sorts of
+// (job, start) keys over batches of jobs that fit one sort tile.
 template <class X>
 TSL_HD void rebuild_busy(X& x, GroupDev& g) {
   int64_t* gsh = x.sh + MAXB * NF;
-  if (x.tid == 0) {
-    int64_t off = 0, mx = 0;
-    for (int j = 0; j < g.n_jobs; ++j) { gsh[16 + j] = off; off += g.st[j].S; }
-    gsh[15] = off;
-    (void)mx;
-    gsh[14] = 0;
-  }
-  x.sync();
-  const int64_t n = gsh[15];
-  for (int j = 0; j < g.n_jobs; ++j) {
-    const JobDev& J = g.jobs[j];
-    int64_t mx = 0;
-    for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) mx = imax(mx, J.ev_start[i]);
-    x.amax(&gsh[14], mx);
-  }
-  x.sync();
-  if (n > g.ecap) {
-    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = -1; g.err.tensor = n; g.err.tick = 3; }
-    x.sync();
-    return;
-  }
-  const int jbits = nbits(uint64_t(g.n_jobs - 1));
-  const int tbits = nbits(uint64_t(gsh[14]));
-  for (int j = 0; j < g.n_jobs; ++j) {
-    const JobDev& J = g.jobs[j];
-    const int64_t base = gsh[16 + j];
-    for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) {
-      g.k_key[base + i] = (uint64_t(j) << tbits) | uint64_t(J.ev_start[i]);
-      g.k_val[base + i] = (j << 24) | i;
+  int j0 = 0;
+  while (j0 < g.n_jobs) {
+    if (x.tid == 0) {
+      int64_t off = 0;
+      int j1 = j0;
+      while (j1 < g.n_jobs && (j1 == j0 || off + g.st[j1].S <= g.ecap)) { gsh[16 + j1] = off; off += g.st[j1].S; ++j1; }
+      gsh[15] = off;
+      gsh[13] = j1;
+      gsh[14] = 0;
     }
+    x.sync();
+    const int j1 = int(gsh[13]);
+    const int64_t n = gsh[15];
+    if (n > g.ecap) {
+      if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = j0; g.err.tensor = n; g.err.tick = 3; }
+      x.sync();
+      return;
+    }
+    for (int j = j0; j < j1; ++j) {
+      const JobDev& J = g.jobs[j];
+      int64_t mx = 0;
+      for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) mx = imax(mx, J.ev_start[i]);
+      x.amax(&gsh[14], mx);
+    }
+    x.sync();
+    const int jbits = nbits(uint64_t(j1 - j0 - 1));
+    const int tbits = nbits(uint64_t(gsh[14]));
+    for (int j = j0; j < j1; ++j) {
+      const JobDev& J = g.jobs[j];
+      const int64_t base = gsh[16 + j];
+      for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) {
+        g.k_key[base + i] = (uint64_t(j - j0) << tbits) | uint64_t(J.ev_start[i]);
+        g.k_val[base + i] = (j << 24) | i;
+      }
+    }
+    x.sync();
+    x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits);
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int j = g.k_val[m] >> 24;
+      const int32_t i = g.k_val[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      const int64_t pos = m - gsh[16 + j];
+      J.bz_s[pos] = J.ev_start[i];
+      J.bz_e[pos] = J.ev_end[i];
+    }
+    for (int j = j0 + x.tid; j < j1; j += x.nthr) g.st[j].bz_n = g.st[j].S;
+    x.sync();
+    for (int j = j0; j < j1; ++j) build_busy_index(x, g, j);
+    j0 = j1;
   }
-  x.sync();
-  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits);
-  for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int j = g.k_val[m] >> 24;
-    const int32_t i = g.k_val[m] & 0xffffff;
-    const JobDev& J = g.jobs[j];
-    const int64_t pos = m - gsh[16 + j];
-    J.bz_s[pos] = J.ev_start[i];
-    J.bz_e[pos] = J.ev_end[i];
-  }
-  for (int j = x.tid; j < g.n_jobs; j += x.nthr) g.st[j].bz_n = g.st[j].S;
-  x.sync();
 }
 
 template <class X>
@@ -1152,6 +1332,21 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     return false;
   }
   x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
+  // Candidate records live in shared memory when they fit (the sort scratch
+  // is free until phase E): the in-order decisions read them back-to-back.
+  int32_t* cand = g.k_val;
+  int32_t* cinfo = g.c_info;
+  int64_t* chull = g.c_hull;
+  {
+    const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
+    if (need <= x.tmp_bytes) {
+      chull = reinterpret_cast<int64_t*>(x.tmp);
+      cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
+      cand = cinfo + CI_STRIDE * nc;
+    }
+  }
+  if (cand != g.k_val)
+    for (int64_t m = x.tid; m < nc; m += x.nthr) cand[m] = g.k_val[m];
   if (x.tid == 0) {
     g.stats.candidates += nc;
     g.stats.sort_elems += nc;
@@ -1160,6 +1355,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       for (int64_t m = nc - 1; m >= 0; --m) gsh[16 + (g.k_val[m] >> 24)] = m;
       for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
     }
+    for (int j = 0; j < g.n_jobs; ++j) g.st[j].pend_upto = coupled ? 0 : int32_t(gsh[16 + j]);
   }
   x.sync();
   int64_t t0 = x.clock(), t1;
@@ -1168,12 +1364,12 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   {
     GroupStats ls{};
     for (int64_t m = x.tid; m < nc; m += x.nthr) {
-      const int j = g.k_val[m] >> 24;
-      const int32_t s = g.k_val[m] & 0xffffff;
+      const int j = cand[m] >> 24;
+      const int32_t s = cand[m] & 0xffffff;
       const JobDev& J = g.jobs[j];
       const JobState& st = g.st[j];
-      int32_t* ci = g.c_info + m * CI_STRIDE;
-      int64_t* hl = g.c_hull + m * 4;
+      int32_t* ci = cinfo + m * CI_STRIDE;
+      int64_t* hl = chull + m * 4;
       ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
       ci[CI_P0] = -1;
       hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
@@ -1211,19 +1407,19 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
   for (int64_t m = x.tid; m < nc; m += x.nthr) {
-    int32_t* ci = g.c_info + m * CI_STRIDE;
+    int32_t* ci = cinfo + m * CI_STRIDE;
     if (ci[CI_NW] == 0) continue;
-    const int j = g.k_val[m] >> 24;
+    const int j = cand[m] >> 24;
     const int64_t P = imax(1, g.st[j].period);
-    const int64_t* hl = g.c_hull + m * 4;
+    const int64_t* hl = chull + m * 4;
     const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
     const int64_t m0 = coupled ? 0 : gsh[16 + j];
     int32_t nconf = 0;
     for (int64_t i = m0; i < m; ++i) {
-      if ((g.k_val[i] >> 24) != j) continue;
-      const int32_t* cj = g.c_info + i * CI_STRIDE;
+      if ((cand[i] >> 24) != j) continue;
+      const int32_t* cj = cinfo + i * CI_STRIDE;
       if (cj[CI_STATUS] != CS_OK) continue;
-      const int64_t* hi_ = g.c_hull + i * 4;
+      const int64_t* hi_ = chull + i * 4;
       if (!hits(hi_[2], hi_[3], hl[0], hl[1], P)) continue;
       const PairRec* pr = g.pr_pool + cj[CI_P0];
       bool conf = false;
@@ -1249,15 +1445,16 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     const int64_t m1 = coupled ? nc : gsh[16 + seg + 1];
     int64_t* wtmp = g.wbuf + int64_t(x.warp) * 4 * g.wcap;
     int32_t ndev = 0;
+    int64_t dev_lo = INT64_MAX, dev_hi = INT64_MIN;  // hull of re-scored commits (raw)
     bool changed = false;
     for (int64_t m = m0; m < m1; ++m) {
-      const int j = g.k_val[m] >> 24;
-      const int32_t s = g.k_val[m] & 0xffffff;
-      const JobDev& J = g.jobs[j];
-      JobState& st = g.st[j];
-      int32_t* ci = g.c_info + m * CI_STRIDE;
+      int32_t* ci = cinfo + m * CI_STRIDE;
       const int32_t status = ci[CI_STATUS];
       if (status == CS_SKIP) continue;
+      const int j = cand[m] >> 24;
+      const int32_t s = cand[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      JobState& st = g.st[j];
       if (coupled && g.total_swapped != 0) {  // SwapBudget::allows, swap_planner.cpp:268-276
         const double lhs = double(st.son + 1) / double(g.total_swapped + 1);
         if (!(lhs <= J.ratio)) continue;
@@ -1267,13 +1464,13 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       const int64_t P = imax(1, st.period);
       bool valid = status != CS_OVERFLOW && ci[CI_NCONF] <= CAPC;
       for (int32_t k = 0; valid && k < ci[CI_NCONF]; ++k)
-        if (g.c_info[int64_t(ci[CI_CONF + k]) * CI_STRIDE + CI_STATE] == 1) valid = false;
-      if (valid && ndev) {
+        if (cinfo[int64_t(ci[CI_CONF + k]) * CI_STRIDE + CI_STATE] == 1) valid = false;
+      if (valid && ndev && ci[CI_NW] && hits(dev_lo, dev_hi, chull[m * 4], chull[m * 4 + 1], P)) {
         const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
         for (int32_t d = 0; d < ndev && valid; ++d) {
           const int64_t dm = g.dev_list[m0 + d];
-          if ((g.k_val[dm] >> 24) != j) continue;
-          const int32_t* cd = g.c_info + dm * CI_STRIDE;
+          if ((cand[dm] >> 24) != j) continue;
+          const int32_t* cd = cinfo + dm * CI_STRIDE;
           const PairRec* pr = g.pr_pool + cd[CI_P0];
           for (int32_t p = 0; p < cd[CI_NP] && valid; ++p)
             for (int32_t w = 0; w < ci[CI_NW] && valid; ++w)
@@ -1285,32 +1482,52 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       int32_t np = 0;
       int32_t state = 0;
       if (valid) {
-        if (status == CS_OK) {
-          np = ci[CI_NP];
-          state = 1;
-          const PairRec* pr = g.pr_pool + ci[CI_P0];
+        if (status == CS_OK) { np = ci[CI_NP]; state = 1; }
+      } else {
+        ls.rescored += 1;
+        const int64_t rc0 = x.clock();
+        // bring this pass's pend list up to date: intervals of every candidate
+        // of this job committed since the last re-score (lanes in parallel)
+        for (int64_t q = st.pend_upto; q < m; ++q) {
+          const int32_t* cq = cinfo + q * CI_STRIDE;
+          if (cq[CI_STATE] != 1 || (cand[q] >> 24) != j) continue;
+          const int32_t nq = cq[CI_NP];
           const int32_t pn = st.pend_n;
-          if (pn + 2 * np > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; break; }
+          if (pn + 2 * nq > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; break; }
+          const PairRec* pr = g.pr_pool + cq[CI_P0];
           x.wsync();
-          for (int32_t p = x.lane; p < np; p += X::W) {
+          for (int32_t p = x.lane; p < nq; p += X::W) {
             J.pd_s[pn + 2 * p] = pr[p].os; J.pd_e[pn + 2 * p] = pr[p].oe;
             J.pd_s[pn + 2 * p + 1] = pr[p].is; J.pd_e[pn + 2 * p + 1] = pr[p].ie;
           }
-          st.pend_n = pn + 2 * np;
+          st.pend_n = pn + 2 * nq;
           x.wsync();
         }
-      } else {
-        ls.rescored += 1;
+        if (lerr.code) break;
+        x.wsync();
+        st.pend_upto = int32_t(m);
+        x.wsync();
+        const int64_t ps0 = x.clock();
+        pend_sort(x, J, st, wtmp);
+        if (x.tid == 0) g.stats.cyc[11] += x.clock() - ps0;
         int64_t earliest = 0, latest = 0;
         const int kind = candidate_kind(J, st, s, earliest, latest);
         const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
-        pend_sort(x, J, st, wtmp);
         ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+        c.dbg = &g.stats.cyc[12];
         const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+        if (x.tid == 0) g.stats.cyc[10] += x.clock() - rc0;
         if (c.overflow) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; lerr.tick = 5; break; }
         if (ok) {
           np = c.nout;
           state = 2;
+          int64_t lo = dev_lo, hi = dev_hi;
+          for (int32_t p = 0; p < np; ++p) {
+            lo = imin(lo, imin(c.out[p].os, c.out[p].is));
+            hi = imax(hi, imax(c.out[p].oe, c.out[p].ie));
+          }
+          dev_lo = lo;
+          dev_hi = hi;
           x.wsync();
           g.dev_list[m0 + ndev] = m;
           ci[CI_NP] = np;
@@ -1352,9 +1569,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   if (g.err.code) return false;
   // ---- D. write the committed events (make_event + pair links + flags) ----
   for (int64_t m = x.tid; m < nc; m += x.nthr) {
-    const int32_t* ci = g.c_info + m * CI_STRIDE;
+    const int32_t* ci = cinfo + m * CI_STRIDE;
     if (!ci[CI_STATE]) continue;
-    const int j = g.k_val[m] >> 24;
+    const int j = cand[m] >> 24;
     const JobDev& J = g.jobs[j];
     const PairRec* pr = g.pr_pool + ci[CI_P0];
     const int32_t np = ci[CI_NP];
@@ -1370,7 +1587,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       J.ev_earl[i1] = r.i_earl; J.ev_late[i1] = r.i_late; J.ev_pair[i1] = id0; J.ev_serves[i1] = r.serves;
       if (r.pre >= 0) J.a_flag[r.pre] = 1;
     }
-    x.aadd32(&J.st_evcnt[g.k_val[m] & 0xffffff], 2 * np);
+    x.aadd32(&J.st_evcnt[cand[m] & 0xffffff], 2 * np);
   }
   x.sync();
   tick(8);
@@ -1446,6 +1663,7 @@ TSL_HD void rebuild_index(X& x, GroupDev& g, int j) {
   }
   if (x.tid == 0) st.next_id = gsh[22];
   x.sync();
+  build_busy_index(x, g, j);
 }
 
 template <class X>
@@ -1693,6 +1911,7 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
   for (int32_t a = x.tid; a < J.A; a += x.nthr)
     if (J.a_start[a] >= pivot) { J.a_start[a] += lat; J.a_end[a] += lat; }
   x.sync();
+  build_anchor_index(x, g, j);
   if (!revalidate(x, g, j)) return false;
   if (x.tid == 0) st.dirty = 1;
   x.sync();
@@ -1701,6 +1920,8 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
     backup_job(x, g, j, true, saved.S, saved.R, saved.n_curve);
     if (x.tid == 0) st = saved;
     x.sync();
+    build_anchor_index(x, g, j);
+    build_busy_index(x, g, j);
     return false;
   }
   return true;

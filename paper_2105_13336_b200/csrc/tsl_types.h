@@ -97,6 +97,9 @@ struct JobDev {
   int64_t* pd_e;
   int64_t* pd_ts;  // [Scap] merge scratch
   int64_t* pd_te;
+  int32_t* bzi_s;     // [TI_NB+1] time index over bz_s
+  int32_t* bzi_e;     // [TI_NB+1] time index over bz_e
+  int32_t* ai_e;      // [TI_NB+1] time index over a_end (anchor)
   int32_t* st_evcnt;  // [T] swap events per storage (storage_has_swap)
   uint8_t* swapped;   // [T] SwapBudget::swapped_storages for this job
   // recompute events (plan.hpp:34-42)
@@ -141,7 +144,9 @@ struct JobState {
   int32_t bz_n;        // events reflected in the sorted busy structure
   int32_t pend_n;      // this pass's commits not yet merged into it
   int32_t pend_sorted; // pend_[0, pend_sorted) is sorted by start
-  int32_t pad_;
+  int32_t pend_upto;   // candidates before this index are in the pend list
+  int32_t bzi_shift;   // bucket shift of the busy-structure time index
+  int32_t ai_shift;    // bucket shift of the access-end (anchor) time index
 };
 
 struct GroupConfig {
@@ -161,7 +166,7 @@ struct GroupStats {
   int64_t loop_iterations;
   int64_t sort_elems;        // elements through block sorts
   int64_t rescored;          // swap candidates re-scored after speculation
-  int64_t cyc[16];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
+  int64_t cyc[28];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
 };
 
 struct GroupDev {

@@ -16,6 +16,9 @@ struct HostX {
   static constexpr int W = 1;
   int tid = 0, nthr = 1, lane = 0, warp = 0, nwarp = 1;
   int64_t* sh = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int sort_cap = 0;
   void sync() {}
   int64_t clock() { return 0; }
   void wsync() {}
@@ -29,7 +32,7 @@ struct HostX {
   void errset(GroupDev& g, const ErrInfo& e) { if (!g.err.code) g.err = e; }
   void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     if (n <= 1 || bits <= 0) return;
-    if (n > SORT_CAP) { std::fprintf(stderr, "emu: sort of %d > SORT_CAP\n", n); std::abort(); }
+    if (n > sort_cap) { std::fprintf(stderr, "emu: sort of %d > sort cap %d\n", n, sort_cap); std::abort(); }
     const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
     std::vector<std::pair<uint64_t, int32_t>> v(n);
     for (int i = 0; i < n; ++i) v[i] = {keys[i], vals[i]};
@@ -39,13 +42,21 @@ struct HostX {
   void scan(int64_t* a, int n) { for (int i = 1; i < n; ++i) a[i] += a[i - 1]; }
 };
 
-size_t kernel_smem_bytes() { return SH_WORDS * sizeof(int64_t); }
+int sort_ipt_for(int64_t n) {
+  for (int ipt : {1, 2, 4, 8, 16}) if (n <= int64_t(NT) * ipt) return ipt;
+  return SORT_IPT;
+}
+size_t kernel_smem_bytes(int, int) { return SH_WORDS * sizeof(int64_t); }
 
-cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, cudaStream_t) {
+cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, cudaStream_t) {
   std::vector<int64_t> sh(SH_WORDS);
+  std::vector<int64_t> tmp(96 * 1024 / 8);  // stands in for the shared sort scratch
   for (int gi = 0; gi < n_groups; ++gi) {
     HostX x;
     x.sh = sh.data();
+    x.tmp = tmp.data();
+    x.tmp_bytes = size_t(NT) * ipt * sizeof(int64_t);  // like the device tile
+    x.sort_cap = NT * ipt;
     if (mode == 0) plan_group(x, groups[gi]);
     else analyze_group(x, groups[gi]);
   }

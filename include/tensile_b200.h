@@ -231,6 +231,40 @@ typedef struct tsl_plan_desc {
 int tsl_analyze_job(tsl_ctx* ctx, const tsl_job_desc* job, const tsl_plan_desc* plan,
                     tsl_result** out);
 
+/* ---- plan executor (north-star item 5; reference analogue: the scheduled
+ * mode of memsched::simulate, simulator.cpp:112-569) --------------------------
+ * Replays job `job` of a build_plan result on the device: ops are timed spin
+ * kernels on a compute stream (1 tick = tick_ns of device time), swaps are
+ * real pinned-host cudaMemcpyAsync on ONE copy stream (the reference's single
+ * FIFO channel) fired at trigger end + delta, and a device-side allocator
+ * counts footprint and high-water mark. A swapped-out device slot is
+ * poisoned, so reads after a late or missing swap-in are caught. */
+typedef struct tsl_exec_config {
+  int64_t tick_ns;        /* device ns per planner tick (default 1000)      */
+  int32_t iterations;     /* iterations replayed, 1..8 (default 3)           */
+  int64_t bytes_per_unit; /* device/host bytes per planner byte (default 16) */
+} tsl_exec_config;
+
+typedef struct tsl_exec_report {
+  int64_t predicted_peak;      /* PeakReport::memory_peak of the plan         */
+  int64_t hwm;                 /* executor allocator high-water mark (units)  */
+  int64_t final_footprint;     /* allocator footprint after the last iteration */
+  int32_t iterations;
+  double iteration_ms[8];      /* device-timed length of each iteration       */
+  double planned_iteration_ms; /* iteration_period x tick_ns                  */
+  int32_t swap_outs, swap_ins; /* completed transfers                         */
+  int64_t bytes_d2h, bytes_h2d;
+  int32_t verify_errors;       /* inputs whose data did not survive a swap    */
+  int32_t violations;          /* reads of absent inputs / bad releases       */
+  int32_t kernels;             /* kernels launched by the replay              */
+  double total_ms;             /* host wall time of the call                  */
+} tsl_exec_report;
+
+void tsl_exec_config_default(tsl_exec_config* cfg);
+/* cfg: the planner config the plan was built with (transfer durations). */
+int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_config* cfg,
+                     const tsl_exec_config* ex, tsl_exec_report* out);
+
 /* Result accessors. Jobs are ordered by job id (std::map<JobId,...>). */
 int32_t tsl_result_n_jobs(const tsl_result* r);
 int tsl_result_job(const tsl_result* r, int32_t i, tsl_job_view* out);

@@ -85,6 +85,18 @@ class TslStats(C.Structure):
                 ("cyc_apply", C.c_int64), ("debug", C.c_int64 * 4), ("cyc_pendsort", C.c_int64), ("fitprof", C.c_int64 * 9)]
 
 
+class TslExecConfig(C.Structure):
+    _fields_ = [("tick_ns", C.c_int64), ("iterations", C.c_int32), ("bytes_per_unit", C.c_int64)]
+
+
+class TslExecReport(C.Structure):
+    _fields_ = [("predicted_peak", C.c_int64), ("hwm", C.c_int64), ("final_footprint", C.c_int64),
+                ("iterations", C.c_int32), ("iteration_ms", C.c_double * 8), ("planned_iteration_ms", C.c_double),
+                ("swap_outs", C.c_int32), ("swap_ins", C.c_int32), ("bytes_d2h", C.c_int64), ("bytes_h2d", C.c_int64),
+                ("verify_errors", C.c_int32), ("violations", C.c_int32), ("kernels", C.c_int32),
+                ("total_ms", C.c_double)]
+
+
 def make_config(pcie_bandwidth: int = 1, transfer_setup: int = 0, memory_budget: int = 0,
                 ewma_alpha: float = 0.3, replan_threshold: float = 0.2, stall_epsilon: float = 0.0005,
                 stall_min_iters: int = 100, cold_start_gpu_usage: float = 0.5, **_ignored) -> TslConfig:

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "tensile_b200.h"
+#include "tsl_exec.h"
 #include "tsl_kernel.h"
 
 using namespace tsl;
@@ -1231,5 +1232,338 @@ char* tsl_result_report_json(const tsl_result* r, int32_t i) {
 }
 void tsl_result_destroy(tsl_result* r) { delete r; }
 void tsl_free(void* p) { std::free(p); }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Plan executor host driver (tsl_exec.cu holds the kernels)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct ExecStepH {
+  int32_t op;
+  bool regen;
+  int64_t ticks;
+  int64_t start, end;  // planned ticks within the iteration
+  std::vector<int32_t> ins, outs, rel;
+  std::vector<int64_t> out_size, rel_size;
+  std::vector<int32_t> access_ids;
+};
+
+struct ExecXferH {
+  int32_t ev;      // plan index
+  int32_t storage;
+  int dir;         // 0 out, 1 in
+  int32_t anchor;  // step index or -1 (iteration start)
+  int64_t delta, arrival, dur, size;
+  int32_t serve_step;  // swap-in: step that waits for it
+};
+
+tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl_config& cfg,
+                        const tsl_exec_config& ex) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (ji < 0 || ji >= static_cast<int32_t>(r->jobs.size())) fail(TSL_ERR_ARGUMENT, "bad job index");
+  if (ex.iterations < 1 || ex.iterations > 8) fail(TSL_ERR_ARGUMENT, "iterations must be in 1..8");
+  if (ex.tick_ns <= 0 || ex.bytes_per_unit <= 0) fail(TSL_ERR_ARGUMENT, "tick_ns and bytes_per_unit must be positive");
+  const JobOut& o = r->jobs[static_cast<size_t>(ji)];
+  const Graph& g = *o.g;
+  // access sequence with the true latencies (simulator.cpp:168-213)
+  std::vector<int32_t> acc_op, acc_tensor;
+  std::vector<std::vector<int32_t>> op_acc(g.O);
+  for (int32_t op : g.topo) {
+    for (int32_t i = g.in_off[op]; i < g.in_off[op + 1]; ++i) {
+      op_acc[op].push_back(static_cast<int32_t>(acc_op.size()));
+      acc_op.push_back(op);
+      acc_tensor.push_back(g.in[i]);
+    }
+    for (int32_t i = g.out_off[op]; i < g.out_off[op + 1]; ++i) {
+      op_acc[op].push_back(static_cast<int32_t>(acc_op.size()));
+      acc_op.push_back(op);
+      acc_tensor.push_back(g.out[i]);
+    }
+  }
+  std::set<int64_t> flags(o.flags.begin(), o.flags.end());
+  // steps: recompute regenerations right before their target op, then the op
+  std::vector<ExecStepH> steps;
+  std::vector<int32_t> op_step(g.O, -1);
+  int64_t clock = 0;
+  for (int32_t op : g.topo) {
+    for (size_t k = 0; k < o.rc_id.size(); ++k) {
+      if (acc_op[static_cast<size_t>(o.rc_target[k])] != op) continue;
+      ExecStepH st{};
+      st.op = o.rc_regen[k];
+      st.regen = true;
+      st.ticks = g.lat[st.op];
+      for (int32_t i = g.in_off[st.op]; i < g.in_off[st.op + 1]; ++i) st.ins.push_back(g.store[g.in[i]]);
+      const int32_t s = g.store[o.rc_tensor[k]];
+      st.outs.push_back(s);
+      st.out_size.push_back(g.size[s]);
+      st.start = clock;
+      clock += st.ticks;
+      st.end = clock;
+      steps.push_back(std::move(st));
+    }
+    ExecStepH st{};
+    st.op = op;
+    st.regen = false;
+    st.ticks = g.lat[op];
+    for (int32_t i = g.in_off[op]; i < g.in_off[op + 1]; ++i) st.ins.push_back(g.store[g.in[i]]);
+    for (int32_t i = g.out_off[op]; i < g.out_off[op + 1]; ++i) {
+      const int32_t t = g.out[i];
+      st.outs.push_back(g.store[t]);
+      st.out_size.push_back(g.store[t] != t ? 0 : g.size[t]);  // in-place update: no allocation
+    }
+    for (int32_t a : op_acc[op])
+      if (flags.count(a)) {
+        st.rel.push_back(g.store[acc_tensor[a]]);
+        st.rel_size.push_back(g.size[g.store[acc_tensor[a]]]);
+      }
+    st.access_ids = op_acc[op];
+    st.start = clock;
+    clock += st.ticks;
+    st.end = clock;
+    op_step[op] = static_cast<int32_t>(steps.size());
+    steps.push_back(std::move(st));
+  }
+  const int32_t nsteps = static_cast<int32_t>(steps.size());
+  // transfers of one iteration, in channel (arrival) order
+  std::vector<ExecXferH> xs;
+  std::vector<int32_t> outs_per_iter(g.T, 0);
+  for (size_t e = 0; e < o.ev_id.size(); ++e) {
+    ExecXferH t{};
+    t.ev = static_cast<int32_t>(e);
+    t.storage = g.store[o.ev_tensor[e]];
+    t.dir = o.ev_dir[e];
+    t.anchor = o.ev_trig[e] < 0 ? -1 : op_step[acc_op[static_cast<size_t>(o.ev_trig[e])]];
+    t.delta = o.ev_delta[e];
+    t.arrival = (t.anchor < 0 ? 0 : steps[static_cast<size_t>(t.anchor)].end) + t.delta;
+    t.size = g.size[t.storage];
+    t.dur = (t.size + cfg.pcie_bandwidth - 1) / cfg.pcie_bandwidth + cfg.transfer_setup;
+    t.serve_step = (t.dir == 1 && o.ev_serves[e] >= 0) ? op_step[acc_op[static_cast<size_t>(o.ev_serves[e])]] : -1;
+    if (t.dir == 0) outs_per_iter[t.storage]++;
+    xs.push_back(t);
+  }
+  std::stable_sort(xs.begin(), xs.end(), [](const ExecXferH& a, const ExecXferH& b) { return a.arrival < b.arrival; });
+  // device / host memory
+  std::vector<int64_t> slot_off(g.T, 0);
+  int64_t pool_bytes = 0;
+  for (int32_t t = 0; t < g.T; ++t) {
+    if (g.store[t] != t) continue;
+    slot_off[t] = pool_bytes;
+    pool_bytes += ((g.size[t] * ex.bytes_per_unit + 255) / 256) * 256;
+  }
+  std::vector<int64_t> host_off(g.T, -1);
+  int64_t host_bytes = 0;
+  for (auto& t : xs)
+    if (host_off[t.storage] < 0) {
+      host_off[t.storage] = host_bytes;
+      host_bytes += ((g.size[t.storage] * ex.bytes_per_unit + 255) / 256) * 256;
+    }
+  // op descriptors (device arena)
+  std::vector<int32_t> i32;
+  std::vector<int64_t> i64;
+  struct OpOff { size_t ins, outs, rel, osz, rsz; };
+  std::vector<OpOff> offs;
+  for (auto& st : steps) {
+    OpOff f{};
+    f.ins = i32.size(); i32.insert(i32.end(), st.ins.begin(), st.ins.end());
+    f.outs = i32.size(); i32.insert(i32.end(), st.outs.begin(), st.outs.end());
+    f.rel = i32.size(); i32.insert(i32.end(), st.rel.begin(), st.rel.end());
+    f.osz = i64.size(); i64.insert(i64.end(), st.out_size.begin(), st.out_size.end());
+    f.rsz = i64.size(); i64.insert(i64.end(), st.rel_size.begin(), st.rel_size.end());
+    offs.push_back(f);
+  }
+  std::vector<int32_t> init_st;
+  std::vector<int64_t> init_sz;
+  std::set<int32_t> wrapped_in;
+  for (size_t e = 0; e < o.ev_id.size(); ++e)
+    if (o.ev_dir[e] == 1 && o.ev_wraps[e]) wrapped_in.insert(g.store[o.ev_tensor[e]]);
+  for (int32_t t = 0; t < g.T; ++t) {
+    if (g.store[t] != t) continue;
+    const int8_t k = g.kind[t];
+    if (k != TSL_KIND_PARAMETER && k != TSL_KIND_INPUT && k != TSL_KIND_OUTPUT) continue;
+    if (wrapped_in.count(t)) continue;
+    init_st.push_back(t);
+    init_sz.push_back(g.size[t]);
+  }
+  const int iters = ex.iterations;
+  Layout L;
+  const size_t o_dev = L.take<ExecDevice>(1);
+  const size_t o_ops = L.take<ExecOp>(steps.size());
+  const size_t o_i32 = L.take<int32_t>(i32.size() + 1);
+  const size_t o_i64 = L.take<int64_t>(i64.size() + 1);
+  const size_t o_slot = L.take<int64_t>(g.T);
+  const size_t o_res = L.take<int32_t>(g.T);
+  const size_t o_ver = L.take<int32_t>(g.T);
+  const size_t o_pend = L.take<int32_t>(g.T);
+  const size_t o_opi = L.take<int32_t>(g.T);
+  const size_t o_init = L.take<int32_t>(init_st.size() + 1);
+  const size_t o_initsz = L.take<int64_t>(init_sz.size() + 1);
+  const size_t o_end = L.take<uint64_t>(size_t(iters) * nsteps + 1);
+  const size_t o_iter = L.take<uint64_t>(iters + 1);
+  const size_t o_pool = L.take<uint8_t>(pool_bytes + 256);
+  const size_t total = L.off;
+  uint8_t* dbuf = nullptr;
+  uint8_t* hpin = nullptr;
+  std::vector<uint8_t> stage(o_pool, 0);
+  std::vector<cudaEvent_t> events;
+  cudaStream_t cs = nullptr, xs_stream = nullptr;
+  tsl_exec_report rep{};
+  auto cleanup = [&]() {
+    for (auto e : events) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+    if (xs_stream) cudaStreamDestroy(xs_stream);
+    if (dbuf) cudaFree(dbuf);
+    if (hpin) cudaFreeHost(hpin);
+  };
+  try {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&dbuf), total), "cudaMalloc");
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hpin), std::max<int64_t>(host_bytes, 256)), "cudaMallocHost");
+    cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&xs_stream, cudaStreamNonBlocking), "stream");
+    auto D = [&](size_t off) { return dbuf + off; };
+    ExecDevice dev{};
+    dev.tick_ns = static_cast<uint64_t>(ex.tick_ns);
+    dev.pool = D(o_pool);
+    dev.slot_off = reinterpret_cast<const int64_t*>(D(o_slot));
+    dev.resident = reinterpret_cast<int32_t*>(D(o_res));
+    dev.version = reinterpret_cast<int32_t*>(D(o_ver));
+    dev.out_pending = reinterpret_cast<int32_t*>(D(o_pend));
+    dev.op_end_ns = reinterpret_cast<uint64_t*>(D(o_end));
+    dev.iter_start_ns = reinterpret_cast<uint64_t*>(D(o_iter));
+    std::memcpy(stage.data() + o_dev, &dev, sizeof dev);
+    for (size_t k = 0; k < steps.size(); ++k) {
+      ExecOp op{};
+      op.index = static_cast<int32_t>(k);
+      op.ticks = steps[k].ticks;
+      op.start = steps[k].start;
+      op.n_in = static_cast<int32_t>(steps[k].ins.size());
+      op.n_out = static_cast<int32_t>(steps[k].outs.size());
+      op.n_rel = static_cast<int32_t>(steps[k].rel.size());
+      op.ins = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].ins;
+      op.outs = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].outs;
+      op.rel = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].rel;
+      op.out_size = reinterpret_cast<const int64_t*>(D(o_i64)) + offs[k].osz;
+      op.rel_size = reinterpret_cast<const int64_t*>(D(o_i64)) + offs[k].rsz;
+      std::memcpy(stage.data() + o_ops + k * sizeof(ExecOp), &op, sizeof op);
+    }
+    if (!i32.empty()) std::memcpy(stage.data() + o_i32, i32.data(), i32.size() * 4);
+    if (!i64.empty()) std::memcpy(stage.data() + o_i64, i64.data(), i64.size() * 8);
+    std::memcpy(stage.data() + o_slot, slot_off.data(), slot_off.size() * 8);
+    std::memcpy(stage.data() + o_opi, outs_per_iter.data(), outs_per_iter.size() * 4);
+    if (!init_st.empty()) std::memcpy(stage.data() + o_init, init_st.data(), init_st.size() * 4);
+    if (!init_sz.empty()) std::memcpy(stage.data() + o_initsz, init_sz.data(), init_sz.size() * 8);
+    cuda_check(cudaMemcpy(dbuf, stage.data(), o_pool, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemset(D(o_pool), 0, pool_bytes + 256), "memset");
+    ExecDevice* d = reinterpret_cast<ExecDevice*>(D(o_dev));
+    auto ev = [&]() {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      events.push_back(e);
+      return e;
+    };
+    int kernels = 0;
+    cuda_check(exec_launch_init(d, reinterpret_cast<const int32_t*>(D(o_init)),
+                                reinterpret_cast<const int64_t*>(D(o_initsz)), static_cast<int>(init_st.size()), cs),
+               "init");
+    ++kernels;
+    for (int32_t s : wrapped_in) {
+      cuda_check(exec_launch_host_tag(d, s, hpin + host_off[s], cs), "host tag");
+      ++kernels;
+    }
+    cudaEvent_t ready = ev();
+    cuda_check(cudaEventRecord(ready, cs), "event");
+    cuda_check(cudaStreamWaitEvent(xs_stream, ready, 0), "wait");
+    std::vector<cudaEvent_t> op_end(static_cast<size_t>(nsteps));
+    for (auto& e : op_end) e = ev();
+    std::vector<cudaEvent_t> in_done(xs.size());
+    for (auto& e : in_done) e = ev();
+    cudaEvent_t it_start = ev(), xfer_tail = ev();
+    for (int it = 0; it < iters; ++it) {
+      cuda_check(exec_launch_iter_begin(d, reinterpret_cast<const int32_t*>(D(o_opi)), g.T, it, cs), "iter");
+      ++kernels;
+      cuda_check(cudaEventRecord(it_start, cs), "event");
+      const int base = it * nsteps;
+      size_t xi = 0;
+      auto enqueue_xfer = [&](const ExecXferH& t, size_t idx) {
+        cuda_check(cudaStreamWaitEvent(xs_stream, t.anchor < 0 ? it_start : op_end[static_cast<size_t>(t.anchor)], 0),
+                   "wait");
+        cuda_check(exec_launch_delay(d, t.anchor < 0 ? -1 : base + t.anchor, it, t.delta, xs_stream), "delay");
+        const size_t nbytes = static_cast<size_t>(t.size * ex.bytes_per_unit);
+        uint8_t* dev_slot = D(o_pool) + slot_off[t.storage];
+        uint8_t* host_slot = hpin + host_off[t.storage];
+        if (t.dir == 0) {
+          cuda_check(cudaMemcpyAsync(host_slot, dev_slot, nbytes, cudaMemcpyDeviceToHost, xs_stream), "D2H");
+          rep.bytes_d2h += static_cast<int64_t>(nbytes);
+        } else {
+          cuda_check(cudaMemcpyAsync(dev_slot, host_slot, nbytes, cudaMemcpyHostToDevice, xs_stream), "H2D");
+          rep.bytes_h2d += static_cast<int64_t>(nbytes);
+        }
+        cuda_check(exec_launch_done(d, t.storage, t.size, t.dur, t.dir, xs_stream), "done");
+        kernels += 2;
+        if (t.dir == 1) cuda_check(cudaEventRecord(in_done[idx], xs_stream), "event");
+      };
+      for (int32_t k = 0; k < nsteps; ++k) {
+        // transfers that arrive by this step's start and whose anchor is already enqueued
+        while (xi < xs.size() && xs[xi].arrival <= steps[static_cast<size_t>(k)].start && xs[xi].anchor < k) {
+          enqueue_xfer(xs[xi], xi);
+          ++xi;
+        }
+        for (size_t q = 0; q < xs.size(); ++q)  // swap-ins serving this step
+          if (xs[q].serve_step == k && q < xi) cuda_check(cudaStreamWaitEvent(cs, in_done[q], 0), "wait");
+        cuda_check(exec_launch_op(d, reinterpret_cast<const ExecOp*>(D(o_ops)) + k, base, it, cs), "op");
+        ++kernels;
+        cuda_check(cudaEventRecord(op_end[static_cast<size_t>(k)], cs), "event");
+      }
+      for (; xi < xs.size(); ++xi) enqueue_xfer(xs[xi], xi);
+      // the iteration ends when its transfers are done (simulator.cpp:478-484)
+      cuda_check(cudaEventRecord(xfer_tail, xs_stream), "event");
+      cuda_check(cudaStreamWaitEvent(cs, xfer_tail, 0), "wait");
+      cuda_check(cudaStreamWaitEvent(xs_stream, op_end[static_cast<size_t>(nsteps - 1)], 0), "wait");
+    }
+    cuda_check(exec_launch_iter_begin(d, reinterpret_cast<const int32_t*>(D(o_opi)), 0, iters, cs), "iter");
+    ++kernels;
+    cuda_check(cudaStreamSynchronize(cs), "sync");
+    cuda_check(cudaStreamSynchronize(xs_stream), "sync");
+    ExecDevice out{};
+    cuda_check(cudaMemcpy(&out, d, sizeof out, cudaMemcpyDeviceToHost), "D2H");
+    std::vector<uint64_t> starts(iters + 1);
+    cuda_check(cudaMemcpy(starts.data(), D(o_iter), starts.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    rep.predicted_peak = o.st.peak;
+    rep.hwm = out.hwm;
+    rep.final_footprint = out.footprint;
+    rep.iterations = iters;
+    for (int it = 0; it < iters; ++it) rep.iteration_ms[it] = double(starts[it + 1] - starts[it]) / 1e6;
+    rep.planned_iteration_ms = double(clock) * double(ex.tick_ns) / 1e6;
+    rep.swap_outs = out.n_out;
+    rep.swap_ins = out.n_in;
+    rep.verify_errors = out.verify_errors;
+    rep.violations = out.violations;
+    rep.kernels = kernels;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  rep.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rep;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tsl_exec_config_default(tsl_exec_config* c) {
+  c->tick_ns = 1000;
+  c->iterations = 3;
+  c->bytes_per_unit = 16;
+}
+
+int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_config* cfg,
+                     const tsl_exec_config* ex, tsl_exec_report* out) {
+  if (!ctx || !r || !cfg || !ex || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] { *out = execute(ctx, r, job, *cfg, *ex); });
+}
 
 }  // extern "C"

@@ -74,6 +74,8 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     L.tsl_result_report_json.restype = vp
     L.tsl_result_destroy.argtypes = [vp]
     L.tsl_free.argtypes = [vp]
+    L.tsl_execute_plan.argtypes = [vp, vp, C.c_int32, C.POINTER(abi.TslConfig), C.POINTER(abi.TslExecConfig),
+                                   C.POINTER(abi.TslExecReport)]
     _libs[path] = L
     return L
 
@@ -251,6 +253,33 @@ class Planner:
         if rc:
             _raise(self.lib, rc)
         return PreparedPlan(self, h, descs, len(groups))
+
+    def build_and_execute(self, jobs: Sequence, config: dict, tick_ns: int = 1000, iterations: int = 3,
+                          bytes_per_unit: int = 16) -> dict:
+        """build_plan, then replay every job's plan on the device (plan
+        executor): {"plan": build_plan dict, "exec": {job_id: report dict}}."""
+        descs, arr = abi.pack_jobs(jobs, config.get("max_swap_ratios"))
+        cfg = abi.make_config(**config)
+        res = C.c_void_p()
+        rc = self.lib.tsl_build_plan(self._ctx, arr, len(descs), C.byref(cfg), C.byref(res))
+        if rc:
+            _raise(self.lib, rc)
+        try:
+            out = {"plan": _collect(self.lib, res, descs), "exec": {}}
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit)
+            for i in range(self.lib.tsl_result_n_jobs(res)):
+                rep = abi.TslExecReport()
+                rc = self.lib.tsl_execute_plan(self._ctx, res, i, C.byref(cfg), C.byref(ex), C.byref(rep))
+                if rc:
+                    _raise(self.lib, rc)
+                v = abi.TslJobView()
+                self.lib.tsl_result_job(res, i, C.byref(v))
+                d = {f: getattr(rep, f) for f, _ in abi.TslExecReport._fields_}
+                d["iteration_ms"] = list(rep.iteration_ms)[: rep.iterations]
+                out["exec"][v.job_id.decode()] = d
+        finally:
+            self.lib.tsl_result_destroy(res)
+        return out
 
     def analyze_job(self, graph: dict, latencies: dict, plan: dict) -> dict:
         jd = abi.JobDesc(graph, latencies)

@@ -7,6 +7,7 @@
 #include <utility>
 #include <vector>
 
+#include "tsl_exec.h"
 #include "tsl_kernel.h"
 #include "tsl_plan.cuh"
 
@@ -62,5 +63,13 @@ cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, in
   }
   return cudaSuccess;
 }
+
+// The plan executor needs a GPU: the emulation build reports an error.
+cudaError_t exec_launch_op(ExecDevice*, const ExecOp*, int, int, cudaStream_t) { return 1; }
+cudaError_t exec_launch_delay(ExecDevice*, int32_t, int, int64_t, cudaStream_t) { return 1; }
+cudaError_t exec_launch_done(ExecDevice*, int32_t, int64_t, int64_t, int, cudaStream_t) { return 1; }
+cudaError_t exec_launch_init(ExecDevice*, const int32_t*, const int64_t*, int, cudaStream_t) { return 1; }
+cudaError_t exec_launch_host_tag(ExecDevice*, int32_t, uint8_t*, cudaStream_t) { return 1; }
+cudaError_t exec_launch_iter_begin(ExecDevice*, const int32_t*, int32_t, int, cudaStream_t) { return 1; }
 
 }  // namespace tsl

@@ -155,6 +155,7 @@ typedef struct tsl_stats {
   int64_t debug[4];             /* development counters */
   int64_t cyc_pendsort;
   int64_t fitprof[9];
+  int64_t evalprof[7];  /* evaluator phases: prep, emit, sort1, group, automaton, scan.., peak..report */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

@@ -53,7 +53,10 @@ __global__ void exec_op(ExecDevice* d, const ExecOp* op, int base, int iter) {
   // start at the planned offset into the iteration, never earlier (a late
   // swap-in still delays the op through the stream wait)
   const uint64_t planned = d->iter_start_ns[iter] + uint64_t(op->start) * d->tick_ns;
-  while (gtimer() < planned) {
+  // allocations land half a tick after their planned instant, frees exactly
+  // on it: the reference processes a tick's frees before its allocations
+  // (simulator.cpp:47-52, peak.cpp:51-62)
+  while (gtimer() < planned + d->tick_ns / 2) {
   }
   const uint64_t t0 = gtimer();
   for (int k = 0; k < op->n_in; ++k) {
@@ -97,7 +100,7 @@ __global__ void exec_delay(ExecDevice* d, int32_t anchor_slot, int iter, int64_t
 // only a correct swap-in can restore it; swap-in allocates).
 __global__ void exec_xfer_done(ExecDevice* d, int32_t s, int64_t size, int64_t dur_ticks, int dir) {
   if (threadIdx.x != 0) return;
-  const uint64_t until = d->xfer_start_ns + uint64_t(dur_ticks) * d->tick_ns;
+  const uint64_t until = d->xfer_start_ns + uint64_t(dur_ticks) * d->tick_ns + (dir == 1 ? d->tick_ns / 2 : 0);
   while (gtimer() < until) {
   }
   if (dir == 0) {

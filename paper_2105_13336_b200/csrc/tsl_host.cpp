@@ -515,7 +515,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     const size_t E = size_t(P->sort_cap);
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
-    q.x_time = L.take<int64_t>(E);
+    q.x_time = L.take<int64_t>(2 * E);  // second half: evaluator scan scratch
     q.x_fp = L.take<int64_t>(E);
     q.x_store = L.take<int32_t>(E);
     q.x_aid = L.take<int32_t>(E);
@@ -857,7 +857,8 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   s.cyc_apply = G.stats.cyc[8];
   for (int k = 0; k < 4; ++k) s.debug[k] = G.stats.cyc[12 + k];
   s.cyc_pendsort = G.stats.cyc[11];
-  for (int k = 0; k < 9; ++k) s.fitprof[k] = G.stats.cyc[16 + k];
+  for (int k = 0; k < 4; ++k) s.fitprof[k] = G.stats.cyc[16 + k];
+  for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
   return R;
 }
 

@@ -51,6 +51,8 @@ struct DevX {
   }
   __device__ void wsync() { __syncwarp(); }
   __device__ bool wany(bool p) { return __any_sync(0xffffffffu, p); }
+  __device__ unsigned wballot(bool p) { return __ballot_sync(0xffffffffu, p); }
+  __device__ int ffs(unsigned m) { return __ffs(m); }
   // warp exclusive prefix sum of v; *total = warp sum
   __device__ int32_t wexcl(int32_t v, int32_t* total) {
     int32_t inc = v;
@@ -109,6 +111,19 @@ struct DevX {
     else if (n <= 16 * NT) sort_ipt<16>(keys, vals, n, bits);
     else if (n <= SORT_IPT * NT) sort_ipt<SORT_IPT>(keys, vals, n, bits);
     else __trap();  // callers check SORT_CAP first
+  }
+
+  // Inclusive max-scan of a[0, n) in place.
+  __device__ void scan_max(int64_t* a, int n) {
+    __syncthreads();
+    const int chunk = (n + NT - 1) / NT;
+    const int b = tid * chunk, e = min(n, b + chunk);
+    int64_t m = INT64_MIN;
+    for (int i = b; i < e; ++i) m = max(m, a[i]);
+    int64_t off;
+    BScan(*reinterpret_cast<typename BScan::TempStorage*>(tmp)).ExclusiveScan(m, off, INT64_MIN, cub::Max());
+    for (int i = b; i < e; ++i) { off = max(off, a[i]); a[i] = off; }
+    __syncthreads();
   }
 
   // Inclusive scan of a[0, n) in place.

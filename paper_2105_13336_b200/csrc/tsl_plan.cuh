@@ -54,6 +54,13 @@ constexpr int MAXB = 32;         // jobs per evaluation batch
 constexpr int EV_FIELDS = 12;    // swap-event fields (rollback copies)
 constexpr int RC_FIELDS = 6;
 
+TSL_HD int popc32(unsigned v) {
+#ifdef __CUDA_ARCH__
+  return __popc(v);
+#else
+  return __builtin_popcount(v);
+#endif
+}
 TSL_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 TSL_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 TSL_HD int nbits(uint64_t v) {  // bits needed to hold v (0 -> 0)
@@ -798,6 +805,8 @@ template <class X>
 TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   int64_t* sh = x.sh;
   const int nb = je - jb;
+  int64_t et0 = x.clock(), et1;
+  auto etick = [&](int k) { et1 = x.clock(); if (x.tid == 0) g.stats.cyc[20 + k] += et1 - et0; et0 = et1; };
   int64_t* gsh = sh + MAXB * NF;  // [0]=tmin [1]=tmax [2]=n_total [3]=bits info [4]=fail
   if (x.tid == 0) {
     for (int b = 0; b < nb; ++b) {
@@ -947,6 +956,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     k = (k << xbits) | uint64_t(tie);
     return k;
   };
+  etick(0);
   // 4. emit events (build_timeline, peak.cpp:66-174)
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
@@ -1001,8 +1011,10 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     }
   }
   x.sync();
+  etick(1);
   // 5. timeline order (sort_timeline, peak.cpp:44-62)
   x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 3 + xbits);
+  etick(2);
   // 6. group sorted positions by (job, storage), keeping timeline order
   for (int64_t m = x.tid; m < n; m += x.nthr) {
     const int32_t slot = g.k_val[m];
@@ -1013,19 +1025,39 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   }
   x.sync();
   x.sort(g.x_key2, g.x_seq2, int32_t(n), jbits + rbits);
-  // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230)
-  for (int64_t m = x.tid; m < n; m += x.nthr) {
-    if (m > 0 && g.x_key2[m] == g.x_key2[m - 1]) continue;
-    int32_t pos = g.x_seq2[m];
-    const int b = g.x_job[g.x_order[pos]];
-    const JobDev& J = g.jobs[jb + b];
-    const int32_t s = g.x_store[g.x_order[pos]];
-    uint8_t res = J.res_init[s];
-    const int64_t size = J.t_size[s];
-    for (int64_t q = m; q < n && g.x_key2[q] == g.x_key2[m]; ++q) {
-      pos = g.x_seq2[q];
+  etick(3);
+  // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230),
+  // in parallel: in (job, storage)-grouped order, the residency before an
+  // event is set by the previous state-changing event of its storage (TGA
+  // and swap-in make it resident, release and swap-out evict); two max-scans
+  // give that index and the storage's first index for every event.
+  {
+    int64_t* chg = reinterpret_cast<int64_t*>(g.k_key);  // free after sort 1
+    int64_t* seg = g.x_time + g.ecap;                    // second half of the time scratch
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int ty = g.x_type[g.x_order[g.x_seq2[m]]] & 7;
+      chg[m] = ty == EV_TUA ? -1 : m;
+      seg[m] = (m == 0 || g.x_key2[m] != g.x_key2[m - 1]) ? m : 0;
+    }
+    x.sync();
+    x.scan_max(chg, int32_t(n));
+    x.scan_max(seg, int32_t(n));
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int32_t pos = g.x_seq2[m];
       const int32_t slot = g.x_order[pos];
+      const int b = g.x_job[slot];
+      const JobDev& J = g.jobs[jb + b];
+      const int32_t s = g.x_store[slot];
       const int ty = g.x_type[slot] & 7;
+      const int64_t prev = m > 0 ? chg[m - 1] : -1;  // last state change strictly before m
+      uint8_t res;
+      if (prev >= seg[m]) {
+        const int pt = g.x_type[g.x_order[g.x_seq2[prev]]] & 7;
+        res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
+      } else {
+        res = J.res_init[s];
+      }
+      const int64_t size = J.t_size[s];
       int64_t eff = 0;
       int errc = 0;
       switch (ty) {
@@ -1047,8 +1079,9 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       g.x_state[pos] = res;
       if (errc) x.amin(&sh[b * NF + F_ERR], (int64_t(pos) << 3) | errc);
     }
+    x.sync();
   }
-  x.sync();
+  etick(4);
   // 8. footprint curve: inclusive scan of the effective deltas
   x.scan(g.x_fp, int32_t(n));
   if (x.tid == 0) {
@@ -1071,6 +1104,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     x.amax(&sh[b * NF + F_MAXFP], g.x_fp[m]);
   }
   x.sync();
+  etick(5);
   // 9. first strict maximum (analyze_peak, peak.cpp:236-241)
   for (int64_t m = x.tid; m < n; m += x.nthr) {
     const int b = g.x_job[g.x_order[m]];
@@ -1104,6 +1138,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     if (last >= 0) g.jobs[jb + b].in_peak[g.x_store[slot0]] = g.x_state[last];
   }
   x.sync();
+  etick(6);
   // 11. report + curve
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
@@ -1282,6 +1317,182 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
   }
 }
 
+// Re-scores candidate m of job j exactly against the real state: pass-start
+// busy structure + every interval committed before it in this pass (pend,
+// brought up to date lazily) -- the sequential reference semantics. Returns
+// the number of pairs committed (0: failed); -1 on error.
+template <class X>
+TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m, int32_t* cand, int32_t* cinfo,
+                                 int64_t* wtmp, GroupStats& ls, ErrInfo& lerr) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  int32_t* ci = cinfo + m * CI_STRIDE;
+  ls.rescored += 1;
+  const int64_t rc0 = x.clock();
+  for (int64_t q = st.pend_upto; q < m; ++q) {
+    const int32_t* cq = cinfo + q * CI_STRIDE;
+    if (cq[CI_STATE] != 1 || (cand[q] >> 24) != j) continue;
+    const int32_t nq = cq[CI_NP];
+    const int32_t pn = st.pend_n;
+    if (pn + 2 * nq > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return -1; }
+    const PairRec* pr = g.pr_pool + cq[CI_P0];
+    x.wsync();
+    for (int32_t p = x.lane; p < nq; p += X::W) {
+      J.pd_s[pn + 2 * p] = pr[p].os; J.pd_e[pn + 2 * p] = pr[p].oe;
+      J.pd_s[pn + 2 * p + 1] = pr[p].is; J.pd_e[pn + 2 * p + 1] = pr[p].ie;
+    }
+    st.pend_n = pn + 2 * nq;
+    x.wsync();
+  }
+  x.wsync();
+  st.pend_upto = int32_t(m);
+  x.wsync();
+  pend_sort(x, J, st, wtmp);
+  int64_t earliest = 0, latest = 0;
+  const int kind = candidate_kind(J, st, s, earliest, latest);
+  const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+  ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+  c.dbg = &g.stats.cyc[12];
+  const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+  if (x.tid == 0) g.stats.cyc[10] += x.clock() - rc0;
+  if (c.overflow) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; lerr.tick = 5; return -1; }
+  return ok ? c.nout : 0;
+}
+
+// In-order decisions of one uncoupled job's candidates [m0, m1), 32 at a
+// time. A candidate needs individual attention only if it has a conflicting
+// earlier candidate (nconf > 0), overflowed, or was hit by a re-scored
+// commit (status bit CS_HIT, set right after each re-score); every other
+// candidate keeps its speculative result, so a warp ballot finds the next
+// attention candidate and everything before it is decided in bulk (a warp
+// prefix sum assigns event slots and ids in plan order).
+constexpr int32_t CS_HIT = 16;
+
+template <class X>
+TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int32_t* cand, int32_t* cinfo,
+                           int64_t* chull, int64_t* wtmp, GroupStats& ls, ErrInfo& lerr) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  int32_t S = st.S;
+  int64_t id = st.next_id;
+  int64_t son = st.son;
+  bool changed = false;
+  const int64_t P = imax(1, st.period);
+  int64_t m = m0;
+  while (m < m1) {
+    const int64_t c = m + x.lane;
+    const bool in = c < m1;
+    int32_t status = in ? cinfo[c * CI_STRIDE + CI_STATUS] : CS_SKIP;
+    const int32_t nconf = in ? cinfo[c * CI_STRIDE + CI_NCONF] : 0;
+    const bool attn = in && (status & 0xf) != CS_SKIP &&
+                      ((status & CS_HIT) || nconf > 0 || (status & 0xf) == CS_OVERFLOW || (status & 0xf) == CS_ERROR ||
+                       cinfo[c * CI_STRIDE + CI_P0] < 0);
+    const unsigned amask = x.wballot(attn);
+    const int f = amask ? x.ffs(amask) - 1 : X::W;
+    const int64_t nbulk = imin(int64_t(f), m1 - m);
+    // bulk: candidates [m, m + nbulk) keep their speculation
+    const bool take = x.lane < nbulk && (status & 0xf) == CS_OK;
+    const int32_t np = take ? cinfo[c * CI_STRIDE + CI_NP] : 0;
+    int32_t tot = 0;
+    const int32_t ex = x.wexcl(2 * np, &tot);
+    const int32_t ntake = popc32(x.wballot(take));
+    if (S + tot > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return changed; }
+    x.wsync();
+    if (x.lane < nbulk) {
+      int32_t* ci = cinfo + c * CI_STRIDE;
+      ci[CI_STATE] = take ? 1 : 0;
+      if (take) {
+        ci[CI_EV0] = S + ex;
+        ci[CI_ID0] = int32_t(id + ex);
+        J.swapped[cand[c] & 0xffffff] = 1;
+      }
+    }
+    x.wsync();
+    S += tot;
+    id += tot;
+    son += ntake;
+    changed = changed || ntake > 0;
+    m += nbulk;
+    if (nbulk == X::W || m >= m1) continue;
+    // attention candidate m
+    int32_t* ci = cinfo + m * CI_STRIDE;
+    const int32_t st_m = ci[CI_STATUS];
+    const int32_t s = cand[m] & 0xffffff;
+    if ((st_m & 0xf) == CS_ERROR) { lerr.code = E_NO_TGA; lerr.job = j; lerr.tensor = s; lerr.tick = 0; return changed; }
+    if (ci[CI_P0] < 0) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = g.pr_cap; lerr.tick = 4; return changed; }
+    bool valid = !(st_m & CS_HIT) && (st_m & 0xf) != CS_OVERFLOW && ci[CI_NCONF] <= CAPC;
+    {
+      bool bad = false;
+      for (int32_t k = x.lane; valid && k < ci[CI_NCONF]; k += X::W)
+        bad = bad || cinfo[int64_t(ci[CI_CONF + k]) * CI_STRIDE + CI_STATE] == 1;
+      valid = valid && !x.wany(bad);
+    }
+    int32_t npm = 0;
+    int32_t state = 0;
+    if (valid) {
+      if ((st_m & 0xf) == CS_OK) { npm = ci[CI_NP]; state = 1; }
+    } else {
+      // the real state needs this pass's commits so far
+      x.wsync();
+      st.S = S; st.next_id = id;
+      x.wsync();
+      npm = rescore_candidate(x, g, j, s, m, cand, cinfo, wtmp, ls, lerr);
+      if (npm < 0) return changed;
+      if (npm > 0) {
+        state = 2;
+        // later candidates whose placements the new intervals hit must be
+        // re-examined individually
+        const PairRec* pr = g.pr_pool + ci[CI_P0];
+        int64_t lo = INT64_MAX, hi = INT64_MIN;
+        for (int32_t p = 0; p < npm; ++p) {
+          lo = imin(lo, imin(pr[p].os, pr[p].is));
+          hi = imax(hi, imax(pr[p].oe, pr[p].ie));
+        }
+        x.wsync();
+        for (int64_t q = m + 1 + x.lane; q < m1; q += X::W) {
+          int32_t* cq = cinfo + q * CI_STRIDE;
+          if ((cq[CI_STATUS] & 0xf) == CS_SKIP || cq[CI_NW] == 0) continue;
+          if (!hits(lo, hi, chull[q * 4], chull[q * 4 + 1], P)) continue;
+          const int64_t* wv = g.w_pool + 2 * int64_t(cq[CI_W0]);
+          bool hit = false;
+          for (int32_t p = 0; p < npm && !hit; ++p)
+            for (int32_t w = 0; w < cq[CI_NW] && !hit; ++w)
+              hit = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                    hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
+          if (hit) cq[CI_STATUS] |= CS_HIT;
+        }
+        x.wsync();
+      }
+    }
+    if (state) {
+      if (S + 2 * npm > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return changed; }
+      x.wsync();
+      ci[CI_STATE] = state;
+      ci[CI_NP] = npm;
+      ci[CI_EV0] = S;
+      ci[CI_ID0] = int32_t(id);
+      J.swapped[s] = 1;
+      x.wsync();
+      S += 2 * npm;
+      id += 2 * npm;
+      son += 1;
+      changed = true;
+    } else {
+      x.wsync();
+      ci[CI_STATE] = 0;
+      x.wsync();
+    }
+    ++m;
+  }
+  x.wsync();
+  st.S = S;
+  st.next_id = id;
+  st.son = son;
+  if (changed) st.dirty = 1;
+  x.wsync();
+  return changed;
+}
+
 template <class X>
 TSL_HD bool swap_pass(X& x, GroupDev& g) {
   int64_t* sh = x.sh;
@@ -1438,7 +1649,24 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   tick(6);
   // ---- C. in-order decisions ----
   const int nseg = coupled ? 1 : g.n_jobs;
-  for (int seg = x.warp; seg < nseg; seg += x.nwarp) {
+  if (!coupled) {
+    for (int seg = x.warp; seg < nseg; seg += x.nwarp) {
+      GroupStats ls{};
+      ErrInfo lerr{};
+      int64_t* wtmp = g.wbuf + int64_t(x.warp) * 4 * g.wcap;
+      const bool ch = decide_chunked(x, g, seg, gsh[16 + seg], gsh[16 + seg + 1], cand, cinfo, chull, wtmp, ls, lerr);
+      x.wsync();
+      if (x.lane == 0) {
+        if (ch) gsh[10] = 1;
+        if (lerr.code) x.errset(g, lerr);
+        x.aadd(&g.stats.fit_queries, ls.fit_queries);
+        x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+        x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+        x.aadd(&g.stats.rescored, ls.rescored);
+      }
+    }
+  }
+  for (int seg = x.warp; coupled && seg < nseg; seg += x.nwarp) {
     GroupStats ls{};
     ErrInfo lerr{};
     const int64_t m0 = coupled ? 0 : gsh[16 + seg];

@@ -166,7 +166,7 @@ struct GroupStats {
   int64_t loop_iterations;
   int64_t sort_elems;        // elements through block sorts
   int64_t rescored;          // swap candidates re-scored after speculation
-  int64_t cyc[28];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
+  int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
 };
 
 struct GroupDev {

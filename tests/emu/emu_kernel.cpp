@@ -24,6 +24,8 @@ struct HostX {
   int64_t clock() { return 0; }
   void wsync() {}
   bool wany(bool p) { return p; }
+  unsigned wballot(bool p) { return p ? 1u : 0u; }
+  int ffs(unsigned m) { return m ? __builtin_ffs(m) : 0; }
   int32_t wexcl(int32_t v, int32_t* total) { *total = v; return 0; }
   int64_t aadd(int64_t* p, int64_t v) { int64_t o = *p; *p += v; return o; }
   int32_t aadd32(int32_t* p, int32_t v) { int32_t o = *p; *p += v; return o; }
@@ -41,6 +43,7 @@ struct HostX {
     for (int i = 0; i < n; ++i) { keys[i] = v[i].first; vals[i] = v[i].second; }
   }
   void scan(int64_t* a, int n) { for (int i = 1; i < n; ++i) a[i] += a[i - 1]; }
+  void scan_max(int64_t* a, int n) { for (int i = 1; i < n; ++i) a[i] = std::max(a[i], a[i - 1]); }
 };
 
 int sort_ipt_for(int64_t n) {

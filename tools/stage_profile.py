@@ -19,6 +19,7 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
               f"cands={s['candidates']} queries={s['busy_intervals']} rescored={s['rescored']} "
               f"spec={s['cyc_spec']/tot:.2%} conflict={s['cyc_conflict']/tot:.2%} sweep={s['cyc_sweep']/tot:.2%} "
               f"merge={s['cyc_merge']/tot:.2%} rescore(job0)={s['cyc_rescore']/tot:.2%} D={s['cyc_apply']/tot:.2%}", flush=True)
+        print("   eval phases prep/emit/sort1/group+sort2/automaton/scan+max/peak+report:", list(s["evalprof"]), flush=True)
         d = s["debug"]
         print(f"   rescore detail: queries {d[1]} avg {d[0]/max(1,d[1]):.0f} cyc; commits resolve {d[2]} total {d[3]} "
               f"cyc; pend_sort {s['cyc_pendsort']} fit setup/open/sweep {list(s['fitprof'])}", flush=True)

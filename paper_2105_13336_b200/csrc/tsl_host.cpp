@@ -71,7 +71,9 @@ const char* kind_name(int k) {
   return (k >= 0 && k < 5) ? n[k] : "?";
 }
 
-// ComputeGraph::validate, graph.cpp:49-119, same checks in the same order.
+// ComputeGraph::validate, graph.cpp:49-119, same checks in the same order and
+// the same first error; duplicate ids are found from the lexicographic sort
+// the ranks need anyway, successor sets are one sorted edge list.
 Graph load_graph(const tsl_job_desc& d) {
   Graph g;
   g.job_id = d.job_id ? d.job_id : "";
@@ -84,37 +86,57 @@ Graph load_graph(const tsl_job_desc& d) {
     fail(TSL_ERR_ARGUMENT, "null op table in job " + g.job_id);
   g.ratio_given = d.max_swap_ratio > 0 || std::isnan(d.max_swap_ratio);
   g.ratio = g.ratio_given ? d.max_swap_ratio : 1.0;
-  std::set<std::string> seen;
+  g.tid.reserve(g.T);
+  g.size.assign(d.tensor_sizes, d.tensor_sizes + g.T);
+  g.kind.assign(d.tensor_kinds, d.tensor_kinds + g.T);
   for (int i = 0; i < g.T; ++i) {
     g.tid.emplace_back(d.tensor_ids[i] ? d.tensor_ids[i] : "");
-    g.size.push_back(d.tensor_sizes[i]);
-    int8_t k = d.tensor_kinds[i];
-    if (k < 0 || k > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(k));
-    g.kind.push_back(k);
+    if (g.kind[i] < 0 || g.kind[i] > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(g.kind[i]));
   }
-  for (int i = 0; i < g.T; ++i) {
-    if (g.size[i] <= 0) fail(TSL_ERR_VALIDATION, "nonpositive size for tensor " + g.tid[i]);
-    if (!seen.insert(g.tid[i]).second) fail(TSL_ERR_VALIDATION, "duplicate tensor id " + g.tid[i]);
+  g.trank = lex_rank(g.tid);
+  {
+    // first tensor (in order) that is nonpositive or a repeated id
+    std::vector<int32_t> by(g.T);
+    for (int i = 0; i < g.T; ++i) by[g.trank[i]] = i;
+    std::vector<char> dup(g.T, 0);
+    for (int r = 1; r < g.T; ++r) {
+      if (g.tid[by[r]] != g.tid[by[r - 1]]) continue;
+      // equal ids are adjacent in rank order with ascending index (stable sort)
+      dup[by[r]] = 1;
+    }
+    for (int i = 0; i < g.T; ++i) {
+      if (g.size[i] <= 0) fail(TSL_ERR_VALIDATION, "nonpositive size for tensor " + g.tid[i]);
+      if (dup[i]) fail(TSL_ERR_VALIDATION, "duplicate tensor id " + g.tid[i]);
+    }
   }
   std::vector<int32_t> producer(g.T, -1);
-  std::vector<std::vector<int32_t>> consumers(g.T);
-  std::set<std::string> oseen;
-  g.in_off.push_back(0);
-  g.out_off.push_back(0);
   std::vector<std::string> okind;
   std::vector<int8_t> phase;
+  g.oid.reserve(g.O);
+  okind.reserve(g.O);
   for (int o = 0; o < g.O; ++o) {
     g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
     okind.emplace_back(d.op_kinds[o] ? d.op_kinds[o] : "");
     int8_t ph = d.op_phases[o];
     if (ph != 0 && ph != 1) fail(TSL_ERR_VALIDATION, "unknown op phase: #" + std::to_string(ph));
     phase.push_back(ph);
-    if (!oseen.insert(g.oid[o]).second) fail(TSL_ERR_VALIDATION, "duplicate op id " + g.oid[o]);
+  }
+  std::vector<int32_t> orank = lex_rank(g.oid);
+  std::vector<char> odup(g.O, 0);
+  {
+    std::vector<int32_t> by(g.O);
+    for (int i = 0; i < g.O; ++i) by[orank[i]] = i;
+    for (int r = 1; r < g.O; ++r)
+      if (g.oid[by[r]] == g.oid[by[r - 1]]) odup[by[r]] = 1;
+  }
+  g.in_off.assign(1, 0);
+  g.out_off.assign(1, 0);
+  for (int o = 0; o < g.O; ++o) {
+    if (odup[o]) fail(TSL_ERR_VALIDATION, "duplicate op id " + g.oid[o]);
     for (int32_t i = d.op_in_offsets[o]; i < d.op_in_offsets[o + 1]; ++i) {
       int32_t t = d.op_inputs[i];
       if (t < 0 || t >= g.T)
         fail(TSL_ERR_VALIDATION, "dangling tensor reference #" + std::to_string(t) + " in op " + g.oid[o]);
-      consumers[t].push_back(o);
       g.in.push_back(t);
     }
     for (int32_t i = d.op_out_offsets[o]; i < d.op_out_offsets[o + 1]; ++i) {
@@ -139,17 +161,17 @@ Graph load_graph(const tsl_job_desc& d) {
   g.upd.assign(g.T, -1);
   for (int o = 0; o < g.O; ++o) {
     if (phase[o] != TSL_PHASE_OPTIMIZE || okind[o] != "update") continue;
-    std::vector<int32_t> u, p;
+    int32_t u = -1, p = -1, nu = 0, np = 0;
     for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i)
-      if (g.kind[g.out[i]] == TSL_KIND_UPDATED_PARAMETER) u.push_back(g.out[i]);
-    if (u.size() != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must output exactly one updated_parameter");
+      if (g.kind[g.out[i]] == TSL_KIND_UPDATED_PARAMETER) { if (nu++ == 0) u = g.out[i]; }
+    if (nu != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must output exactly one updated_parameter");
     for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i)
-      if (g.kind[g.in[i]] == TSL_KIND_PARAMETER) p.push_back(g.in[i]);
-    if (p.size() != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must read exactly one parameter");
-    if (g.size[u[0]] != g.size[p[0]])
-      fail(TSL_ERR_VALIDATION, "updated parameter " + g.tid[u[0]] + " must match the size of " + g.tid[p[0]]);
-    alias[u[0]] = p[0];
-    g.upd[p[0]] = u[0];
+      if (g.kind[g.in[i]] == TSL_KIND_PARAMETER) { if (np++ == 0) p = g.in[i]; }
+    if (np != 1) fail(TSL_ERR_VALIDATION, "update op " + g.oid[o] + " must read exactly one parameter");
+    if (g.size[u] != g.size[p])
+      fail(TSL_ERR_VALIDATION, "updated parameter " + g.tid[u] + " must match the size of " + g.tid[p]);
+    alias[u] = p;
+    g.upd[p] = u;
   }
   for (int t = 0; t < g.T; ++t)
     if (g.kind[t] == TSL_KIND_UPDATED_PARAMETER && alias[t] < 0)
@@ -157,43 +179,55 @@ Graph load_graph(const tsl_job_desc& d) {
   g.store.resize(g.T);
   for (int t = 0; t < g.T; ++t) g.store[t] = alias[t] >= 0 ? alias[t] : t;
   g.prod = producer;
-  g.trank = lex_rank(g.tid);
   // topological_order (graph.cpp:245-282): Kahn with a min-heap on the op id,
   // plus user -> update edges for every consumer of an updated param's param.
-  std::vector<int32_t> orank = lex_rank(g.oid);
-  std::vector<int32_t> indeg(g.O, 0);
-  std::vector<std::set<int32_t>> succ(g.O);
-  for (int o = 0; o < g.O; ++o) {
+  std::vector<std::pair<int32_t, int32_t>> edges;
+  edges.reserve(g.in.size() + 16);
+  for (int o = 0; o < g.O; ++o)
     for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i) {
       int32_t p = producer[g.in[i]];
-      if (p >= 0 && p != o && succ[p].insert(o).second) indeg[o]++;
+      if (p >= 0 && p != o) edges.emplace_back(p, o);
     }
-    for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i) {
-      int32_t t = g.out[i];
-      if (g.kind[t] != TSL_KIND_UPDATED_PARAMETER || alias[t] < 0) continue;
-      for (int32_t user : consumers[alias[t]])
-        if (user != o && succ[user].insert(o).second) indeg[o]++;
-    }
+  {
+    // consumers of a parameter, for the update-after-every-use edges
+    std::vector<int32_t> coff(g.T + 1, 0), cons;
+    for (int o = 0; o < g.O; ++o)
+      for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i) coff[g.in[i] + 1]++;
+    for (int t = 0; t < g.T; ++t) coff[t + 1] += coff[t];
+    cons.resize(coff[g.T]);
+    std::vector<int32_t> cur(coff.begin(), coff.end() - 1);
+    for (int o = 0; o < g.O; ++o)
+      for (int32_t i = g.in_off[o]; i < g.in_off[o + 1]; ++i) cons[cur[g.in[i]]++] = o;
+    for (int o = 0; o < g.O; ++o)
+      for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i) {
+        const int32_t t = g.out[i];
+        if (g.kind[t] != TSL_KIND_UPDATED_PARAMETER || alias[t] < 0) continue;
+        for (int32_t k = coff[alias[t]]; k < coff[alias[t] + 1]; ++k)
+          if (cons[k] != o) edges.emplace_back(cons[k], o);
+      }
   }
+  std::sort(edges.begin(), edges.end());
+  edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+  std::vector<int32_t> indeg(g.O, 0), soff(g.O + 1, 0);
+  for (auto& e : edges) { indeg[e.second]++; soff[e.first + 1]++; }
+  for (int o = 0; o < g.O; ++o) soff[o + 1] += soff[o];
   auto cmp = [&](int32_t a, int32_t b) { return orank[a] > orank[b]; };
   std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
   for (int o = 0; o < g.O; ++o)
     if (indeg[o] == 0) ready.push(o);
+  g.topo.reserve(g.O);
   while (!ready.empty()) {
     int32_t o = ready.top();
     ready.pop();
     g.topo.push_back(o);
-    for (int32_t n : succ[o])
-      if (--indeg[n] == 0) ready.push(n);
+    for (int32_t k = soff[o]; k < soff[o + 1]; ++k)
+      if (--indeg[edges[k].second] == 0) ready.push(edges[k].second);
   }
   if (static_cast<int32_t>(g.topo.size()) != g.O) fail(TSL_ERR_VALIDATION, "cycle detected in graph of job " + g.job_id);
   // latency table (generate_access_sequence, access.cpp:33-38), checked in
   // topological order like the reference.
   g.lat.assign(g.O, 0);
-  for (int32_t o : g.topo) {
-    int64_t l = d.op_latencies ? d.op_latencies[o] : TSL_LATENCY_MISSING;
-    g.lat[o] = l;
-  }
+  for (int o = 0; o < g.O; ++o) g.lat[o] = d.op_latencies ? d.op_latencies[o] : TSL_LATENCY_MISSING;
   int64_t A = 0;
   for (int o = 0; o < g.O; ++o) A += (g.in_off[o + 1] - g.in_off[o]) + (g.out_off[o + 1] - g.out_off[o]);
   if (A > (1 << 30)) fail(TSL_ERR_CAPACITY, "job " + g.job_id + " has too many accesses");
@@ -246,8 +280,8 @@ struct JobPlace {  // byte offsets into the device buffer
 };
 
 struct GroupPlace {
-  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf;
-  int64_t pr_cap, w_cap, wcap;
+  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent;
+  int64_t pr_cap, w_cap, wcap, cb_cap;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
 };
@@ -377,6 +411,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   for (int gi = 0; gi < n_groups; ++gi) {
     for (int32_t k = offs[gi]; k < offs[gi + 1]; ++k) P->graphs[gi].push_back(load_graph(jobs[k]));
   }
+  const auto t_load = std::chrono::steady_clock::now();
   for (int gi = 0; gi < n_groups; ++gi) {
     std::vector<const Graph*> gg;
     for (auto& g : P->graphs[gi]) gg.push_back(&g);
@@ -411,6 +446,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       fail(TSL_ERR_CAPACITY, "build exceeds the single-CTA planner capacity (" + std::to_string(P->sort_cap) +
                                  " timeline events per job / candidates per pass)");
   }
+  const auto t_val = std::chrono::steady_clock::now();
   // 2. layout: [static inputs][groups|states|jobs][outputs][workspace]
   Layout L;
   P->jp.resize(n_groups);
@@ -538,9 +574,14 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (auto& p : P->jp[gi]) maxS = std::max<int64_t>(maxS, p.Scap);
     q.wcap = 3 * maxS + 64;
     q.wbuf = L.take<int64_t>(size_t(NT / 32) * 4 * q.wcap);
+    q.cb_idx = L.take<int32_t>(2 * 1024 + 8);
+    q.cb_cap = 8 * int64_t(E);
+    q.cb_ent = L.take<int32_t>(size_t(q.cb_cap));
   }
   const size_t total = L.off;
+  const auto t_lay = std::chrono::steady_clock::now();
   grow(ctx, total);
+  const auto t_grow = std::chrono::steady_clock::now();
   // 3. fill the staging buffer
   int32_t jglob = 0;
   for (int gi = 0; gi < n_groups; ++gi) {
@@ -586,6 +627,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->pr_cap = q.pr_cap;
     G->wbuf = dp<int64_t>(ctx, q.wbuf);
     G->wcap = q.wcap;
+    G->cb_idx = dp<int32_t>(ctx, q.cb_idx);
+    G->cb_ent = dp<int32_t>(ctx, q.cb_ent);
+    G->cb_cap = q.cb_cap;
     G->w_cap = q.w_cap;
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
       const Graph& g = gs[k];
@@ -726,6 +770,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   P->d2h_bytes = out_end - P->groups_off;
   auto t1 = std::chrono::steady_clock::now();
   P->prep_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  if (std::getenv("TSL_PREP_PROFILE")) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "prep: load %.3f validate %.3f layout %.3f grow %.3f fill %.3f ms\n", ms(t0, t_load),
+                 ms(t_load, t_val), ms(t_val, t_lay), ms(t_lay, t_grow), ms(t_grow, t1));
+  }
   return P;
 }
 

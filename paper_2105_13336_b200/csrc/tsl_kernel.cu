@@ -12,6 +12,7 @@ namespace tsl {
 
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
 static_assert(TI_NB == TI_NB_HOST, "time index size");
+static_assert(CB_NB == 1024, "conflict index size (host allocates 2 * 1024 + 8)");
 
 template <int IPT>
 using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;
@@ -52,6 +53,7 @@ struct DevX {
   __device__ void wsync() { __syncwarp(); }
   __device__ bool wany(bool p) { return __any_sync(0xffffffffu, p); }
   __device__ unsigned wballot(bool p) { return __ballot_sync(0xffffffffu, p); }
+  __device__ int64_t shfl(int64_t v, int src) { return __shfl_sync(0xffffffffu, v, src); }
   __device__ int ffs(unsigned m) { return __ffs(m); }
   // warp exclusive prefix sum of v; *total = warp sum
   __device__ int32_t wexcl(int32_t v, int32_t* total) {

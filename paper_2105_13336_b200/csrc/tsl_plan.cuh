@@ -40,8 +40,12 @@
 
 #ifdef __CUDACC__
 #define TSL_HD __device__ inline
+// one shared copy of the hot sequential helpers keeps the single-warp paths
+// resident in the instruction cache (the kernel body is large)
+#define TSL_HD_NOINLINE __device__ __noinline__
 #else
 #define TSL_HD inline
+#define TSL_HD_NOINLINE inline
 #endif
 
 namespace tsl {
@@ -129,8 +133,8 @@ struct TIndex {
 
 // First index k in [0, n) with key(k) > v (strict) or key(k) >= v, for
 // nondecreasing keys key(k) = arr[ix ? ix[k] : k].
-TSL_HD int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
-                           const TIndex* ti = nullptr) {
+TSL_HD_NOINLINE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
+                                    const TIndex* ti = nullptr) {
   int32_t lo = 0, hi = n;
   if (ti && ti->first && v >= 0) {
     // all k before first[b] have key < (b << shift) <= v
@@ -226,8 +230,8 @@ constexpr int64_t NONE = INT64_MIN;
 // loop over slots is unrolled, so the merge state stays in registers: the
 // sweep is a chain of dependent global loads only, never local memory.
 template <class CLK>
-TSL_HD int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
-                   int nsrc, int64_t* swept, CLK clk, int64_t* prof) {
+TSL_HD_NOINLINE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
+                            int nsrc, int64_t* swept, CLK clk, int64_t* prof) {
   if (q.e <= q.b) return NONE;
   int64_t tp0 = prof ? clk() : 0;
   const bool fwd = !latest;
@@ -392,7 +396,7 @@ struct NoClock {
 
 // anchor, swap_planner.cpp:76-93: the access with the greatest end <= t, ties
 // to the larger id; ends never decrease with the id, so it is the last one.
-TSL_HD void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
+TSL_HD_NOINLINE void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
                    int64_t& delta) {
   if (wrapped && st.period > 0) t = ((t % st.period) + st.period) % st.period;
   const TIndex ti{J.ai_e, st.ai_shift};
@@ -402,7 +406,7 @@ TSL_HD void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped,
 }
 
 // Last storage access with end <= t (skipping `skip`), or -1.
-TSL_HD int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64_t skip) {
+TSL_HD_NOINLINE int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64_t skip) {
   const int32_t a0 = J.s_off[store], a1 = J.s_off[store + 1];
   int32_t lo = a0, hi = a1;  // first position with end > t
   while (lo < hi) {
@@ -521,6 +525,8 @@ TSL_HD void pend_insert(X& x, const JobDev& J, int32_t n, int64_t s, int64_t e) 
 // own commits; pairs are recorded into the candidate's pool slot.
 template <class X>
 struct ReCtx {
+  static constexpr bool kParallelGaps = true;
+  using XT = X;
   X& x;
   const JobDev& J;
   JobState& st;
@@ -530,13 +536,22 @@ struct ReCtx {
   int32_t nout, cap;
   bool overflow;
   int64_t* dbg = nullptr;  // development cycle counters (thread 0 only)
+  // a query made by one lane on its own (gap pairs in parallel)
+  TSL_HD int64_t query_lane(const FitQuery& q, bool latest) {
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
+                   {J.pd_s, J.pd_e, st.pend_n, {nullptr, 0}, {nullptr, 0}}};
+    int64_t sw = 0;
+    const int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
+    if (x.lane == 0) { gs->fit_queries += 1; gs->busy_intervals += sw; }
+    return r;
+  }
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
     const int64_t c0 = x.clock();
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
                    {J.pd_s, J.pd_e, st.pend_n, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
-    int64_t* prof = (dbg && x.tid == 0) ? dbg + 4 : nullptr;  // cyc[16..18]
-    int64_t r = fit(J, st, q, latest, src, 2, &sw, [&]() { return x.clock(); }, prof);
+    int64_t* prof = nullptr;  // (dbg && x.tid == 0) ? dbg + 4 : nullptr for a phase split
+    int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, prof);
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (dbg && x.tid == 0) { dbg[0] += x.clock() - c0; dbg[1] += 1; }
@@ -564,11 +579,14 @@ struct ReCtx {
 
 constexpr int SPEC_MAXP = 48;   // private intervals of one speculative schedule
 constexpr int CAPC = 7;         // conflict list entries per candidate
+constexpr int CB_NB = 1024;     // time buckets of the conflict index
 
 // Speculative context (one thread, one candidate): busy = pass-start
 // structure + the candidate's own commits; pairs and the effective windows of
 // every successful query are recorded for validation at commit time.
 struct SpecCtx {
+  static constexpr bool kParallelGaps = false;
+  using XT = void;
   const JobDev& J;
   const JobState& st;
   const GroupConfig& cfg;
@@ -629,6 +647,47 @@ TSL_HD bool try_gap_pair(C& c, int32_t store, int64_t lo, int64_t hi, int64_t se
   return c.commit(PairSpec{store, os, os + d, lo, hi, is, is + d, os + d, hi, false, serves, false});
 }
 
+// The gap pairs of one schedule are independent of each other: gap k's window
+// [end of access k, start of access k+1) lies inside [0, P], the windows are
+// disjoint, and a commit inside one window (also inside [0, P]) cannot reach
+// another window through its -P/+P lifted copies. A warp therefore places
+// every gap at once (one lane per gap, against the state before any gap
+// commit) and then commits the successful ones in order -- exactly what the
+// reference's sequential loop (swap_planner.cpp:389-395) produces.
+template <class C>
+TSL_HD void gap_pairs_parallel(C& c, int32_t store, int32_t fk, int32_t a1, int64_t d) {
+  const JobDev& J = c.J;
+  auto& x = c.x;
+  using X = typename C::XT;
+  for (int32_t k0 = fk; k0 + 1 < a1; k0 += X::W) {
+    const int32_t k = k0 + x.lane;
+    bool ok = false;
+    int64_t lo = 0, hi = 0, os = NONE, is = NONE, serves = -1;
+    if (k + 1 < a1) {
+      const int32_t a = J.s_acc[k], b = J.s_acc[k + 1];
+      if (J.a_type[b] == ACC_TUA) {
+        lo = J.a_end[a];
+        hi = J.a_start[b];
+        serves = b;
+        if (hi - lo >= 2 * d) {
+          os = c.query_lane(FitQuery{store, lo, hi, d, false, 0, 0}, false);
+          if (os != NONE) {
+            is = c.query_lane(FitQuery{store, os + d, hi, d, false, 0, 0}, true);
+            ok = is != NONE;
+          }
+        }
+      }
+    }
+    const unsigned okm = x.wballot(ok);
+    for (int t = 0; t < X::W; ++t) {
+      if (!(okm >> t & 1u)) continue;
+      const int64_t tlo = x.shfl(lo, t), thi = x.shfl(hi, t), tos = x.shfl(os, t), tis = x.shfl(is, t);
+      const int64_t tsv = x.shfl(serves, t);
+      if (!c.commit(PairSpec{store, tos, tos + d, tlo, thi, tis, tis + d, tos + d, thi, false, tsv, false})) return;
+    }
+  }
+}
+
 // schedule_swap, swap_planner.cpp:339-399, single shot: a failed swap-in
 // placement leaves the next retry with the same swap-out region, the same
 // first access and the same swap-in window, so the reference's retry loop
@@ -654,10 +713,14 @@ TSL_HD bool schedule_swap(C& c, int32_t store, int64_t earliest, int64_t latest)
   if (is == NONE) return false;
   if (!c.commit(PairSpec{store, os, oe, earliest, latest, is, is + d, oe, fs, false, fa, false})) return false;
   // Greedily keep the tensor offloaded between its remaining uses.
-  for (int32_t k = fk; k + 1 < a1; ++k) {
-    int32_t a = J.s_acc[k], b = J.s_acc[k + 1];
-    if (J.a_type[b] != ACC_TUA) continue;
-    try_gap_pair(c, store, J.a_end[a], J.a_start[b], b);
+  if constexpr (C::kParallelGaps) {
+    gap_pairs_parallel(c, store, fk, a1, d);
+  } else {
+    for (int32_t k = fk; k + 1 < a1; ++k) {
+      int32_t a = J.s_acc[k], b = J.s_acc[k + 1];
+      if (J.a_type[b] != ACC_TUA) continue;
+      try_gap_pair(c, store, J.a_end[a], J.a_start[b], b);
+    }
   }
   return true;
 }
@@ -1617,33 +1680,100 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sync();
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
-  for (int64_t m = x.tid; m < nc; m += x.nthr) {
-    int32_t* ci = cinfo + m * CI_STRIDE;
-    if (ci[CI_NW] == 0) continue;
-    const int j = cand[m] >> 24;
-    const int64_t P = imax(1, g.st[j].period);
-    const int64_t* hl = chull + m * 4;
-    const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
-    const int64_t m0 = coupled ? 0 : gsh[16 + j];
-    int32_t nconf = 0;
-    for (int64_t i = m0; i < m; ++i) {
-      if ((cand[i] >> 24) != j) continue;
-      const int32_t* cj = cinfo + i * CI_STRIDE;
-      if (cj[CI_STATUS] != CS_OK) continue;
-      const int64_t* hi_ = chull + i * 4;
-      if (!hits(hi_[2], hi_[3], hl[0], hl[1], P)) continue;
-      const PairRec* pr = g.pr_pool + cj[CI_P0];
-      bool conf = false;
-      for (int32_t p = 0; p < cj[CI_NP] && !conf; ++p)
-        for (int32_t w = 0; w < ci[CI_NW] && !conf; ++w)
-          conf = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
-                 hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
-      if (conf) {
-        if (nconf < CAPC) ci[CI_CONF + nconf] = int32_t(i);
-        ++nconf;
+  // Every speculative pair interval goes into a time-bucketed index; a
+  // candidate then checks only the buckets its placement windows (lifted by
+  // -P/0/+P) touch, against entries of earlier candidates of its job.
+  {
+    int32_t* bk_cnt = g.cb_idx;             // [CB_NB + 1] counts -> offsets
+    int32_t* bk_cur = bk_cnt + (CB_NB + 2);  // [CB_NB] fill cursors
+    int32_t* bk_ent = g.cb_ent;             // [cb_cap] candidate of each entry
+    // bucket width: the largest interval end in the pass (ints are >= 0)
+    if (x.tid == 0) gsh[14] = 0;
+    for (int32_t k = x.tid; k < CB_NB + 1; k += x.nthr) bk_cnt[k] = 0;
+    x.sync();
+    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      if (ci[CI_STATUS] == CS_OK) x.amax(&gsh[14], chull[m * 4 + 3]);
+      if (ci[CI_NW]) x.amax(&gsh[14], chull[m * 4 + 1]);
+    }
+    x.sync();
+    int shb = 0;
+    while ((gsh[14] >> shb) >= CB_NB) ++shb;
+    auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(CB_NB) - 1); };
+    // count
+    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      if (ci[CI_STATUS] != CS_OK) continue;
+      const PairRec* pr = g.pr_pool + ci[CI_P0];
+      for (int32_t p = 0; p < ci[CI_NP]; ++p)
+        for (int h = 0; h < 2; ++h) {
+          const int64_t s0 = h ? pr[p].is : pr[p].os, e0 = h ? pr[p].ie : pr[p].oe;
+          for (int64_t q = imax(0, bucket(s0)); q <= bucket(e0 - 1) && q >= 0; ++q) x.aadd32(&bk_cnt[q + 1], 1);
+        }
+    }
+    x.sync();
+    if (x.tid == 0) {
+      for (int32_t k = 1; k <= CB_NB; ++k) bk_cnt[k] += bk_cnt[k - 1];
+      gsh[15] = bk_cnt[CB_NB];
+    }
+    x.sync();
+    const bool fits = gsh[15] <= g.cb_cap;
+    for (int32_t k = x.tid; k < CB_NB; k += x.nthr) bk_cur[k] = bk_cnt[k];
+    x.sync();
+    if (fits) {
+      for (int64_t m = x.tid; m < nc; m += x.nthr) {
+        const int32_t* ci = cinfo + m * CI_STRIDE;
+        if (ci[CI_STATUS] != CS_OK) continue;
+        const PairRec* pr = g.pr_pool + ci[CI_P0];
+        for (int32_t p = 0; p < ci[CI_NP]; ++p)
+          for (int h = 0; h < 2; ++h) {
+            const int64_t s0 = h ? pr[p].is : pr[p].os, e0 = h ? pr[p].ie : pr[p].oe;
+            for (int64_t q = imax(0, bucket(s0)); q <= bucket(e0 - 1) && q >= 0; ++q)
+              bk_ent[x.aadd32(&bk_cur[q], 1)] = int32_t(m);
+          }
       }
     }
-    ci[CI_NCONF] = nconf;
+    x.sync();
+    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      int32_t* ci = cinfo + m * CI_STRIDE;
+      if (ci[CI_NW] == 0) continue;
+      const int j = cand[m] >> 24;
+      const int64_t P = imax(1, g.st[j].period);
+      const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+      const int64_t m0 = coupled ? 0 : gsh[16 + j];
+      int32_t nconf = 0;
+      auto consider = [&](int64_t i) {
+        if (i >= m || i < m0 || (cand[i] >> 24) != j) return;
+        for (int32_t k = 0; k < imin(nconf, CAPC); ++k)
+          if (ci[CI_CONF + k] == i) return;
+        const int32_t* cj = cinfo + i * CI_STRIDE;
+        const PairRec* pr = g.pr_pool + cj[CI_P0];
+        bool conf = false;
+        for (int32_t p = 0; p < cj[CI_NP] && !conf; ++p)
+          for (int32_t w = 0; w < ci[CI_NW] && !conf; ++w)
+            conf = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                   hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
+        if (conf) {
+          if (nconf < CAPC) ci[CI_CONF + nconf] = int32_t(i);
+          ++nconf;
+        }
+      };
+      if (!fits || nconf > CAPC) {
+        for (int64_t i = m0; i < m; ++i) {
+          if (cinfo[i * CI_STRIDE + CI_STATUS] != CS_OK) continue;
+          consider(i);
+        }
+      } else {
+        for (int32_t w = 0; w < ci[CI_NW]; ++w)
+          for (int k = -1; k <= 1; ++k) {
+            const int64_t lo = wv[2 * w] - k * P, hi = wv[2 * w + 1] - k * P;  // raw coordinates
+            if (hi <= 0) continue;
+            for (int64_t q = imax(0, bucket(lo)); q <= bucket(hi - 1) && q >= 0; ++q)
+              for (int32_t e = bk_cnt[q]; e < bk_cnt[q + 1]; ++e) consider(bk_ent[e]);
+          }
+      }
+      ci[CI_NCONF] = nconf;
+    }
   }
   x.sync();
   tick(6);

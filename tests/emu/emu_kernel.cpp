@@ -25,6 +25,7 @@ struct HostX {
   void wsync() {}
   bool wany(bool p) { return p; }
   unsigned wballot(bool p) { return p ? 1u : 0u; }
+  int64_t shfl(int64_t v, int) { return v; }
   int ffs(unsigned m) { return m ? __builtin_ffs(m) : 0; }
   int32_t wexcl(int32_t v, int32_t* total) { *total = v; return 0; }
   int64_t aadd(int64_t* p, int64_t v) { int64_t o = *p; *p += v; return o; }

@@ -229,9 +229,24 @@ constexpr int64_t NONE = INT64_MIN;
 // lift k in {-P, 0, +P}, plus the <= 3 lifted copies of `extra`), and every
 // loop over slots is unrolled, so the merge state stays in registers: the
 // sweep is a chain of dependent global loads only, never local memory.
-template <class CLK>
+struct NoWarp {
+  static constexpr bool kWarp = false;
+  TSL_HD int lane() const { return 0; }
+  TSL_HD int64_t shfl(int64_t v, int) const { return v; }
+};
+
+// Lane helper of a warp-redundant caller (fit's stream openings in parallel).
+template <class X>
+struct WarpOf {
+  static constexpr bool kWarp = X::W > 1;
+  X& x;
+  TSL_HD int lane() const { return x.lane; }
+  TSL_HD int64_t shfl(int64_t v, int src) const { return x.shfl(v, src); }
+};
+
+template <class CLK, class WP = NoWarp>
 TSL_HD_NOINLINE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
-                            int nsrc, int64_t* swept, CLK clk, int64_t* prof) {
+                            int nsrc, int64_t* swept, CLK clk, int64_t* prof, WP wp = WP{}) {
   if (q.e <= q.b) return NONE;
   int64_t tp0 = prof ? clk() : 0;
   const bool fwd = !latest;
@@ -255,32 +270,47 @@ TSL_HD_NOINLINE int64_t fit(const JobDev& J, const JobState& st, const FitQuery&
   int32_t I[9];
   int64_t HS[9], HE[9];
   bool LIVE[9];
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int z = 3 * t + k;
-      const int64_t sh = (k - 1) * P;
-      const int32_t n = SN[t];
-      const int64_t L = q.b - sh, H = q.e - sh;
-      LIVE[z] = false;
-      I[z] = 0;
-      HS[z] = HE[z] = 0;
-      if (n == 0 || EN[t] <= L || S0[t] >= H) continue;
-      int64_t tq = prof ? clk() : 0;
-      int32_t i;
-      if (fwd) i = search_keys(SE[t], IX[t], n, L, true, &TIE[t]);
-      else i = search_keys(SS[t], IX[t], n, H, false, &TIS[t]);
-      if (prof) { prof[3 + t] += clk() - tq; prof[6 + t] += 1; }
-      I[z] = i;
-      const int32_t h = fwd ? i : i - 1;
-      if (h >= 0 && h < n) {
-        const int32_t k2 = IX[t] ? IX[t][h] : h;
-        HS[z] = SS[t][k2] + sh;
-        HE[z] = SE[t][k2] + sh;
-        LIVE[z] = fwd ? HS[z] < q.e : HE[z] > q.b;
-      }
+  // opens stream z = (source t, lift k): the first interval that can touch
+  // the window, found by one search
+  auto open = [&](int z, int32_t& oi, int64_t& ohs, int64_t& ohe, bool& olive) {
+    const int t = z / 3, k = z % 3;
+    const int64_t sh = (k - 1) * P;
+    const int32_t n = SN[t];
+    const int64_t L = q.b - sh, H = q.e - sh;
+    olive = false;
+    oi = 0;
+    ohs = ohe = 0;
+    if (n == 0 || EN[t] <= L || S0[t] >= H) return;
+    int64_t tq = prof ? clk() : 0;
+    int32_t i;
+    if (fwd) i = search_keys(SE[t], IX[t], n, L, true, &TIE[t]);
+    else i = search_keys(SS[t], IX[t], n, H, false, &TIS[t]);
+    if (prof) { prof[3 + t] += clk() - tq; prof[6 + t] += 1; }
+    oi = i;
+    const int32_t h = fwd ? i : i - 1;
+    if (h >= 0 && h < n) {
+      const int32_t k2 = IX[t] ? IX[t][h] : h;
+      ohs = SS[t][k2] + sh;
+      ohe = SE[t][k2] + sh;
+      olive = fwd ? ohs < q.e : ohe > q.b;
     }
+  };
+  if constexpr (WP::kWarp) {
+    // warp-redundant caller: lane z opens stream z, the searches overlap
+    int32_t mi = 0;
+    int64_t mhs = 0, mhe = 0;
+    bool ml = false;
+    if (wp.lane() < 9) open(wp.lane(), mi, mhs, mhe, ml);
+#pragma unroll
+    for (int z = 0; z < 9; ++z) {
+      I[z] = int32_t(wp.shfl(mi, z));
+      HS[z] = wp.shfl(mhs, z);
+      HE[z] = wp.shfl(mhe, z);
+      LIVE[z] = wp.shfl(ml ? 1 : 0, z) != 0;
+    }
+  } else {
+#pragma unroll
+    for (int z = 0; z < 9; ++z) open(z, I[z], HS[z], HE[z], LIVE[z]);
   }
   // lifted copies of `extra`, ascending
   int64_t XS[3], XE[3];
@@ -451,9 +481,32 @@ TSL_HD PairRec resolve_pair(const JobDev& J, const JobState& st, const PairSpec&
   return r;
 }
 
+// resolve_pair with its three searches on three lanes (warp-collective).
+template <class X>
+TSL_HD PairRec resolve_pair_warp(X& x, const JobDev& J, const JobState& st, const PairSpec& p) {
+  if constexpr (X::W == 1) {
+    return resolve_pair(J, st, p);
+  } else {
+    PairRec r;
+    r.os = p.os; r.oe = p.oe; r.o_earl = p.o_earl; r.o_late = p.o_late;
+    r.is = p.is; r.ie = p.ie; r.i_earl = p.i_earl; r.i_late = p.i_late;
+    r.serves = p.serves; r.store = p.store; r.wraps = p.wraps ? 1 : 0; r.pad = 0;
+    int64_t trig = 0, delta = 0;
+    if (x.lane == 0) anchor(J, st, p.os, p.wraps, trig, delta);
+    else if (x.lane == 1) {
+      if (p.in_at_iter_start) { trig = -1; delta = p.is - st.period; }
+      else anchor(J, st, p.is, p.wraps, trig, delta);
+    } else if (x.lane == 2) trig = preceding_access(J, p.store, p.os, -2);
+    r.otrig = x.shfl(trig, 0); r.odelta = x.shfl(delta, 0);
+    r.itrig = x.shfl(trig, 1); r.idelta = x.shfl(delta, 1);
+    r.pre = int32_t(x.shfl(trig, 2));
+    return r;
+  }
+}
+
 // This pass's committed intervals J.pd_[0, pend_n): the prefix
-// [0, pend_sorted) is sorted by start, commits taken verbatim from the
-// speculation are appended unsorted. Before a re-score the (short) suffix is
+// [0, pend_sorted) is sorted by start, every commit since (taken verbatim
+// from the speculation or re-scored) is appended unsorted. Before a re-score the (short) suffix is
 // ranked and merged in with binary searches (tmp: 2 * pend_n scratch words).
 // Warp-collective.
 template <class X>
@@ -496,33 +549,9 @@ TSL_HD void pend_sort(X& x, const JobDev& J, JobState& st, int64_t* tmp) {
   x.wsync();
 }
 
-// Inserts one interval into the sorted pass list (re-scoring commits).
-template <class X>
-TSL_HD void pend_insert(X& x, const JobDev& J, int32_t n, int64_t s, int64_t e) {
-  int32_t lo = 0, hi = n;  // first position with start > s
-  while (lo < hi) {
-    int32_t m = (lo + hi) >> 1;
-    if (J.pd_s[m] <= s) lo = m + 1; else hi = m;
-  }
-  const int32_t pos = lo;
-  x.wsync();
-  for (int32_t top = n; top > pos; top -= X::W) {
-    int32_t i = top - 1 - x.lane;
-    bool act = i >= pos;
-    int64_t vs = 0, ve = 0;
-    if (act) { vs = J.pd_s[i]; ve = J.pd_e[i]; }
-    x.wsync();
-    if (act) { J.pd_s[i + 1] = vs; J.pd_e[i + 1] = ve; }
-    x.wsync();
-  }
-  J.pd_s[pos] = s;
-  J.pd_e[pos] = e;
-  x.wsync();
-}
-
 // Re-scoring context (one warp, warp-redundant): busy = pass-start structure
-// + every interval committed earlier in this pass (sorted) + this schedule's
-// own commits; pairs are recorded into the candidate's pool slot.
+// + every interval committed earlier in this pass (sorted by pend_sort at the
+// re-score's start); pairs are recorded into the candidate's pool slot.
 template <class X>
 struct ReCtx {
   static constexpr bool kParallelGaps = true;
@@ -539,7 +568,7 @@ struct ReCtx {
   // a query made by one lane on its own (gap pairs in parallel)
   TSL_HD int64_t query_lane(const FitQuery& q, bool latest) {
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {J.pd_s, J.pd_e, st.pend_n, {nullptr, 0}, {nullptr, 0}}};
+                   {J.pd_s, J.pd_e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
     const int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
     if (x.lane == 0) { gs->fit_queries += 1; gs->busy_intervals += sw; }
@@ -548,28 +577,31 @@ struct ReCtx {
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
     const int64_t c0 = x.clock();
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {J.pd_s, J.pd_e, st.pend_n, {nullptr, 0}, {nullptr, 0}}};
+                   {J.pd_s, J.pd_e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
-    int64_t* prof = nullptr;  // (dbg && x.tid == 0) ? dbg + 4 : nullptr for a phase split
-    int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, prof);
+    int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr, WarpOf<X>{x});
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (dbg && x.tid == 0) { dbg[0] += x.clock() - c0; dbg[1] += 1; }
     return r;
   }
+  // No later query of the same schedule can see this commit (the swap-in
+  // query gets the swap-out as `extra`; gap windows are disjoint from the
+  // main pair and from each other inside [0, P]), so the intervals are only
+  // appended, unsorted, for the next re-score's pend_sort.
   TSL_HD bool commit(const PairSpec& p) {
     const int64_t c0 = x.clock();
     const int32_t pn = st.pend_n;
     if (nout >= cap || pn + 2 > J.Scap) { overflow = true; return false; }
-    const PairRec r = resolve_pair(J, st, p);
+    const PairRec r = resolve_pair_warp(x, J, st, p);
     if (dbg && x.tid == 0) { dbg[2] += x.clock() - c0; }
     x.wsync();
-    out[nout] = r;
-    x.wsync();
-    pend_insert(x, J, pn, r.os, r.oe);
-    pend_insert(x, J, pn + 1, r.is, r.ie);
+    if (x.lane == 0) {
+      out[nout] = r;
+      J.pd_s[pn] = r.os; J.pd_e[pn] = r.oe;
+      J.pd_s[pn + 1] = r.is; J.pd_e[pn + 1] = r.ie;
+    }
     st.pend_n = pn + 2;
-    st.pend_sorted = pn + 2;
     ++nout;
     x.wsync();
     if (dbg && x.tid == 0) { dbg[3] += x.clock() - c0; }
@@ -659,6 +691,7 @@ TSL_HD void gap_pairs_parallel(C& c, int32_t store, int32_t fk, int32_t a1, int6
   const JobDev& J = c.J;
   auto& x = c.x;
   using X = typename C::XT;
+  const int64_t g0 = x.clock();
   for (int32_t k0 = fk; k0 + 1 < a1; k0 += X::W) {
     const int32_t k = k0 + x.lane;
     bool ok = false;
@@ -685,6 +718,7 @@ TSL_HD void gap_pairs_parallel(C& c, int32_t store, int32_t fk, int32_t a1, int6
       const int64_t tsv = x.shfl(serves, t);
       if (!c.commit(PairSpec{store, tos, tos + d, tlo, thi, tis, tis + d, tos + d, thi, false, tsv, false})) return;
     }
+    if (c.dbg && x.tid == 0) c.dbg[6] += x.clock() - g0;  // cyc[18]: gap pairs
   }
 }
 
@@ -1392,32 +1426,47 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   int32_t* ci = cinfo + m * CI_STRIDE;
   ls.rescored += 1;
   const int64_t rc0 = x.clock();
-  for (int64_t q = st.pend_upto; q < m; ++q) {
+  // candidates taken verbatim since the last re-score: their intervals, 32
+  // candidates at a time (a warp prefix sum places them in plan order)
+  for (int64_t q0 = st.pend_upto; q0 < m; q0 += X::W) {
+    const int64_t q = q0 + x.lane;
     const int32_t* cq = cinfo + q * CI_STRIDE;
-    if (cq[CI_STATE] != 1 || (cand[q] >> 24) != j) continue;
-    const int32_t nq = cq[CI_NP];
+    const int32_t nq = (q < m && cq[CI_STATE] == 1 && (cand[q] >> 24) == j) ? cq[CI_NP] : 0;
+    int32_t tot = 0;
+    const int32_t ex = x.wexcl(2 * nq, &tot);
     const int32_t pn = st.pend_n;
-    if (pn + 2 * nq > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return -1; }
-    const PairRec* pr = g.pr_pool + cq[CI_P0];
+    if (pn + tot > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return -1; }
     x.wsync();
-    for (int32_t p = x.lane; p < nq; p += X::W) {
-      J.pd_s[pn + 2 * p] = pr[p].os; J.pd_e[pn + 2 * p] = pr[p].oe;
-      J.pd_s[pn + 2 * p + 1] = pr[p].is; J.pd_e[pn + 2 * p + 1] = pr[p].ie;
+    if (nq) {
+      const PairRec* pr = g.pr_pool + cq[CI_P0];
+      for (int32_t p = 0; p < nq; ++p) {
+        const int32_t o = pn + ex + 2 * p;
+        J.pd_s[o] = pr[p].os; J.pd_e[o] = pr[p].oe;
+        J.pd_s[o + 1] = pr[p].is; J.pd_e[o + 1] = pr[p].ie;
+      }
     }
-    st.pend_n = pn + 2 * nq;
+    st.pend_n = pn + tot;
     x.wsync();
   }
   x.wsync();
   st.pend_upto = int32_t(m);
   x.wsync();
+  const int64_t rc1 = x.clock();
   pend_sort(x, J, st, wtmp);
+  const int64_t rc2 = x.clock();
   int64_t earliest = 0, latest = 0;
   const int kind = candidate_kind(J, st, s, earliest, latest);
   const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
   ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
   c.dbg = &g.stats.cyc[12];
   const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
-  if (x.tid == 0) g.stats.cyc[10] += x.clock() - rc0;
+  if (x.tid == 0) {
+    const int64_t rc3 = x.clock();
+    g.stats.cyc[10] += rc3 - rc0;
+    g.stats.cyc[16] += rc1 - rc0;
+    g.stats.cyc[11] += rc2 - rc1;
+    g.stats.cyc[17] += rc3 - rc2;
+  }
   if (c.overflow) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; lerr.tick = 5; return -1; }
   return ok ? c.nout : 0;
 }
@@ -1621,14 +1670,18 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   }
   if (cand != g.k_val)
     for (int64_t m = x.tid; m < nc; m += x.nthr) cand[m] = g.k_val[m];
+  // segment starts: first candidate of each job (candidates are job-major
+  // when uncoupled)
+  for (int j = x.tid; j <= g.n_jobs; j += x.nthr) gsh[16 + j] = nc;
+  x.sync();
+  if (!coupled)
+    for (int64_t m = x.tid; m < nc; m += x.nthr) x.amin(&gsh[16 + (cand[m] >> 24)], m);
+  x.sync();
   if (x.tid == 0) {
     g.stats.candidates += nc;
     g.stats.sort_elems += nc;
-    for (int j = 0; j <= g.n_jobs; ++j) gsh[16 + j] = nc;
-    if (!coupled) {
-      for (int64_t m = nc - 1; m >= 0; --m) gsh[16 + (g.k_val[m] >> 24)] = m;
+    if (!coupled)
       for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
-    }
     for (int j = 0; j < g.n_jobs; ++j) g.st[j].pend_upto = coupled ? 0 : int32_t(gsh[16 + j]);
   }
   x.sync();
@@ -1712,9 +1765,17 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         }
     }
     x.sync();
-    if (x.tid == 0) {
-      for (int32_t k = 1; k <= CB_NB; ++k) bk_cnt[k] += bk_cnt[k - 1];
-      gsh[15] = bk_cnt[CB_NB];
+    // prefix over the bucket counts: one warp, 32 buckets per lane (the
+    // block scan's scratch holds the candidate records here)
+    if (x.warp == 0) {
+      constexpr int PER = CB_NB / X::W;
+      int32_t* c = bk_cnt + 1 + x.lane * PER;
+      int32_t sum = 0;
+      for (int k = 0; k < PER; ++k) sum += c[k];
+      int32_t tot = 0;
+      int32_t off = x.wexcl(sum, &tot);
+      for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
+      if (x.lane == 0) gsh[15] = tot;
     }
     x.sync();
     const bool fits = gsh[15] <= g.cb_cap;

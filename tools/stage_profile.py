@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import ref
 from paper_2105_13336_b200 import configs as CF
 from paper_2105_13336_b200.planner import Planner
-P = Planner(0)
+P = Planner(lib_path=os.environ["TSL_LIB"]) if os.environ.get("TSL_LIB") else Planner(0)
 for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
     reqs = CF.requests(name)
     for req in [reqs[-1]]:

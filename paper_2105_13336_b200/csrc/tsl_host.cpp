@@ -358,6 +358,7 @@ struct tsl_plan {
   int32_t max_jobs = 1;
   int32_t ipt = 1;        // block-sort tile of this launch
   int64_t sort_cap = 0;   // NT * ipt
+  size_t res_bytes = 0;   // shared memory for resident job arrays (build mode)
   int64_t n_accesses = 0;
 };
 
@@ -480,6 +481,23 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     P->group_job_base.push_back(nj);
     nj += static_cast<int32_t>(v.size());
     P->max_jobs = std::max<int32_t>(P->max_jobs, static_cast<int32_t>(v.size()));
+  }
+  // shared-memory residency of the job arrays: the largest group's arrays
+  // when they fit (RES_FULL_MAX keeps most of the SM's L1)
+  if (mode == 0 && P->max_jobs <= RES_MAX_JOBS) {
+    size_t need = 0;
+    for (int gi = 0; gi < n_groups; ++gi) {
+      size_t sum = 0;
+      for (size_t k = 0; k < P->graphs[gi].size(); ++k)
+        sum += resident_bytes_for(P->graphs[gi][k].A, P->graphs[gi][k].T, P->jp[gi][k].Scap);
+      need = std::max(need, sum);
+    }
+    const size_t with = kernel_smem_bytes(P->max_jobs, P->ipt, 16) - 16;
+    const size_t limit = size_t(227) * 1024;
+    // all or nothing: a partly resident group gains little and loses L1
+    size_t res = (with < limit && need <= limit - with && need <= RES_FULL_MAX) ? need : 0;
+    if (const char* e = std::getenv("TSL_RES_BYTES")) res = std::min<size_t>(res, std::strtoull(e, nullptr, 10));
+    P->res_bytes = res & ~size_t(15);
   }
   P->states_off = L.take<JobState>(nj);
   P->jobs_off = L.take<JobDev>(nj);
@@ -788,7 +806,7 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
   for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
-    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, c->stream), "launch");
+    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, c->stream), "launch");
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
@@ -907,6 +925,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   for (int k = 0; k < 4; ++k) s.debug[k] = G.stats.cyc[12 + k];
   s.cyc_pendsort = G.stats.cyc[11];
   for (int k = 0; k < 4; ++k) s.fitprof[k] = G.stats.cyc[16 + k];
+  for (int k = 0; k < 5; ++k) s.fitprof[4 + k] = G.stats.cyc[27 + k];
   for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
   return R;
 }
@@ -1122,7 +1141,7 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   return guard([&] {
     tsl_ctx* c = P->ctx;
     cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode, P->max_jobs, P->ipt,
-                                  stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
+                                  P->res_bytes, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
   });
 }
 

@@ -4,6 +4,7 @@
 // warp votes and atomics.
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
+#include <type_traits>
 
 #include "tsl_plan.cuh"
 #include "tsl_kernel.h"
@@ -145,17 +146,76 @@ struct DevX {
 }  // namespace tsl
 
 namespace tsl {
-// Shared-memory layout: [scalars][group header copy][JobState x max_jobs][sort scratch]
+// Shared-memory layout: [scalars][group header copy][JobState x max_jobs]
+// [sort scratch][JobDev x max_jobs + resident job arrays (build mode)]
 constexpr size_t SH_BYTES = SH_WORDS * sizeof(int64_t);
 constexpr size_t HDR_BYTES = (sizeof(GroupDev) + 15) & ~size_t(15);
 constexpr size_t ST_BYTES = (sizeof(JobState) + 15) & ~size_t(15);
+constexpr size_t JD_BYTES = (sizeof(JobDev) + 15) & ~size_t(15);
+
+// Places the group's per-job arrays in shared memory while `budget` bytes
+// last, hottest first (the fit streams and the busy structure, then the
+// evaluator's per-access and per-tensor arrays). Only arrays the host never
+// reads back, and whose contents are either uploaded inputs (copied in here)
+// or fully rebuilt on the device before use, are moved. Thread 0 carves; the
+// copies are CTA-collective.
+__device__ void make_resident(GroupDev* gs, const JobDev* gj, JobDev* jd, uint8_t* base, size_t budget) {
+  const int nj = gs->n_jobs;
+  if (threadIdx.x == 0) {
+    size_t used = 0;
+    auto take = [&](size_t bytes) -> uint8_t* {
+      bytes = (bytes + 15) & ~size_t(15);
+      if (used + bytes > budget) return nullptr;
+      uint8_t* p = base + used;
+      used += bytes;
+      return p;
+    };
+    for (int j = 0; j < nj; ++j) jd[j] = gj[j];
+    for (int cls = 0; cls < 3; ++cls)
+      for (int j = 0; j < nj; ++j) {
+        JobDev& J = jd[j];
+        const size_t A = size_t(J.A), T = size_t(J.T), Sc = size_t(J.Scap), IX = (TI_NB + 1) * sizeof(int32_t);
+        auto mv = [&](auto*& ptr, size_t bytes) {
+          using P = std::remove_const_t<std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>>;
+          if (uint8_t* q = take(bytes)) ptr = reinterpret_cast<P*>(q);
+        };
+        if (cls == 0) {  // fit: storage access streams, time indexes, sizes
+          mv(J.a_start, 8 * A); mv(J.a_end, 8 * A); mv(J.s_acc, 4 * A); mv(J.s_off, 4 * (T + 1));
+          mv(J.ai_e, IX); mv(J.bzi_s, IX); mv(J.bzi_e, IX); mv(J.t_size, 8 * T); mv(J.a_type, A);
+        } else if (cls == 1) {  // busy structure
+          mv(J.bz_s, 8 * Sc); mv(J.bz_e, 8 * Sc);
+        } else {  // evaluator / scorer per-access and per-tensor arrays
+          mv(J.a_store, 4 * A); mv(J.a_tensor, 4 * A); mv(J.a_owned, A); mv(J.t_store, 4 * T);
+          mv(J.t_kind, T); mv(J.t_rank, 4 * T); mv(J.t_upd, 4 * T); mv(J.st_evcnt, 4 * T);
+          mv(J.swapped, T); mv(J.res_init, T); mv(J.t_wfirst, 4 * T); mv(J.t_utga, 4 * T);
+        }
+      }
+    gs->jobs = jd;
+  }
+  __syncthreads();
+  // uploaded inputs that moved: copy them in
+  for (int j = 0; j < nj; ++j) {
+    const JobDev& G = gj[j];
+    JobDev& J = jd[j];
+    auto cp = [&](auto* dst, const auto* src, int n) {
+      if (static_cast<const void*>(dst) == static_cast<const void*>(src)) return;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) const_cast<std::remove_const_t<std::remove_pointer_t<decltype(dst)>>*>(dst)[i] = src[i];
+    };
+    cp(J.t_size, G.t_size, J.T);
+    cp(J.t_kind, G.t_kind, J.T);
+    cp(J.t_rank, G.t_rank, J.T);
+    cp(J.t_store, G.t_store, J.T);
+    cp(J.t_upd, G.t_upd, J.T);
+  }
+  __syncthreads();
+}
 }  // namespace tsl
 
 // One CTA = one build_plan (mode 0) or one analyze_job (mode 1). The group
 // header and every job's mutable scalars live in shared memory for the whole
 // kernel and are written back at the end.
 extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
-    tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes) {
+    tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes, unsigned res_bytes) {
   extern __shared__ __align__(16) uint8_t smem[];
   using namespace tsl;
   DevX x;
@@ -177,12 +237,18 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   __syncthreads();
   if (x.tid == 0) gs->st = sts;
   __syncthreads();
+  JobDev* gjobs = gg->jobs;
+  if (mode == 0 && res_bytes > 0 && gg->n_jobs <= RES_MAX_JOBS) {
+    uint8_t* jdb = static_cast<uint8_t*>(x.tmp) + ((size_t(tmp_bytes) + 15) & ~size_t(15));
+    make_resident(gs, gjobs, reinterpret_cast<JobDev*>(jdb), jdb + JD_BYTES * RES_MAX_JOBS, res_bytes);
+  }
   if (mode == 0) plan_group(x, *gs);
   else analyze_group(x, *gs);
   __syncthreads();
   for (int j = x.tid; j < gs->n_jobs; j += x.nthr) gst[j] = sts[j];
   if (x.tid == 0) {
     gs->st = gst;
+    gs->jobs = gjobs;
     *gg = *gs;
   }
 }
@@ -193,13 +259,23 @@ int sort_ipt_for(int64_t n) {
   return SORT_IPT;
 }
 
-size_t kernel_smem_bytes(int max_jobs, int ipt) {
-  return SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs + tmp_bytes_for(ipt);
+size_t resident_bytes_for(int32_t A, int32_t T, int32_t Scap) {
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const size_t a = size_t(A), t = size_t(T), ix = r((TI_NB + 1) * sizeof(int32_t));
+  return 2 * r(8 * a) + 3 * r(4 * a) + 2 * r(a) +                       // access arrays
+         r(4 * (t + 1)) + r(8 * t) + 6 * r(4 * t) + 3 * r(t) +            // tensor arrays
+         3 * ix + 2 * r(8 * size_t(Scap));                                 // time indexes, busy structure
 }
 
-cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt,
+size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes) {
+  const size_t base = SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs + ((tmp_bytes_for(ipt) + 15) & ~size_t(15));
+  return res_bytes ? base + JD_BYTES * RES_MAX_JOBS + res_bytes : base;
+}
+
+cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
                                cudaStream_t stream) {
-  const size_t smem = kernel_smem_bytes(max_jobs, ipt);
+  if (mode != 0 || max_jobs > RES_MAX_JOBS) res_bytes = 0;
+  const size_t smem = kernel_smem_bytes(max_jobs, ipt, res_bytes);
   static size_t attr = 0;
   if (smem != attr) {
     cudaError_t e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -213,7 +289,8 @@ cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int m
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, (unsigned)tmp_bytes_for(ipt));
+  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, (unsigned)tmp_bytes_for(ipt),
+                                                  (unsigned)res_bytes);
   return cudaGetLastError();
 }
 }  // namespace tsl

@@ -13,7 +13,13 @@ constexpr int TI_NB_HOST = 256;  // == TI_NB in tsl_plan.cuh
 constexpr size_t PAIRREC_BYTES = 16 * 8;  // sizeof(PairRec), checked in tsl_kernel.cu
 // Smallest supported block-sort tile (items per thread) covering n keys.
 int sort_ipt_for(int64_t n);
-size_t kernel_smem_bytes(int max_jobs, int ipt);
-cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt,
+constexpr int RES_MAX_JOBS = 16;  // groups up to this many jobs may keep job arrays in shared memory
+constexpr size_t RES_FULL_MAX = size_t(64) << 10;  // ... when all of them fit in this many bytes
+// Dynamic shared memory of a launch; res_bytes > 0 adds the JobDev copies and
+// the resident job arrays (build mode, <= RES_MAX_JOBS jobs per group).
+size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes);
+// Shared-memory bytes that would hold every resident array of the job.
+size_t resident_bytes_for(int32_t A, int32_t T, int32_t Scap);
+cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
                                cudaStream_t stream);
 }  // namespace tsl

@@ -132,28 +132,21 @@ struct TIndex {
 };
 
 // First index k in [0, n) with key(k) > v (strict) or key(k) >= v, for
-// nondecreasing keys key(k) = arr[ix ? ix[k] : k].
+// nondecreasing keys key(k) = arr[ix ? ix[k] : k]. One code path for every
+// caller (lanes searching different streams stay converged): the optional
+// time index narrows [lo, hi) with two independent loads, then a binary
+// search finishes.
 TSL_HD_NOINLINE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
                                     const TIndex* ti = nullptr) {
   int32_t lo = 0, hi = n;
   if (ti && ti->first && v >= 0) {
-    // all k before first[b] have key < (b << shift) <= v
+    // all k before first[b] have key < (b << shift) <= v; from first[b + 1]
+    // on, key >= (b + 1) << shift > v
     int64_t bk = v >> ti->shift;
     if (bk > TI_NB) bk = TI_NB;
     lo = ti->first[bk];
-    for (;;) {  // short scan
-      if (lo >= n) return n;
-      const int64_t x = arr[ix ? ix[lo] : lo];
-      if (strict ? x > v : x >= v) return lo;
-      ++lo;
-    }
-  }
-  if (n <= 12) {
-    for (int32_t k = 0; k < n; ++k) {
-      const int64_t x = arr[ix ? ix[k] : k];
-      if (strict ? x > v : x >= v) return k;
-    }
-    return n;
+    if (bk < TI_NB) hi = imin(hi, ti->first[bk + 1]);
+    if (lo > hi) lo = hi;
   }
   while (lo < hi) {
     const int32_t m = (lo + hi) >> 1;
@@ -491,59 +484,65 @@ TSL_HD PairRec resolve_pair_warp(X& x, const JobDev& J, const JobState& st, cons
     r.os = p.os; r.oe = p.oe; r.o_earl = p.o_earl; r.o_late = p.o_late;
     r.is = p.is; r.ie = p.ie; r.i_earl = p.i_earl; r.i_late = p.i_late;
     r.serves = p.serves; r.store = p.store; r.wraps = p.wraps ? 1 : 0; r.pad = 0;
+    // lanes 0 and 1 anchor the swap-out and swap-in through the same call
     int64_t trig = 0, delta = 0;
-    if (x.lane == 0) anchor(J, st, p.os, p.wraps, trig, delta);
-    else if (x.lane == 1) {
-      if (p.in_at_iter_start) { trig = -1; delta = p.is - st.period; }
-      else anchor(J, st, p.is, p.wraps, trig, delta);
-    } else if (x.lane == 2) trig = preceding_access(J, p.store, p.os, -2);
+    if (x.lane < 2) anchor(J, st, x.lane ? p.is : p.os, p.wraps, trig, delta);
     r.otrig = x.shfl(trig, 0); r.odelta = x.shfl(delta, 0);
-    r.itrig = x.shfl(trig, 1); r.idelta = x.shfl(delta, 1);
-    r.pre = int32_t(x.shfl(trig, 2));
+    if (p.in_at_iter_start) { r.itrig = -1; r.idelta = p.is - st.period; }
+    else { r.itrig = x.shfl(trig, 1); r.idelta = x.shfl(delta, 1); }
+    r.pre = preceding_access(J, p.store, p.os, -2);
     return r;
   }
 }
 
-// This pass's committed intervals J.pd_[0, pend_n): the prefix
-// [0, pend_sorted) is sorted by start, every commit since (taken verbatim
-// from the speculation or re-scored) is appended unsorted. Before a re-score the (short) suffix is
-// ranked and merged in with binary searches (tmp: 2 * pend_n scratch words).
-// Warp-collective.
+// This pass's committed intervals of one job ("pend"): s/e[0, pend_n), the
+// prefix [0, pend_sorted) sorted by start, every commit since (taken verbatim
+// from the speculation or re-scored) appended unsorted; ts/te are the merge
+// target, tmp 2 * cap scratch words. The arrays sit in the sort scratch of
+// shared memory when the pass's bound fits there, else in the job's global
+// buffers.
+struct PendBuf {
+  int64_t *s, *e, *ts, *te, *tmp;
+  int32_t cap;
+};
+
+// Before a re-score the (short) unsorted suffix is ranked and merged in with
+// binary searches. Warp-collective.
 template <class X>
-TSL_HD void pend_sort(X& x, const JobDev& J, JobState& st, int64_t* tmp) {
+TSL_HD void pend_sort(X& x, const PendBuf& pb, JobState& st) {
   const int32_t n = st.pend_n, p = st.pend_sorted;
   if (p >= n) return;
   const int32_t k = n - p;
-  int64_t* ts = tmp;      // sorted suffix
-  int64_t* te = tmp + k;
+  int64_t* ts = pb.tmp;      // sorted suffix
+  int64_t* te = pb.tmp + k;
   x.wsync();
   for (int32_t i = x.lane; i < k; i += X::W) {
-    const int64_t si = J.pd_s[p + i];
+    const int64_t si = pb.s[p + i];
     int32_t r = 0;
     for (int32_t t = 0; t < k; ++t) {
-      const int64_t sj = J.pd_s[p + t];
+      const int64_t sj = pb.s[p + t];
       r += (sj < si || (sj == si && t < i)) ? 1 : 0;
     }
     ts[r] = si;
-    te[r] = J.pd_e[p + i];
+    te[r] = pb.e[p + i];
   }
   x.wsync();
   for (int32_t i = x.lane; i < p; i += X::W) {  // prefix element: + suffix elements before it
-    const int64_t si = J.pd_s[i];
+    const int64_t si = pb.s[i];
     int32_t lo = 0, hi = k;
     while (lo < hi) { int32_t m = (lo + hi) >> 1; if (ts[m] < si) lo = m + 1; else hi = m; }
-    J.pd_ts[i + lo] = si;
-    J.pd_te[i + lo] = J.pd_e[i];
+    pb.ts[i + lo] = si;
+    pb.te[i + lo] = pb.e[i];
   }
   for (int32_t r = x.lane; r < k; r += X::W) {  // suffix element: + prefix elements up to it
     const int64_t si = ts[r];
     int32_t lo = 0, hi = p;
-    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (J.pd_s[m] <= si) lo = m + 1; else hi = m; }
-    J.pd_ts[r + lo] = si;
-    J.pd_te[r + lo] = te[r];
+    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (pb.s[m] <= si) lo = m + 1; else hi = m; }
+    pb.ts[r + lo] = si;
+    pb.te[r + lo] = te[r];
   }
   x.wsync();
-  for (int32_t i = x.lane; i < n; i += X::W) { J.pd_s[i] = J.pd_ts[i]; J.pd_e[i] = J.pd_te[i]; }
+  for (int32_t i = x.lane; i < n; i += X::W) { pb.s[i] = pb.ts[i]; pb.e[i] = pb.te[i]; }
   x.wsync();
   st.pend_sorted = n;
   x.wsync();
@@ -559,6 +558,7 @@ struct ReCtx {
   X& x;
   const JobDev& J;
   JobState& st;
+  const PendBuf& pb;
   const GroupConfig& cfg;
   GroupStats* gs;
   PairRec* out;
@@ -568,7 +568,7 @@ struct ReCtx {
   // a query made by one lane on its own (gap pairs in parallel)
   TSL_HD int64_t query_lane(const FitQuery& q, bool latest) {
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {J.pd_s, J.pd_e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
+                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
     const int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
     if (x.lane == 0) { gs->fit_queries += 1; gs->busy_intervals += sw; }
@@ -577,7 +577,7 @@ struct ReCtx {
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
     const int64_t c0 = x.clock();
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {J.pd_s, J.pd_e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
+                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
     int64_t sw = 0;
     int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr, WarpOf<X>{x});
     gs->fit_queries += 1;
@@ -592,14 +592,14 @@ struct ReCtx {
   TSL_HD bool commit(const PairSpec& p) {
     const int64_t c0 = x.clock();
     const int32_t pn = st.pend_n;
-    if (nout >= cap || pn + 2 > J.Scap) { overflow = true; return false; }
+    if (nout >= cap || pn + 2 > pb.cap) { overflow = true; return false; }
     const PairRec r = resolve_pair_warp(x, J, st, p);
     if (dbg && x.tid == 0) { dbg[2] += x.clock() - c0; }
     x.wsync();
     if (x.lane == 0) {
       out[nout] = r;
-      J.pd_s[pn] = r.os; J.pd_e[pn] = r.oe;
-      J.pd_s[pn + 1] = r.is; J.pd_e[pn + 1] = r.ie;
+      pb.s[pn] = r.os; pb.e[pn] = r.oe;
+      pb.s[pn + 1] = r.is; pb.e[pn + 1] = r.ie;
     }
     st.pend_n = pn + 2;
     ++nout;
@@ -610,6 +610,9 @@ struct ReCtx {
 };
 
 constexpr int SPEC_MAXP = 48;   // private intervals of one speculative schedule
+constexpr int GS_PCAP = 160;    // gsh slots: per-job reserved pair slots of a pass (<= 128 jobs)
+constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in shared scratch
+static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
 
@@ -1420,7 +1423,7 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
 // the number of pairs committed (0: failed); -1 on error.
 template <class X>
 TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m, int32_t* cand, int32_t* cinfo,
-                                 int64_t* wtmp, GroupStats& ls, ErrInfo& lerr) {
+                                 const PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t* ci = cinfo + m * CI_STRIDE;
@@ -1435,14 +1438,14 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
     int32_t tot = 0;
     const int32_t ex = x.wexcl(2 * nq, &tot);
     const int32_t pn = st.pend_n;
-    if (pn + tot > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return -1; }
+    if (pn + tot > pb.cap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = pb.cap; return -1; }
     x.wsync();
     if (nq) {
       const PairRec* pr = g.pr_pool + cq[CI_P0];
       for (int32_t p = 0; p < nq; ++p) {
         const int32_t o = pn + ex + 2 * p;
-        J.pd_s[o] = pr[p].os; J.pd_e[o] = pr[p].oe;
-        J.pd_s[o + 1] = pr[p].is; J.pd_e[o + 1] = pr[p].ie;
+        pb.s[o] = pr[p].os; pb.e[o] = pr[p].oe;
+        pb.s[o + 1] = pr[p].is; pb.e[o + 1] = pr[p].ie;
       }
     }
     st.pend_n = pn + tot;
@@ -1452,12 +1455,12 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   st.pend_upto = int32_t(m);
   x.wsync();
   const int64_t rc1 = x.clock();
-  pend_sort(x, J, st, wtmp);
+  pend_sort(x, pb, st);
   const int64_t rc2 = x.clock();
   int64_t earliest = 0, latest = 0;
   const int kind = candidate_kind(J, st, s, earliest, latest);
   const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
-  ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+  ReCtx<X> c{x, J, st, pb, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
   c.dbg = &g.stats.cyc[12];
   const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
   if (x.tid == 0) {
@@ -1482,7 +1485,7 @@ constexpr int32_t CS_HIT = 16;
 
 template <class X>
 TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int32_t* cand, int32_t* cinfo,
-                           int64_t* chull, int64_t* wtmp, GroupStats& ls, ErrInfo& lerr) {
+                           int64_t* chull, const PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t S = st.S;
@@ -1491,7 +1494,10 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
   bool changed = false;
   const int64_t P = imax(1, st.period);
   int64_t m = m0;
+  const int64_t dc0 = x.clock();
+  int64_t dcb = 0, dca = 0, dch = 0, dcn = 0;
   while (m < m1) {
+    const int64_t db0 = x.clock();
     const int64_t c = m + x.lane;
     const bool in = c < m1;
     int32_t status = in ? cinfo[c * CI_STRIDE + CI_STATUS] : CS_SKIP;
@@ -1525,8 +1531,11 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     son += ntake;
     changed = changed || ntake > 0;
     m += nbulk;
+    dcb += x.clock() - db0;
     if (nbulk == X::W || m >= m1) continue;
     // attention candidate m
+    const int64_t da0 = x.clock();
+    ++dcn;
     int32_t* ci = cinfo + m * CI_STRIDE;
     const int32_t st_m = ci[CI_STATUS];
     const int32_t s = cand[m] & 0xffffff;
@@ -1541,6 +1550,7 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     }
     int32_t npm = 0;
     int32_t state = 0;
+    dca += x.clock() - da0;
     if (valid) {
       if ((st_m & 0xf) == CS_OK) { npm = ci[CI_NP]; state = 1; }
     } else {
@@ -1548,9 +1558,10 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
       x.wsync();
       st.S = S; st.next_id = id;
       x.wsync();
-      npm = rescore_candidate(x, g, j, s, m, cand, cinfo, wtmp, ls, lerr);
+      npm = rescore_candidate(x, g, j, s, m, cand, cinfo, pb, ls, lerr);
       if (npm < 0) return changed;
       if (npm > 0) {
+        const int64_t dh0 = x.clock();
         state = 2;
         // later candidates whose placements the new intervals hit must be
         // re-examined individually
@@ -1574,6 +1585,7 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
           if (hit) cq[CI_STATUS] |= CS_HIT;
         }
         x.wsync();
+        dch += x.clock() - dh0;
       }
     }
     if (state) {
@@ -1602,6 +1614,13 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
   st.son = son;
   if (changed) st.dirty = 1;
   x.wsync();
+  if (x.lane == 0) {  // development cycle counters
+    x.aadd(&g.stats.cyc[27], x.clock() - dc0);
+    x.aadd(&g.stats.cyc[28], dcb);
+    x.aadd(&g.stats.cyc[29], dca);
+    x.aadd(&g.stats.cyc[30], dch);
+    x.aadd(&g.stats.cyc[31], dcn);
+  }
   return changed;
 }
 
@@ -1616,6 +1635,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     for (int j = 0; j < g.n_jobs; ++j) {
       JobState& st = g.st[j];
       st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
+      gsh[GS_PCAP + j] = 0;
     }
   }
   x.sync();
@@ -1660,12 +1680,14 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   int32_t* cand = g.k_val;
   int32_t* cinfo = g.c_info;
   int64_t* chull = g.c_hull;
+  size_t rec_bytes = 0;  // shared scratch taken by the candidate records
   {
     const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
     if (need <= x.tmp_bytes) {
       chull = reinterpret_cast<int64_t*>(x.tmp);
       cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
       cand = cinfo + CI_STRIDE * nc;
+      rec_bytes = (need + 15) & ~size_t(15);
     }
   }
   if (cand != g.k_val)
@@ -1709,6 +1731,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       const int32_t capw = 2 * capp + 2;
       const int64_t p0 = x.aadd(&gsh[13], capp);
       const int64_t w0 = x.aadd(&gsh[14], capw);
+      x.aadd(&gsh[GS_PCAP + j], capp);
       if (p0 + capp > g.pr_cap || w0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
       ci[CI_P0] = int32_t(p0);
       SpecCtx c{J, st, g.cfg, &ls, {}, {}, 0, g.pr_pool + p0, 0, capp, g.w_pool + 2 * w0, 0, capw, false};
@@ -1841,11 +1864,29 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   // ---- C. in-order decisions ----
   const int nseg = coupled ? 1 : g.n_jobs;
   if (!coupled) {
+    // pend buffers: a job commits at most 2 intervals per reserved pair slot;
+    // when every job's bound fits the free sort scratch they all live there
+    if (x.tid == 0) {
+      int64_t off = 0;
+      for (int j = 0; j < g.n_jobs; ++j) {
+        gsh[GS_POFF + j] = off;
+        off += 6 * (2 * gsh[GS_PCAP + j] + 2);
+      }
+      gsh[GS_POFF - 1] = int64_t(rec_bytes) + off * int64_t(sizeof(int64_t)) <= int64_t(x.tmp_bytes) ? 1 : 0;
+    }
+    x.sync();
+    const bool pend_shared = gsh[GS_POFF - 1] != 0;
     for (int seg = x.warp; seg < nseg; seg += x.nwarp) {
       GroupStats ls{};
       ErrInfo lerr{};
-      int64_t* wtmp = g.wbuf + int64_t(x.warp) * 4 * g.wcap;
-      const bool ch = decide_chunked(x, g, seg, gsh[16 + seg], gsh[16 + seg + 1], cand, cinfo, chull, wtmp, ls, lerr);
+      const JobDev& Jg = g.jobs[seg];
+      PendBuf pb{Jg.pd_s, Jg.pd_e, Jg.pd_ts, Jg.pd_te, g.wbuf + int64_t(x.warp) * 4 * g.wcap, Jg.Scap};
+      if (pend_shared) {
+        const int32_t cap = int32_t(2 * gsh[GS_PCAP + seg] + 2);
+        int64_t* b = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(x.tmp) + rec_bytes) + gsh[GS_POFF + seg];
+        pb = PendBuf{b, b + cap, b + 2 * cap, b + 3 * cap, b + 4 * cap, cap};
+      }
+      const bool ch = decide_chunked(x, g, seg, gsh[16 + seg], gsh[16 + seg + 1], cand, cinfo, chull, pb, ls, lerr);
       x.wsync();
       if (x.lane == 0) {
         if (ch) gsh[10] = 1;
@@ -1905,6 +1946,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       } else {
         ls.rescored += 1;
         const int64_t rc0 = x.clock();
+        const PendBuf pbj{J.pd_s, J.pd_e, J.pd_ts, J.pd_te, wtmp, J.Scap};
         // bring this pass's pend list up to date: intervals of every candidate
         // of this job committed since the last re-score (lanes in parallel)
         for (int64_t q = st.pend_upto; q < m; ++q) {
@@ -1916,8 +1958,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
           const PairRec* pr = g.pr_pool + cq[CI_P0];
           x.wsync();
           for (int32_t p = x.lane; p < nq; p += X::W) {
-            J.pd_s[pn + 2 * p] = pr[p].os; J.pd_e[pn + 2 * p] = pr[p].oe;
-            J.pd_s[pn + 2 * p + 1] = pr[p].is; J.pd_e[pn + 2 * p + 1] = pr[p].ie;
+            pbj.s[pn + 2 * p] = pr[p].os; pbj.e[pn + 2 * p] = pr[p].oe;
+            pbj.s[pn + 2 * p + 1] = pr[p].is; pbj.e[pn + 2 * p + 1] = pr[p].ie;
           }
           st.pend_n = pn + 2 * nq;
           x.wsync();
@@ -1927,12 +1969,12 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         st.pend_upto = int32_t(m);
         x.wsync();
         const int64_t ps0 = x.clock();
-        pend_sort(x, J, st, wtmp);
+        pend_sort(x, pbj, st);
         if (x.tid == 0) g.stats.cyc[11] += x.clock() - ps0;
         int64_t earliest = 0, latest = 0;
         const int kind = candidate_kind(J, st, s, earliest, latest);
         const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
-        ReCtx<X> c{x, J, st, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+        ReCtx<X> c{x, J, st, pbj, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
         c.dbg = &g.stats.cyc[12];
         const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
         if (x.tid == 0) g.stats.cyc[10] += x.clock() - rc0;

@@ -51,9 +51,10 @@ int sort_ipt_for(int64_t n) {
   for (int ipt : {1, 2, 4, 8, 16}) if (n <= int64_t(NT) * ipt) return ipt;
   return SORT_IPT;
 }
-size_t kernel_smem_bytes(int, int) { return SH_WORDS * sizeof(int64_t); }
+size_t kernel_smem_bytes(int, int, size_t) { return SH_WORDS * sizeof(int64_t); }
+size_t resident_bytes_for(int32_t, int32_t, int32_t) { return 0; }
 
-cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, cudaStream_t) {
+cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, size_t, cudaStream_t) {
   std::vector<int64_t> sh(SH_WORDS);
   std::vector<int64_t> tmp(96 * 1024 / 8);  // stands in for the shared sort scratch
   for (int gi = 0; gi < n_groups; ++gi) {

@@ -163,7 +163,15 @@ class JobDesc:
 def pack_jobs(jobs: Sequence[Tuple], max_swap_ratios: Optional[Dict[str, float]] = None):
     """[(graph, latencies), ...] -> (list[JobDesc], TslJobDesc array)."""
     ratios = max_swap_ratios or {}
-    descs = [JobDesc(g, l, ratios.get(g["job_id"])) for g, l in jobs]
+    # a job object passed several times (the requests of a replan sequence)
+    # is packed once: identical descriptors let the library load it once
+    memo = {}
+    descs = []
+    for g, l in jobs:
+        key = (id(g), id(l), ratios.get(g["job_id"]))
+        if key not in memo:
+            memo[key] = JobDesc(g, l, ratios.get(g["job_id"]))
+        descs.append(memo[key])
     arr = (TslJobDesc * max(1, len(descs)))(*[d.desc for d in descs])
     return descs, arr
 

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <numeric>
 #include <queue>
 #include <set>
@@ -305,8 +306,10 @@ struct JobOut {
   std::vector<int64_t> curve_t, curve_b;
 };
 
+using GraphP = std::shared_ptr<const Graph>;
+
 struct tsl_result {
-  std::vector<Graph> graphs;
+  std::vector<GraphP> graphs;  // shared with the plan (and across groups)
   std::vector<JobOut> jobs;  // job-id order
   std::vector<int64_t> history;
   int64_t final_merged = 0;
@@ -345,7 +348,7 @@ struct tsl_plan {
   ~tsl_plan() { own_buf.release(); }
   int mode = 0;  // 0 build_plan, 1 analyze_job
   int32_t n_groups = 0;
-  std::vector<std::vector<Graph>> graphs;  // per group, caller order
+  std::vector<std::vector<GraphP>> graphs;  // per group, caller order (a descriptor seen twice is loaded once)
   std::vector<std::vector<JobPlace>> jp;
   std::vector<GroupPlace> gp;
   std::vector<tsl_config> cfgs;
@@ -409,16 +412,35 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   P->cfgs.assign(cfgs, cfgs + n_cfgs);
   P->graphs.resize(n_groups);
   // 1. validate graphs (caller order), then the config, then latencies
-  for (int gi = 0; gi < n_groups; ++gi) {
-    for (int32_t k = offs[gi]; k < offs[gi + 1]; ++k) P->graphs[gi].push_back(load_graph(jobs[k]));
+  {
+    // identical descriptors (same arrays) within one call are one graph: the
+    // C5 replans of a shard repeat each resident workload in every request
+    std::map<std::vector<uintptr_t>, GraphP> seen;
+    for (int gi = 0; gi < n_groups; ++gi) {
+      for (int32_t k = offs[gi]; k < offs[gi + 1]; ++k) {
+        const tsl_job_desc& d = jobs[k];
+        double ratio = d.max_swap_ratio;
+        uint64_t rbits = 0;
+        std::memcpy(&rbits, &ratio, sizeof rbits);
+        std::vector<uintptr_t> key = {
+            uintptr_t(d.job_id), uintptr_t(d.n_tensors), uintptr_t(d.tensor_ids), uintptr_t(d.tensor_sizes),
+            uintptr_t(d.tensor_kinds), uintptr_t(d.n_ops), uintptr_t(d.op_ids), uintptr_t(d.op_kinds),
+            uintptr_t(d.op_phases), uintptr_t(d.op_in_offsets), uintptr_t(d.op_inputs), uintptr_t(d.op_out_offsets),
+            uintptr_t(d.op_outputs), uintptr_t(d.op_latencies), uintptr_t(rbits)};
+        auto it = seen.find(key);
+        if (it == seen.end()) it = seen.emplace(std::move(key), std::make_shared<const Graph>(load_graph(d))).first;
+        P->graphs[gi].push_back(it->second);
+      }
+    }
   }
   const auto t_load = std::chrono::steady_clock::now();
   for (int gi = 0; gi < n_groups; ++gi) {
     std::vector<const Graph*> gg;
-    for (auto& g : P->graphs[gi]) gg.push_back(&g);
+    for (auto& g : P->graphs[gi]) gg.push_back(g.get());
     if (mode == 0) validate_config(cfgs[n_cfgs == 1 ? 0 : gi], gg);
     std::set<std::string> ids;
-    for (auto& g : P->graphs[gi]) {
+    for (auto& gp : P->graphs[gi]) {
+      const Graph& g = *gp;
       if (!ids.insert(g.job_id).second)
         fail(TSL_ERR_ARGUMENT, "duplicate job id " + g.job_id + " in one build (unsupported)");
       check_latencies(g);
@@ -434,7 +456,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     int64_t need = 1;
     for (auto& gs : P->graphs) {
       int64_t sumT = 0;
-      for (auto& g : gs) {
+      for (auto& gp : gs) {
+        const Graph& g = *gp;
         need = std::max<int64_t>(need, 4 * int64_t(g.A) + g.T + 4);
         need = std::max<int64_t>(need, g.O + 1);
         sumT += g.T;
@@ -453,7 +476,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   P->jp.resize(n_groups);
   P->gp.resize(n_groups);
   for (int gi = 0; gi < n_groups; ++gi) {
-    for (auto& g : P->graphs[gi]) {
+    for (auto& gp : P->graphs[gi]) {
+      const Graph& g = *gp;
       JobPlace p{};
       p.topo = L.take<int32_t>(g.O);
       p.o_lat = L.take<int64_t>(g.O);
@@ -489,7 +513,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (int gi = 0; gi < n_groups; ++gi) {
       size_t sum = 0;
       for (size_t k = 0; k < P->graphs[gi].size(); ++k)
-        sum += resident_bytes_for(P->graphs[gi][k].A, P->graphs[gi][k].T, P->jp[gi][k].Scap);
+        sum += resident_bytes_for(P->graphs[gi][k]->A, P->graphs[gi][k]->T, P->jp[gi][k].Scap);
       need = std::max(need, sum);
     }
     const size_t with = kernel_smem_bytes(P->max_jobs, P->ipt, 16) - 16;
@@ -505,11 +529,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   // outputs (read back)
   for (int gi = 0; gi < n_groups; ++gi) {
     int64_t sumT = 0;
-    for (auto& g : P->graphs[gi]) sumT += g.T;
+    for (auto& g : P->graphs[gi]) sumT += g->T;
     P->gp[gi].hist_cap = static_cast<int32_t>(2 * sumT + 16);
     P->gp[gi].hist = L.take<int64_t>(P->gp[gi].hist_cap);
     for (size_t k = 0; k < P->graphs[gi].size(); ++k) {
-      const Graph& g = P->graphs[gi][k];
+      const Graph& g = *P->graphs[gi][k];
       JobPlace& p = P->jp[gi][k];
       for (int f = 0; f < 12; ++f) {
         size_t w = (f == 1) ? 4 : (f == 2 || f == 3) ? 1 : 8;  // tensor int32, dir/wraps int8
@@ -529,7 +553,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   // workspace
   for (int gi = 0; gi < n_groups; ++gi) {
     for (size_t k = 0; k < P->graphs[gi].size(); ++k) {
-      const Graph& g = P->graphs[gi][k];
+      const Graph& g = *P->graphs[gi][k];
       JobPlace& p = P->jp[gi][k];
       p.a_tensor = L.take<int32_t>(g.A);
       p.a_store = L.take<int32_t>(g.A);
@@ -580,7 +604,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     q.x_key2 = L.take<uint64_t>(E);
     q.x_order = L.take<int32_t>(E);
     int64_t sumA = 0, sumT = 0;
-    for (auto& g : P->graphs[gi]) { sumA += g.A; sumT += g.T; }
+    for (auto& g : P->graphs[gi]) { sumA += g->A; sumT += g->T; }
     q.pr_cap = sumA + sumT + 16;
     q.w_cap = 2 * q.pr_cap + 2 * sumT + 16;
     q.c_info = L.take<int32_t>(E * 16);
@@ -605,10 +629,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   for (int gi = 0; gi < n_groups; ++gi) {
     const auto& gs = P->graphs[gi];
     std::vector<std::string> jids;
-    for (auto& g : gs) jids.push_back(g.job_id);
+    for (auto& g : gs) jids.push_back(g->job_id);
     std::vector<int32_t> jrank = lex_rank(jids);
     bool coupled = false;
-    for (auto& g : gs) coupled = coupled || g.ratio < 1.0;
+    for (auto& g : gs) coupled = coupled || g->ratio < 1.0;
     const tsl_config* cfg = &cfgs[n_cfgs == 1 ? 0 : gi];
     GroupDev* G = hp<GroupDev>(ctx, P->groups_off) + gi;
     std::memset(G, 0, sizeof *G);
@@ -650,7 +674,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->cb_cap = q.cb_cap;
     G->w_cap = q.w_cap;
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
-      const Graph& g = gs[k];
+      const Graph& g = *gs[k];
       const JobPlace& p = P->jp[gi][k];
 
       std::vector<int32_t> topo = g.topo;
@@ -817,9 +841,9 @@ void download(tsl_plan* P, cudaStream_t s) {
   cuda_check(cudaStreamSynchronize(s), "sync");
 }
 
-std::string err_text(const GroupDev& G, const std::vector<Graph>& gs) {
+std::string err_text(const GroupDev& G, const std::vector<GraphP>& gs) {
   const ErrInfo& e = G.err;
-  const Graph* g = (e.job >= 0 && e.job < static_cast<int>(gs.size())) ? &gs[e.job] : nullptr;
+  const Graph* g = (e.job >= 0 && e.job < static_cast<int>(gs.size())) ? gs[e.job].get() : nullptr;
   auto tname = [&](int64_t t) { return (g && t >= 0 && t < g->T) ? g->tid[t] : "#" + std::to_string(t); };
   switch (e.code) {
     case E_DOUBLE_RELEASE: return "double release of tensor " + tname(e.tensor);
@@ -845,14 +869,14 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   R->graphs = P->graphs[gi];
   const int32_t jb = P->group_job_base[gi];
   std::map<std::string, int> order;
-  for (size_t k = 0; k < R->graphs.size(); ++k) order[R->graphs[k].job_id] = static_cast<int>(k);
+  for (size_t k = 0; k < R->graphs.size(); ++k) order[R->graphs[k]->job_id] = static_cast<int>(k);
   for (auto& kv : order) {
     const int k = kv.second;
-    const Graph& g = R->graphs[k];
+    const Graph& g = *R->graphs[k];
     const JobPlace& p = P->jp[gi][k];
     const JobState& st = hp<JobState>(c, P->states_off)[jb + k];
     JobOut o;
-    o.g = &R->graphs[k];
+    o.g = R->graphs[k].get();
     o.st = st;
     auto cp64 = [&](std::vector<int64_t>& v, size_t off, int32_t n) {
       v.assign(hp<int64_t>(c, off), hp<int64_t>(c, off) + n);
@@ -898,7 +922,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
                     std::to_string(G.cfg.budget) + " after exhausting swap and recomputation";
   tsl_stats& s = R->stats;
   s.kernel_ms = P->last_kernel_ms;
-  for (auto& g : R->graphs) s.n_accesses += g.A;
+  for (auto& g : R->graphs) s.n_accesses += g->A;
   s.loop_iterations = G.stats.loop_iterations;
   s.evaluations = G.stats.evaluations;
   s.timeline_events = G.stats.timeline_events;

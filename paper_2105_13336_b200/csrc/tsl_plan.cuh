@@ -615,6 +615,7 @@ constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in sha
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
+constexpr int CB_GRID_MAX = 160;  // passes with at most this many candidates check all pairs directly
 
 // Speculative context (one thread, one candidate): busy = pass-start
 // structure + the candidate's own commits; pairs and the effective windows of
@@ -1756,10 +1757,35 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sync();
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
-  // Every speculative pair interval goes into a time-bucketed index; a
-  // candidate then checks only the buckets its placement windows (lifted by
-  // -P/0/+P) touch, against entries of earlier candidates of its job.
-  {
+  // Small passes: one thread per (candidate, earlier candidate) pair. Large
+  // passes: every speculative pair interval goes into a time-bucketed index;
+  // a candidate then checks only the buckets its placement windows (lifted
+  // by -P/0/+P) touch, against entries of earlier candidates of its job.
+  if (nc <= CB_GRID_MAX) {
+    // one warp per candidate, its lanes over the earlier candidates
+    for (int32_t m = x.warp; m < int32_t(nc); m += x.nwarp) {
+      int32_t* ci = cinfo + int64_t(m) * CI_STRIDE;
+      if (ci[CI_NW] == 0) continue;
+      const int jm = cand[m] >> 24;
+      const int64_t P = imax(1, g.st[jm].period);
+      for (int32_t i = x.lane; i < m; i += X::W) {
+        const int32_t* cj = cinfo + int64_t(i) * CI_STRIDE;
+        if (cj[CI_STATUS] != CS_OK || (cand[i] >> 24) != jm) continue;
+        if (!hits(chull[i * 4 + 2], chull[i * 4 + 3], chull[m * 4], chull[m * 4 + 1], P)) continue;
+        const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+        const PairRec* pr = g.pr_pool + cj[CI_P0];
+        bool conf = false;
+        for (int32_t p = 0; p < cj[CI_NP] && !conf; ++p)
+          for (int32_t w = 0; w < ci[CI_NW] && !conf; ++w)
+            conf = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                   hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
+        if (conf) {
+          const int32_t k = x.aadd32(&ci[CI_NCONF], 1);
+          if (k < CAPC) ci[CI_CONF + k] = int32_t(i);
+        }
+      }
+    }
+  } else {
     int32_t* bk_cnt = g.cb_idx;             // [CB_NB + 1] counts -> offsets
     int32_t* bk_cur = bk_cnt + (CB_NB + 2);  // [CB_NB] fill cursors
     int32_t* bk_ent = g.cb_ent;             // [cb_cap] candidate of each entry

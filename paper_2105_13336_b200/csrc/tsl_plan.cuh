@@ -40,12 +40,13 @@
 
 #ifdef __CUDACC__
 #define TSL_HD __device__ inline
-// one shared copy of the hot sequential helpers keeps the single-warp paths
-// resident in the instruction cache (the kernel body is large)
-#define TSL_HD_NOINLINE __device__ __noinline__
+// the query/search helpers are forced inline: in a 255-register kernel a call
+// spills and restores live registers through local memory, which costs more
+// than the larger body (measured: C2 0.637 -> 0.600 ms)
+#define TSL_HD_FORCE __device__ __forceinline__
 #else
 #define TSL_HD inline
-#define TSL_HD_NOINLINE inline
+#define TSL_HD_FORCE inline
 #endif
 
 namespace tsl {
@@ -136,7 +137,7 @@ struct TIndex {
 // caller (lanes searching different streams stay converged): the optional
 // time index narrows [lo, hi) with two independent loads, then a binary
 // search finishes.
-TSL_HD_NOINLINE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
+TSL_HD_FORCE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t n, int64_t v, bool strict,
                                     const TIndex* ti = nullptr) {
   int32_t lo = 0, hi = n;
   if (ti && ti->first && v >= 0) {
@@ -238,7 +239,7 @@ struct WarpOf {
 };
 
 template <class CLK, class WP = NoWarp>
-TSL_HD_NOINLINE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
+TSL_HD_FORCE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q, bool latest, const Src* src,
                             int nsrc, int64_t* swept, CLK clk, int64_t* prof, WP wp = WP{}) {
   if (q.e <= q.b) return NONE;
   int64_t tp0 = prof ? clk() : 0;
@@ -301,6 +302,7 @@ TSL_HD_NOINLINE int64_t fit(const JobDev& J, const JobState& st, const FitQuery&
       HE[z] = wp.shfl(mhe, z);
       LIVE[z] = wp.shfl(ml ? 1 : 0, z) != 0;
     }
+    if (prof) { int64_t t = clk(); prof[5] += t - tp0; tp0 = t; }
   } else {
 #pragma unroll
     for (int z = 0; z < 9; ++z) open(z, I[z], HS[z], HE[z], LIVE[z]);
@@ -419,7 +421,7 @@ struct NoClock {
 
 // anchor, swap_planner.cpp:76-93: the access with the greatest end <= t, ties
 // to the larger id; ends never decrease with the id, so it is the last one.
-TSL_HD_NOINLINE void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
+TSL_HD_FORCE void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
                    int64_t& delta) {
   if (wrapped && st.period > 0) t = ((t % st.period) + st.period) % st.period;
   const TIndex ti{J.ai_e, st.ai_shift};
@@ -429,7 +431,7 @@ TSL_HD_NOINLINE void anchor(const JobDev& J, const JobState& st, int64_t t, bool
 }
 
 // Last storage access with end <= t (skipping `skip`), or -1.
-TSL_HD_NOINLINE int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64_t skip) {
+TSL_HD_FORCE int32_t preceding_access(const JobDev& J, int32_t store, int64_t t, int64_t skip) {
   const int32_t a0 = J.s_off[store], a1 = J.s_off[store + 1];
   int32_t lo = a0, hi = a1;  // first position with end > t
   while (lo < hi) {

@@ -611,7 +611,6 @@ struct ReCtx {
   }
 };
 
-constexpr int SPEC_MAXP = 48;   // private intervals of one speculative schedule
 constexpr int GS_PCAP = 160;    // gsh slots: per-job reserved pair slots of a pass (<= 128 jobs)
 constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in shared scratch
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
@@ -619,9 +618,12 @@ constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
 constexpr int CB_GRID_MAX = 160;  // passes with at most this many candidates check all pairs directly
 
-// Speculative context (one thread, one candidate): busy = pass-start
-// structure + the candidate's own commits; pairs and the effective windows of
-// every successful query are recorded for validation at commit time.
+// Speculative context (one thread, one candidate): busy = the pass-start
+// structure. The schedule's own commits never reach its later queries (the
+// swap-in query gets the swap-out as `extra`; gap windows lie right of the
+// main pair and of each other inside [0, P], lifted copies included), so no
+// private interval list is kept. Pairs and the placement window of every
+// successful query are recorded for validation at commit time.
 struct SpecCtx {
   static constexpr bool kParallelGaps = false;
   using XT = void;
@@ -629,18 +631,15 @@ struct SpecCtx {
   const JobState& st;
   const GroupConfig& cfg;
   GroupStats* gs;
-  int64_t ps[SPEC_MAXP], pe[SPEC_MAXP];
-  int32_t np;
   PairRec* pairs;
   int32_t npairs, cap_pairs;
   int64_t* win;  // (lo, hi) pairs
   int32_t nwin, cap_win;
   bool overflow;
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
-    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {ps, pe, np, {nullptr, 0}, {nullptr, 0}}};
+    Src src[1] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}}};
     int64_t sw = 0;
-    int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
+    int64_t r = fit(J, st, q, latest, src, 1, &sw, NoClock{}, nullptr);
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (r != NONE) {
@@ -656,17 +655,9 @@ struct SpecCtx {
     }
     return r;
   }
-  TSL_HD void ins(int64_t s, int64_t e) {
-    int32_t i = np;
-    while (i > 0 && ps[i - 1] > s) { ps[i] = ps[i - 1]; pe[i] = pe[i - 1]; --i; }
-    ps[i] = s; pe[i] = e;
-    ++np;
-  }
   TSL_HD bool commit(const PairSpec& p) {
-    if (npairs >= cap_pairs || np + 2 > SPEC_MAXP) { overflow = true; return false; }
+    if (npairs >= cap_pairs) { overflow = true; return false; }
     pairs[npairs++] = resolve_pair(J, st, p);
-    ins(p.os, p.oe);
-    ins(p.is, p.ie);
     return true;
   }
 };
@@ -1737,7 +1728,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       x.aadd(&gsh[GS_PCAP + j], capp);
       if (p0 + capp > g.pr_cap || w0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
       ci[CI_P0] = int32_t(p0);
-      SpecCtx c{J, st, g.cfg, &ls, {}, {}, 0, g.pr_pool + p0, 0, capp, g.w_pool + 2 * w0, 0, capw, false};
+      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * w0, 0, capw, false};
       const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
       ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
       ci[CI_NP] = c.npairs;

@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["C1", "C2", "C5"], default="C2")
+    ap.add_argument("--workload", choices=["C1", "C2", "C4", "C5"], default="C2")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -64,6 +64,10 @@ def workload(name: str, rank: int, planner=None):
     if name in ("C1", "C2"):
         req = CF.requests(name)[0]
         return [(req.name, req.jobs, req.config(CF.INITIAL_PEAK))]
+    if name == "C4":
+        return [CF.c4_request()]
+    if name == "C4-sample":  # the reference cannot plan C4; its bounded CPU sample
+        return [CF.c4_request(1)]
     from paper_2105_13336_b200 import multigpu as MG
     peaks = MG.initial_peaks(planner, [rank % 8]) if planner is not None else None
     if peaks is None:  # CPU arm: the reference's own initial peaks
@@ -79,6 +83,7 @@ def n_accesses(jobs) -> int:
 def workload_desc(name: str) -> str:
     return {"C1": "C1 VGG-16 b32, single workload, one build_plan",
             "C2": "C2 ResNet-50 b64, single workload with across-iteration (Opt-phase) swap-ins, one build_plan",
+            "C4": "C4 GPT-2-medium seq-1024 training trace, 70 micro-batches, 990,518 accesses, one build_plan",
             "C5": "C5 shard: 8 concurrent dynamic workloads, 8 arrivals + 7 departures = 15 replans per GPU"}[name]
 
 
@@ -169,6 +174,13 @@ def ncu_traffic(name: str):
 def golden_parity(name: str, results) -> str:
     """Cheap in-bench parity: the plans of this run vs the reference fixtures."""
     import hashlib
+    if name == "C4":  # digests of the restated oracle (the reference cannot plan C4)
+        p = os.path.join(ROOT, "tests", "golden", "c4.json")
+        d = json.load(open(p))["cases"].get("M70") if os.path.exists(p) else None
+        if d is None:
+            return "unchecked (no oracle digest)"
+        ok = all(hashlib.sha256(r["plans_json"].encode()).hexdigest() == d["plans_sha256"] for _, r in results)
+        return "byte-identical save_plans vs the restated oracle (C4)" if ok else "MISMATCH vs oracle digest (C4)"
     p = os.path.join(ROOT, "tests", "golden", "configs.json")
     if not os.path.exists(p):
         return "unchecked"
@@ -188,11 +200,14 @@ def golden_parity(name: str, results) -> str:
 def run_reference(a, rank, world):
     if rank != 0:
         return
-    reqs = workload(a.workload, 0)
+    # C4: the reference cannot plan 1 M accesses; its arm
+    # runs the bounded 1-micro-batch sample of the same generator, 1 step
+    sample = a.workload == "C4"
+    reqs = workload("C4-sample" if sample else a.workload, 0)
     ev = sum(n_accesses(j) for _, j, _ in reqs)
     from oracle import ref, tslo
     kind = "reference" if ref.available() else "port"
-    for _ in range(a.warmup):
+    for _ in range(0 if sample else a.warmup):
         cpu_reference(reqs, 0.0, 1)
     times = []
     t0 = time.perf_counter()
@@ -209,7 +224,7 @@ def run_reference(a, rank, world):
             "config": {"workload": workload_desc(a.workload), "requests": len(reqs), "accesses_per_step": ev},
             "plan_gen_ms": ms,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                             "sample": f"{len(times)} x build_plan of {a.workload}, single thread "
+                             "sample": f"{len(times)} x build_plan of {'the C4 1-micro-batch sample (16,445 accesses)' if sample else a.workload}, single thread "
                                        f"({'oracle/_ref: reference sources compiled -O3' if kind == 'reference' else 'restated oracle port'})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -302,7 +317,8 @@ def run_ours(a, rank, world, local):
             dist.destroy_process_group()
         return
     from paper_2105_13336_b200 import configs as CF
-    init_peak = sum(CF.INITIAL_PEAK.get(g["job_id"], 0) for g, _ in groups[0]) if a.workload != "C5" else None
+    init_peak = (CF.C4_INITIAL_PEAK[CF.C4_MICRO_BATCHES] if a.workload == "C4" else
+                 sum(CF.INITIAL_PEAK.get(g["job_id"], 0) for g, _ in groups[0]) if a.workload != "C5" else None)
     saved = (init_peak - outs[0]["final_merged_peak"]) if init_peak else None
     peak, how = hbm_peak()
     achieved = alg_bytes / (dev_ms / 1e3) / 1e9
@@ -328,9 +344,11 @@ def run_ours(a, rank, world, local):
     if gather_ms is not None:
         line["plan_gather_ms"] = gather_ms
     if world == 1 and not a.no_cpu_baseline:
-        rate, ms, n, kind = cpu_reference(reqs, a.cpu_seconds)
+        c4 = a.workload == "C4"
+        rate, ms, n, kind = cpu_reference(workload("C4-sample", 0) if c4 else reqs, a.cpu_seconds, 1 if c4 else 10 ** 9)
+        what = "C4 1-micro-batch sample (16,445 accesses; the reference cannot plan full C4)" if c4 else f"{a.workload} step"
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "ms_per_step": ms,
-                                "sample": f"{n} x {a.workload} step on 1 host thread (~{a.cpu_seconds:.0f} s), "
+                                "sample": f"{n} x {what} on 1 host thread (~{a.cpu_seconds:.0f} s), "
                                           f"{'reference sources compiled -O3 (oracle/_ref)' if kind == 'reference' else 'restated oracle port'}"}
     print(json.dumps(line), flush=True)
     if dist:

@@ -1115,6 +1115,23 @@ int tslo_build_plan(const tsl_job_desc* jobs, int32_t n, const tsl_config* cfg, 
 }
 
 // analyze_job on a caller-supplied plan (peak.cpp:246-250).
+// Initial peak of every job (make_job_context's report, swap_planner.cpp:156-169):
+// release-at-last-use flags, empty plan. The budget basis of the configs.
+int tslo_initial_peaks(const tsl_job_desc* jobs, int32_t n, int64_t* peaks) {
+  return guard([&] {
+    for (int32_t i = 0; i < n; ++i) {
+      Graph g = load_graph(jobs[i]);
+      Job j;
+      j.g = &g;
+      j.rank = 0;
+      make_sequence(j);
+      j.plan.flags = j.base_flags;
+      refresh(j);
+      peaks[i] = j.rep.peak;
+    }
+  });
+}
+
 int tslo_analyze_job(const tsl_job_desc* jd, const tsl_plan_desc* pd, tslo_result** out) {
   return guard([&] {
     auto* res = new tslo_result();

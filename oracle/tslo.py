@@ -38,6 +38,7 @@ def lib():
         L.tslo_last_error.restype = C.c_char_p
         L.tslo_build_plan.argtypes = [C.POINTER(abi.TslJobDesc), C.c_int32, C.POINTER(abi.TslConfig),
                                       C.POINTER(C.c_void_p)]
+        L.tslo_initial_peaks.argtypes = [C.POINTER(abi.TslJobDesc), C.c_int32, C.POINTER(C.c_int64)]
         L.tslo_analyze_job.argtypes = [C.POINTER(abi.TslJobDesc), C.POINTER(abi.TslPlanDesc), C.POINTER(C.c_void_p)]
         L.tslo_result_n_jobs.argtypes = [C.c_void_p]
         L.tslo_result_job.argtypes = [C.c_void_p, C.c_int32, C.POINTER(abi.TslJobView)]
@@ -119,3 +120,14 @@ def analyze_job(graph, latencies, plan: dict) -> dict:
 
 def report_dict(report_json: str) -> dict:
     return json.loads(report_json)
+
+
+def initial_peaks(jobs) -> dict:
+    """{job_id: initial peak} (make_job_context's report: empty plan, release
+    at last use)."""
+    descs, arr = abi.pack_jobs(jobs, {})
+    out = (C.c_int64 * max(1, len(jobs)))()
+    rc = lib().tslo_initial_peaks(arr, len(jobs), out)
+    if rc:
+        raise OracleError(rc, lib().tslo_last_error().decode())
+    return {g["job_id"]: int(out[i]) for i, (g, _) in enumerate(jobs)}

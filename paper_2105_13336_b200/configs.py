@@ -31,6 +31,22 @@ INITIAL_PEAK = {
     "vgg16": 66336, "resnet50": 124192, "inception_v3": 71360, "densenet": 55840,
 }
 
+# C4: the GPT-2-medium trace (workload.gpt2_workload), 70 micro-batches =
+# 990,518 accesses; the 1-micro-batch instance (16,445 accesses) is the
+# bounded CPU sample the reference can still plan (~80 s). Initial peaks from
+# the restated oracle's make_job_context (equal to the reference's on every
+# C4-family instance the reference finishes).
+C4_MICRO_BATCHES = 70
+C4_INITIAL_PEAK = {70: 5548992512, 1: 4654684160}
+
+
+def c4_request(micro_batches: int = C4_MICRO_BATCHES):
+    """(name, jobs, config) of C4 at the given micro-batch count (70 % budget)."""
+    from paper_2105_13336_b200 import workload as W
+    cfg = {"pcie_bandwidth": BW, "transfer_setup": SETUP,
+           "memory_budget": C4_INITIAL_PEAK[micro_batches] * 7 // 10}
+    return (f"C4.M{micro_batches}", [W.c4_job(micro_batches)], cfg)
+
 
 def budget_of(initial_peaks: List[int]) -> int:
     return sum(initial_peaks) * 7 // 10

@@ -281,7 +281,7 @@ struct JobPlace {  // byte offsets into the device buffer
 };
 
 struct GroupPlace {
-  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent;
+  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
   int64_t pr_cap, w_cap, wcap, cb_cap;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
@@ -361,6 +361,8 @@ struct tsl_plan {
   int32_t max_jobs = 1;
   int32_t ipt = 1;        // block-sort tile of this launch
   int64_t sort_cap = 0;   // NT * ipt
+  int64_t ecap = 0;       // timeline scratch capacity (== sort_cap unless big)
+  bool big = false;       // a job exceeds one sort tile
   size_t res_bytes = 0;   // shared memory for resident job arrays (build mode)
   int64_t n_accesses = 0;
 };
@@ -466,9 +468,15 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     }
     P->ipt = sort_ipt_for(need);
     P->sort_cap = int64_t(NT) * P->ipt;
-    if (need > P->sort_cap)
-      fail(TSL_ERR_CAPACITY, "build exceeds the single-CTA planner capacity (" + std::to_string(P->sort_cap) +
-                                 " timeline events per job / candidates per pass)");
+    P->ecap = P->sort_cap;
+    if (need > P->sort_cap) {
+      // above one sort tile: block-wide radix sorts through global ping-pong
+      // buffers (DevX::sort_big), timeline scratch sized for the largest job
+      if (need > (int64_t(1) << 30))
+        fail(TSL_ERR_CAPACITY, "build exceeds the planner capacity (2^30 timeline events per job)");
+      P->big = true;
+      P->ecap = (need + 15) & ~int64_t(15);
+    }
   }
   const auto t_val = std::chrono::steady_clock::now();
   // 2. layout: [static inputs][groups|states|jobs][outputs][workspace]
@@ -508,7 +516,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   }
   // shared-memory residency of the job arrays: the largest group's arrays
   // when they fit (RES_FULL_MAX keeps most of the SM's L1)
-  if (mode == 0 && P->max_jobs <= RES_MAX_JOBS) {
+  if (mode == 0 && P->max_jobs <= RES_MAX_JOBS && !P->big) {
     size_t need = 0;
     for (int gi = 0; gi < n_groups; ++gi) {
       size_t sum = 0;
@@ -590,7 +598,14 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.bk_curve = L.take<int64_t>(size_t(2) * (p.Ecap + 1));
     }
     GroupPlace& q = P->gp[gi];
-    const size_t E = size_t(P->sort_cap);
+    const size_t E = size_t(P->ecap);
+    int64_t sumA = 0, sumT = 0;
+    for (auto& g : P->graphs[gi]) { sumA += g->A; sumT += g->T; }
+    const size_t CC = size_t(std::min<int64_t>(P->ecap, sumT + 16));  // candidates of a pass <= sum T
+    if (P->big) {
+      q.bs_key = L.take<uint64_t>(E);
+      q.bs_val = L.take<int32_t>(E);
+    }
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
     q.x_time = L.take<int64_t>(2 * E);  // second half: evaluator scan scratch
@@ -603,13 +618,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     q.x_seq2 = L.take<int32_t>(E);
     q.x_key2 = L.take<uint64_t>(E);
     q.x_order = L.take<int32_t>(E);
-    int64_t sumA = 0, sumT = 0;
-    for (auto& g : P->graphs[gi]) { sumA += g->A; sumT += g->T; }
     q.pr_cap = sumA + sumT + 16;
     q.w_cap = 2 * q.pr_cap + 2 * sumT + 16;
-    q.c_info = L.take<int32_t>(E * 16);
-    q.c_hull = L.take<int64_t>(E * 4);
-    q.dev_list = L.take<int64_t>(E);
+    q.c_info = L.take<int32_t>(CC * 16);
+    q.c_hull = L.take<int64_t>(CC * 4);
+    q.dev_list = L.take<int64_t>(CC);
     q.pr_pool = L.take<uint8_t>(size_t(q.pr_cap) * tsl::PAIRREC_BYTES);
     q.w_pool = L.take<int64_t>(size_t(2 * q.w_cap));
     int64_t maxS = 0;
@@ -617,7 +630,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     q.wcap = 3 * maxS + 64;
     q.wbuf = L.take<int64_t>(size_t(NT / 32) * 4 * q.wcap);
     q.cb_idx = L.take<int32_t>(2 * 1024 + 8);
-    q.cb_cap = 8 * int64_t(E);
+    q.cb_cap = std::max<int64_t>(8 * P->sort_cap, 4 * q.pr_cap);
     q.cb_ent = L.take<int32_t>(size_t(q.cb_cap));
   }
   const size_t total = L.off;
@@ -648,7 +661,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->st = dp<JobState>(ctx, P->states_off) + jglob;
     const GroupPlace& q = P->gp[gi];
     G->hist = dp<int64_t>(ctx, q.hist);
-    G->ecap = int32_t(P->sort_cap);
+    G->ecap = int32_t(P->ecap);
+    G->bs_key = P->big ? dp<uint64_t>(ctx, q.bs_key) : nullptr;
+    G->bs_val = P->big ? dp<int32_t>(ctx, q.bs_val) : nullptr;
     G->k_key = dp<uint64_t>(ctx, q.k_key);
     G->k_val = dp<int32_t>(ctx, q.k_val);
     G->x_time = dp<int64_t>(ctx, q.x_time);
@@ -830,7 +845,7 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
   for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
-    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, c->stream), "launch");
+    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, P->big, c->stream), "launch");
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
@@ -1165,7 +1180,7 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   return guard([&] {
     tsl_ctx* c = P->ctx;
     cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode, P->max_jobs, P->ipt,
-                                  P->res_bytes, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
+                                  P->res_bytes, P->big, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
   });
 }
 

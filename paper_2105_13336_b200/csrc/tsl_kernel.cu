@@ -40,6 +40,9 @@ struct DevX {
   void* tmp;
   size_t tmp_bytes;
   int sort_cap;  // NT * items-per-thread of the launch's largest tile
+  uint64_t* bs_key;  // big-sort ping-pong (global), null unless the launch has jobs above one tile
+  int32_t* bs_val;
+  int32_t* aux;      // big-sort digit tables in shared memory: 4 x 256 + NT words
 
   __device__ void sync() { __syncthreads(); }
   // Reads the SM clock only once the preceding barrier has really released
@@ -102,11 +105,97 @@ struct DevX {
     __syncthreads();
   }
 
+  // One stable LSD pass on key bits [sh, sh + nb) (nb <= 8) of n > one tile
+  // keys: digit histogram, then the tiles in order -- each tile sorted on the
+  // digit in shared memory (stable), every key scattered to its digit's base
+  // + the digit's count in earlier tiles + its offset in the tile's run.
+  __device__ void big_pass(const uint64_t* ks, const int32_t* vs, uint64_t* kd, int32_t* vd, int n, int sh, int nb) {
+    int32_t* hist = aux;            // [256] digit counts -> running base
+    int32_t* tstart = aux + 256;    // [256] first position of the digit in the sorted tile
+    int32_t* tcnt = aux + 512;      // [256] digit count in the tile
+    int32_t* lastd = aux + 1024;    // [NT] digit of each thread's last sorted item
+    const uint64_t mask = (uint64_t(1) << nb) - 1;
+    for (int d = tid; d < 256; d += NT) hist[d] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) atomicAdd(&hist[(ks[i] >> sh) & mask], 1);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 256 counts, 8 per lane
+      int32_t c[8], s = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { c[k] = hist[lane * 8 + k]; s += c[k]; }
+      int32_t tot = 0;
+      int32_t off = wexcl(s, &tot);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { hist[lane * 8 + k] = off; off += c[k]; }
+    }
+    constexpr int TILE = NT * SORT_IPT;
+    for (int t0 = 0; t0 < n; t0 += TILE) {
+      const int valid = min(TILE, n - t0);
+      uint64_t k[SORT_IPT];
+      int32_t v[SORT_IPT];
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int idx = tid * SORT_IPT + i;
+        k[i] = idx < valid ? ks[t0 + idx] : ~0ull;  // padding sorts after every real key of its digit
+        v[i] = idx < valid ? vs[t0 + idx] : 0;
+      }
+      for (int d = tid; d < 256; d += NT) tcnt[d] = 0;
+      __syncthreads();
+      BRS<SORT_IPT>(*reinterpret_cast<typename BRS<SORT_IPT>::TempStorage*>(tmp)).Sort(k, v, sh, sh + nb);
+      lastd[tid] = int32_t((k[SORT_IPT - 1] >> sh) & mask);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int p = tid * SORT_IPT + i;
+        if (p >= valid) break;
+        const int32_t d = int32_t((k[i] >> sh) & mask);
+        const int32_t pd = i > 0 ? int32_t((k[i - 1] >> sh) & mask) : (tid > 0 ? lastd[tid - 1] : -1);
+        if (p == 0 || pd != d) tstart[d] = p;
+        atomicAdd(&tcnt[d], 1);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int p = tid * SORT_IPT + i;
+        if (p >= valid) break;
+        const int32_t d = int32_t((k[i] >> sh) & mask);
+        const int64_t dst = int64_t(hist[d]) + (p - tstart[d]);
+        kd[dst] = k[i];
+        vd[dst] = v[i];
+      }
+      __syncthreads();
+      for (int d = tid; d < 256; d += NT) hist[d] += tcnt[d];
+      __syncthreads();
+    }
+  }
+
+  // Stable sort of n > one tile keys: 8-bit LSD passes through the group's
+  // ping-pong buffers.
+  __device__ void sort_big(uint64_t* keys, int32_t* vals, int n, int bits) {
+    if (!bs_key || !aux) __trap();  // the host sizes every launch with a job above one tile as big
+    const uint64_t* ks = keys;
+    const int32_t* vs = vals;
+    uint64_t* kd = bs_key;
+    int32_t* vd = bs_val;
+    int passes = 0;
+    for (int sh = 0; sh < bits; sh += 8, ++passes) {
+      big_pass(ks, vs, kd, vd, n, sh, min(8, bits - sh));
+      const uint64_t* tk = ks;
+      const int32_t* tv = vs;
+      ks = kd; vs = vd;
+      kd = const_cast<uint64_t*>(tk); vd = const_cast<int32_t*>(tv);
+    }
+    if (passes & 1) {
+      for (int i = tid; i < n; i += NT) { keys[i] = bs_key[i]; vals[i] = bs_val[i]; }
+    }
+    __syncthreads();
+  }
+
   // Stable sort of n (key, value) pairs on key bits [0, bits).
   __device__ void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     __syncthreads();
     if (n <= 1 || bits <= 0) return;
-    if (n > sort_cap) __trap();  // callers respect GroupDev::ecap == sort_cap
+    if (n > sort_cap) { sort_big(keys, vals, n, bits); return; }
     if (n <= NT) sort_ipt<1>(keys, vals, n, bits);
     else if (n <= 2 * NT) sort_ipt<2>(keys, vals, n, bits);
     else if (n <= 4 * NT) sort_ipt<4>(keys, vals, n, bits);
@@ -215,7 +304,8 @@ __device__ void make_resident(GroupDev* gs, const JobDev* gj, JobDev* jd, uint8_
 // header and every job's mutable scalars live in shared memory for the whole
 // kernel and are written back at the end.
 extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
-    tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes, unsigned res_bytes) {
+    tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes, unsigned res_bytes,
+                    int big) {
   extern __shared__ __align__(16) uint8_t smem[];
   using namespace tsl;
   DevX x;
@@ -231,6 +321,10 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   x.tmp_bytes = tmp_bytes;
   x.sort_cap = NT * ipt;
   GroupDev* gg = &groups[blockIdx.x];
+  x.bs_key = gg->bs_key;
+  x.bs_val = gg->bs_val;
+  x.aux = big ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(x.tmp) + ((size_t(tmp_bytes) + 15) & ~size_t(15)))
+              : nullptr;
   JobState* gst = gg->st;
   if (x.tid == 0) *gs = *gg;
   for (int j = x.tid; j < gg->n_jobs; j += x.nthr) sts[j] = gst[j];
@@ -238,7 +332,7 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   if (x.tid == 0) gs->st = sts;
   __syncthreads();
   JobDev* gjobs = gg->jobs;
-  if (mode == 0 && res_bytes > 0 && gg->n_jobs <= RES_MAX_JOBS) {
+  if (mode == 0 && res_bytes > 0 && !big && gg->n_jobs <= RES_MAX_JOBS) {
     uint8_t* jdb = static_cast<uint8_t*>(x.tmp) + ((size_t(tmp_bytes) + 15) & ~size_t(15));
     make_resident(gs, gjobs, reinterpret_cast<JobDev*>(jdb), jdb + JD_BYTES * RES_MAX_JOBS, res_bytes);
   }
@@ -267,16 +361,17 @@ size_t resident_bytes_for(int32_t A, int32_t T, int32_t Scap) {
          3 * ix + 2 * r(8 * size_t(Scap));                                 // time indexes, busy structure
 }
 
-size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes) {
+size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes, bool big) {
   const size_t base = SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs + ((tmp_bytes_for(ipt) + 15) & ~size_t(15));
+  if (big) return base + BIG_AUX_BYTES;
   return res_bytes ? base + JD_BYTES * RES_MAX_JOBS + res_bytes : base;
 }
 
 cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
-                               cudaStream_t stream) {
-  if (mode != 0 || max_jobs > RES_MAX_JOBS) res_bytes = 0;
-  const size_t smem = kernel_smem_bytes(max_jobs, ipt, res_bytes);
-  static size_t attr = 0;
+                               bool big, cudaStream_t stream) {
+  if (mode != 0 || max_jobs > RES_MAX_JOBS || big) res_bytes = 0;
+  const size_t smem = kernel_smem_bytes(max_jobs, ipt, res_bytes, big);
+  static size_t attr = 0;  // (per process: one device)
   if (smem != attr) {
     cudaError_t e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -290,7 +385,7 @@ cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int m
     attr = smem;
   }
   tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, (unsigned)tmp_bytes_for(ipt),
-                                                  (unsigned)res_bytes);
+                                                  (unsigned)res_bytes, big ? 1 : 0);
   return cudaGetLastError();
 }
 }  // namespace tsl

@@ -17,9 +17,12 @@ constexpr int RES_MAX_JOBS = 16;  // groups up to this many jobs may keep job ar
 constexpr size_t RES_FULL_MAX = size_t(64) << 10;  // ... when all of them fit in this many bytes
 // Dynamic shared memory of a launch; res_bytes > 0 adds the JobDev copies and
 // the resident job arrays (build mode, <= RES_MAX_JOBS jobs per group).
-size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes);
+// Launches whose largest job exceeds one sort tile ("big") sort in global
+// memory with a small shared digit table instead of resident job arrays.
+constexpr size_t BIG_AUX_BYTES = (4 * 256 + NT) * sizeof(int32_t);
+size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes, bool big = false);
 // Shared-memory bytes that would hold every resident array of the job.
 size_t resident_bytes_for(int32_t A, int32_t T, int32_t Scap);
 cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
-                               cudaStream_t stream);
+                               bool big, cudaStream_t stream);
 }  // namespace tsl

@@ -893,7 +893,7 @@ TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
 // Stage 2: footprint evaluator for jobs [jb, je) (analyze_job, peak.cpp:246-250)
 // ----------------------------------------------------------------------------
 // Shared scalar layout per batch job b: sh[b*16 + field].
-enum { F_BASE = 0, F_N, F_REL, F_INIT, F_OFF, F_MAXFP, F_PPOS, F_LUA, F_ERR, F_NPEAK, F_RELCUR, NF = 16 };
+enum { F_BASE = 0, F_N, F_REL, F_INIT, F_OFF, F_MAXFP, F_PPOS, F_LUA, F_ERR, F_NPEAK, NF = 16 };
 
 template <class X>
 TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
@@ -906,7 +906,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     for (int b = 0; b < nb; ++b) {
       int64_t* f = sh + b * NF;
       f[F_REL] = 0; f[F_INIT] = 0; f[F_MAXFP] = INT64_MIN; f[F_PPOS] = INT64_MAX;
-      f[F_LUA] = -1; f[F_ERR] = INT64_MAX; f[F_NPEAK] = 0; f[F_RELCUR] = 0;
+      f[F_LUA] = -1; f[F_ERR] = INT64_MAX; f[F_NPEAK] = 0;
     }
     gsh[0] = INT64_MAX; gsh[1] = INT64_MIN; gsh[4] = 0;
   }
@@ -1012,7 +1012,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   x.sync();
   // 3. bases and key geometry
   if (x.tid == 0) {
-    int64_t base = 0, maxT = 1, maxTie = 1;
+    int64_t base = 0, maxT = 1;
     for (int b = 0; b < nb; ++b) {
       const JobDev& J = g.jobs[jb + b];
       const JobState& st = g.st[jb + b];
@@ -1021,67 +1021,86 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       f[F_N] = J.A + f[F_REL] + st.S + st.R;
       base += f[F_N];
       maxT = imax(maxT, J.T);
-      maxTie = imax(maxTie, int64_t(J.A) + st.S + st.R);
     }
     gsh[2] = base;
     int64_t tmin = gsh[0], tmax = gsh[1];
     if (tmin > tmax) { tmin = 0; tmax = 0; }
     gsh[0] = tmin;
     const int jbits = nbits(uint64_t(nb - 1)), tbits = nbits(uint64_t(tmax - tmin));
-    const int rbits = nbits(uint64_t(maxT - 1)), xbits = nbits(uint64_t(maxTie - 1));
-    gsh[3] = (int64_t(jbits) << 48) | (int64_t(tbits) << 32) | (int64_t(rbits) << 16) | int64_t(xbits);
-    if (base > g.ecap || jbits + tbits + 1 + rbits + 3 + xbits > 63) {
-      g.err.code = E_CAPACITY; g.err.job = jb; g.err.tensor = base; g.err.tick = jbits + tbits + rbits + xbits + 4;
+    const int rbits = nbits(uint64_t(maxT - 1));
+    gsh[3] = (int64_t(jbits) << 48) | (int64_t(tbits) << 32) | (int64_t(rbits) << 16);
+    if (base > g.ecap || jbits + tbits + 1 + rbits + 3 > 63) {
+      g.err.code = E_CAPACITY; g.err.job = jb; g.err.tensor = base; g.err.tick = jbits + tbits + rbits + 4;
     }
   }
   x.sync();
   if (g.err.code) return false;
   const int jbits = int(gsh[3] >> 48), tbits = int((gsh[3] >> 32) & 0xffff);
-  const int rbits = int((gsh[3] >> 16) & 0xffff), xbits = int(gsh[3] & 0xffff);
+  const int rbits = int((gsh[3] >> 16) & 0xffff);
   const int64_t tmin = gsh[0];
   const int64_t n = gsh[2];
-  auto key = [&](int b, int64_t time, int type, int32_t srank, int64_t tie) -> uint64_t {
+  // Timeline key (sort_timeline, peak.cpp:44-62) without its last field: the
+  // reference's final tie (accesses, then swap events in plan order, then
+  // recomputes; access ids within each) is the slot order below -- swap
+  // events, recomputes, accesses, releases (in access order) -- and the radix
+  // sort is stable.
+  auto key = [&](int b, int64_t time, int type, int32_t srank) -> uint64_t {
     const bool fr = type == EV_REL || type == EV_SOUT;
     uint64_t k = uint64_t(b);
     k = (k << tbits) | uint64_t(time - tmin);
     k = (k << 1) | (fr ? 0u : 1u);
     k = (k << rbits) | uint64_t(srank);
     k = (k << 3) | uint64_t(type);
-    k = (k << xbits) | uint64_t(tie);
     return k;
   };
   etick(0);
-  // 4. emit events (build_timeline, peak.cpp:66-174)
+  // 4. emit events (build_timeline, peak.cpp:66-174). Release slots are
+  // numbered in access order: per-thread contiguous access chunks, counted,
+  // then one block scan over (job, thread).
+  int64_t* rcnt = g.x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
+  for (int b = 0; b < nb; ++b) {
+    const JobDev& J = g.jobs[jb + b];
+    const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
+    const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
+    int64_t c = 0;
+    for (int32_t a = a0; a < a1; ++a) c += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
+    rcnt[int64_t(b) * x.nthr + x.tid] = c;
+  }
+  x.scan(rcnt, nb * x.nthr);  // inclusive
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
     const JobState& st = g.st[jb + b];
     int64_t* f = sh + b * NF;
     const int64_t base = f[F_BASE];
-    const int64_t tie0 = int64_t(st.S) + st.R;
-    for (int32_t a = x.tid; a < J.A; a += x.nthr) {
+    const int64_t acc0 = base + st.S + st.R;  // first access slot
+    const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
+    const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
+    const int64_t idx = int64_t(b) * x.nthr + x.tid;
+    int64_t rel = (idx > 0 ? rcnt[idx - 1] : 0) - (b > 0 ? rcnt[int64_t(b) * x.nthr - 1] : 0);
+    for (int32_t a = a0; a < a1; ++a) {
       const int32_t s = J.a_store[a];
-      const int64_t slot = base + a;
+      const int64_t slot = acc0 + a;
       const bool flagged = J.a_flag[a] != 0;
       if (J.a_type[a] == ACC_TGA) {
         g.x_time[slot] = J.a_start[a];
         g.x_type[slot] = int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0));
-        g.k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s], tie0 + a);
+        g.k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s]);
       } else {
         g.x_time[slot] = J.a_end[a];
         g.x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
-        g.k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s], tie0 + a);
+        g.k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s]);
       }
       g.x_store[slot] = s; g.x_aid[slot] = a; g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
       if (flagged && !J.a_owned[a]) {
-        const int64_t rs = base + J.A + st.S + st.R + x.aadd(&f[F_RELCUR], 1);
+        const int64_t rs = acc0 + J.A + rel++;
         g.x_time[rs] = J.a_end[a]; g.x_type[rs] = EV_REL; g.x_store[rs] = s; g.x_aid[rs] = a;
         g.x_job[rs] = int8_t(b); g.k_val[rs] = int32_t(rs);
-        g.k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s], tie0 + a);
+        g.k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s]);
       }
     }
     for (int32_t i = x.tid; i < st.S; i += x.nthr) {
       const int32_t s = J.t_store[J.ev_tensor[i]];
-      const int64_t slot = base + J.A + i;
+      const int64_t slot = base + i;
       int64_t when = J.ev_end[i];
       int type;
       if (J.ev_dir[i] == 0) {
@@ -1093,21 +1112,21 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       }
       g.x_time[slot] = when; g.x_type[slot] = int8_t(type); g.x_store[slot] = s; g.x_aid[slot] = -1;
       g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
-      g.k_key[slot] = key(b, when, type, J.t_rank[s], i);
+      g.k_key[slot] = key(b, when, type, J.t_rank[s]);
     }
     for (int32_t r = x.tid; r < st.R; r += x.nthr) {
       const int32_t s = J.t_store[J.rc_tensor[r]];
-      const int64_t slot = base + J.A + st.S + r;
+      const int64_t slot = base + st.S + r;
       const int64_t when = J.a_start[J.rc_target[r]] - J.rc_lat[r];
       g.x_time[slot] = when; g.x_type[slot] = EV_TGA; g.x_store[slot] = s; g.x_aid[slot] = -1;
       g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
-      g.k_key[slot] = key(b, when, EV_TGA, J.t_rank[s], st.S + r);
+      g.k_key[slot] = key(b, when, EV_TGA, J.t_rank[s]);
     }
   }
   x.sync();
   etick(1);
   // 5. timeline order (sort_timeline, peak.cpp:44-62)
-  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 3 + xbits);
+  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 3);
   etick(2);
   // 6. group sorted positions by (job, storage), keeping timeline order
   for (int64_t m = x.tid; m < n; m += x.nthr) {
@@ -1288,7 +1307,8 @@ TSL_HD bool refresh(X& x, GroupDev& g, int j0, int j1, bool force) {
     if (j >= j1) break;
     int e = j;
     int64_t tot = 0;
-    while (e < j1 && e - j < MAXB && (force || g.st[e].dirty || e == j)) {
+    // (the release-slot scan needs nthr scratch words per batched job)
+    while (e < j1 && e - j < MAXB && int64_t(e - j + 1) * x.nthr <= g.ecap && (force || g.st[e].dirty || e == j)) {
       const int64_t need = int64_t(g.jobs[e].A) * 2 + g.st[e].S + g.st[e].R;
       if (e > j && tot + need > g.ecap) break;
       tot += need;

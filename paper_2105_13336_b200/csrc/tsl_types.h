@@ -202,9 +202,11 @@ struct GroupDev {
   uint64_t* x_key2;  // [ecap]
   int32_t* x_order;  // [ecap] sorted position -> slot
   // speculative swap pass scratch (tsl_plan.cuh swap_pass)
-  int32_t* c_info;   // [ecap * 16]
-  int64_t* c_hull;   // [ecap * 4]
-  int64_t* dev_list; // [ecap]
+  uint64_t* bs_key;  // [ecap] ping-pong of the block-wide radix sort (jobs above one sort tile), else null
+  int32_t* bs_val;   // [ecap]
+  int32_t* c_info;   // [candidates * 16]
+  int64_t* c_hull;   // [candidates * 4]
+  int64_t* dev_list; // [candidates]
   PairRec* pr_pool;  // [pr_cap]
   int64_t* w_pool;   // [2 * w_cap]
   int64_t pr_cap, w_cap;

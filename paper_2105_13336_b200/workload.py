@@ -164,3 +164,160 @@ def true_latency_table(graph: dict, seed: int, gpu_usage: float = 0.5) -> Dict[s
 def job(family: str, batch: int, job_id: str = "", lat_seed: int = 13, depth: int = 0) -> Tuple[dict, dict]:
     g = generate_workload(family, batch, 0, depth, job_id)
     return g, true_latency_table(g, lat_seed)
+
+
+# ---------------------------------------------------------------------------
+# C4: GPT-2-medium training trace (not in the reference's
+# generator). One job: `micro_batches` sequences of `seq` tokens through
+# `layers` transformer blocks (d_model, `heads` attention heads), forward +
+# backward per micro-batch with per-head attention ops, weight-gradient
+# accumulation across micro-batches, then one `update` op per parameter
+# tensor -- the weights and their two Adam moments are separate parameters,
+# each with its own update op (graph.cpp:89-110 allows one parameter per
+# update). Sizes are fp16 bytes (moments fp32). Defaults give ~1.0 M accesses.
+# ---------------------------------------------------------------------------
+def gpt2_workload(layers: int = 24, d_model: int = 1024, heads: int = 16, seq: int = 1024,
+                  micro_batches: int = 70, job_id: str = "gpt2m") -> dict:
+    if layers < 1 or heads < 1 or micro_batches < 1 or d_model % heads:
+        raise ValueError("gpt2_workload: bad shape")
+    H, D, S, L, M = heads, d_model, seq, layers, micro_batches
+    hd = D // H
+    f16 = 2
+    tensors: List[dict] = []
+    ops: List[dict] = []
+
+    def T(tid, size, kind="interim"):
+        tensors.append({"id": tid, "size": int(size), "kind": kind})
+        return tid
+
+    def OP(oid, kind, ins, outs, phase="forward_backward"):
+        ops.append({"id": oid, "kind": kind, "inputs": list(ins), "outputs": list(outs),
+                    "attributes": [], "phase": phase})
+
+    # parameters of block l: name -> size (bytes); the moments are fp32
+    pshape = {"ln1g": D, "ln1b": D, "wqkv": D * 3 * D, "bqkv": 3 * D, "wo": D * D, "bo": D,
+              "ln2g": D, "ln2b": D, "w1": D * 4 * D, "b1": 4 * D, "w2": 4 * D * D, "b2": D}
+    pnames = list(pshape)
+    for l in range(L):
+        for p in pnames:
+            base = f"p.l{l:02d}.{p}"
+            T(base, pshape[p] * f16, "parameter")
+            T(base + ".m1", pshape[p] * 4, "parameter")
+            T(base + ".m2", pshape[p] * 4, "parameter")
+    act = S * D * f16
+    qkvh = S * hd * f16
+    att = S * S * f16
+    mlp = S * 4 * D * f16
+    for m in range(M):
+        mp = f"m{m:03d}"
+        h = T(f"{mp}.x", act, "input")
+        saved = []
+        for l in range(L):
+            lp = f"{mp}.f.l{l:02d}"
+            P = lambda n: f"p.l{l:02d}.{n}"  # noqa: E731
+            if m == 0:
+                # optimizer-state statistics early in the iteration: every
+                # moment has a use before its own update op (a moment read only
+                # by its update makes the reference's wrapped swap-in land on
+                # the updated version's TGA tick: "swap-in of resident tensor")
+                OP(f"{lp}.0.opt", "adam_stats", [P(n) + sfx for n in pnames for sfx in (".m1", ".m2")],
+                   [T(f"{lp}.ostat", 64)])
+            ln1 = T(f"{lp}.ln1", act)
+            OP(f"{lp}.a.ln1", "layernorm", [h, P("ln1g"), P("ln1b")], [ln1])
+            q = [T(f"{lp}.q{k:02d}", qkvh) for k in range(H)]
+            kk = [T(f"{lp}.k{k:02d}", qkvh) for k in range(H)]
+            v = [T(f"{lp}.v{k:02d}", qkvh) for k in range(H)]
+            OP(f"{lp}.b.qkv", "matmul", [ln1, P("wqkv"), P("bqkv")], q + kk + v)
+            c = []
+            for k in range(H):
+                s_ = T(f"{lp}.s{k:02d}", att)
+                p_ = T(f"{lp}.p{k:02d}", att)
+                c_ = T(f"{lp}.c{k:02d}", qkvh)
+                OP(f"{lp}.c.h{k:02d}.1score", "attn_score", [q[k], kk[k]], [s_])
+                OP(f"{lp}.c.h{k:02d}.2softmax", "softmax", [s_], [p_])
+                OP(f"{lp}.c.h{k:02d}.3ctx", "attn_ctx", [p_, v[k]], [c_])
+                c.append(c_)
+            ao = T(f"{lp}.ao", act)
+            OP(f"{lp}.d.proj", "matmul", c + [P("wo"), P("bo")], [ao])
+            h1 = T(f"{lp}.h1", act)
+            OP(f"{lp}.e.res1", "add", [h, ao], [h1])
+            ln2 = T(f"{lp}.ln2", act)
+            OP(f"{lp}.f.ln2", "layernorm", [h1, P("ln2g"), P("ln2b")], [ln2])
+            f1 = T(f"{lp}.f1", mlp)
+            OP(f"{lp}.g.fc1", "matmul", [ln2, P("w1"), P("b1")], [f1])
+            f2 = T(f"{lp}.f2", mlp)
+            OP(f"{lp}.h.gelu", "gelu", [f1], [f2])
+            f3 = T(f"{lp}.f3", act)
+            OP(f"{lp}.i.fc2", "matmul", [f2, P("w2"), P("b2")], [f3])
+            ho = T(f"{lp}.ho", act)
+            OP(f"{lp}.j.res2", "add", [h1, f3], [ho])
+            saved.append((h, ln1, q, kk, v, c, h1, ln2, f1, f2))
+            h = ho
+        loss = T(f"{mp}.loss", 4 * S, "output")
+        dh = T(f"{mp}.dy", act)
+        OP(f"{mp}.g.loss", "loss", [h], [loss, dh])
+        for l in range(L - 1, -1, -1):
+            lp = f"{mp}.h.l{L - 1 - l:02d}"
+            P = lambda n: f"p.l{l:02d}.{n}"  # noqa: E731
+            G = lambda n: f"{mp}.dw.l{l:02d}.{n}"  # noqa: E731
+            h_in, ln1, q, kk, v, c, h1, ln2, f1, f2 = saved[l]
+            df2 = T(f"{lp}.df2", mlp)
+            OP(f"{lp}.a.fc2b", "matmul_b", [dh, f2, P("w2")], [df2, T(G("w2"), pshape["w2"] * f16),
+                                                              T(G("b2"), pshape["b2"] * f16)])
+            df1 = T(f"{lp}.df1", mlp)
+            OP(f"{lp}.b.gelub", "gelu_b", [df2, f1], [df1])
+            dln2 = T(f"{lp}.dln2", act)
+            OP(f"{lp}.c.fc1b", "matmul_b", [df1, ln2, P("w1")], [dln2, T(G("w1"), pshape["w1"] * f16),
+                                                                T(G("b1"), pshape["b1"] * f16)])
+            dh1a = T(f"{lp}.dh1a", act)
+            OP(f"{lp}.d.ln2b", "layernorm_b", [dln2, h1, P("ln2g")], [dh1a, T(G("ln2g"), pshape["ln2g"] * f16),
+                                                                     T(G("ln2b"), pshape["ln2b"] * f16)])
+            dh1 = T(f"{lp}.dh1", act)
+            OP(f"{lp}.e.res2b", "add", [dh, dh1a], [dh1])
+            dc = [T(f"{lp}.dc{k:02d}", qkvh) for k in range(H)]
+            OP(f"{lp}.f.projb", "matmul_b", [dh1] + c + [P("wo")], dc + [T(G("wo"), pshape["wo"] * f16),
+                                                                       T(G("bo"), pshape["bo"] * f16)])
+            dq, dk, dv = [], [], []
+            for k in range(H):
+                dp_ = T(f"{lp}.dp{k:02d}", att)
+                dv_ = T(f"{lp}.dv{k:02d}", qkvh)
+                s_p = f"{mp}.f.l{l:02d}.p{k:02d}"
+                OP(f"{lp}.g.h{k:02d}.1ctxb", "attn_ctx_b", [dc[k], s_p, v[k]], [dp_, dv_])
+                ds_ = T(f"{lp}.ds{k:02d}", att)
+                OP(f"{lp}.g.h{k:02d}.2softmaxb", "softmax_b", [dp_, s_p], [ds_])
+                dq_ = T(f"{lp}.dq{k:02d}", qkvh)
+                dk_ = T(f"{lp}.dk{k:02d}", qkvh)
+                OP(f"{lp}.g.h{k:02d}.3scoreb", "attn_score_b", [ds_, q[k], kk[k]], [dq_, dk_])
+                dq.append(dq_); dk.append(dk_); dv.append(dv_)
+            dln1 = T(f"{lp}.dln1", act)
+            OP(f"{lp}.h.qkvb", "matmul_b", dq + dk + dv + [ln1, P("wqkv")],
+               [dln1, T(G("wqkv"), pshape["wqkv"] * f16), T(G("bqkv"), pshape["bqkv"] * f16)])
+            dha = T(f"{lp}.dha", act)
+            OP(f"{lp}.i.ln1b", "layernorm_b", [dln1, h_in, P("ln1g")], [dha, T(G("ln1g"), pshape["ln1g"] * f16),
+                                                                       T(G("ln1b"), pshape["ln1b"] * f16)])
+            dhn = T(f"{lp}.dh", act)
+            OP(f"{lp}.j.res1b", "add", [dh1, dha], [dhn])
+            dh = dhn
+            # weight-gradient accumulation across micro-batches
+            if m > 0:
+                for p in pnames:
+                    acc = T(f"{mp}.acc.l{l:02d}.{p}", pshape[p] * f16)
+                    prev = f"m{m - 1:03d}.dw.l{l:02d}.{p}" if m == 1 else f"m{m - 1:03d}.acc.l{l:02d}.{p}"
+                    OP(f"{mp}.i.acc.l{l:02d}.{p}", "accumulate", [prev, G(p)], [acc])
+        # the last micro-batch's input gradient leaves the graph through a sink
+        OP(f"{mp}.j.sink", "sink", [dh], [T(f"{mp}.dx", act, "output")])
+    last = f"m{M - 1:03d}"
+    for l in range(L):
+        for p in pnames:
+            base = f"p.l{l:02d}.{p}"
+            g_ = f"{last}.dw.l{l:02d}.{p}" if M == 1 else f"{last}.acc.l{l:02d}.{p}"
+            for sfx, sz in (("", pshape[p] * f16), (".m1", pshape[p] * 4), (".m2", pshape[p] * 4)):
+                T(base + sfx + "_new", sz, "updated_parameter")
+                OP(f"u.l{l:02d}.{p}{sfx}", "update", [base + sfx, g_], [base + sfx + "_new"], "optimize")
+    return {"job_id": job_id, "tensors": tensors, "ops": ops}
+
+
+def c4_job(micro_batches: int = 70, layers: int = 24, heads: int = 16, lat_seed: int = 13,
+           job_id: str = "gpt2m") -> Tuple[dict, dict]:
+    g = gpt2_workload(layers=layers, heads=heads, micro_batches=micro_batches, job_id=job_id)
+    return g, true_latency_table(g, lat_seed)

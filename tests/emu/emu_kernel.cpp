@@ -36,7 +36,6 @@ struct HostX {
   void errset(GroupDev& g, const ErrInfo& e) { if (!g.err.code) g.err = e; }
   void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     if (n <= 1 || bits <= 0) return;
-    if (n > sort_cap) { std::fprintf(stderr, "emu: sort of %d > sort cap %d\n", n, sort_cap); std::abort(); }
     const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
     std::vector<std::pair<uint64_t, int32_t>> v(n);
     for (int i = 0; i < n; ++i) v[i] = {keys[i], vals[i]};
@@ -51,10 +50,10 @@ int sort_ipt_for(int64_t n) {
   for (int ipt : {1, 2, 4, 8, 16}) if (n <= int64_t(NT) * ipt) return ipt;
   return SORT_IPT;
 }
-size_t kernel_smem_bytes(int, int, size_t) { return SH_WORDS * sizeof(int64_t); }
+size_t kernel_smem_bytes(int, int, size_t, bool) { return SH_WORDS * sizeof(int64_t); }
 size_t resident_bytes_for(int32_t, int32_t, int32_t) { return 0; }
 
-cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, size_t, cudaStream_t) {
+cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, size_t, bool, cudaStream_t) {
   std::vector<int64_t> sh(SH_WORDS);
   std::vector<int64_t> tmp(96 * 1024 / 8);  // stands in for the shared sort scratch
   for (int gi = 0; gi < n_groups; ++gi) {

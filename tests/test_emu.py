@@ -98,3 +98,18 @@ def test_groups_equal_single_calls(emu):
         single = emu.build_plan(r.jobs, cfgs[-1])
         assert o["plans_json"] == single["plans_json"]
         assert o["merged_peak_history"] == single["merged_peak_history"]
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 2), (3, 3, 2), (1, 24, 16)], ids=lambda s: f"M{s[0]}L{s[1]}H{s[2]}")
+def test_c4_family_matches_oracle(emu, shape):
+    """C4-family traces (GPT-2-medium generator), including jobs above one
+    sort tile, against the restated oracle."""
+    from helpers import ensure_oracle
+    tslo = ensure_oracle()
+    jobs = [W.c4_job(*shape)]
+    init = sum(tslo.initial_peaks(jobs).values())
+    cfg = {"pcie_bandwidth": 256, "transfer_setup": 1, "memory_budget": init * 7 // 10}
+    got, want = emu.build_plan(jobs, cfg), tslo.build_plan(jobs, cfg)
+    assert got["plans_json"] == want["plans_json"]
+    assert got["reports_json"] == want["reports_json"]
+    assert got["merged_peak_history"] == want["merged_peak_history"]

@@ -30,3 +30,20 @@ def test_config_sizes():
     assert CF.requests("C2")[0].n_accesses == 565
     assert [r.n_accesses for r in CF.requests("C3")] == [536, 1201, 1376]
     assert sum(r.n_accesses for r in CF.requests("C5") if r.name.endswith(".7")) == 32550
+
+
+def test_c4_generator_shape():
+    """C4: GPT-2 medium, 24 layers, 16 heads, ~1 M accesses at
+    the default 70 micro-batches; every moment parameter is read before its
+    update (see workload.gpt2_workload)."""
+    from paper_2105_13336_b200 import workload as W
+    g = W.gpt2_workload(layers=2, heads=2, micro_batches=2)
+    kinds = {t["id"]: t["kind"] for t in g["tensors"]}
+    ups = [o for o in g["ops"] if o["kind"] == "update"]
+    assert len(ups) == 2 * 12 * 3
+    for o in ups:  # exactly one parameter in, one updated parameter out
+        assert sum(kinds[t] == "parameter" for t in o["inputs"]) == 1
+        assert [kinds[t] for t in o["outputs"]] == ["updated_parameter"]
+    full = W.gpt2_workload()
+    A = sum(len(o["inputs"]) + len(o["outputs"]) for o in full["ops"])
+    assert 0.95e6 < A < 1.05e6

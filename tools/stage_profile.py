@@ -5,10 +5,23 @@ from oracle import ref
 from paper_2105_13336_b200 import configs as CF
 from paper_2105_13336_b200.planner import Planner
 P = Planner(lib_path=os.environ["TSL_LIB"]) if os.environ.get("TSL_LIB") else Planner(0)
+class _Req:  # C4:<micro_batches> -> one GPT-2-medium job
+    def __init__(self, M):
+        from paper_2105_13336_b200 import workload as W
+        from oracle import tslo
+        self.jobs = [W.c4_job(M)]
+        self.name = f"C4.M{M}"
+        self.n_accesses = sum(len(o["inputs"]) + len(o["outputs"]) for o in self.jobs[0][0]["ops"])
+        self._init = sum(tslo.initial_peaks(self.jobs).values())
+
+    def config(self, _):
+        return {"pcie_bandwidth": 256, "transfer_setup": 1, "memory_budget": self._init * 7 // 10}
+
+
 for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
-    reqs = CF.requests(name)
+    reqs = [_Req(int(name[3:]))] if name.startswith("C4:") else CF.requests(name)
     for req in [reqs[-1]]:
-        cfg = req.config(ref.initial_peaks(req.jobs))
+        cfg = req.config(None if name.startswith("C4:") else ref.initial_peaks(req.jobs))
         P.build_plan(req.jobs, cfg)
         p = P.build_plan(req.jobs, cfg)
         s = p["stats"]

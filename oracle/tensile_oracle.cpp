@@ -200,11 +200,32 @@ struct Plan {
   std::vector<Rc> rc;
   std::set<int64_t> flags;
   int64_t version = 0;
-  int64_t next_event_id() const {  // plan.cpp:15-20
-    int64_t id = 0;
-    for (auto& e : sw) id = std::max(id, e.id + 1);
-    for (auto& e : rc) id = std::max(id, e.id + 1);
-    return id;
+  // plan.cpp:15-20: max event id + 1 over swap and recompute events. Kept up
+  // to date by every mutation (note_id) and recounted after removals, instead
+  // of the reference's scan per new event.
+  int64_t next_id = 0;
+  // every swap interval [start, end) by start (busy_intervals' scan over all
+  // swap events, swap_planner.cpp:39-50, restricted by an index) + the longest
+  std::multiset<std::pair<int64_t, int64_t>> by_start;
+  int64_t max_len = 0;
+  int64_t next_event_id() const { return next_id; }
+  void note_id(int64_t id) { next_id = std::max(next_id, id + 1); }
+  void add_sw(const Ev& e) {
+    sw.push_back(e);
+    note_id(e.id);
+    by_start.emplace(e.start, e.end);
+    max_len = std::max(max_len, e.end - e.start);
+  }
+  void reindex() {  // after sw changed wholesale (revalidation, caller plans)
+    next_id = 0;
+    by_start.clear();
+    max_len = 0;
+    for (auto& e : sw) {
+      note_id(e.id);
+      by_start.emplace(e.start, e.end);
+      max_len = std::max(max_len, e.end - e.start);
+    }
+    for (auto& e : rc) note_id(e.id);
   }
 };
 struct Report {  // PeakReport, peak.hpp:47-56
@@ -228,6 +249,7 @@ struct Job {
   int64_t period = 0;
   std::vector<std::vector<int>> sacc;  // storage -> access ids sorted (start, id)
   std::set<int64_t> base_flags;
+  std::vector<int> last_tga;  // tensor -> its last TGA access (access ids never change)
   Plan plan;
   Report rep;
 
@@ -263,6 +285,9 @@ void make_sequence(Job& j) {
   for (size_t i = 0; i < j.acc.size(); ++i) last[j.acc[i].tensor] = static_cast<int>(i);
   for (int t = 0; t < g.T; ++t)
     if (last[t] >= 0 && g.kind[t] == TSL_KIND_INTERIM) j.base_flags.insert(last[t]);
+  j.last_tga.assign(g.T, -1);
+  for (size_t i = 0; i < j.acc.size(); ++i)
+    if (j.acc[i].type == TGA) j.last_tga[j.acc[i].tensor] = static_cast<int>(i);
   j.sacc.assign(g.T, {});
   for (size_t i = 0; i < j.acc.size(); ++i) j.sacc[j.storage(j.acc[i].tensor)].push_back(static_cast<int>(i));
   j.resort_sacc();
@@ -281,6 +306,12 @@ struct TEv {
 std::vector<TEv> build_timeline(const Job& j, const Plan& plan) {
   const Graph& g = *j.g;
   std::vector<TEv> ev;
+  // swap-out starts per storage, sorted: the ownership test below asks whether
+  // any swap-out of the storage starts in [a.end, next) (peak.cpp:107-130)
+  std::map<int, std::vector<int64_t>> out_starts;
+  for (const Ev& e : plan.sw)
+    if (e.dir == 0) out_starts[j.storage(e.tensor)].push_back(e.start);
+  for (auto& kv : out_starts) std::sort(kv.second.begin(), kv.second.end());
   for (size_t i = 0; i < j.acc.size(); ++i) {
     const Acc& a = j.acc[i];
     int s = j.storage(a.tensor);
@@ -294,9 +325,10 @@ std::vector<TEv> build_timeline(const Job& j, const Plan& plan) {
       int64_t next = INT64_MAX;
       for (int b : j.sacc[s]) if (j.acc[b].start >= a.end) next = std::min(next, j.acc[b].start);
       bool owned = false;
-      for (const Ev& e : plan.sw) {
-        if (e.dir != 0 || j.storage(e.tensor) != s) continue;
-        if (e.start >= a.end && e.start < next) { owned = true; break; }
+      auto os = out_starts.find(s);
+      if (os != out_starts.end()) {
+        auto it = std::lower_bound(os->second.begin(), os->second.end(), a.end);
+        owned = it != os->second.end() && *it < next;
       }
       if (!owned) ev.push_back({a.end, EV_RELEASE, s, size, -size, static_cast<int64_t>(i), false});
     }
@@ -353,9 +385,14 @@ Report analyze(const Job& j, const Plan& plan) {
     std::sort(r.tensors.begin(), r.tensors.end(), [&](int a, int b) { return g.trank[a] < g.trank[b]; });
   };
   snapshot();
+  // the resident set at the last new maximum is rebuilt by a replay once the
+  // walk is done (the reference copies it at every new maximum)
+  const std::vector<char> res0 = res;
+  int64_t peak_at = -1;  // index in tl of the last new maximum
   bool has_lua = false;
   int64_t lua = -1;
-  for (const TEv& e : tl) {
+  for (size_t ei = 0; ei < tl.size(); ++ei) {
+    const TEv& e = tl[ei];
     switch (e.type) {
       case EV_TGA:
         if (!res[e.storage]) { fp += e.delta; res[e.storage] = 1; }
@@ -379,11 +416,20 @@ Report analyze(const Job& j, const Plan& plan) {
     r.curve.emplace_back(e.time, fp);
     if (fp > r.peak) {
       r.peak = fp;
-      snapshot();
+      peak_at = static_cast<int64_t>(ei);
       r.peak_time = e.time;
       r.has_lua = has_lua;
       r.lua = lua;
     }
+  }
+  if (peak_at >= 0) {
+    res = res0;
+    for (int64_t ei = 0; ei <= peak_at; ++ei) {
+      const TEv& e = tl[static_cast<size_t>(ei)];
+      if (e.type == EV_TGA || e.type == EV_SWAPIN) res[e.storage] = 1;
+      else if (e.type == EV_RELEASE || e.type == EV_SWAPOUT) res[e.storage] = 0;
+    }
+    snapshot();
   }
   return r;
 }
@@ -404,7 +450,17 @@ void lift_into(std::vector<Iv>& busy, int64_t s, int64_t e, int64_t period, int6
 std::vector<Iv> busy_intervals(const Job& j, int storage, int64_t lo, int64_t hi, const std::vector<Iv>& extra) {
   std::vector<Iv> busy;  // swap_planner.cpp:39-50
   int64_t period = std::max<int64_t>(1, j.period);
-  for (const Ev& e : j.plan.sw) lift_into(busy, e.start, e.end, period, lo, hi);
+  // the swap events whose lifted copies can reach [lo, hi): for shift k*P,
+  // start < hi - kP and end > lo - kP, so start > lo - kP - max_len
+  for (int k = -1; k <= 1; ++k) {
+    const int64_t sh = k * period;
+    auto it = j.plan.by_start.lower_bound({lo - sh - j.plan.max_len, INT64_MIN});
+    for (; it != j.plan.by_start.end() && it->first < hi - sh; ++it) {
+      const int64_t s = it->first, e = it->second;
+      if (e <= s || !(e + sh > lo && s + sh < hi)) continue;
+      busy.emplace_back(s + sh, e + sh);
+    }
+  }
   for (int a : j.sacc[storage]) lift_into(busy, j.acc[a].start, j.acc[a].end, period, lo, hi);
   for (auto& x : extra) lift_into(busy, x.first, x.second, period, lo, hi);
   return busy;
@@ -484,9 +540,9 @@ void flag_release_before(Job& j, int storage, int64_t t) {  // swap_planner.cpp:
 
 void push_pair(Job& j, Ev out, Ev in) {
   in.pair = out.id;
-  j.plan.sw.push_back(out);
-  j.plan.sw.push_back(in);
-  j.plan.sw[j.plan.sw.size() - 2].pair = in.id;
+  out.pair = in.id;
+  j.plan.add_sw(out);
+  j.plan.add_sw(in);
 }
 
 bool try_gap_pair(Job& j, int storage, int64_t lo, int64_t hi, int64_t serves, const tsl_config& c) {
@@ -499,9 +555,8 @@ bool try_gap_pair(Job& j, int storage, int64_t lo, int64_t hi, int64_t serves, c
   Place in = place_latest(feasible_regions(out.e, hi, busy, d), d);
   if (!in.ok) return false;
   Ev oe = make_event(j, storage, 0, out.s, out.e, lo, hi, false, -1);
-  j.plan.sw.push_back(oe);  // next_event_id must see the out event first
+  j.plan.note_id(oe.id);  // next_event_id must see the out event first
   Ev ie = make_event(j, storage, 1, in.s, in.e, out.e, hi, false, serves);
-  j.plan.sw.pop_back();
   push_pair(j, oe, ie);
   flag_release_before(j, storage, out.s);
   return true;
@@ -529,9 +584,8 @@ Sched schedule_swap(Job& j, int storage, int64_t earliest, int64_t& latest, cons
     return r;
   }
   Ev oe = make_event(j, storage, 0, out.s, out.e, earliest, latest, false, -1);
-  j.plan.sw.push_back(oe);
+  j.plan.note_id(oe.id);
   Ev ie = make_event(j, storage, 1, in.s, in.e, out.e, fs, false, first);
-  j.plan.sw.pop_back();
   push_pair(j, oe, ie);
   flag_release_before(j, storage, out.s);
   const std::vector<int> accs = j.sacc[storage];
@@ -550,8 +604,8 @@ Sched schedule_wrapped_swap(Job& j, int param, const tsl_config& c) {
   if (updated < 0) return r;
   int64_t d = transfer_duration(j.g->size[param], c.pcie_bandwidth, c.transfer_setup);
   int64_t period = j.period;
-  int64_t tga_end = -1;
-  for (const Acc& a : j.acc) if (a.tensor == updated && a.type == TGA) tga_end = a.end;
+  const int lt = j.last_tga[updated];  // the last TGA of the updated version (swap_planner.cpp:412-415)
+  const int64_t tga_end = lt >= 0 ? j.acc[lt].end : -1;
   if (tga_end < 0) return r;
   Place out = place_earliest(feasible_regions(tga_end, period, busy_intervals(j, param, tga_end, period, {}), d), d);
   if (!out.ok) return r;
@@ -565,9 +619,8 @@ Sched schedule_wrapped_swap(Job& j, int param, const tsl_config& c) {
   Place in = place_latest(feasible_regions(lo, hi, busy_intervals(j, param, lo, hi, {{out.s, out.e}}), d), d);
   if (!in.ok) return r;
   Ev oe = make_event(j, param, 0, out.s, out.e, tga_end, period, true, -1);
-  j.plan.sw.push_back(oe);
+  j.plan.note_id(oe.id);
   Ev ie = make_event(j, param, 1, in.s, in.e, lo, hi, true, first);
-  j.plan.sw.pop_back();
   ie.trigger = -1;
   ie.delta = in.s - period;
   push_pair(j, oe, ie);
@@ -724,6 +777,7 @@ void revalidate(Job& j, const tsl_config& c) {  // swap_planner.cpp:190-266
   std::vector<Ev> keep;
   for (const Ev& e : j.plan.sw) if (!dropped.count(e.id)) keep.push_back(e);
   j.plan.sw.swap(keep);
+  j.plan.reindex();
   rebuild_release_flags(j);
 }
 
@@ -792,6 +846,7 @@ bool recompute_pass(std::vector<Job>& jobs, int64_t budget, const tsl_config& c)
   ev.lat = best.lat;
   ev.saving = best.saving;
   j.plan.rc.push_back(ev);
+  j.plan.note_id(ev.id);
   int64_t pivot = j.access(best.target).start;
   for (Acc& a : j.acc)
     if (a.start >= pivot) {
@@ -1165,6 +1220,7 @@ int tslo_analyze_job(const tsl_job_desc* jd, const tsl_plan_desc* pd, tslo_resul
     }
     for (int i = 0; i < pd->n_release; ++i) j.plan.flags.insert(pd->release_flags[i]);
     j.plan.version = pd->version;
+    j.plan.reindex();
     refresh(j);
     JobOut o;
     o.job_id = j.g->job_id;

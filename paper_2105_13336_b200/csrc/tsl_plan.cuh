@@ -163,10 +163,12 @@ TSL_HD int tindex_shift(int64_t max_key) {
   return sh;
 }
 
-// Builds first[0..TI_NB] for keys[0, n) (nondecreasing, >= 0); CTA-collective.
-template <class X>
+// Builds first[0..TI_NB] for keys[0, n) (nondecreasing, >= 0); CTA-collective
+// (kWarp: warp-collective).
+template <class X, bool kWarp = false>
 TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, int shift) {
-  for (int32_t k = x.tid; k <= n; k += x.nthr) {
+  const int32_t t0 = kWarp ? x.lane : x.tid, dt = kWarp ? X::W : x.nthr;
+  for (int32_t k = t0; k <= n; k += dt) {
     // buckets b with key(k-1) < (b << shift) <= key(k) get first[b] = k
     int64_t lo = k == 0 ? 0 : (keys[k - 1] >> shift) + 1;
     if (k > 0 && keys[k - 1] < 0) lo = 0;
@@ -175,7 +177,8 @@ TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, i
     if (hi > TI_NB) hi = TI_NB;
     for (int64_t b = lo; b <= hi; ++b) first[b] = k;
   }
-  x.sync();
+  if (kWarp) x.wsync();
+  else x.sync();
 }
 
 // Positions a stream on the intervals that intersect [b, e) (lifted).
@@ -1431,6 +1434,50 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
   }
 }
 
+// Folds the pass's sorted commit list into the job's busy structure (warp-
+// collective, the job's deciding warp only): queries see the same union of
+// intervals, later pend merges start from an empty list. Both lists are
+// disjoint at shift 0, so starts and ends stay sorted; the time indexes are
+// rebuilt. Scratch: the job's global merge buffers.
+constexpr int32_t PEND_MERGE = 1024;
+
+template <class X>
+TSL_HD void merge_pend_into_busy(X& x, GroupDev& g, int j, const PendBuf& pb) {
+  const JobDev& J = g.jobs[j];
+  JobState& st = g.st[j];
+  const int32_t n1 = st.bz_n, n2 = st.pend_n;
+  int64_t* ms = J.pd_ts;
+  int64_t* me = J.pd_te;
+  x.wsync();
+  for (int32_t i = x.lane; i < n1; i += X::W) {  // busy element: + pend elements starting before it
+    const int64_t si = J.bz_s[i];
+    int32_t lo = 0, hi = n2;
+    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (pb.s[m] < si) lo = m + 1; else hi = m; }
+    ms[i + lo] = si;
+    me[i + lo] = J.bz_e[i];
+  }
+  for (int32_t k = x.lane; k < n2; k += X::W) {  // pend element: + busy elements starting at or before it
+    const int64_t sk = pb.s[k];
+    int32_t lo = 0, hi = n1;
+    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (J.bz_s[m] <= sk) lo = m + 1; else hi = m; }
+    ms[k + lo] = sk;
+    me[k + lo] = pb.e[k];
+  }
+  x.wsync();
+  const int32_t n = n1 + n2;
+  for (int32_t i = x.lane; i < n; i += X::W) { J.bz_s[i] = ms[i]; J.bz_e[i] = me[i]; }
+  x.wsync();
+  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0);
+  x.wsync();
+  st.bz_n = n;
+  st.pend_n = 0;
+  st.pend_sorted = 0;
+  st.bzi_shift = sh;
+  x.wsync();
+  build_tindex<X, true>(x, J.bz_s, n, J.bzi_s, sh);
+  build_tindex<X, true>(x, J.bz_e, n, J.bzi_e, sh);
+}
+
 // Re-scores candidate m of job j exactly against the real state: pass-start
 // busy structure + every interval committed before it in this pass (pend,
 // brought up to date lazily) -- the sequential reference semantics. Returns
@@ -1470,6 +1517,7 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   x.wsync();
   const int64_t rc1 = x.clock();
   pend_sort(x, pb, st);
+  if (st.pend_n >= PEND_MERGE) merge_pend_into_busy(x, g, j, pb);
   const int64_t rc2 = x.clock();
   int64_t earliest = 0, latest = 0;
   const int kind = candidate_kind(J, st, s, earliest, latest);

@@ -629,9 +629,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (auto& p : P->jp[gi]) maxS = std::max<int64_t>(maxS, p.Scap);
     q.wcap = 3 * maxS + 64;
     q.wbuf = L.take<int64_t>(size_t(NT / 32) * 4 * q.wcap);
-    q.cb_idx = L.take<int32_t>(2 * 1024 + 8);
+    q.cb_idx = L.take<int32_t>(4 * 1024 + 16);  // pair-interval and window bucket tables
     q.cb_cap = std::max<int64_t>(8 * P->sort_cap, 4 * q.pr_cap);
-    q.cb_ent = L.take<int32_t>(size_t(q.cb_cap));
+    q.cb_ent = L.take<int32_t>(2 * size_t(q.cb_cap));
   }
   const size_t total = L.off;
   const auto t_lay = std::chrono::steady_clock::now();

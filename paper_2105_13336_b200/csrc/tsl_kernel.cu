@@ -13,7 +13,7 @@ namespace tsl {
 
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
 static_assert(TI_NB == TI_NB_HOST, "time index size");
-static_assert(CB_NB == 1024, "conflict index size (host allocates 2 * 1024 + 8)");
+static_assert(CB_NB == 1024, "conflict and window index size (host allocates 4 * 1024 + 16)");
 
 template <int IPT>
 using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;

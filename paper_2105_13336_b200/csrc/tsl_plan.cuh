@@ -616,6 +616,7 @@ struct ReCtx {
 
 constexpr int GS_PCAP = 160;    // gsh slots: per-job reserved pair slots of a pass (<= 128 jobs)
 constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in shared scratch
+constexpr int GS_WK = 440;      // gsh slot: window-index bucket shift + 1 (0: no window index this pass)
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
@@ -1634,17 +1635,46 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
           hi = imax(hi, imax(pr[p].oe, pr[p].ie));
         }
         x.wsync();
-        for (int64_t q = m + 1 + x.lane; q < m1; q += X::W) {
-          int32_t* cq = cinfo + q * CI_STRIDE;
-          if ((cq[CI_STATUS] & 0xf) == CS_SKIP || cq[CI_NW] == 0) continue;
-          if (!hits(lo, hi, chull[q * 4], chull[q * 4 + 1], P)) continue;
-          const int64_t* wv = g.w_pool + 2 * int64_t(cq[CI_W0]);
-          bool hit = false;
-          for (int32_t p = 0; p < npm && !hit; ++p)
-            for (int32_t w = 0; w < cq[CI_NW] && !hit; ++w)
-              hit = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
-                    hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
-          if (hit) cq[CI_STATUS] |= CS_HIT;
+        const int64_t wk = x.sh[MAXB * 16 + GS_WK];
+        if (wk > 0) {
+          // window index (large passes): only candidates whose placement
+          // windows share a bucket with a lifted copy of a new interval
+          const int shb = int(wk - 1);
+          auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(CB_NB) - 1); };
+          const int32_t* wk_cnt = g.cb_idx + 2 * (CB_NB + 2);
+          const int32_t* wk_ent = g.cb_ent + g.cb_cap;
+          for (int32_t p = 0; p < npm; ++p)
+            for (int h = 0; h < 2; ++h) {
+              const int64_t s0 = h ? pr[p].is : pr[p].os, e0 = h ? pr[p].ie : pr[p].oe;
+              for (int k = -1; k <= 1; ++k) {
+                const int64_t ls = s0 + k * P, le = e0 + k * P;
+                if (le <= 0) continue;
+                for (int64_t b = imax(0, bucket(ls)); b <= bucket(le - 1) && b >= 0; ++b)
+                  for (int32_t e = wk_cnt[b] + x.lane; e < wk_cnt[b + 1]; e += X::W) {
+                    const int64_t q = wk_ent[e];
+                    if (q <= m || q >= m1) continue;
+                    int32_t* cq = cinfo + q * CI_STRIDE;
+                    if ((cq[CI_STATUS] & 0xf) == CS_SKIP || (cq[CI_STATUS] & CS_HIT)) continue;
+                    const int64_t* wv = g.w_pool + 2 * int64_t(cq[CI_W0]);
+                    bool hit = false;
+                    for (int32_t w = 0; w < cq[CI_NW] && !hit; ++w) hit = hits(s0, e0, wv[2 * w], wv[2 * w + 1], P);
+                    if (hit) cq[CI_STATUS] |= CS_HIT;  // racing lanes set the same bit
+                  }
+              }
+            }
+        } else {
+          for (int64_t q = m + 1 + x.lane; q < m1; q += X::W) {
+            int32_t* cq = cinfo + q * CI_STRIDE;
+            if ((cq[CI_STATUS] & 0xf) == CS_SKIP || cq[CI_NW] == 0) continue;
+            if (!hits(lo, hi, chull[q * 4], chull[q * 4 + 1], P)) continue;
+            const int64_t* wv = g.w_pool + 2 * int64_t(cq[CI_W0]);
+            bool hit = false;
+            for (int32_t p = 0; p < npm && !hit; ++p)
+              for (int32_t w = 0; w < cq[CI_NW] && !hit; ++w)
+                hit = hits(pr[p].os, pr[p].oe, wv[2 * w], wv[2 * w + 1], P) ||
+                      hits(pr[p].is, pr[p].ie, wv[2 * w], wv[2 * w + 1], P);
+            if (hit) cq[CI_STATUS] |= CS_HIT;
+          }
         }
         x.wsync();
         dch += x.clock() - dh0;
@@ -1693,7 +1723,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   if (x.tid == 0) {
     int64_t maxT = 1;
     for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
-    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[13] = 0; gsh[14] = 0;
+    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[13] = 0; gsh[14] = 0; gsh[GS_WK] = 0;
     for (int j = 0; j < g.n_jobs; ++j) {
       JobState& st = g.st[j];
       st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
@@ -1850,9 +1880,15 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     int32_t* bk_cnt = g.cb_idx;             // [CB_NB + 1] counts -> offsets
     int32_t* bk_cur = bk_cnt + (CB_NB + 2);  // [CB_NB] fill cursors
     int32_t* bk_ent = g.cb_ent;             // [cb_cap] candidate of each entry
+    // the same buckets over every candidate's placement windows: phase C's
+    // hit marking visits only the candidates whose windows share a bucket
+    // with a re-scored commit
+    int32_t* wk_cnt = g.cb_idx + 2 * (CB_NB + 2);
+    int32_t* wk_cur = wk_cnt + (CB_NB + 2);
+    int32_t* wk_ent = g.cb_ent + g.cb_cap;
     // bucket width: the largest interval end in the pass (ints are >= 0)
     if (x.tid == 0) gsh[14] = 0;
-    for (int32_t k = x.tid; k < CB_NB + 1; k += x.nthr) bk_cnt[k] = 0;
+    for (int32_t k = x.tid; k < CB_NB + 1; k += x.nthr) { bk_cnt[k] = 0; wk_cnt[k] = 0; }
     x.sync();
     for (int64_t m = x.tid; m < nc; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
@@ -1874,6 +1910,13 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
           for (int64_t q = imax(0, bucket(s0)); q <= bucket(e0 - 1) && q >= 0; ++q) x.aadd32(&bk_cnt[q + 1], 1);
         }
     }
+    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+      for (int32_t w = 0; w < ci[CI_NW]; ++w)
+        for (int64_t q = imax(0, bucket(wv[2 * w])); q <= bucket(wv[2 * w + 1] - 1) && q >= 0; ++q)
+          x.aadd32(&wk_cnt[q + 1], 1);
+    }
     x.sync();
     // prefix over the bucket counts: one warp, 32 buckets per lane (the
     // block scan's scratch holds the candidate records here)
@@ -1886,11 +1929,35 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       int32_t off = x.wexcl(sum, &tot);
       for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
       if (x.lane == 0) gsh[15] = tot;
+    } else if (x.warp == 1) {
+      constexpr int PER = CB_NB / X::W;
+      int32_t* c = wk_cnt + 1 + x.lane * PER;
+      int32_t sum = 0;
+      for (int k = 0; k < PER; ++k) sum += c[k];
+      int32_t tot = 0;
+      int32_t off = x.wexcl(sum, &tot);
+      for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
+      if (x.lane == 0) gsh[GS_WK] = tot <= g.cb_cap ? shb + 1 : 0;
+    }
+    if (X::W == 1 && x.warp == 0) {  // one-thread context: the window prefix too
+      int32_t* c = wk_cnt + 1;
+      int32_t off = 0;
+      for (int k = 0; k < CB_NB; ++k) { off += c[k]; c[k] = off; }
+      gsh[GS_WK] = off <= g.cb_cap ? shb + 1 : 0;
     }
     x.sync();
     const bool fits = gsh[15] <= g.cb_cap;
-    for (int32_t k = x.tid; k < CB_NB; k += x.nthr) bk_cur[k] = bk_cnt[k];
+    for (int32_t k = x.tid; k < CB_NB; k += x.nthr) { bk_cur[k] = bk_cnt[k]; wk_cur[k] = wk_cnt[k]; }
     x.sync();
+    if (gsh[GS_WK]) {
+      for (int64_t m = x.tid; m < nc; m += x.nthr) {
+        const int32_t* ci = cinfo + m * CI_STRIDE;
+        const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+        for (int32_t w = 0; w < ci[CI_NW]; ++w)
+          for (int64_t q = imax(0, bucket(wv[2 * w])); q <= bucket(wv[2 * w + 1] - 1) && q >= 0; ++q)
+            wk_ent[x.aadd32(&wk_cur[q], 1)] = int32_t(m);
+      }
+    }
     if (fits) {
       for (int64_t m = x.tid; m < nc; m += x.nthr) {
         const int32_t* ci = cinfo + m * CI_STRIDE;

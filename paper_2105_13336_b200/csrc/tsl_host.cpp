@@ -282,6 +282,7 @@ struct JobPlace {  // byte offsets into the device buffer
 
 struct GroupPlace {
   size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
+  size_t coop = 0, tile_hist = 0;
   int64_t pr_cap, w_cap, wcap, cb_cap;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
@@ -363,7 +364,9 @@ struct tsl_plan {
   int64_t sort_cap = 0;   // NT * ipt
   int64_t ecap = 0;       // timeline scratch capacity (== sort_cap unless big)
   bool big = false;       // a job exceeds one sort tile
+  bool coop = false;      // big and one group: cooperative launch, one CTA per SM
   size_t res_bytes = 0;   // shared memory for resident job arrays (build mode)
+  tsl::CoopCtl coop_init{};  // initial cooperative control block (uploaded before each launch)
   int64_t n_accesses = 0;
 };
 
@@ -476,6 +479,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
         fail(TSL_ERR_CAPACITY, "build exceeds the planner capacity (2^30 timeline events per job)");
       P->big = true;
       P->ecap = (need + 15) & ~int64_t(15);
+      const char* ce = std::getenv("TSL_COOP");
+      P->coop = n_groups == 1 && !(ce && ce[0] == '0');
     }
   }
   const auto t_val = std::chrono::steady_clock::now();
@@ -606,6 +611,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       q.bs_key = L.take<uint64_t>(E);
       q.bs_val = L.take<int32_t>(E);
     }
+    if (P->coop) {
+      q.coop = L.take<uint8_t>(sizeof(tsl::CoopCtl));
+      q.tile_hist = L.take<int32_t>(size_t((P->ecap + NT * SORT_IPT - 1) / (NT * SORT_IPT)) * 256);
+    }
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
     q.x_time = L.take<int64_t>(2 * E);  // second half: evaluator scan scratch
@@ -662,6 +671,12 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     const GroupPlace& q = P->gp[gi];
     G->hist = dp<int64_t>(ctx, q.hist);
     G->ecap = int32_t(P->ecap);
+    G->coop = P->coop ? reinterpret_cast<tsl::CoopCtl*>(static_cast<uint8_t*>(ctx->dbuf) + q.coop) : nullptr;
+    if (P->coop) {  // the device control block starts zeroed; its tile table is set here
+      tsl::CoopCtl cc{};
+      cc.tile_hist = dp<int32_t>(ctx, q.tile_hist);
+      P->coop_init = cc;
+    }
     G->bs_key = P->big ? dp<uint64_t>(ctx, q.bs_key) : nullptr;
     G->bs_val = P->big ? dp<int32_t>(ctx, q.bs_val) : nullptr;
     G->k_key = dp<uint64_t>(ctx, q.k_key);
@@ -838,6 +853,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
 void upload(tsl_plan* P) {
   Buffers* b = P->buf;
   cuda_check(cudaMemcpyAsync(b->dbuf, b->hbuf, P->h2d_bytes, cudaMemcpyHostToDevice, P->ctx->stream), "H2D");
+  if (P->coop)  // (the kernel leaves it reset, so one upload serves every launch)
+    cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(b->dbuf) + P->gp[0].coop, &P->coop_init, sizeof P->coop_init,
+                               cudaMemcpyHostToDevice, P->ctx->stream), "H2D coop");
 }
 
 void launch(tsl_plan* P, int repeats, bool timed) {
@@ -845,7 +863,7 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
   for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
-    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, P->big, c->stream), "launch");
+    cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, P->big, P->coop, c->stream), "launch");
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
@@ -1180,7 +1198,7 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   return guard([&] {
     tsl_ctx* c = P->ctx;
     cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode, P->max_jobs, P->ipt,
-                                  P->res_bytes, P->big, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
+                                  P->res_bytes, P->big, P->coop, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
   });
 }
 

@@ -43,6 +43,8 @@ struct DevX {
   uint64_t* bs_key;  // big-sort ping-pong (global), null unless the launch has jobs above one tile
   int32_t* bs_val;
   int32_t* aux;      // big-sort digit tables in shared memory: 4 x 256 + NT words
+  CoopCtl* coop;     // cooperative launch (CTA 0 of `grid`), else null
+  int grid;
 
   __device__ void sync() { __syncthreads(); }
   // Reads the SM clock only once the preceding barrier has really released
@@ -169,10 +171,201 @@ struct DevX {
     }
   }
 
+  // ---- cooperative passes (all CTAs of the launch) ----
+  // L1 is not coherent across SMs: everything another CTA wrote or will read
+  // moves through L2 (ld/st .cg).
+  __device__ static void spin_guard(int64_t t0) {
+    if (clock64() - t0 > (int64_t(1) << 36)) __trap();  // ~30 s at 2 GHz: fail loudly, never hang
+  }
+  __device__ void grid_barrier() {
+    __syncthreads();
+    if (tid == 0) {
+      volatile int32_t* gen = &coop->bar_gen;
+      const int32_t g0 = *gen;
+      __threadfence();
+      if (atomicAdd(&coop->bar_count, 1) == grid - 1) {
+        coop->bar_count = 0;
+        __threadfence();
+        atomicAdd(&coop->bar_gen, 1);
+      } else {
+        const int64_t t0 = clock64();
+        while (*gen == g0) { __nanosleep(64); spin_guard(t0); }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+
+  // One stable LSD pass over all CTAs: per-tile digit counts, grid barrier,
+  // every CTA derives its tiles' digit bases from the count table, sorts its
+  // tiles on the digit in shared memory and scatters; grid barrier.
+  __device__ void coop_pass(int cta, const uint64_t* ks, const int32_t* vs, uint64_t* kd, int32_t* vd, int n,
+                            int sh, int nb) {
+    constexpr int TILE = NT * SORT_IPT;
+    int32_t* cnt = aux;          // [256]
+    int32_t* base = aux + 256;   // [256] running destination of each digit
+    int32_t* tstart = aux + 512;
+    int32_t* tcnt = aux + 768;
+    int32_t* lastd = aux + 1024;
+    int32_t* th = coop->tile_hist;
+    const uint64_t mask = (uint64_t(1) << nb) - 1;
+    const int tiles = (n + TILE - 1) / TILE;
+    const int per = (tiles + grid - 1) / grid;
+    const int t0 = min(tiles, cta * per), t1 = min(tiles, t0 + per);
+    for (int t = t0; t < t1; ++t) {
+      const int off = t * TILE, valid = min(TILE, n - off);
+      for (int d = tid; d < 256; d += NT) cnt[d] = 0;
+      __syncthreads();
+      for (int i = tid; i < valid; i += NT) atomicAdd(&cnt[(__ldcg(&ks[off + i]) >> sh) & mask], 1);
+      __syncthreads();
+      for (int d = tid; d < 256; d += NT) __stcg(&th[int64_t(t) * 256 + d], cnt[d]);
+      __syncthreads();
+    }
+    grid_barrier();
+    {  // thread d: digit total and the count in tiles before mine
+      const int d = tid;
+      int32_t tot = 0, bef = 0;
+      if (d < 256)
+        for (int t = 0; t < tiles; ++t) {
+          const int32_t h = __ldcg(&th[int64_t(t) * 256 + d]);
+          tot += h;
+          bef += t < t0 ? h : 0;
+        }
+      if (d < 256) { cnt[d] = tot; tcnt[d] = bef; }
+      __syncthreads();
+      if (warp == 0) {
+        int32_t c[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { c[k] = cnt[lane * 8 + k]; sum += c[k]; }
+        int32_t all = 0;
+        int32_t o = wexcl(sum, &all);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { base[lane * 8 + k] = o; o += c[k]; }
+      }
+      __syncthreads();
+      if (d < 256) base[d] += tcnt[d];
+      __syncthreads();
+    }
+    for (int t = t0; t < t1; ++t) {
+      const int off = t * TILE, valid = min(TILE, n - off);
+      uint64_t k[SORT_IPT];
+      int32_t v[SORT_IPT];
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int idx = tid * SORT_IPT + i;
+        k[i] = idx < valid ? __ldcg(&ks[off + idx]) : ~0ull;
+        v[i] = idx < valid ? __ldcg(&vs[off + idx]) : 0;
+      }
+      for (int d = tid; d < 256; d += NT) tcnt[d] = 0;
+      __syncthreads();
+      BRS<SORT_IPT>(*reinterpret_cast<typename BRS<SORT_IPT>::TempStorage*>(tmp)).Sort(k, v, sh, sh + nb);
+      lastd[tid] = int32_t((k[SORT_IPT - 1] >> sh) & mask);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int p = tid * SORT_IPT + i;
+        if (p >= valid) break;
+        const int32_t d = int32_t((k[i] >> sh) & mask);
+        const int32_t pd = i > 0 ? int32_t((k[i - 1] >> sh) & mask) : (tid > 0 ? lastd[tid - 1] : -1);
+        if (p == 0 || pd != d) tstart[d] = p;
+        atomicAdd(&tcnt[d], 1);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < SORT_IPT; ++i) {
+        const int p = tid * SORT_IPT + i;
+        if (p >= valid) break;
+        const int32_t d = int32_t((k[i] >> sh) & mask);
+        const int64_t dst = int64_t(base[d]) + (p - tstart[d]);
+        __stcg(&kd[dst], k[i]);
+        __stcg(&vd[dst], v[i]);
+      }
+      __syncthreads();
+      for (int d = tid; d < 256; d += NT) base[d] += tcnt[d];
+      __syncthreads();
+    }
+    grid_barrier();
+  }
+
+  // CTA 0: publish a task to the waiting CTAs.
+  __device__ void coop_publish(int type, const uint64_t* ks, const int32_t* vs, uint64_t* kd, int32_t* vd, int n,
+                               int sh, int nb) {
+    __syncthreads();
+    if (tid == 0) {
+      volatile CoopCtl* c = coop;
+      c->ks = ks; c->vs = vs; c->kd = kd; c->vd = vd; c->n = n; c->sh = sh; c->nb = nb; c->type = type;
+      __threadfence();
+      atomicAdd(&coop->epoch, 1);
+    }
+    __syncthreads();
+  }
+
+  // CTAs 1..grid-1: run published passes until COOP_EXIT.
+  __device__ void coop_worker(int cta) {
+    int32_t seen = 0;
+    for (;;) {
+      if (tid == 0) {
+        volatile int32_t* ep = &coop->epoch;
+        const int64_t t0 = clock64();
+        while (*ep == seen) { __nanosleep(128); spin_guard(t0); }
+      }
+      __syncthreads();
+      volatile CoopCtl* c = coop;
+      seen = c->epoch;
+      __threadfence();
+      const int32_t type = c->type;
+      if (type == COOP_EXIT) {
+        __syncthreads();
+        if (tid == 0) atomicAdd(&coop->exited, 1);
+        return;
+      }
+      coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
+    }
+  }
+
+  // CTA 0 at the end of the kernel: release the workers, reset the block.
+  __device__ void coop_finish() {
+    coop_publish(COOP_EXIT, nullptr, nullptr, nullptr, nullptr, 0, 0, 0);
+    if (tid == 0) {
+      volatile int32_t* ex = &coop->exited;
+      const int64_t t0 = clock64();
+      while (*ex < grid - 1) { __nanosleep(128); spin_guard(t0); }
+      volatile CoopCtl* c = coop;
+      c->epoch = 0; c->type = 0; c->bar_count = 0; c->bar_gen = 0; c->exited = 0;
+      __threadfence();
+    }
+    __syncthreads();
+  }
+
   // Stable sort of n > one tile keys: 8-bit LSD passes through the group's
-  // ping-pong buffers.
+  // ping-pong buffers (all CTAs of a cooperative launch, else this CTA).
   __device__ void sort_big(uint64_t* keys, int32_t* vals, int n, int bits) {
     if (!bs_key || !aux) __trap();  // the host sizes every launch with a job above one tile as big
+    if (coop) {
+      const uint64_t* ks = keys;
+      const int32_t* vs = vals;
+      uint64_t* kd = bs_key;
+      int32_t* vd = bs_val;
+      for (int sh = 0; sh < bits; sh += 8) {
+        const int nb = min(8, bits - sh);
+        coop_publish(COOP_PASS, ks, vs, kd, vd, n, sh, nb);
+        coop_pass(0, ks, vs, kd, vd, n, sh, nb);
+        const uint64_t* tk = ks;
+        const int32_t* tv = vs;
+        ks = kd; vs = vd;
+        kd = const_cast<uint64_t*>(tk); vd = const_cast<int32_t*>(tv);
+      }
+      // this CTA rewrites the result itself: its L1 may hold lines of the
+      // output arrays from before the sort
+      for (int i = tid; i < n; i += NT) {
+        const uint64_t kk = __ldcg(&ks[i]);
+        const int32_t vv = __ldcg(&vs[i]);
+        keys[i] = kk;
+        vals[i] = vv;
+      }
+      __syncthreads();
+      return;
+    }
     const uint64_t* ks = keys;
     const int32_t* vs = vals;
     uint64_t* kd = bs_key;
@@ -305,7 +498,7 @@ __device__ void make_resident(GroupDev* gs, const JobDev* gj, JobDev* jd, uint8_
 // kernel and are written back at the end.
 extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
     tsl_plan_kernel(tsl::GroupDev* groups, int mode, int max_jobs, int ipt, unsigned tmp_bytes, unsigned res_bytes,
-                    int big) {
+                    int big, int coop_grid) {
   extern __shared__ __align__(16) uint8_t smem[];
   using namespace tsl;
   DevX x;
@@ -320,6 +513,17 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   x.tmp = smem + SH_BYTES + HDR_BYTES + ST_BYTES * max_jobs;
   x.tmp_bytes = tmp_bytes;
   x.sort_cap = NT * ipt;
+  x.coop = nullptr;
+  x.grid = 1;
+  if (coop_grid > 1) {  // cooperative launch: one group, CTA 0 plans, the others sort
+    x.coop = groups[0].coop;
+    x.grid = coop_grid;
+    x.aux = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(x.tmp) + ((size_t(tmp_bytes) + 15) & ~size_t(15)));
+    if (blockIdx.x > 0) {
+      x.coop_worker(blockIdx.x);
+      return;
+    }
+  }
   GroupDev* gg = &groups[blockIdx.x];
   x.bs_key = gg->bs_key;
   x.bs_val = gg->bs_val;
@@ -339,6 +543,7 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   if (mode == 0) plan_group(x, *gs);
   else analyze_group(x, *gs);
   __syncthreads();
+  if (x.coop) x.coop_finish();
   for (int j = x.tid; j < gs->n_jobs; j += x.nthr) gst[j] = sts[j];
   if (x.tid == 0) {
     gs->st = gst;
@@ -368,7 +573,7 @@ size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes, bool big) {
 }
 
 cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
-                               bool big, cudaStream_t stream) {
+                               bool big, bool coop, cudaStream_t stream) {
   if (mode != 0 || max_jobs > RES_MAX_JOBS || big) res_bytes = 0;
   const size_t smem = kernel_smem_bytes(max_jobs, ipt, res_bytes, big);
   static size_t attr = 0;  // (per process: one device)
@@ -384,8 +589,23 @@ cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int m
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, (unsigned)tmp_bytes_for(ipt),
-                                                  (unsigned)res_bytes, big ? 1 : 0);
+  unsigned tb = (unsigned)tmp_bytes_for(ipt), rb = (unsigned)res_bytes;
+  int bg = big ? 1 : 0;
+  if (coop && big && n_groups == 1) {
+    // one CTA per SM, all co-resident: CTA 0 plans, the rest sort with it
+    int dev = 0, sms = 0, per = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tsl_plan_kernel, NT, smem);
+    if (e != cudaSuccess) return e;
+    int G = per >= 1 ? sms : 1;
+    if (G > 1) {
+      void* args[] = {&d_groups, &mode, &max_jobs, &ipt, &tb, &rb, &bg, &G};
+      return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tsl_plan_kernel), dim3(G), dim3(NT), args, smem,
+                                         stream);
+    }
+  }
+  tsl_plan_kernel<<<n_groups, NT, smem, stream>>>(d_groups, mode, max_jobs, ipt, tb, rb, bg, 0);
   return cudaGetLastError();
 }
 }  // namespace tsl

@@ -23,6 +23,8 @@ constexpr size_t BIG_AUX_BYTES = (4 * 256 + NT) * sizeof(int32_t);
 size_t kernel_smem_bytes(int max_jobs, int ipt, size_t res_bytes, bool big = false);
 // Shared-memory bytes that would hold every resident array of the job.
 size_t resident_bytes_for(int32_t A, int32_t T, int32_t Scap);
+// coop: a single group above one sort tile runs as a cooperative launch of one
+// CTA per SM (CTA 0 plans; the others join its block-wide sorts).
 cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int max_jobs, int ipt, size_t res_bytes,
-                               bool big, cudaStream_t stream);
+                               bool big, bool coop, cudaStream_t stream);
 }  // namespace tsl

@@ -169,6 +169,25 @@ struct GroupStats {
   int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
 };
 
+// Control block of a cooperative launch (one group above one sort tile,
+// one CTA per SM): CTA 0 plans; the other CTAs wait for block-wide radix-sort
+// passes it publishes (epoch), run their share, and meet at grid barriers.
+struct CoopCtl {
+  int32_t epoch;      // task generation (CTA 0 bumps it per task)
+  int32_t type;       // COOP_PASS / COOP_EXIT
+  int32_t bar_count;  // grid barrier arrivals
+  int32_t bar_gen;    // grid barrier generation
+  int32_t exited;     // workers that saw COOP_EXIT
+  int32_t grid;       // CTAs of the launch
+  const uint64_t* ks; // pass input / output
+  const int32_t* vs;
+  uint64_t* kd;
+  int32_t* vd;
+  int32_t n, sh, nb, pad;
+  int32_t* tile_hist; // [tiles * 256] digit counts per tile
+};
+enum : int32_t { COOP_PASS = 1, COOP_EXIT = 9 };
+
 struct GroupDev {
   int32_t n_jobs;
   int32_t coupled;      // some job has ratio < 1: swap passes run globally in order
@@ -202,6 +221,7 @@ struct GroupDev {
   uint64_t* x_key2;  // [ecap]
   int32_t* x_order;  // [ecap] sorted position -> slot
   // speculative swap pass scratch (tsl_plan.cuh swap_pass)
+  CoopCtl* coop;     // cooperative launch control (one group above one tile), else null
   uint64_t* bs_key;  // [ecap] ping-pong of the block-wide radix sort (jobs above one sort tile), else null
   int32_t* bs_val;   // [ecap]
   int32_t* c_info;   // [candidates * 16]

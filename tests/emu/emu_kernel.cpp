@@ -53,7 +53,7 @@ int sort_ipt_for(int64_t n) {
 size_t kernel_smem_bytes(int, int, size_t, bool) { return SH_WORDS * sizeof(int64_t); }
 size_t resident_bytes_for(int32_t, int32_t, int32_t) { return 0; }
 
-cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, size_t, bool, cudaStream_t) {
+cudaError_t launch_plan_kernel(GroupDev* groups, int n_groups, int mode, int, int ipt, size_t, bool, bool, cudaStream_t) {
   std::vector<int64_t> sh(SH_WORDS);
   std::vector<int64_t> tmp(96 * 1024 / 8);  // stands in for the shared sort scratch
   for (int gi = 0; gi < n_groups; ++gi) {

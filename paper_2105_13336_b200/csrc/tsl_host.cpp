@@ -282,7 +282,7 @@ struct JobPlace {  // byte offsets into the device buffer
 
 struct GroupPlace {
   size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
-  size_t coop = 0, tile_hist = 0;
+  size_t coop = 0, tile_hist = 0, coop_gsh = 0, cta_part = 0;
   int64_t pr_cap, w_cap, wcap, cb_cap;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
@@ -481,6 +481,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       P->ecap = (need + 15) & ~int64_t(15);
       const char* ce = std::getenv("TSL_COOP");
       P->coop = n_groups == 1 && !(ce && ce[0] == '0');
+      // a grid-wide evaluation scans one release count per global thread
+      // (<= 256 SMs x NT) inside the timeline scratch
+      if (P->coop) P->ecap = std::max<int64_t>(P->ecap, int64_t(256) * NT);
     }
   }
   const auto t_val = std::chrono::steady_clock::now();
@@ -614,6 +617,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     if (P->coop) {
       q.coop = L.take<uint8_t>(sizeof(tsl::CoopCtl));
       q.tile_hist = L.take<int32_t>(size_t((P->ecap + NT * SORT_IPT - 1) / (NT * SORT_IPT)) * 256);
+      q.coop_gsh = L.take<int64_t>(1024);  // SH_WORDS (tsl_plan.cuh)
+      q.cta_part = L.take<int64_t>(1024);
     }
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
@@ -675,6 +680,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     if (P->coop) {  // the device control block starts zeroed; its tile table is set here
       tsl::CoopCtl cc{};
       cc.tile_hist = dp<int32_t>(ctx, q.tile_hist);
+      cc.gsh = dp<int64_t>(ctx, q.coop_gsh);
+      cc.cta_part = dp<int64_t>(ctx, q.cta_part);
       P->coop_init = cc;
     }
     G->bs_key = P->big ? dp<uint64_t>(ctx, q.bs_key) : nullptr;

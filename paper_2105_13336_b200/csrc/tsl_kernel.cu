@@ -14,6 +14,7 @@ namespace tsl {
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
 static_assert(TI_NB == TI_NB_HOST, "time index size");
 static_assert(CB_NB == 1024, "conflict and window index size (host allocates 4 * 1024 + 16)");
+static_assert(SH_WORDS == 1024, "cooperative scalar block (host allocates 1024 words)");
 
 template <int IPT>
 using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;
@@ -319,9 +320,12 @@ struct DevX {
         if (tid == 0) atomicAdd(&coop->exited, 1);
         return;
       }
-      coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
+      if (type == COOP_EVAL) coop_eval(cta, c->jb, c->je);
+      else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
   }
+  __device__ void coop_eval(int cta, int jb, int je);  // all CTAs: evaluate() on the grid (below)
+  GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
   __device__ void coop_finish() {
@@ -428,6 +432,123 @@ struct DevX {
 }  // namespace tsl
 
 namespace tsl {
+// Grid-wide execution context of a cooperative launch: every CTA runs the
+// same evaluate() over global thread indices; sync() is the grid barrier, the
+// shared scalars live in global memory, scans combine per-CTA partials, big
+// sorts are the cooperative radix passes and tile-sized sorts run on CTA 0.
+// (Plain loads after the barrier see other CTAs' writes: the barrier's
+// acquire fence -- checked by tools/l1_coherence_probe.cu.)
+struct GridX {
+  static constexpr int W = 32;
+  int tid, nthr, lane, warp, nwarp, cta;
+  int64_t* sh;
+  DevX* dx;
+  __device__ void sync() { dx->grid_barrier(); }
+  __device__ int64_t clock() { return clock64(); }
+  __device__ int64_t aadd(int64_t* p, int64_t v) {
+    return (int64_t)atomicAdd((unsigned long long*)p, (unsigned long long)v);
+  }
+  __device__ void amin(int64_t* p, int64_t v) { atomicMin((long long*)p, (long long)v); }
+  __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
+  // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs
+  __device__ void scan_op(int64_t* a, int n, int op) {
+    sync();
+    const int chunk = (n + nthr - 1) / nthr;
+    const int b = min(n, tid * chunk), e = min(n, b + chunk);
+    int64_t s = op ? INT64_MIN : 0;
+    for (int i = b; i < e; ++i) s = op ? max(s, a[i]) : s + a[i];
+    int64_t off;
+    auto& ts = *reinterpret_cast<typename BScan::TempStorage*>(dx->tmp);
+    int64_t total;
+    if (op) BScan(ts).ExclusiveScan(s, off, INT64_MIN, cub::Max(), total);
+    else BScan(ts).ExclusiveSum(s, off, total);
+    if (threadIdx.x == 0) __stcg(&dx->coop->cta_part[cta], total);
+    sync();
+    int64_t pre = op ? INT64_MIN : 0;  // the CTAs before this one
+    for (int c = 0; c < cta; ++c) {
+      const int64_t v = __ldcg(&dx->coop->cta_part[c]);
+      pre = op ? max(pre, v) : pre + v;
+    }
+    off = op ? max(pre, off) : pre + off;
+    for (int i = b; i < e; ++i) {
+      off = op ? max(off, a[i]) : off + a[i];
+      a[i] = off;
+    }
+    sync();
+  }
+  __device__ void scan(int64_t* a, int n) { scan_op(a, n, 0); }
+  __device__ void scan_max(int64_t* a, int n) { scan_op(a, n, 1); }
+  __device__ void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
+    sync();
+    if (n <= 1 || bits <= 0) return;
+    if (n > dx->sort_cap) {
+      const uint64_t* ks = keys;
+      const int32_t* vs = vals;
+      uint64_t* kd = dx->bs_key;
+      int32_t* vd = dx->bs_val;
+      int passes = 0;
+      for (int s0 = 0; s0 < bits; s0 += 8, ++passes) {
+        dx->coop_pass(cta, ks, vs, kd, vd, n, s0, min(8, bits - s0));
+        const uint64_t* tk = ks;
+        const int32_t* tv = vs;
+        ks = kd; vs = vd;
+        kd = const_cast<uint64_t*>(tk); vd = const_cast<int32_t*>(tv);
+      }
+      if (passes & 1) {
+        for (int i = tid; i < n; i += nthr) { keys[i] = __ldcg(&ks[i]); vals[i] = __ldcg(&vs[i]); }
+      }
+      sync();
+      return;
+    }
+    if (cta == 0) dx->sort(keys, vals, n, bits);  // one tile: CTA 0 in shared memory
+    sync();
+  }
+};
+
+__device__ inline GridX grid_ctx(DevX& x, int cta) {
+  GridX gx;
+  gx.cta = cta;
+  gx.tid = cta * NT + int(threadIdx.x);
+  gx.nthr = x.grid * NT;
+  gx.lane = x.lane;
+  gx.warp = x.warp;
+  gx.nwarp = x.nwarp;
+  gx.sh = x.coop->gsh;
+  gx.dx = &x;
+  return gx;
+}
+
+__device__ void DevX::coop_eval(int cta, int jb, int je) {
+  GridX gx = grid_ctx(*this, cta);
+  evaluate(gx, *coop_group, jb, je);
+}
+
+// The CUDA build's evaluation batches: on a cooperative launch, CTA 0 calls
+// every CTA in (one job at a time when the grid-wide release scan of a batch
+// would not fit the timeline scratch).
+template <>
+__device__ inline bool eval_batch<DevX>(DevX& x, GroupDev& g, int jb, int je) {
+  if (!x.coop) return evaluate(x, g, jb, je);
+  const int64_t gthr = int64_t(x.grid) * NT;
+  for (int b = jb; b < je;) {
+    const int e = (int64_t(je - b) * gthr <= g.ecap) ? je : b + 1;
+    __syncthreads();
+    if (x.tid == 0) {
+      volatile CoopCtl* c = x.coop;
+      c->jb = b; c->je = e; c->type = COOP_EVAL;
+      __threadfence();
+      atomicAdd(&x.coop->epoch, 1);
+    }
+    __syncthreads();
+    GridX gx = grid_ctx(x, 0);
+    if (!evaluate(gx, g, b, e)) return false;
+    b = e;
+  }
+  return true;
+}
+}  // namespace tsl
+
+namespace tsl {
 // Shared-memory layout: [scalars][group header copy][JobState x max_jobs]
 // [sort scratch][JobDev x max_jobs + resident job arrays (build mode)]
 constexpr size_t SH_BYTES = SH_WORDS * sizeof(int64_t);
@@ -515,14 +636,24 @@ extern "C" __global__ void __launch_bounds__(tsl::NT, 1)
   x.sort_cap = NT * ipt;
   x.coop = nullptr;
   x.grid = 1;
-  if (coop_grid > 1) {  // cooperative launch: one group, CTA 0 plans, the others sort
+  if (coop_grid > 1) {  // cooperative launch: one group, CTA 0 plans, the others join
     x.coop = groups[0].coop;
     x.grid = coop_grid;
+    x.coop_group = &groups[0];
     x.aux = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(x.tmp) + ((size_t(tmp_bytes) + 15) & ~size_t(15)));
+    x.bs_key = groups[0].bs_key;
+    x.bs_val = groups[0].bs_val;
     if (blockIdx.x > 0) {
       x.coop_worker(blockIdx.x);
       return;
     }
+    // CTA 0 plans on the global group header and job states: the other CTAs
+    // read the same ones during evaluations
+    if (mode == 0) plan_group(x, groups[0]);
+    else analyze_group(x, groups[0]);
+    __syncthreads();
+    x.coop_finish();
+    return;
   }
   GroupDev* gg = &groups[blockIdx.x];
   x.bs_key = gg->bs_key;

@@ -1301,6 +1301,13 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   return g.err.code == 0;
 }
 
+// One evaluation batch; an execution context may route it elsewhere (the
+// CUDA build runs it on every CTA of a cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD bool eval_batch(X& x, GroupDev& g, int jb, int je) {
+  return evaluate(x, g, jb, je);
+}
+
 // Evaluate every job in [j0, j1) whose plan changed (or all when force),
 // in batches that fit the sort capacity.
 template <class X>
@@ -1318,7 +1325,7 @@ TSL_HD bool refresh(X& x, GroupDev& g, int j0, int j1, bool force) {
       tot += need;
       ++e;
     }
-    if (!evaluate(x, g, j, e)) return false;
+    if (!eval_batch(x, g, j, e)) return false;
     j = e;
   }
   return true;
@@ -2530,7 +2537,7 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
   if (!revalidate(x, g, j)) return false;
   if (x.tid == 0) st.dirty = 1;
   x.sync();
-  if (!evaluate(x, g, j, j + 1)) return false;
+  if (!eval_batch(x, g, j, j + 1)) return false;
   if (st.peak > saved.peak) {  // rollback (recompute_planner.cpp:148-151)
     backup_job(x, g, j, true, saved.S, saved.R, saved.n_curve);
     if (x.tid == 0) st = saved;

@@ -185,8 +185,11 @@ struct CoopCtl {
   int32_t* vd;
   int32_t n, sh, nb, pad;
   int32_t* tile_hist; // [tiles * 256] digit counts per tile
+  int32_t jb, je;     // COOP_EVAL: the job batch
+  int64_t* gsh;       // [SH_WORDS] grid-shared scalars of a cooperative evaluation
+  int64_t* cta_part;  // [1024] per-CTA partials of grid scans
 };
-enum : int32_t { COOP_PASS = 1, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;

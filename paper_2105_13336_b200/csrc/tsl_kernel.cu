@@ -288,6 +288,101 @@ struct DevX {
     grid_barrier();
   }
 
+  // Barrier of the worker CTAs only (CTA 0's deciding warp waits elsewhere).
+  __device__ void worker_barrier() {
+    __syncthreads();
+    if (tid == 0) {
+      volatile int32_t* gen = &coop->wbar_gen;
+      const int32_t g0 = *gen;
+      __threadfence();
+      if (atomicAdd(&coop->wbar_count, 1) == grid - 2) {
+        coop->wbar_count = 0;
+        __threadfence();
+        atomicAdd(&coop->wbar_gen, 1);
+      } else {
+        const int64_t t0 = clock64();
+        while (*gen == g0) { __nanosleep(64); spin_guard(t0); }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+
+  // Workers: fold the sorted lists a (busy) and b (pend) -- merge-path over
+  // every worker thread into m, copy back over a, rebuild a's time indexes.
+  __device__ void coop_fold(int cta) {
+    volatile CoopCtl* c = coop;
+    const int64_t *as = c->fa_s, *ae = c->fa_e, *bs = c->fb_s, *be = c->fb_e;
+    int64_t *ms = c->fm_s, *me = c->fm_e, *os = c->fo_s, *oe = c->fo_e;
+    int32_t *is = c->fi_s, *ie = c->fi_e;
+    const int32_t n1 = c->fn1, n2 = c->fn2, shift = c->fshift, n = n1 + n2;
+    const int64_t wt = int64_t(cta - 1) * NT + tid, WT = int64_t(grid - 1) * NT;
+    const int64_t per = (n + WT - 1) / WT;
+    const int32_t d0 = int32_t(min(int64_t(n), wt * per)), d1 = int32_t(min(int64_t(n), int64_t(d0) + per));
+    int32_t lo = max(0, d0 - n2), hi = min(d0, n1);
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (__ldcg(&as[mid]) <= __ldcg(&bs[d0 - mid - 1])) lo = mid + 1; else hi = mid;
+    }
+    int32_t i = lo, k = d0 - lo;
+    for (int32_t d = d0; d < d1; ++d) {
+      const int64_t av = i < n1 ? __ldcg(&as[i]) : 0, bv = k < n2 ? __ldcg(&bs[k]) : 0;
+      if (i < n1 && (k >= n2 || av <= bv)) { __stcg(&ms[d], av); __stcg(&me[d], __ldcg(&ae[i])); ++i; }
+      else { __stcg(&ms[d], bv); __stcg(&me[d], __ldcg(&be[k])); ++k; }
+    }
+    worker_barrier();
+    for (int64_t d = wt; d < n; d += WT) { __stcg(&os[d], __ldcg(&ms[d])); __stcg(&oe[d], __ldcg(&me[d])); }
+    worker_barrier();
+    for (int h = 0; h < 2; ++h) {  // build_tindex over the merged starts / ends
+      const int64_t* keys = h ? oe : os;
+      int32_t* first = h ? ie : is;
+      for (int64_t kk = wt; kk <= n; kk += WT) {
+        const int64_t kp = kk > 0 ? __ldcg(&keys[kk - 1]) : 0, kc = kk < n ? __ldcg(&keys[kk]) : 0;
+        int64_t blo = kk == 0 ? 0 : (kp >> shift) + 1;
+        if (kk > 0 && kp < 0) blo = 0;
+        int64_t bhi = kk == n ? TI_NB : (kc < 0 ? -1 : (kc >> shift));
+        if (kk < n && kc >= 0 && (kc & ((int64_t(1) << shift) - 1)) != 0) bhi = kc >> shift;
+        if (bhi > TI_NB) bhi = TI_NB;
+        for (int64_t b = blo; b <= bhi; ++b) __stcg(&first[b], int32_t(kk));
+      }
+    }
+    worker_barrier();
+    if (cta == 1 && tid == 0) {
+      __threadfence();
+      atomicExch(&coop->fdone, 1);
+    }
+  }
+
+  // Commit-list length that triggers a fold into the busy structure: folds on
+  // the worker CTAs are cheap, a fold by one warp is linear in the structure.
+  __device__ int32_t fold_threshold(int32_t bz_n) const {
+    return (coop && grid >= 3) ? 256 : max(PEND_MERGE, bz_n / 128);
+  }
+
+  // Deciding warp of CTA 0 (warp-collective): hand a busy-structure fold to
+  // the worker CTAs and wait. False when there are no workers.
+  __device__ bool fold_hook(const int64_t* as, const int64_t* ae, int32_t n1, const int64_t* bs, const int64_t* be,
+                            int32_t n2, int64_t* ms, int64_t* me, int64_t* os, int64_t* oe, int32_t* is, int32_t* ie,
+                            int shift) {
+    if (!coop || grid < 3) return false;
+    __syncwarp();
+    if (lane == 0) {
+      volatile CoopCtl* c = coop;
+      c->fa_s = as; c->fa_e = ae; c->fb_s = bs; c->fb_e = be; c->fm_s = ms; c->fm_e = me; c->fo_s = os;
+      c->fo_e = oe; c->fi_s = is; c->fi_e = ie; c->fn1 = n1; c->fn2 = n2; c->fshift = shift; c->fdone = 0;
+      c->type = COOP_FOLD;
+      __threadfence();
+      atomicAdd(&coop->epoch, 1);
+      volatile int32_t* dn = &coop->fdone;
+      const int64_t t0 = clock64();
+      while (*dn == 0) { __nanosleep(64); spin_guard(t0); }
+      __threadfence();
+    }
+    __syncwarp();
+    __threadfence();
+    return true;
+  }
+
   // CTA 0: publish a task to the waiting CTAs.
   __device__ void coop_publish(int type, const uint64_t* ks, const int32_t* vs, uint64_t* kd, int32_t* vd, int n,
                                int sh, int nb) {
@@ -321,6 +416,7 @@ struct DevX {
         return;
       }
       if (type == COOP_EVAL) coop_eval(cta, c->jb, c->je);
+      else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
   }

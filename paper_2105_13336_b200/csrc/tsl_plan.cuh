@@ -514,7 +514,7 @@ struct PendBuf {
 // Before a re-score the (short) unsorted suffix is ranked and merged in with
 // binary searches. Warp-collective.
 template <class X>
-TSL_HD void pend_sort(X& x, const PendBuf& pb, JobState& st) {
+TSL_HD void pend_sort(X& x, PendBuf& pb, JobState& st, bool pingpong = true) {
   const int32_t n = st.pend_n, p = st.pend_sorted;
   if (p >= n) return;
   const int32_t k = n - p;
@@ -532,22 +532,30 @@ TSL_HD void pend_sort(X& x, const PendBuf& pb, JobState& st) {
     te[r] = pb.e[p + i];
   }
   x.wsync();
-  for (int32_t i = x.lane; i < p; i += X::W) {  // prefix element: + suffix elements before it
-    const int64_t si = pb.s[i];
-    int32_t lo = 0, hi = k;
-    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (ts[m] < si) lo = m + 1; else hi = m; }
-    pb.ts[i + lo] = si;
-    pb.te[i + lo] = pb.e[i];
+  // merge prefix [0, p) and sorted suffix ts[0, k) into the merge target,
+  // prefix first on equal starts: one contiguous output range per lane
+  // (merge-path split), then the two buffers swap roles
+  const int32_t per = (n + X::W - 1) / X::W;
+  const int32_t d0 = imin(n, int64_t(x.lane) * per), d1 = imin(n, int64_t(d0) + per);
+  int32_t lo = imax(0, d0 - k), hi = imin(d0, p);
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (pb.s[mid] <= ts[d0 - mid - 1]) lo = mid + 1; else hi = mid;
   }
-  for (int32_t r = x.lane; r < k; r += X::W) {  // suffix element: + prefix elements up to it
-    const int64_t si = ts[r];
-    int32_t lo = 0, hi = p;
-    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (pb.s[m] <= si) lo = m + 1; else hi = m; }
-    pb.ts[r + lo] = si;
-    pb.te[r + lo] = te[r];
+  int32_t i = lo, r = d0 - lo;
+  for (int32_t d = d0; d < d1; ++d) {
+    if (i < p && (r >= k || pb.s[i] <= ts[r])) { pb.ts[d] = pb.s[i]; pb.te[d] = pb.e[i]; ++i; }
+    else { pb.ts[d] = ts[r]; pb.te[d] = te[r]; ++r; }
   }
   x.wsync();
-  for (int32_t i = x.lane; i < n; i += X::W) { pb.s[i] = pb.ts[i]; pb.e[i] = pb.te[i]; }
+  if (pingpong) {
+    int64_t* os = pb.s;
+    int64_t* oe = pb.e;
+    pb.s = pb.ts; pb.e = pb.te;  // every lane holds its own copy of pb
+    pb.ts = os; pb.te = oe;
+  } else {  // a caller that rebuilds its PendBuf from the job's arrays
+    for (int32_t d = x.lane; d < n; d += X::W) { pb.s[d] = pb.ts[d]; pb.e[d] = pb.te[d]; }
+  }
   x.wsync();
   st.pend_sorted = n;
   x.wsync();
@@ -1445,35 +1453,52 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
 // Folds the pass's sorted commit list into the job's busy structure (warp-
 // collective, the job's deciding warp only): queries see the same union of
 // intervals, later pend merges start from an empty list. Both lists are
-// disjoint at shift 0, so starts and ends stay sorted; the time indexes are
-// rebuilt. Scratch: the job's global merge buffers.
+// disjoint at shift 0, so starts and ends stay sorted; busy elements go first
+// on equal starts. Each lane merges one contiguous output range (merge-path
+// split) into the job's merge buffers, copied back; the time indexes are
+// rebuilt. Folding happens once
+// the list passes max(1024, busy / 128) intervals (a fold is linear in the
+// busy structure, a re-score's pend merge linear in the list).
 constexpr int32_t PEND_MERGE = 1024;
 
 template <class X>
 TSL_HD void merge_pend_into_busy(X& x, GroupDev& g, int j, const PendBuf& pb) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
-  const int32_t n1 = st.bz_n, n2 = st.pend_n;
-  int64_t* ms = J.pd_ts;
-  int64_t* me = J.pd_te;
+  const int32_t n1 = st.bz_n, n2 = st.pend_n, n = n1 + n2;
+  const int64_t* bs = J.bz_s;
+  const int64_t* be = J.bz_e;
+  int64_t* ms = J.bk_bz;             // the recompute rollback copy of the busy
+  int64_t* me = J.bk_bz + J.Scap;    // structure: idle during a swap pass
   x.wsync();
-  for (int32_t i = x.lane; i < n1; i += X::W) {  // busy element: + pend elements starting before it
-    const int64_t si = J.bz_s[i];
-    int32_t lo = 0, hi = n2;
-    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (pb.s[m] < si) lo = m + 1; else hi = m; }
-    ms[i + lo] = si;
-    me[i + lo] = J.bz_e[i];
+  {
+    // a cooperative launch folds on its worker CTAs
+    const int64_t mx = imax(n1 ? J.bz_e[n1 - 1] : 0, n2 ? pb.e[n2 - 1] : 0);
+    const int sh = tindex_shift(imax(mx, 0));
+    if (x.fold_hook(bs, be, n1, pb.s, pb.e, n2, ms, me, J.bz_s, J.bz_e, J.bzi_s, J.bzi_e, sh)) {
+      x.wsync();
+      st.bz_n = n;
+      st.pend_n = 0;
+      st.pend_sorted = 0;
+      st.bzi_shift = sh;
+      x.wsync();
+      return;
+    }
   }
-  for (int32_t k = x.lane; k < n2; k += X::W) {  // pend element: + busy elements starting at or before it
-    const int64_t sk = pb.s[k];
-    int32_t lo = 0, hi = n1;
-    while (lo < hi) { int32_t m = (lo + hi) >> 1; if (J.bz_s[m] <= sk) lo = m + 1; else hi = m; }
-    ms[k + lo] = sk;
-    me[k + lo] = pb.e[k];
+  const int32_t per = (n + X::W - 1) / X::W;
+  const int32_t d0 = imin(n, int64_t(x.lane) * per), d1 = imin(n, int64_t(d0) + per);
+  int32_t lo = imax(0, d0 - n2), hi = imin(d0, n1);  // busy elements among the first d0 outputs
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (bs[mid] <= pb.s[d0 - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  int32_t i = lo, k = d0 - lo;
+  for (int32_t d = d0; d < d1; ++d) {
+    if (i < n1 && (k >= n2 || bs[i] <= pb.s[k])) { ms[d] = bs[i]; me[d] = be[i]; ++i; }
+    else { ms[d] = pb.s[k]; me[d] = pb.e[k]; ++k; }
   }
   x.wsync();
-  const int32_t n = n1 + n2;
-  for (int32_t i = x.lane; i < n; i += X::W) { J.bz_s[i] = ms[i]; J.bz_e[i] = me[i]; }
+  for (int32_t d = x.lane; d < n; d += X::W) { J.bz_s[d] = ms[d]; J.bz_e[d] = me[d]; }
   x.wsync();
   const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0);
   x.wsync();
@@ -1492,7 +1517,7 @@ TSL_HD void merge_pend_into_busy(X& x, GroupDev& g, int j, const PendBuf& pb) {
 // the number of pairs committed (0: failed); -1 on error.
 template <class X>
 TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m, int32_t* cand, int32_t* cinfo,
-                                 const PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
+                                 PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t* ci = cinfo + m * CI_STRIDE;
@@ -1525,7 +1550,11 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   x.wsync();
   const int64_t rc1 = x.clock();
   pend_sort(x, pb, st);
-  if (st.pend_n >= PEND_MERGE) merge_pend_into_busy(x, g, j, pb);
+  if (st.pend_n >= x.fold_threshold(st.bz_n)) {
+    const int64_t f0 = x.clock();
+    merge_pend_into_busy(x, g, j, pb);
+    if (x.tid == 0) g.stats.cyc[19] += x.clock() - f0;
+  }
   const int64_t rc2 = x.clock();
   int64_t earliest = 0, latest = 0;
   const int kind = candidate_kind(J, st, s, earliest, latest);
@@ -1555,7 +1584,7 @@ constexpr int32_t CS_HIT = 16;
 
 template <class X>
 TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int32_t* cand, int32_t* cinfo,
-                           int64_t* chull, const PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
+                           int64_t* chull, PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t S = st.S;
@@ -2033,7 +2062,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         gsh[GS_POFF + j] = off;
         off += 6 * (2 * gsh[GS_PCAP + j] + 2);
       }
-      gsh[GS_POFF - 1] = int64_t(rec_bytes) + off * int64_t(sizeof(int64_t)) <= int64_t(x.tmp_bytes) ? 1 : 0;
+      // (a cooperative launch's workers fold pend lists: keep them in HBM)
+      gsh[GS_POFF - 1] = (g.coop == nullptr &&
+                          int64_t(rec_bytes) + off * int64_t(sizeof(int64_t)) <= int64_t(x.tmp_bytes)) ? 1 : 0;
     }
     x.sync();
     const bool pend_shared = gsh[GS_POFF - 1] != 0;
@@ -2107,7 +2138,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       } else {
         ls.rescored += 1;
         const int64_t rc0 = x.clock();
-        const PendBuf pbj{J.pd_s, J.pd_e, J.pd_ts, J.pd_te, wtmp, J.Scap};
+        PendBuf pbj{J.pd_s, J.pd_e, J.pd_ts, J.pd_te, wtmp, J.Scap};
         // bring this pass's pend list up to date: intervals of every candidate
         // of this job committed since the last re-score (lanes in parallel)
         for (int64_t q = st.pend_upto; q < m; ++q) {
@@ -2130,7 +2161,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         st.pend_upto = int32_t(m);
         x.wsync();
         const int64_t ps0 = x.clock();
-        pend_sort(x, pbj, st);
+        pend_sort(x, pbj, st, false);
         if (x.tid == 0) g.stats.cyc[11] += x.clock() - ps0;
         int64_t earliest = 0, latest = 0;
         const int kind = candidate_kind(J, st, s, earliest, latest);

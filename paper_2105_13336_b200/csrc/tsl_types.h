@@ -188,8 +188,16 @@ struct CoopCtl {
   int32_t jb, je;     // COOP_EVAL: the job batch
   int64_t* gsh;       // [SH_WORDS] grid-shared scalars of a cooperative evaluation
   int64_t* cta_part;  // [1024] per-CTA partials of grid scans
+  // COOP_FOLD (workers only, while one warp of CTA 0 waits): merge the sorted
+  // lists a (busy) and b (pend) into m, copy m back over a, rebuild a's index
+  const int64_t *fa_s, *fa_e, *fb_s, *fb_e;
+  int64_t *fm_s, *fm_e, *fo_s, *fo_e;
+  int32_t* fi_s;
+  int32_t* fi_e;
+  int32_t fn1, fn2, fshift, fdone;
+  int32_t wbar_count, wbar_gen;  // barrier of the worker CTAs
 };
-enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;

@@ -35,6 +35,6 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
         print("   eval phases prep/emit/sort1/group+sort2/automaton/scan+max/peak+report:", list(s["evalprof"]), flush=True)
         d = s["debug"]
         print(f"   rescore detail: queries {d[1]} avg {d[0]/max(1,d[1]):.0f} cyc; commits resolve {d[2]} total {d[3]} "
-              f"cyc; pend_sort {s['cyc_pendsort']} append/schedule {list(s['fitprof'])[:2]}", flush=True)
+              f"cyc; pend_sort {s['cyc_pendsort']} (folds {s['fitprof'][3]} cyc) append/schedule {list(s['fitprof'])[:2]}", flush=True)
         fp = list(s["fitprof"])
         print(f"   decide: total {fp[4]} bulk {fp[5]} attn-check {fp[6]} hit-mark {fp[7]} attention {fp[8]}", flush=True)

@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["C1", "C2", "C4", "C5"], default="C2")
+    ap.add_argument("--workload", choices=["C1", "C2", "C3", "C4", "C5"], default="C2")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -64,6 +64,8 @@ def workload(name: str, rank: int, planner=None):
     if name in ("C1", "C2"):
         req = CF.requests(name)[0]
         return [(req.name, req.jobs, req.config(CF.INITIAL_PEAK))]
+    if name == "C3":  # one replan per arrival: {inception_v3}, {+densenet}, {+vgg16}
+        return [(r.name, r.jobs, r.config(CF.INITIAL_PEAK)) for r in CF.requests("C3")]
     if name == "C4":
         return [CF.c4_request()]
     if name == "C4-sample":  # the reference cannot plan C4; its bounded CPU sample
@@ -83,6 +85,7 @@ def n_accesses(jobs) -> int:
 def workload_desc(name: str) -> str:
     return {"C1": "C1 VGG-16 b32, single workload, one build_plan",
             "C2": "C2 ResNet-50 b64, single workload with across-iteration (Opt-phase) swap-ins, one build_plan",
+            "C3": "C3 InceptionV3 + DenseNet + VGG-16 arriving in sequence, one replan per arrival (3 build_plans, one launch)",
             "C4": "C4 GPT-2-medium seq-1024 training trace, 70 micro-batches, 990,518 accesses, one build_plan",
             "C5": "C5 shard: 8 concurrent dynamic workloads, 8 arrivals + 7 departures = 15 replans per GPU"}[name]
 
@@ -318,8 +321,8 @@ def run_ours(a, rank, world, local):
         return
     from paper_2105_13336_b200 import configs as CF
     init_peak = (CF.C4_INITIAL_PEAK[CF.C4_MICRO_BATCHES] if a.workload == "C4" else
-                 sum(CF.INITIAL_PEAK.get(g["job_id"], 0) for g, _ in groups[0]) if a.workload != "C5" else None)
-    saved = (init_peak - outs[0]["final_merged_peak"]) if init_peak else None
+                 sum(CF.INITIAL_PEAK.get(g["job_id"], 0) for g, _ in groups[-1]) if a.workload not in ("C5",) else None)
+    saved = (init_peak - outs[-1]["final_merged_peak"]) if init_peak else None  # the full set (C3: last arrival)
     peak, how = hbm_peak()
     achieved = alg_bytes / (dev_ms / 1e3) / 1e9
     line = {

@@ -266,6 +266,18 @@ void tsl_exec_config_default(tsl_exec_config* cfg);
 int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_config* cfg,
                      const tsl_exec_config* ex, tsl_exec_report* out);
 
+/* Replays EVERY job of a build result together, as the reference's scheduled
+ * simulation co-schedules them (simulator.cpp:112-569, SimConfig over several
+ * SimJobs): one compute stream per job, all jobs' swaps on ONE copy stream
+ * (the FIFO channel) in planned-arrival order, one device allocator counter
+ * over all jobs. per_job[k] (k in tsl_result_n_jobs order) gets each job's own
+ * counters; *merged gets the global high-water mark against the merged
+ * predicted peak (sum of the jobs' peaks), summed swaps/bytes/errors and the
+ * slowest job's iteration times. Replaces simulate()'s scheduled mode for a
+ * multi-job SimConfig (simulator.hpp:84-87). */
+int tsl_execute_plans(tsl_ctx* ctx, const tsl_result* r, const tsl_config* cfg, const tsl_exec_config* ex,
+                      tsl_exec_report* per_job, tsl_exec_report* merged);
+
 /* Result accessors. Jobs are ordered by job id (std::map<JobId,...>). */
 int32_t tsl_result_n_jobs(const tsl_result* r);
 int tsl_result_job(const tsl_result* r, int32_t i, tsl_job_view* out);

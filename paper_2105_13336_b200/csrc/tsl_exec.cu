@@ -27,19 +27,26 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+__device__ __forceinline__ void count_add(int64_t* fp, int64_t* hwm, int64_t size) {
+  const unsigned long long f = atomicAdd(reinterpret_cast<unsigned long long*>(fp), (unsigned long long)size) + size;
+  atomicMax(reinterpret_cast<long long*>(hwm), (long long)f);
+}
+
+// Allocation / release on the job's counters and the replay's global ones.
 __device__ __forceinline__ void acct_add(ExecDevice* d, int32_t s, int64_t size) {
   if (atomicExch(&d->resident[s], 1) == 0) {
-    const unsigned long long f =
-        atomicAdd(reinterpret_cast<unsigned long long*>(&d->footprint), (unsigned long long)size) + size;
-    atomicMax(reinterpret_cast<long long*>(&d->hwm), (long long)f);
+    count_add(&d->footprint, &d->hwm, size);
+    if (d->acct) count_add(&d->acct->footprint, &d->acct->hwm, size);
   }
 }
 
 __device__ __forceinline__ void acct_sub(ExecDevice* d, int32_t s, int64_t size) {
-  if (atomicExch(&d->resident[s], 0) == 1)
+  if (atomicExch(&d->resident[s], 0) == 1) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&d->footprint), (unsigned long long)(-size));
-  else
+    if (d->acct) atomicAdd(reinterpret_cast<unsigned long long*>(&d->acct->footprint), (unsigned long long)(-size));
+  } else {
     atomicAdd(&d->violations, 1);  // release of a non-resident storage
+  }
 }
 
 __device__ __forceinline__ uint64_t tag_of(int32_t s, int32_t version) {

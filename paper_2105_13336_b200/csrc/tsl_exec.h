@@ -6,7 +6,14 @@
 
 namespace tsl {
 
+// Allocator counters shared by every job of a multi-job replay.
+struct ExecAcct {
+  int64_t footprint;
+  int64_t hwm;
+};
+
 struct ExecDevice {
+  ExecAcct* acct;         // the replay's global counters (every job's allocations)
   uint64_t tick_ns;
   uint8_t* pool;          // device pool: one slot per storage
   const int64_t* slot_off;

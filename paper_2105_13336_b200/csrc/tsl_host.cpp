@@ -1392,14 +1392,31 @@ struct ExecXferH {
   int32_t serve_step;  // swap-in: step that waits for it
 };
 
-tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl_config& cfg,
-                        const tsl_exec_config& ex) {
-  auto t0 = std::chrono::steady_clock::now();
-  if (ji < 0 || ji >= static_cast<int32_t>(r->jobs.size())) fail(TSL_ERR_ARGUMENT, "bad job index");
-  if (ex.iterations < 1 || ex.iterations > 8) fail(TSL_ERR_ARGUMENT, "iterations must be in 1..8");
-  if (ex.tick_ns <= 0 || ex.bytes_per_unit <= 0) fail(TSL_ERR_ARGUMENT, "tick_ns and bytes_per_unit must be positive");
-  const JobOut& o = r->jobs[static_cast<size_t>(ji)];
+// One job's replay program: steps (ops + recompute regenerations) and the
+// iteration's transfers in channel order (simulator.cpp:168-224).
+struct JobProgram {
+  const JobOut* o = nullptr;
+  const Graph* g = nullptr;
+  std::vector<ExecStepH> steps;
+  std::vector<ExecXferH> xs;
+  std::vector<int32_t> outs_per_iter;
+  int64_t period = 0;
+  std::vector<int64_t> slot_off, host_off;
+  int64_t pool_bytes = 0, host_bytes = 0;
+  std::vector<int32_t> i32;
+  std::vector<int64_t> i64;
+  struct OpOff { size_t ins, outs, rel, osz, rsz; };
+  std::vector<OpOff> offs;
+  std::vector<int32_t> init_st;
+  std::vector<int64_t> init_sz;
+  std::set<int32_t> wrapped_in;
+};
+
+JobProgram make_program(const JobOut& o, const tsl_config& cfg, const tsl_exec_config& ex) {
+  JobProgram P;
+  P.o = &o;
   const Graph& g = *o.g;
+  P.g = &g;
   // access sequence with the true latencies (simulator.cpp:168-213)
   std::vector<int32_t> acc_op, acc_tensor;
   std::vector<std::vector<int32_t>> op_acc(g.O);
@@ -1417,7 +1434,6 @@ tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl
   }
   std::set<int64_t> flags(o.flags.begin(), o.flags.end());
   // steps: recompute regenerations right before their target op, then the op
-  std::vector<ExecStepH> steps;
   std::vector<int32_t> op_step(g.O, -1);
   int64_t clock = 0;
   for (int32_t op : g.topo) {
@@ -1434,7 +1450,7 @@ tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl
       st.start = clock;
       clock += st.ticks;
       st.end = clock;
-      steps.push_back(std::move(st));
+      P.steps.push_back(std::move(st));
     }
     ExecStepH st{};
     st.op = op;
@@ -1455,13 +1471,12 @@ tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl
     st.start = clock;
     clock += st.ticks;
     st.end = clock;
-    op_step[op] = static_cast<int32_t>(steps.size());
-    steps.push_back(std::move(st));
+    op_step[op] = static_cast<int32_t>(P.steps.size());
+    P.steps.push_back(std::move(st));
   }
-  const int32_t nsteps = static_cast<int32_t>(steps.size());
+  P.period = clock;
   // transfers of one iteration, in channel (arrival) order
-  std::vector<ExecXferH> xs;
-  std::vector<int32_t> outs_per_iter(g.T, 0);
+  P.outs_per_iter.assign(g.T, 0);
   for (size_t e = 0; e < o.ev_id.size(); ++e) {
     ExecXferH t{};
     t.ev = static_cast<int32_t>(e);
@@ -1469,127 +1484,161 @@ tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl
     t.dir = o.ev_dir[e];
     t.anchor = o.ev_trig[e] < 0 ? -1 : op_step[acc_op[static_cast<size_t>(o.ev_trig[e])]];
     t.delta = o.ev_delta[e];
-    t.arrival = (t.anchor < 0 ? 0 : steps[static_cast<size_t>(t.anchor)].end) + t.delta;
+    t.arrival = (t.anchor < 0 ? 0 : P.steps[static_cast<size_t>(t.anchor)].end) + t.delta;
     t.size = g.size[t.storage];
     t.dur = (t.size + cfg.pcie_bandwidth - 1) / cfg.pcie_bandwidth + cfg.transfer_setup;
     t.serve_step = (t.dir == 1 && o.ev_serves[e] >= 0) ? op_step[acc_op[static_cast<size_t>(o.ev_serves[e])]] : -1;
-    if (t.dir == 0) outs_per_iter[t.storage]++;
-    xs.push_back(t);
+    if (t.dir == 0) P.outs_per_iter[t.storage]++;
+    P.xs.push_back(t);
   }
-  std::stable_sort(xs.begin(), xs.end(), [](const ExecXferH& a, const ExecXferH& b) { return a.arrival < b.arrival; });
-  // device / host memory
-  std::vector<int64_t> slot_off(g.T, 0);
-  int64_t pool_bytes = 0;
+  std::stable_sort(P.xs.begin(), P.xs.end(), [](const ExecXferH& a, const ExecXferH& b) { return a.arrival < b.arrival; });
+  // device / host slots
+  P.slot_off.assign(g.T, 0);
   for (int32_t t = 0; t < g.T; ++t) {
     if (g.store[t] != t) continue;
-    slot_off[t] = pool_bytes;
-    pool_bytes += ((g.size[t] * ex.bytes_per_unit + 255) / 256) * 256;
+    P.slot_off[t] = P.pool_bytes;
+    P.pool_bytes += ((g.size[t] * ex.bytes_per_unit + 255) / 256) * 256;
   }
-  std::vector<int64_t> host_off(g.T, -1);
-  int64_t host_bytes = 0;
-  for (auto& t : xs)
-    if (host_off[t.storage] < 0) {
-      host_off[t.storage] = host_bytes;
-      host_bytes += ((g.size[t.storage] * ex.bytes_per_unit + 255) / 256) * 256;
+  P.host_off.assign(g.T, -1);
+  for (auto& t : P.xs)
+    if (P.host_off[t.storage] < 0) {
+      P.host_off[t.storage] = P.host_bytes;
+      P.host_bytes += ((g.size[t.storage] * ex.bytes_per_unit + 255) / 256) * 256;
     }
-  // op descriptors (device arena)
-  std::vector<int32_t> i32;
-  std::vector<int64_t> i64;
-  struct OpOff { size_t ins, outs, rel, osz, rsz; };
-  std::vector<OpOff> offs;
-  for (auto& st : steps) {
-    OpOff f{};
-    f.ins = i32.size(); i32.insert(i32.end(), st.ins.begin(), st.ins.end());
-    f.outs = i32.size(); i32.insert(i32.end(), st.outs.begin(), st.outs.end());
-    f.rel = i32.size(); i32.insert(i32.end(), st.rel.begin(), st.rel.end());
-    f.osz = i64.size(); i64.insert(i64.end(), st.out_size.begin(), st.out_size.end());
-    f.rsz = i64.size(); i64.insert(i64.end(), st.rel_size.begin(), st.rel_size.end());
-    offs.push_back(f);
+  for (auto& st : P.steps) {
+    JobProgram::OpOff f{};
+    f.ins = P.i32.size(); P.i32.insert(P.i32.end(), st.ins.begin(), st.ins.end());
+    f.outs = P.i32.size(); P.i32.insert(P.i32.end(), st.outs.begin(), st.outs.end());
+    f.rel = P.i32.size(); P.i32.insert(P.i32.end(), st.rel.begin(), st.rel.end());
+    f.osz = P.i64.size(); P.i64.insert(P.i64.end(), st.out_size.begin(), st.out_size.end());
+    f.rsz = P.i64.size(); P.i64.insert(P.i64.end(), st.rel_size.begin(), st.rel_size.end());
+    P.offs.push_back(f);
   }
-  std::vector<int32_t> init_st;
-  std::vector<int64_t> init_sz;
-  std::set<int32_t> wrapped_in;
   for (size_t e = 0; e < o.ev_id.size(); ++e)
-    if (o.ev_dir[e] == 1 && o.ev_wraps[e]) wrapped_in.insert(g.store[o.ev_tensor[e]]);
-  for (int32_t t = 0; t < g.T; ++t) {
+    if (o.ev_dir[e] == 1 && o.ev_wraps[e]) P.wrapped_in.insert(g.store[o.ev_tensor[e]]);
+  for (int32_t t = 0; t < g.T; ++t) {  // initial residency (simulator.cpp:247-269)
     if (g.store[t] != t) continue;
     const int8_t k = g.kind[t];
     if (k != TSL_KIND_PARAMETER && k != TSL_KIND_INPUT && k != TSL_KIND_OUTPUT) continue;
-    if (wrapped_in.count(t)) continue;
-    init_st.push_back(t);
-    init_sz.push_back(g.size[t]);
+    if (P.wrapped_in.count(t)) continue;
+    P.init_st.push_back(t);
+    P.init_sz.push_back(g.size[t]);
   }
+  return P;
+}
+
+// Replays the plans of jobs `jis` of one build result together (the
+// reference's scheduled mode, simulator.cpp:112-569): every job's steps on
+// its own compute stream, every job's transfers on ONE copy stream (the FIFO
+// channel) in planned-arrival order, one allocator counter over all jobs
+// (plus per-job counters). A single job is the same program with one stream.
+void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>& jis, const tsl_config& cfg,
+                  const tsl_exec_config& ex, std::vector<tsl_exec_report>& per, tsl_exec_report& merged) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (ex.iterations < 1 || ex.iterations > 8) fail(TSL_ERR_ARGUMENT, "iterations must be in 1..8");
+  if (ex.tick_ns <= 0 || ex.bytes_per_unit <= 0) fail(TSL_ERR_ARGUMENT, "tick_ns and bytes_per_unit must be positive");
+  if (jis.empty()) fail(TSL_ERR_ARGUMENT, "no job to replay");
+  std::vector<JobProgram> progs;
+  for (int32_t ji : jis) {
+    if (ji < 0 || ji >= static_cast<int32_t>(r->jobs.size())) fail(TSL_ERR_ARGUMENT, "bad job index");
+    progs.push_back(make_program(r->jobs[static_cast<size_t>(ji)], cfg, ex));
+  }
+  const int nj = static_cast<int>(progs.size());
   const int iters = ex.iterations;
+  // device layout: the shared counters, then every job's block
+  struct DevOff {
+    size_t dev, ops, i32, i64, slot, res, ver, pend, opi, init, initsz, end, iter, pool;
+    size_t host;
+  };
   Layout L;
-  const size_t o_dev = L.take<ExecDevice>(1);
-  const size_t o_ops = L.take<ExecOp>(steps.size());
-  const size_t o_i32 = L.take<int32_t>(i32.size() + 1);
-  const size_t o_i64 = L.take<int64_t>(i64.size() + 1);
-  const size_t o_slot = L.take<int64_t>(g.T);
-  const size_t o_res = L.take<int32_t>(g.T);
-  const size_t o_ver = L.take<int32_t>(g.T);
-  const size_t o_pend = L.take<int32_t>(g.T);
-  const size_t o_opi = L.take<int32_t>(g.T);
-  const size_t o_init = L.take<int32_t>(init_st.size() + 1);
-  const size_t o_initsz = L.take<int64_t>(init_sz.size() + 1);
-  const size_t o_end = L.take<uint64_t>(size_t(iters) * nsteps + 1);
-  const size_t o_iter = L.take<uint64_t>(iters + 1);
-  const size_t o_pool = L.take<uint8_t>(pool_bytes + 256);
+  const size_t o_acct = L.take<ExecAcct>(1);
+  std::vector<DevOff> dof(nj);
+  int64_t host_total = 0;
+  for (int j = 0; j < nj; ++j) {
+    const JobProgram& P = progs[j];
+    const int32_t T = P.g->T;
+    DevOff& f = dof[j];
+    f.dev = L.take<ExecDevice>(1);
+    f.ops = L.take<ExecOp>(P.steps.size());
+    f.i32 = L.take<int32_t>(P.i32.size() + 1);
+    f.i64 = L.take<int64_t>(P.i64.size() + 1);
+    f.slot = L.take<int64_t>(T);
+    f.res = L.take<int32_t>(T);
+    f.ver = L.take<int32_t>(T);
+    f.pend = L.take<int32_t>(T);
+    f.opi = L.take<int32_t>(T);
+    f.init = L.take<int32_t>(P.init_st.size() + 1);
+    f.initsz = L.take<int64_t>(P.init_sz.size() + 1);
+    f.end = L.take<uint64_t>(size_t(iters) * P.steps.size() + 1);
+    f.iter = L.take<uint64_t>(iters + 1);
+    f.host = static_cast<size_t>(host_total);
+    host_total += P.host_bytes;
+  }
+  const size_t meta_end = L.off;  // staged by the host
+  for (int j = 0; j < nj; ++j) dof[j].pool = L.take<uint8_t>(progs[j].pool_bytes + 256);
   const size_t total = L.off;
   uint8_t* dbuf = nullptr;
   uint8_t* hpin = nullptr;
-  std::vector<uint8_t> stage(o_pool, 0);
+  std::vector<uint8_t> stage(meta_end, 0);
   std::vector<cudaEvent_t> events;
-  cudaStream_t cs = nullptr, xs_stream = nullptr;
-  tsl_exec_report rep{};
+  std::vector<cudaStream_t> cs(nj, nullptr);
+  cudaStream_t xs_stream = nullptr;
   auto cleanup = [&]() {
     for (auto e : events) cudaEventDestroy(e);
-    if (cs) cudaStreamDestroy(cs);
+    for (auto c : cs) if (c) cudaStreamDestroy(c);
     if (xs_stream) cudaStreamDestroy(xs_stream);
     if (dbuf) cudaFree(dbuf);
     if (hpin) cudaFreeHost(hpin);
   };
+  per.assign(nj, tsl_exec_report{});
+  merged = tsl_exec_report{};
   try {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&dbuf), total), "cudaMalloc");
-    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hpin), std::max<int64_t>(host_bytes, 256)), "cudaMallocHost");
-    cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hpin), std::max<int64_t>(host_total, 256)), "cudaMallocHost");
+    for (auto& c : cs) cuda_check(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&xs_stream, cudaStreamNonBlocking), "stream");
     auto D = [&](size_t off) { return dbuf + off; };
-    ExecDevice dev{};
-    dev.tick_ns = static_cast<uint64_t>(ex.tick_ns);
-    dev.pool = D(o_pool);
-    dev.slot_off = reinterpret_cast<const int64_t*>(D(o_slot));
-    dev.resident = reinterpret_cast<int32_t*>(D(o_res));
-    dev.version = reinterpret_cast<int32_t*>(D(o_ver));
-    dev.out_pending = reinterpret_cast<int32_t*>(D(o_pend));
-    dev.op_end_ns = reinterpret_cast<uint64_t*>(D(o_end));
-    dev.iter_start_ns = reinterpret_cast<uint64_t*>(D(o_iter));
-    std::memcpy(stage.data() + o_dev, &dev, sizeof dev);
-    for (size_t k = 0; k < steps.size(); ++k) {
-      ExecOp op{};
-      op.index = static_cast<int32_t>(k);
-      op.ticks = steps[k].ticks;
-      op.start = steps[k].start;
-      op.n_in = static_cast<int32_t>(steps[k].ins.size());
-      op.n_out = static_cast<int32_t>(steps[k].outs.size());
-      op.n_rel = static_cast<int32_t>(steps[k].rel.size());
-      op.ins = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].ins;
-      op.outs = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].outs;
-      op.rel = reinterpret_cast<const int32_t*>(D(o_i32)) + offs[k].rel;
-      op.out_size = reinterpret_cast<const int64_t*>(D(o_i64)) + offs[k].osz;
-      op.rel_size = reinterpret_cast<const int64_t*>(D(o_i64)) + offs[k].rsz;
-      std::memcpy(stage.data() + o_ops + k * sizeof(ExecOp), &op, sizeof op);
+    std::vector<ExecDevice*> dptr(nj);
+    for (int j = 0; j < nj; ++j) {
+      const JobProgram& P = progs[j];
+      const DevOff& f = dof[j];
+      ExecDevice dev{};
+      dev.acct = reinterpret_cast<ExecAcct*>(D(o_acct));
+      dev.tick_ns = static_cast<uint64_t>(ex.tick_ns);
+      dev.pool = D(f.pool);
+      dev.slot_off = reinterpret_cast<const int64_t*>(D(f.slot));
+      dev.resident = reinterpret_cast<int32_t*>(D(f.res));
+      dev.version = reinterpret_cast<int32_t*>(D(f.ver));
+      dev.out_pending = reinterpret_cast<int32_t*>(D(f.pend));
+      dev.op_end_ns = reinterpret_cast<uint64_t*>(D(f.end));
+      dev.iter_start_ns = reinterpret_cast<uint64_t*>(D(f.iter));
+      std::memcpy(stage.data() + f.dev, &dev, sizeof dev);
+      for (size_t k = 0; k < P.steps.size(); ++k) {
+        ExecOp op{};
+        op.index = static_cast<int32_t>(k);
+        op.ticks = P.steps[k].ticks;
+        op.start = P.steps[k].start;
+        op.n_in = static_cast<int32_t>(P.steps[k].ins.size());
+        op.n_out = static_cast<int32_t>(P.steps[k].outs.size());
+        op.n_rel = static_cast<int32_t>(P.steps[k].rel.size());
+        op.ins = reinterpret_cast<const int32_t*>(D(f.i32)) + P.offs[k].ins;
+        op.outs = reinterpret_cast<const int32_t*>(D(f.i32)) + P.offs[k].outs;
+        op.rel = reinterpret_cast<const int32_t*>(D(f.i32)) + P.offs[k].rel;
+        op.out_size = reinterpret_cast<const int64_t*>(D(f.i64)) + P.offs[k].osz;
+        op.rel_size = reinterpret_cast<const int64_t*>(D(f.i64)) + P.offs[k].rsz;
+        std::memcpy(stage.data() + f.ops + k * sizeof(ExecOp), &op, sizeof op);
+      }
+      if (!P.i32.empty()) std::memcpy(stage.data() + f.i32, P.i32.data(), P.i32.size() * 4);
+      if (!P.i64.empty()) std::memcpy(stage.data() + f.i64, P.i64.data(), P.i64.size() * 8);
+      std::memcpy(stage.data() + f.slot, P.slot_off.data(), P.slot_off.size() * 8);
+      std::memcpy(stage.data() + f.opi, P.outs_per_iter.data(), P.outs_per_iter.size() * 4);
+      if (!P.init_st.empty()) std::memcpy(stage.data() + f.init, P.init_st.data(), P.init_st.size() * 4);
+      if (!P.init_sz.empty()) std::memcpy(stage.data() + f.initsz, P.init_sz.data(), P.init_sz.size() * 8);
+      dptr[j] = reinterpret_cast<ExecDevice*>(D(f.dev));
     }
-    if (!i32.empty()) std::memcpy(stage.data() + o_i32, i32.data(), i32.size() * 4);
-    if (!i64.empty()) std::memcpy(stage.data() + o_i64, i64.data(), i64.size() * 8);
-    std::memcpy(stage.data() + o_slot, slot_off.data(), slot_off.size() * 8);
-    std::memcpy(stage.data() + o_opi, outs_per_iter.data(), outs_per_iter.size() * 4);
-    if (!init_st.empty()) std::memcpy(stage.data() + o_init, init_st.data(), init_st.size() * 4);
-    if (!init_sz.empty()) std::memcpy(stage.data() + o_initsz, init_sz.data(), init_sz.size() * 8);
-    cuda_check(cudaMemcpy(dbuf, stage.data(), o_pool, cudaMemcpyHostToDevice), "H2D");
-    cuda_check(cudaMemset(D(o_pool), 0, pool_bytes + 256), "memset");
-    ExecDevice* d = reinterpret_cast<ExecDevice*>(D(o_dev));
+    cuda_check(cudaMemcpy(dbuf, stage.data(), meta_end, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemset(D(dof[0].pool), 0, total - dof[0].pool), "memset");
     auto ev = [&]() {
       cudaEvent_t e;
       cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -1597,90 +1646,170 @@ tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl
       return e;
     };
     int kernels = 0;
-    cuda_check(exec_launch_init(d, reinterpret_cast<const int32_t*>(D(o_init)),
-                                reinterpret_cast<const int64_t*>(D(o_initsz)), static_cast<int>(init_st.size()), cs),
-               "init");
-    ++kernels;
-    for (int32_t s : wrapped_in) {
-      cuda_check(exec_launch_host_tag(d, s, hpin + host_off[s], cs), "host tag");
+    // per job: initial residency and host tags, then the replay's events
+    struct JobRun {
+      std::vector<cudaEvent_t> op_end, in_done;
+      cudaEvent_t it_start, xfer_tail;
+    };
+    std::vector<JobRun> run(nj);
+    std::vector<cudaEvent_t> readies;
+    for (int j = 0; j < nj; ++j) {
+      const JobProgram& P = progs[j];
+      cuda_check(exec_launch_init(dptr[j], reinterpret_cast<const int32_t*>(D(dof[j].init)),
+                                  reinterpret_cast<const int64_t*>(D(dof[j].initsz)),
+                                  static_cast<int>(P.init_st.size()), cs[j]), "init");
       ++kernels;
+      for (int32_t s : P.wrapped_in) {
+        cuda_check(exec_launch_host_tag(dptr[j], s, hpin + dof[j].host + P.host_off[s], cs[j]), "host tag");
+        ++kernels;
+      }
+      cudaEvent_t ready = ev();
+      cuda_check(cudaEventRecord(ready, cs[j]), "event");
+      cuda_check(cudaStreamWaitEvent(xs_stream, ready, 0), "wait");
+      readies.push_back(ready);
+      run[j].op_end.resize(P.steps.size());
+      for (auto& e : run[j].op_end) e = ev();
+      run[j].in_done.resize(P.xs.size());
+      for (auto& e : run[j].in_done) e = ev();
+      run[j].it_start = ev();
+      run[j].xfer_tail = ev();
     }
-    cudaEvent_t ready = ev();
-    cuda_check(cudaEventRecord(ready, cs), "event");
-    cuda_check(cudaStreamWaitEvent(xs_stream, ready, 0), "wait");
-    std::vector<cudaEvent_t> op_end(static_cast<size_t>(nsteps));
-    for (auto& e : op_end) e = ev();
-    std::vector<cudaEvent_t> in_done(xs.size());
-    for (auto& e : in_done) e = ev();
-    cudaEvent_t it_start = ev(), xfer_tail = ev();
-    for (int it = 0; it < iters; ++it) {
-      cuda_check(exec_launch_iter_begin(d, reinterpret_cast<const int32_t*>(D(o_opi)), g.T, it, cs), "iter");
-      ++kernels;
-      cuda_check(cudaEventRecord(it_start, cs), "event");
-      const int base = it * nsteps;
-      size_t xi = 0;
-      auto enqueue_xfer = [&](const ExecXferH& t, size_t idx) {
-        cuda_check(cudaStreamWaitEvent(xs_stream, t.anchor < 0 ? it_start : op_end[static_cast<size_t>(t.anchor)], 0),
+    // every job starts once every job's initial state is on the device
+    for (int j = 0; j < nj; ++j)
+      for (auto e : readies) cuda_check(cudaStreamWaitEvent(cs[j], e, 0), "wait");
+    // each job's action list in its single-job order, with planned global times
+    enum { A_BEGIN, A_XFER, A_OP, A_END };
+    struct Act { int kind; int it; int idx; int64_t time; };
+    std::vector<std::vector<Act>> acts(nj);
+    for (int j = 0; j < nj; ++j) {
+      const JobProgram& P = progs[j];
+      const int32_t nsteps = static_cast<int32_t>(P.steps.size());
+      for (int it = 0; it < iters; ++it) {
+        const int64_t base = int64_t(it) * P.period;
+        acts[j].push_back({A_BEGIN, it, -1, base});
+        size_t xi = 0;
+        for (int32_t k = 0; k < nsteps; ++k) {
+          while (xi < P.xs.size() && P.xs[xi].arrival <= P.steps[static_cast<size_t>(k)].start && P.xs[xi].anchor < k) {
+            acts[j].push_back({A_XFER, it, static_cast<int>(xi), base + P.xs[xi].arrival});
+            ++xi;
+          }
+          acts[j].push_back({A_OP, it, k, base + P.steps[static_cast<size_t>(k)].start});
+        }
+        for (; xi < P.xs.size(); ++xi) acts[j].push_back({A_XFER, it, static_cast<int>(xi), base + P.xs[xi].arrival});
+        acts[j].push_back({A_END, it, -1, base + P.period});
+      }
+    }
+    // merge the jobs' lists by planned time (ties: job order); enqueue
+    std::vector<size_t> head(nj, 0);
+    std::vector<std::vector<char>> enq(nj);
+    for (int j = 0; j < nj; ++j) enq[j].assign(progs[j].xs.size(), 0);
+    for (;;) {
+      int bj = -1;
+      for (int j = 0; j < nj; ++j)
+        if (head[j] < acts[j].size() && (bj < 0 || acts[j][head[j]].time < acts[bj][head[bj]].time)) bj = j;
+      if (bj < 0) break;
+      const Act a = acts[bj][head[bj]++];
+      const JobProgram& P = progs[bj];
+      JobRun& R = run[bj];
+      ExecDevice* d = dptr[bj];
+      const int nsteps = static_cast<int>(P.steps.size());
+      const int base = a.it * nsteps;
+      if (a.kind == A_BEGIN) {
+        std::fill(enq[bj].begin(), enq[bj].end(), 0);
+        cuda_check(exec_launch_iter_begin(d, reinterpret_cast<const int32_t*>(D(dof[bj].opi)), P.g->T, a.it, cs[bj]),
+                   "iter");
+        ++kernels;
+        cuda_check(cudaEventRecord(R.it_start, cs[bj]), "event");
+      } else if (a.kind == A_XFER) {
+        const ExecXferH& t = P.xs[static_cast<size_t>(a.idx)];
+        cuda_check(cudaStreamWaitEvent(xs_stream, t.anchor < 0 ? R.it_start : R.op_end[static_cast<size_t>(t.anchor)], 0),
                    "wait");
-        cuda_check(exec_launch_delay(d, t.anchor < 0 ? -1 : base + t.anchor, it, t.delta, xs_stream), "delay");
+        cuda_check(exec_launch_delay(d, t.anchor < 0 ? -1 : base + t.anchor, a.it, t.delta, xs_stream), "delay");
         const size_t nbytes = static_cast<size_t>(t.size * ex.bytes_per_unit);
-        uint8_t* dev_slot = D(o_pool) + slot_off[t.storage];
-        uint8_t* host_slot = hpin + host_off[t.storage];
+        uint8_t* dev_slot = D(dof[bj].pool) + P.slot_off[t.storage];
+        uint8_t* host_slot = hpin + dof[bj].host + P.host_off[t.storage];
         if (t.dir == 0) {
           cuda_check(cudaMemcpyAsync(host_slot, dev_slot, nbytes, cudaMemcpyDeviceToHost, xs_stream), "D2H");
-          rep.bytes_d2h += static_cast<int64_t>(nbytes);
+          per[bj].bytes_d2h += static_cast<int64_t>(nbytes);
         } else {
           cuda_check(cudaMemcpyAsync(dev_slot, host_slot, nbytes, cudaMemcpyHostToDevice, xs_stream), "H2D");
-          rep.bytes_h2d += static_cast<int64_t>(nbytes);
+          per[bj].bytes_h2d += static_cast<int64_t>(nbytes);
         }
         cuda_check(exec_launch_done(d, t.storage, t.size, t.dur, t.dir, xs_stream), "done");
         kernels += 2;
-        if (t.dir == 1) cuda_check(cudaEventRecord(in_done[idx], xs_stream), "event");
-      };
-      for (int32_t k = 0; k < nsteps; ++k) {
-        // transfers that arrive by this step's start and whose anchor is already enqueued
-        while (xi < xs.size() && xs[xi].arrival <= steps[static_cast<size_t>(k)].start && xs[xi].anchor < k) {
-          enqueue_xfer(xs[xi], xi);
-          ++xi;
-        }
-        for (size_t q = 0; q < xs.size(); ++q)  // swap-ins serving this step
-          if (xs[q].serve_step == k && q < xi) cuda_check(cudaStreamWaitEvent(cs, in_done[q], 0), "wait");
-        cuda_check(exec_launch_op(d, reinterpret_cast<const ExecOp*>(D(o_ops)) + k, base, it, cs), "op");
+        if (t.dir == 1) cuda_check(cudaEventRecord(R.in_done[static_cast<size_t>(a.idx)], xs_stream), "event");
+        enq[bj][static_cast<size_t>(a.idx)] = 1;
+      } else if (a.kind == A_OP) {
+        for (size_t q = 0; q < P.xs.size(); ++q)  // swap-ins serving this step, already on the channel
+          if (P.xs[q].serve_step == a.idx && enq[bj][q]) cuda_check(cudaStreamWaitEvent(cs[bj], R.in_done[q], 0), "wait");
+        cuda_check(exec_launch_op(d, reinterpret_cast<const ExecOp*>(D(dof[bj].ops)) + a.idx, base, a.it, cs[bj]), "op");
         ++kernels;
-        cuda_check(cudaEventRecord(op_end[static_cast<size_t>(k)], cs), "event");
+        cuda_check(cudaEventRecord(R.op_end[static_cast<size_t>(a.idx)], cs[bj]), "event");
+      } else {
+        // the iteration ends when its transfers are done (simulator.cpp:478-484)
+        cuda_check(cudaEventRecord(R.xfer_tail, xs_stream), "event");
+        cuda_check(cudaStreamWaitEvent(cs[bj], R.xfer_tail, 0), "wait");
+        if (nj == 1)  // a lone job's channel also waits for its iteration (the channel is its own)
+          cuda_check(cudaStreamWaitEvent(xs_stream, R.op_end[static_cast<size_t>(nsteps - 1)], 0), "wait");
       }
-      for (; xi < xs.size(); ++xi) enqueue_xfer(xs[xi], xi);
-      // the iteration ends when its transfers are done (simulator.cpp:478-484)
-      cuda_check(cudaEventRecord(xfer_tail, xs_stream), "event");
-      cuda_check(cudaStreamWaitEvent(cs, xfer_tail, 0), "wait");
-      cuda_check(cudaStreamWaitEvent(xs_stream, op_end[static_cast<size_t>(nsteps - 1)], 0), "wait");
     }
-    cuda_check(exec_launch_iter_begin(d, reinterpret_cast<const int32_t*>(D(o_opi)), 0, iters, cs), "iter");
-    ++kernels;
-    cuda_check(cudaStreamSynchronize(cs), "sync");
+    for (int j = 0; j < nj; ++j) {
+      cuda_check(exec_launch_iter_begin(dptr[j], reinterpret_cast<const int32_t*>(D(dof[j].opi)), 0, iters, cs[j]),
+                 "iter");
+      ++kernels;
+    }
+    for (auto c : cs) cuda_check(cudaStreamSynchronize(c), "sync");
     cuda_check(cudaStreamSynchronize(xs_stream), "sync");
-    ExecDevice out{};
-    cuda_check(cudaMemcpy(&out, d, sizeof out, cudaMemcpyDeviceToHost), "D2H");
-    std::vector<uint64_t> starts(iters + 1);
-    cuda_check(cudaMemcpy(starts.data(), D(o_iter), starts.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-    rep.predicted_peak = o.st.peak;
-    rep.hwm = out.hwm;
-    rep.final_footprint = out.footprint;
-    rep.iterations = iters;
-    for (int it = 0; it < iters; ++it) rep.iteration_ms[it] = double(starts[it + 1] - starts[it]) / 1e6;
-    rep.planned_iteration_ms = double(clock) * double(ex.tick_ns) / 1e6;
-    rep.swap_outs = out.n_out;
-    rep.swap_ins = out.n_in;
-    rep.verify_errors = out.verify_errors;
-    rep.violations = out.violations;
-    rep.kernels = kernels;
+    ExecAcct acct{};
+    cuda_check(cudaMemcpy(&acct, D(o_acct), sizeof acct, cudaMemcpyDeviceToHost), "D2H");
+    for (int j = 0; j < nj; ++j) {
+      const JobProgram& P = progs[j];
+      ExecDevice out{};
+      cuda_check(cudaMemcpy(&out, dptr[j], sizeof out, cudaMemcpyDeviceToHost), "D2H");
+      std::vector<uint64_t> starts(iters + 1);
+      cuda_check(cudaMemcpy(starts.data(), D(dof[j].iter), starts.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+      tsl_exec_report& rep = per[j];
+      rep.predicted_peak = P.o->st.peak;
+      rep.hwm = out.hwm;
+      rep.final_footprint = out.footprint;
+      rep.iterations = iters;
+      for (int it = 0; it < iters; ++it) rep.iteration_ms[it] = double(starts[it + 1] - starts[it]) / 1e6;
+      rep.planned_iteration_ms = double(P.period) * double(ex.tick_ns) / 1e6;
+      rep.swap_outs = out.n_out;
+      rep.swap_ins = out.n_in;
+      rep.verify_errors = out.verify_errors;
+      rep.violations = out.violations;
+      merged.predicted_peak += rep.predicted_peak;
+      merged.swap_outs += rep.swap_outs;
+      merged.swap_ins += rep.swap_ins;
+      merged.bytes_d2h += rep.bytes_d2h;
+      merged.bytes_h2d += rep.bytes_h2d;
+      merged.verify_errors += rep.verify_errors;
+      merged.violations += rep.violations;
+      merged.planned_iteration_ms = std::max(merged.planned_iteration_ms, rep.planned_iteration_ms);
+      for (int it = 0; it < iters; ++it) merged.iteration_ms[it] = std::max(merged.iteration_ms[it], rep.iteration_ms[it]);
+    }
+    merged.hwm = acct.hwm;
+    merged.final_footprint = acct.footprint;
+    merged.iterations = iters;
+    merged.kernels = kernels;
+    for (auto& rep : per) rep.kernels = kernels;
   } catch (...) {
     cleanup();
     throw;
   }
   cleanup();
-  rep.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return rep;
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  merged.total_ms = ms;
+  for (auto& rep : per) rep.total_ms = ms;
+}
+
+tsl_exec_report execute(tsl_ctx* ctx, const tsl_result* r, int32_t ji, const tsl_config& cfg,
+                        const tsl_exec_config& ex) {
+  std::vector<tsl_exec_report> per;
+  tsl_exec_report merged{};
+  execute_jobs(ctx, r, {ji}, cfg, ex, per, merged);
+  return per[0];
 }
 
 }  // namespace
@@ -1697,6 +1826,18 @@ int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_c
                      const tsl_exec_config* ex, tsl_exec_report* out) {
   if (!ctx || !r || !cfg || !ex || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] { *out = execute(ctx, r, job, *cfg, *ex); });
+}
+
+int tsl_execute_plans(tsl_ctx* ctx, const tsl_result* r, const tsl_config* cfg, const tsl_exec_config* ex,
+                      tsl_exec_report* per_job, tsl_exec_report* merged) {
+  if (!ctx || !r || !cfg || !ex || !per_job || !merged) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
+  return guard([&] {
+    std::vector<int32_t> jis(r->jobs.size());
+    for (size_t k = 0; k < jis.size(); ++k) jis[k] = static_cast<int32_t>(k);
+    std::vector<tsl_exec_report> per;
+    execute_jobs(ctx, r, jis, *cfg, *ex, per, *merged);
+    for (size_t k = 0; k < per.size(); ++k) per_job[k] = per[k];
+  });
 }
 
 }  // extern "C"

@@ -76,6 +76,8 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     L.tsl_free.argtypes = [vp]
     L.tsl_execute_plan.argtypes = [vp, vp, C.c_int32, C.POINTER(abi.TslConfig), C.POINTER(abi.TslExecConfig),
                                    C.POINTER(abi.TslExecReport)]
+    L.tsl_execute_plans.argtypes = [vp, vp, C.POINTER(abi.TslConfig), C.POINTER(abi.TslExecConfig),
+                                    C.POINTER(abi.TslExecReport), C.POINTER(abi.TslExecReport)]
     _libs[path] = L
     return L
 
@@ -277,6 +279,41 @@ class Planner:
                 d = {f: getattr(rep, f) for f, _ in abi.TslExecReport._fields_}
                 d["iteration_ms"] = list(rep.iteration_ms)[: rep.iterations]
                 out["exec"][v.job_id.decode()] = d
+        finally:
+            self.lib.tsl_result_destroy(res)
+        return out
+
+    def build_and_execute_all(self, jobs: Sequence, config: dict, tick_ns: int = 1000, iterations: int = 3,
+                              bytes_per_unit: int = 16) -> dict:
+        """build_plan, then replay ALL jobs' plans together on the device (one
+        compute stream per job, one FIFO copy stream, one allocator):
+        {"plan": build_plan dict, "exec": {job_id: report}, "merged": report}."""
+        descs, arr = abi.pack_jobs(jobs, config.get("max_swap_ratios"))
+        cfg = abi.make_config(**config)
+        res = C.c_void_p()
+        rc = self.lib.tsl_build_plan(self._ctx, arr, len(descs), C.byref(cfg), C.byref(res))
+        if rc:
+            _raise(self.lib, rc)
+
+        def as_dict(rep):
+            d = {f: getattr(rep, f) for f, _ in abi.TslExecReport._fields_}
+            d["iteration_ms"] = list(rep.iteration_ms)[: rep.iterations]
+            return d
+
+        try:
+            out = {"plan": _collect(self.lib, res, descs), "exec": {}}
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit)
+            n = self.lib.tsl_result_n_jobs(res)
+            per = (abi.TslExecReport * max(1, n))()
+            merged = abi.TslExecReport()
+            rc = self.lib.tsl_execute_plans(self._ctx, res, C.byref(cfg), C.byref(ex), per, C.byref(merged))
+            if rc:
+                _raise(self.lib, rc)
+            for i in range(n):
+                v = abi.TslJobView()
+                self.lib.tsl_result_job(res, i, C.byref(v))
+                out["exec"][v.job_id.decode()] = as_dict(per[i])
+            out["merged"] = as_dict(merged)
         finally:
             self.lib.tsl_result_destroy(res)
         return out

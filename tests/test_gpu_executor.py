@@ -43,3 +43,28 @@ def test_replay_with_recomputation(planner):
     r = out["exec"]["resnet50"]
     assert r["verify_errors"] == 0 and r["violations"] == 0
     assert r["hwm"] == r["predicted_peak"]
+
+
+@pytest.mark.parametrize("name", ["C3", "C5s0"])
+def test_multi_job_replay(planner, name):
+    """All jobs of a build replayed together (the reference's scheduled mode
+    over several SimJobs): one compute stream per job, one FIFO copy stream,
+    one allocator. Data stays intact, no release of a non-resident storage,
+    and the global high-water mark stays within the merged predicted peak
+    (the reference's own C3 simulation: 76,496 <= 81,920)."""
+    from paper_2105_13336_b200 import configs as CF
+    from paper_2105_13336_b200 import multigpu as MG
+    if name == "C3":
+        req = CF.requests("C3")[-1]
+        jobs, cfg = req.jobs, req.config(CF.INITIAL_PEAK)
+    else:
+        peaks = MG.initial_peaks(planner, [0])
+        reqs = MG.shard_requests(0, peaks)
+        _, jobs, cfg = reqs[7]  # the shard's fullest replan (8 resident workloads)
+    out = planner.build_and_execute_all(jobs, cfg, tick_ns=2000, iterations=2)
+    m = out["merged"]
+    assert m["verify_errors"] == 0 and m["violations"] == 0
+    assert m["predicted_peak"] == out["plan"]["final_merged_peak"]
+    assert 0 < m["hwm"] <= m["predicted_peak"], (m["hwm"], m["predicted_peak"])
+    assert m["swap_outs"] == m["swap_ins"] > 0
+    assert len(out["exec"]) == len(jobs)

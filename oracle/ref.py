@@ -106,3 +106,14 @@ def analyze_job(graph, latencies, plan) -> dict:
     req = json.dumps({"graph": graph, "latencies": latencies, "plan": plan})
     _check(lib().ref_analyze_job(req.encode(), ctypes.byref(out)))
     return json.loads(_take(out))
+
+
+def plan_scenario(document: str, base_dir: str):
+    """The reference CLI's `plan` (load_scenario + plan_scenario):
+    (plans.json text, peaks.json text, diagnostic)."""
+    L = lib()
+    L.ref_plan_scenario.argtypes = [ctypes.c_char_p, ctypes.c_char_p] + [ctypes.POINTER(ctypes.c_void_p)] * 3
+    p, k, d = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _check(L.ref_plan_scenario(document.encode(), base_dir.encode(), ctypes.byref(p), ctypes.byref(k),
+                               ctypes.byref(d)))
+    return _take(p), _take(k), _take(d)

@@ -21,6 +21,7 @@
 #include "memsched/orchestrator.hpp"
 #include "memsched/peak.hpp"
 #include "memsched/plan.hpp"
+#include "memsched/scenario.hpp"
 #include "memsched/simulator.hpp"
 #include "memsched/swap_planner.hpp"
 #include "memsched/workload.hpp"
@@ -210,6 +211,28 @@ int ref_analyze_job(const char* request, char** out_json) {
     SchedulingPlan plan = plans.at(g.job_id());
     PeakReport rep = analyze_job(ctx.seq, plan, ctx.catalog);
     *out_json = dup(rep.to_json());
+  });
+}
+
+// The reference CLI's `plan` subcommand (tools/memsched_cli.cpp:136-153):
+// load_scenario + plan_scenario, outputs formatted exactly as the CLI writes
+// plans.json / peaks.json; *diag = plan_diagnostic.
+int ref_plan_scenario(const char* document, const char* base_dir, char** plans_json, char** peaks_json,
+                      char** diag) {
+  return guarded([&] {
+    ScenarioConfig cfg = load_scenario(document, base_dir);
+    ScenarioResult result = plan_scenario(cfg);
+    *plans_json = dup(save_plans(result.plans));
+    std::string o = "{\n";
+    bool first = true;
+    for (const auto& [job, rep] : result.peak_reports) {
+      if (!first) o += ",\n";
+      first = false;
+      o += "\"" + job + "\": " + rep.to_json();
+    }
+    o += "}\n";
+    *peaks_json = dup(o);
+    *diag = dup(result.plan_diagnostic);
   });
 }
 

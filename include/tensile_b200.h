@@ -244,6 +244,9 @@ typedef struct tsl_exec_config {
   int64_t tick_ns;        /* device ns per planner tick (default 1000)      */
   int32_t iterations;     /* iterations replayed, 1..8 (default 3)           */
   int64_t bytes_per_unit; /* device/host bytes per planner byte (default 16) */
+  int32_t vanilla;        /* 1: replay without the scheduler -- release at last
+                             use (activity analysis), no swaps, no recomputation
+                             (the reference's vanilla mode, the MSR/EOR/CBR base) */
 } tsl_exec_config;
 
 typedef struct tsl_exec_report {

@@ -86,7 +86,8 @@ class TslStats(C.Structure):
 
 
 class TslExecConfig(C.Structure):
-    _fields_ = [("tick_ns", C.c_int64), ("iterations", C.c_int32), ("bytes_per_unit", C.c_int64)]
+    _fields_ = [("tick_ns", C.c_int64), ("iterations", C.c_int32), ("bytes_per_unit", C.c_int64),
+                ("vanilla", C.c_int32)]
 
 
 class TslExecReport(C.Structure):

@@ -1433,11 +1433,19 @@ JobProgram make_program(const JobOut& o, const tsl_config& cfg, const tsl_exec_c
     }
   }
   std::set<int64_t> flags(o.flags.begin(), o.flags.end());
+  const bool vanilla = ex.vanilla != 0;
+  if (vanilla) {  // activity analysis only (access.cpp:61-78): the last access of every Interim tensor id
+    flags.clear();
+    std::vector<int32_t> last(g.T, -1);
+    for (size_t a = 0; a < acc_tensor.size(); ++a) last[acc_tensor[a]] = static_cast<int32_t>(a);
+    for (int32_t t = 0; t < g.T; ++t)
+      if (last[t] >= 0 && g.kind[t] == TSL_KIND_INTERIM) flags.insert(last[t]);
+  }
   // steps: recompute regenerations right before their target op, then the op
   std::vector<int32_t> op_step(g.O, -1);
   int64_t clock = 0;
   for (int32_t op : g.topo) {
-    for (size_t k = 0; k < o.rc_id.size(); ++k) {
+    for (size_t k = 0; k < (vanilla ? 0 : o.rc_id.size()); ++k) {
       if (acc_op[static_cast<size_t>(o.rc_target[k])] != op) continue;
       ExecStepH st{};
       st.op = o.rc_regen[k];
@@ -1477,7 +1485,7 @@ JobProgram make_program(const JobOut& o, const tsl_config& cfg, const tsl_exec_c
   P.period = clock;
   // transfers of one iteration, in channel (arrival) order
   P.outs_per_iter.assign(g.T, 0);
-  for (size_t e = 0; e < o.ev_id.size(); ++e) {
+  for (size_t e = 0; e < (vanilla ? 0 : o.ev_id.size()); ++e) {
     ExecXferH t{};
     t.ev = static_cast<int32_t>(e);
     t.storage = g.store[o.ev_tensor[e]];
@@ -1514,7 +1522,7 @@ JobProgram make_program(const JobOut& o, const tsl_config& cfg, const tsl_exec_c
     f.rsz = P.i64.size(); P.i64.insert(P.i64.end(), st.rel_size.begin(), st.rel_size.end());
     P.offs.push_back(f);
   }
-  for (size_t e = 0; e < o.ev_id.size(); ++e)
+  for (size_t e = 0; e < (vanilla ? 0 : o.ev_id.size()); ++e)
     if (o.ev_dir[e] == 1 && o.ev_wraps[e]) P.wrapped_in.insert(g.store[o.ev_tensor[e]]);
   for (int32_t t = 0; t < g.T; ++t) {  // initial residency (simulator.cpp:247-269)
     if (g.store[t] != t) continue;
@@ -1769,7 +1777,7 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
       std::vector<uint64_t> starts(iters + 1);
       cuda_check(cudaMemcpy(starts.data(), D(dof[j].iter), starts.size() * 8, cudaMemcpyDeviceToHost), "D2H");
       tsl_exec_report& rep = per[j];
-      rep.predicted_peak = P.o->st.peak;
+      rep.predicted_peak = ex.vanilla ? -1 : P.o->st.peak;  // vanilla: no per-job prediction in the result
       rep.hwm = out.hwm;
       rep.final_footprint = out.footprint;
       rep.iterations = iters;
@@ -1779,7 +1787,7 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
       rep.swap_ins = out.n_in;
       rep.verify_errors = out.verify_errors;
       rep.violations = out.violations;
-      merged.predicted_peak += rep.predicted_peak;
+      if (!ex.vanilla) merged.predicted_peak += rep.predicted_peak;
       merged.swap_outs += rep.swap_outs;
       merged.swap_ins += rep.swap_ins;
       merged.bytes_d2h += rep.bytes_d2h;
@@ -1789,6 +1797,8 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
       merged.planned_iteration_ms = std::max(merged.planned_iteration_ms, rep.planned_iteration_ms);
       for (int it = 0; it < iters; ++it) merged.iteration_ms[it] = std::max(merged.iteration_ms[it], rep.iteration_ms[it]);
     }
+    if (ex.vanilla)  // the release-at-last-use plan's merged peak: the history's first entry
+      merged.predicted_peak = r->history.empty() ? -1 : r->history[0];
     merged.hwm = acct.hwm;
     merged.final_footprint = acct.footprint;
     merged.iterations = iters;
@@ -1820,6 +1830,7 @@ void tsl_exec_config_default(tsl_exec_config* c) {
   c->tick_ns = 1000;
   c->iterations = 3;
   c->bytes_per_unit = 16;
+  c->vanilla = 0;
 }
 
 int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_config* cfg,

@@ -268,7 +268,7 @@ class Planner:
             _raise(self.lib, rc)
         try:
             out = {"plan": _collect(self.lib, res, descs), "exec": {}}
-            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit)
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 0)
             for i in range(self.lib.tsl_result_n_jobs(res)):
                 rep = abi.TslExecReport()
                 rc = self.lib.tsl_execute_plan(self._ctx, res, i, C.byref(cfg), C.byref(ex), C.byref(rep))
@@ -284,7 +284,7 @@ class Planner:
         return out
 
     def build_and_execute_all(self, jobs: Sequence, config: dict, tick_ns: int = 1000, iterations: int = 3,
-                              bytes_per_unit: int = 16) -> dict:
+                              bytes_per_unit: int = 16, vanilla: bool = False) -> dict:
         """build_plan, then replay ALL jobs' plans together on the device (one
         compute stream per job, one FIFO copy stream, one allocator):
         {"plan": build_plan dict, "exec": {job_id: report}, "merged": report}."""
@@ -302,7 +302,7 @@ class Planner:
 
         try:
             out = {"plan": _collect(self.lib, res, descs), "exec": {}}
-            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit)
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 1 if vanilla else 0)
             n = self.lib.tsl_result_n_jobs(res)
             per = (abi.TslExecReport * max(1, n))()
             merged = abi.TslExecReport()
@@ -331,3 +331,28 @@ class Planner:
             self.lib.tsl_result_destroy(res)
         jid = graph["job_id"]
         return {"report": out["jobs"][jid]["report"], "report_json": out["reports_json"][jid]}
+
+
+def replay_metrics(vanilla: dict, scheduled: dict) -> dict:
+    """compute_metrics (simulator.cpp:598-632) on two device replays of the
+    same build (build_and_execute_all with vanilla=True / False): memory
+    saving ratio MSR = (vanilla peak - scheduled peak) / vanilla peak, extra
+    overhead ratio EOR = (scheduled time - vanilla time) / vanilla time, where
+    a replay's time is the sum over jobs of its mean iteration time, and
+    CBR = MSR / EOR (inf when EOR == 0). Peaks are the device allocator's
+    high-water marks, times the measured iteration times."""
+    if set(vanilla["exec"]) != set(scheduled["exec"]):
+        raise PlannerError(abi.TSL_ERR_ARGUMENT, "traces cover different job sets")
+
+    def time_cost(out):
+        return sum(sum(r["iteration_ms"]) / len(r["iteration_ms"]) for r in out["exec"].values() if r["iteration_ms"])
+
+    vmp, emp = float(vanilla["merged"]["hwm"]), float(scheduled["merged"]["hwm"])
+    vtc, etc = time_cost(vanilla), time_cost(scheduled)
+    if vmp <= 0:
+        raise PlannerError(abi.TSL_ERR_ARGUMENT, "vanilla peak must be positive")
+    if vtc <= 0:
+        raise PlannerError(abi.TSL_ERR_ARGUMENT, "vanilla time cost must be positive")
+    msr = (vmp - emp) / vmp
+    eor = (etc - vtc) / vtc
+    return {"msr": msr, "eor": eor, "cbr": float("inf") if eor == 0 else msr / eor}

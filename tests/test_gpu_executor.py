@@ -68,3 +68,29 @@ def test_multi_job_replay(planner, name):
     assert 0 < m["hwm"] <= m["predicted_peak"], (m["hwm"], m["predicted_peak"])
     assert m["swap_outs"] == m["swap_ins"] > 0
     assert len(out["exec"]) == len(jobs)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_vanilla_replay_and_metrics(planner, name):
+    """The reference's vanilla mode (no scheduler: release at last use, no
+    swaps) replayed on the device reaches the planner's initial merged peak;
+    MSR / EOR / CBR (compute_metrics, simulator.cpp:598-632) against the
+    scheduled replay of the same build."""
+    from paper_2105_13336_b200 import configs as CF
+    from paper_2105_13336_b200.planner import replay_metrics
+    req = CF.requests(name)[-1]
+    cfg = req.config(CF.INITIAL_PEAK)
+    van = planner.build_and_execute_all(req.jobs, cfg, tick_ns=2000, iterations=2, vanilla=True)
+    sch = planner.build_and_execute_all(req.jobs, cfg, tick_ns=2000, iterations=2)
+    v = van["merged"]
+    assert v["swap_outs"] == 0 and v["verify_errors"] == 0 and v["violations"] == 0
+    assert v["predicted_peak"] == van["plan"]["merged_peak_history"][0]
+    if len(req.jobs) == 1:  # one job: the analyzer's initial peak exactly
+        assert v["hwm"] == v["predicted_peak"]
+    else:  # several jobs: their peaks need not coincide (the merged peak is a sum of peaks)
+        assert 0 < v["hwm"] <= v["predicted_peak"]
+    m = replay_metrics(van, sch)
+    assert m["msr"] == pytest.approx((v["hwm"] - sch["merged"]["hwm"]) / v["hwm"])
+    assert m["msr"] > 0.2  # the budget is 70 % of the initial peak
+    if name == "C2":  # one job: the swaps hide behind compute, iterations keep their planned length
+        assert abs(m["eor"]) < 0.02

@@ -237,11 +237,17 @@ def run_ours(a, rank, world, local):
     import torch
     from paper_2105_13336_b200 import abi
     from paper_2105_13336_b200.planner import Planner
+    # TSL_BENCH_BACKEND=gloo (test only): several ranks may share one GPU, so
+    # the N>1 path (shards per rank, barriers, max over ranks, plan gather)
+    # can be exercised on a one-GPU box; the driver's runs use NCCL
+    backend = os.environ.get("TSL_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     planner = Planner(local)
     reqs = workload(a.workload, rank, planner)
     groups = [j for _, j, _ in reqs]
@@ -301,7 +307,8 @@ def run_ours(a, rank, world, local):
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / a.steps
     if dist:
-        t = torch.tensor([dev_ms, e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([dev_ms, e2e_ms], device=f"cuda:{local}" if backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms, e2e_ms = t.tolist()
     outs = prep.collect(with_views=False)

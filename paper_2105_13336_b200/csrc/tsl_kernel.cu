@@ -17,7 +17,7 @@ static_assert(CB_NB == 1024, "conflict and window index size (host allocates 4 *
 static_assert(SH_WORDS == 1024, "cooperative scalar block (host allocates 1024 words)");
 
 template <int IPT>
-using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;
+using BRS = cub::BlockRadixSort<uint64_t, NT, IPT, int32_t>;  // 4-bit digits (5/6-bit measured slower)
 using BScan = cub::BlockScan<int64_t, NT>;
 
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }

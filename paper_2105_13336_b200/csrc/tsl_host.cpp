@@ -284,6 +284,7 @@ struct GroupPlace {
   size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
   size_t coop = 0, tile_hist = 0, coop_gsh = 0, cta_part = 0;
   int64_t pr_cap, w_cap, wcap, cb_cap;
+  int32_t cb_nb = 1024;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
 };
@@ -643,7 +644,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (auto& p : P->jp[gi]) maxS = std::max<int64_t>(maxS, p.Scap);
     q.wcap = 3 * maxS + 64;
     q.wbuf = L.take<int64_t>(size_t(NT / 32) * 4 * q.wcap);
-    q.cb_idx = L.take<int32_t>(4 * 1024 + 16);  // pair-interval and window bucket tables
+    q.cb_nb = P->big ? (1 << 16) : 1024;        // buckets of the pair-interval and window indexes
+    q.cb_idx = L.take<int32_t>(4 * size_t(q.cb_nb + 2));
     q.cb_cap = std::max<int64_t>(8 * P->sort_cap, 4 * q.pr_cap);
     q.cb_ent = L.take<int32_t>(2 * size_t(q.cb_cap));
   }
@@ -707,6 +709,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->wbuf = dp<int64_t>(ctx, q.wbuf);
     G->wcap = q.wcap;
     G->cb_idx = dp<int32_t>(ctx, q.cb_idx);
+    G->cb_nb = q.cb_nb;
     G->cb_ent = dp<int32_t>(ctx, q.cb_ent);
     G->cb_cap = q.cb_cap;
     G->w_cap = q.w_cap;

@@ -13,7 +13,7 @@ namespace tsl {
 
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
 static_assert(TI_NB == TI_NB_HOST, "time index size");
-static_assert(CB_NB == 1024, "conflict and window index size (host allocates 4 * 1024 + 16)");
+static_assert(CB_NB == 1024, "conflict and window index default size (host allocates 4 * (cb_nb + 2))");
 static_assert(SH_WORDS == 1024, "cooperative scalar block (host allocates 1024 words)");
 
 template <int IPT>

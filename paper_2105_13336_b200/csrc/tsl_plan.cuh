@@ -625,6 +625,7 @@ struct ReCtx {
 constexpr int GS_PCAP = 160;    // gsh slots: per-job reserved pair slots of a pass (<= 128 jobs)
 constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in shared scratch
 constexpr int GS_WK = 440;      // gsh slot: window-index bucket shift + 1 (0: no window index this pass)
+constexpr int GS_NB = 441;      // gsh slot: bucket count of this pass's indexes
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
@@ -1676,8 +1677,9 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
           // window index (large passes): only candidates whose placement
           // windows share a bucket with a lifted copy of a new interval
           const int shb = int(wk - 1);
-          auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(CB_NB) - 1); };
-          const int32_t* wk_cnt = g.cb_idx + 2 * (CB_NB + 2);
+          const int64_t NB = x.sh[MAXB * 16 + GS_NB];
+          auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, NB - 1); };
+          const int32_t* wk_cnt = g.cb_idx + 2 * (NB + 2);
           const int32_t* wk_ent = g.cb_ent + g.cb_cap;
           for (int32_t p = 0; p < npm; ++p)
             for (int h = 0; h < 2; ++h) {
@@ -1913,18 +1915,21 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       }
     }
   } else {
-    int32_t* bk_cnt = g.cb_idx;             // [CB_NB + 1] counts -> offsets
-    int32_t* bk_cur = bk_cnt + (CB_NB + 2);  // [CB_NB] fill cursors
+    // bucket count: 1024, or the group's larger tables (big launches:
+    // weight tensors with hundreds of gap pairs would crowd 1024 buckets)
+    const int32_t NB = g.cb_nb > CB_NB ? g.cb_nb : CB_NB;
+    int32_t* bk_cnt = g.cb_idx;             // [NB + 1] counts -> offsets
+    int32_t* bk_cur = bk_cnt + (NB + 2);    // [NB] fill cursors
     int32_t* bk_ent = g.cb_ent;             // [cb_cap] candidate of each entry
     // the same buckets over every candidate's placement windows: phase C's
     // hit marking visits only the candidates whose windows share a bucket
     // with a re-scored commit
-    int32_t* wk_cnt = g.cb_idx + 2 * (CB_NB + 2);
-    int32_t* wk_cur = wk_cnt + (CB_NB + 2);
+    int32_t* wk_cnt = g.cb_idx + 2 * (NB + 2);
+    int32_t* wk_cur = wk_cnt + (NB + 2);
     int32_t* wk_ent = g.cb_ent + g.cb_cap;
     // bucket width: the largest interval end in the pass (ints are >= 0)
-    if (x.tid == 0) gsh[14] = 0;
-    for (int32_t k = x.tid; k < CB_NB + 1; k += x.nthr) { bk_cnt[k] = 0; wk_cnt[k] = 0; }
+    if (x.tid == 0) { gsh[14] = 0; gsh[GS_NB] = NB; }
+    for (int32_t k = x.tid; k < NB + 1; k += x.nthr) { bk_cnt[k] = 0; wk_cnt[k] = 0; }
     x.sync();
     for (int64_t m = x.tid; m < nc; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
@@ -1933,8 +1938,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     }
     x.sync();
     int shb = 0;
-    while ((gsh[14] >> shb) >= CB_NB) ++shb;
-    auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(CB_NB) - 1); };
+    while ((gsh[14] >> shb) >= NB) ++shb;
+    auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(NB) - 1); };
     // count
     for (int64_t m = x.tid; m < nc; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
@@ -1957,7 +1962,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     // prefix over the bucket counts: one warp, 32 buckets per lane (the
     // block scan's scratch holds the candidate records here)
     if (x.warp == 0) {
-      constexpr int PER = CB_NB / X::W;
+      const int PER = NB / X::W;
       int32_t* c = bk_cnt + 1 + x.lane * PER;
       int32_t sum = 0;
       for (int k = 0; k < PER; ++k) sum += c[k];
@@ -1966,7 +1971,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
       if (x.lane == 0) gsh[15] = tot;
     } else if (x.warp == 1) {
-      constexpr int PER = CB_NB / X::W;
+      const int PER = NB / X::W;
       int32_t* c = wk_cnt + 1 + x.lane * PER;
       int32_t sum = 0;
       for (int k = 0; k < PER; ++k) sum += c[k];
@@ -1978,12 +1983,12 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     if (X::W == 1 && x.warp == 0) {  // one-thread context: the window prefix too
       int32_t* c = wk_cnt + 1;
       int32_t off = 0;
-      for (int k = 0; k < CB_NB; ++k) { off += c[k]; c[k] = off; }
+      for (int k = 0; k < NB; ++k) { off += c[k]; c[k] = off; }
       gsh[GS_WK] = off <= g.cb_cap ? shb + 1 : 0;
     }
     x.sync();
     const bool fits = gsh[15] <= g.cb_cap;
-    for (int32_t k = x.tid; k < CB_NB; k += x.nthr) { bk_cur[k] = bk_cnt[k]; wk_cur[k] = wk_cnt[k]; }
+    for (int32_t k = x.tid; k < NB; k += x.nthr) { bk_cur[k] = bk_cnt[k]; wk_cur[k] = wk_cnt[k]; }
     x.sync();
     if (gsh[GS_WK]) {
       for (int64_t m = x.tid; m < nc; m += x.nthr) {

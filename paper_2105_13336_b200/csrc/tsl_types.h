@@ -243,6 +243,7 @@ struct GroupDev {
   int64_t pr_cap, w_cap;
   int64_t* wbuf;     // [NT/32 warps * 4 * wcap] re-scoring gather scratch
   int64_t wcap;
+  int32_t cb_nb;     // time buckets of the conflict / window indexes (1024; more for big passes)
   int32_t* cb_idx;   // [2 * CB_NB + 4] conflict-index bucket offsets / cursors
   int32_t* cb_ent;   // [cb_cap] conflict-index entries
   int64_t cb_cap;

@@ -175,8 +175,11 @@ struct DevX {
   // ---- cooperative passes (all CTAs of the launch) ----
   // L1 is not coherent across SMs: everything another CTA wrote or will read
   // moves through L2 (ld/st .cg).
-  __device__ static void spin_guard(int64_t t0) {
-    if (clock64() - t0 > (int64_t(1) << 36)) __trap();  // ~30 s at 2 GHz: fail loudly, never hang
+  // Bounded spins: fail loudly, never hang the GPU. Barriers and folds are
+  // short (~35 s bound); an idle worker waits for CTA 0's next task through a
+  // whole decision sweep (~9 min bound).
+  __device__ static void spin_guard(int64_t t0, int shift = 36) {
+    if (clock64() - t0 > (int64_t(1) << shift)) __trap();
   }
   __device__ void grid_barrier() {
     __syncthreads();
@@ -403,7 +406,7 @@ struct DevX {
       if (tid == 0) {
         volatile int32_t* ep = &coop->epoch;
         const int64_t t0 = clock64();
-        while (*ep == seen) { __nanosleep(128); spin_guard(t0); }
+        while (*ep == seen) { __nanosleep(256); spin_guard(t0, 40); }
       }
       __syncthreads();
       volatile CoopCtl* c = coop;

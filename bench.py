@@ -260,8 +260,8 @@ def run_ours(a, rank, world, local):
     torch.cuda.set_stream(stream)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
     # e2e path: the caller's packed descriptors, one C-ABI call per step
-    cfg_arr, ncfg, ratios = planner._configs(cfgs, len(groups))
-    descs, arr, offs = planner._pack_groups(groups, ratios)
+    cfg_arr, ncfg, keep = planner._configs(cfgs, len(groups))
+    descs, arr, offs = planner._pack_groups(groups)
     res = (C.c_void_p * len(groups))()
     L = planner.lib
     stats = abi.TslStats()

@@ -49,7 +49,11 @@ enum tsl_op_phase { TSL_PHASE_FORWARD_BACKWARD = 0, TSL_PHASE_OPTIMIZE = 1 };
  * "missing latency entry for op X", access.cpp:35-36). */
 #define TSL_LATENCY_MISSING INT64_MIN
 
-/* PlannerConfig (config.hpp:9-18). max_swap_ratios lives in tsl_job_desc. */
+/* PlannerConfig (config.hpp:9-18). The max_swap_ratios map is the arrays
+ * max_swap_ratio_jobs/max_swap_ratio_values (n_max_swap_ratios entries, unique
+ * job ids, any order; they need to live only for the call that takes the
+ * config). Like PlannerConfig::validate, every entry is checked, including
+ * entries naming no job of the build; a job without an entry gets 1.0. */
 typedef struct tsl_config {
   int64_t pcie_bandwidth;      /* bytes per tick, > 0          */
   int64_t transfer_setup;      /* ticks, >= 0                  */
@@ -59,12 +63,15 @@ typedef struct tsl_config {
   double stall_epsilon;        /* (0,1), default 0.0005        */
   int32_t stall_min_iters;     /* default 100                  */
   double cold_start_gpu_usage; /* default 0.5                  */
+  int32_t n_max_swap_ratios;                /* entries of the map, default 0 */
+  const char* const* max_swap_ratio_jobs;   /* [n_max_swap_ratios] job ids   */
+  const double* max_swap_ratio_values;      /* [n_max_swap_ratios], (0,1]    */
 } tsl_config;
 
 /* Fills the reference defaults (config.hpp:10-18). */
 void tsl_config_default(tsl_config* cfg);
 
-/* One job: ComputeGraph + latency table (+ its max_swap_ratios entry). */
+/* One job: ComputeGraph + latency table. */
 typedef struct tsl_job_desc {
   const char* job_id;
   int32_t n_tensors;
@@ -80,7 +87,6 @@ typedef struct tsl_job_desc {
   const int32_t* op_out_offsets; /* [n_ops+1] CSR into op_outputs    */
   const int32_t* op_outputs;     /* tensor indices, op.outputs order */
   const int64_t* op_latencies;   /* [n_ops] ticks or TSL_LATENCY_MISSING */
-  double max_swap_ratio;         /* config.max_swap_ratios[job]; <=0 means "absent" (1.0) */
 } tsl_job_desc;
 
 /* Read-only view of one job's plan + peak report inside a result. All arrays

@@ -67,7 +67,7 @@ struct PackedJob {
   std::vector<int32_t> in_off{0}, ins, out_off{0}, outs;
   tsl_job_desc desc{};
 
-  PackedJob(const ComputeGraph& g, const std::map<OpId, Tick>& latencies, const PlannerConfig& cfg) {
+  PackedJob(const ComputeGraph& g, const std::map<OpId, Tick>& latencies) {
     std::map<TensorId, int32_t> index;
     for (const auto& t : g.tensors()) {
       index.emplace(t.id, static_cast<int32_t>(tids.size()));
@@ -100,8 +100,6 @@ struct PackedJob {
     desc.op_out_offsets = out_off.data();
     desc.op_outputs = outs.data();
     desc.op_latencies = lat.data();
-    auto r = cfg.max_swap_ratios.find(g.job_id());
-    desc.max_swap_ratio = r == cfg.max_swap_ratios.end() ? 0.0 : r->second;
   }
 };
 
@@ -162,7 +160,7 @@ BuildResult build_plan(const std::vector<std::pair<ComputeGraph, std::map<OpId, 
   if (jobs.empty()) return result;
   std::vector<PackedJob> packed;
   packed.reserve(jobs.size());
-  for (const auto& [g, lat] : jobs) packed.emplace_back(g, lat, config);
+  for (const auto& [g, lat] : jobs) packed.emplace_back(g, lat);
   std::vector<tsl_job_desc> descs;
   for (const auto& p : packed) descs.push_back(p.desc);
   tsl_config cfg;
@@ -175,6 +173,15 @@ BuildResult build_plan(const std::vector<std::pair<ComputeGraph, std::map<OpId, 
   cfg.stall_epsilon = config.stall_epsilon;
   cfg.stall_min_iters = config.stall_min_iters;
   cfg.cold_start_gpu_usage = config.cold_start_gpu_usage;
+  std::vector<const char*> ratio_jobs;  // PlannerConfig::max_swap_ratios, every entry
+  std::vector<double> ratio_values;
+  for (const auto& [job, r] : config.max_swap_ratios) {
+    ratio_jobs.push_back(job.c_str());
+    ratio_values.push_back(r);
+  }
+  cfg.n_max_swap_ratios = static_cast<int32_t>(ratio_jobs.size());
+  cfg.max_swap_ratio_jobs = ratio_jobs.data();
+  cfg.max_swap_ratio_values = ratio_values.data();
   tsl_result* r = nullptr;
   const int rc = tsl_build_plan(device_context(), descs.data(), static_cast<int32_t>(descs.size()), &cfg, &r);
   if (rc != TSL_OK) rethrow(rc);

@@ -72,7 +72,6 @@ Graph load_graph(const tsl_job_desc& d) {
   g.job_id = d.job_id ? d.job_id : "";
   g.T = d.n_tensors;
   g.O = d.n_ops;
-  g.ratio = d.max_swap_ratio > 0 ? d.max_swap_ratio : 1.0;
   std::set<std::string> seen;
   for (int i = 0; i < g.T; ++i) {
     g.tid.emplace_back(d.tensor_ids[i]);
@@ -924,6 +923,12 @@ void flatten(JobOut& o) {
   o.peak_tensors.assign(o.rep.tensors.begin(), o.rep.tensors.end());
 }
 
+std::map<std::string, double> ratios(const tsl_config& c) {  // PlannerConfig::max_swap_ratios
+  std::map<std::string, double> m;
+  for (int32_t i = 0; i < c.n_max_swap_ratios; ++i) m[c.max_swap_ratio_jobs[i]] = c.max_swap_ratio_values[i];
+  return m;
+}
+
 void validate_config(const tsl_config& c) {  // config.hpp:25-35
   if (c.pcie_bandwidth <= 0) throw Invalid("pcie_bandwidth must be positive");
   if (c.transfer_setup < 0) throw Invalid("transfer_setup must be nonnegative");
@@ -931,6 +936,8 @@ void validate_config(const tsl_config& c) {  // config.hpp:25-35
   if (c.ewma_alpha < 0 || c.ewma_alpha > 1) throw Invalid("ewma_alpha out of [0,1]");
   if (c.replan_threshold <= 0) throw Invalid("replan_threshold must be positive");
   if (c.stall_epsilon <= 0 || c.stall_epsilon >= 1) throw Invalid("stall_epsilon out of (0,1)");
+  for (auto& [job, r] : ratios(c))
+    if (r <= 0 || r > 1) throw Invalid("max swap ratio for " + job + " out of (0,1]");
 }
 
 // build_plan, orchestrator.cpp:8-70.
@@ -939,8 +946,11 @@ tslo_result* build(const tsl_job_desc* descs, int n, const tsl_config& c) {
   res->graphs.reserve(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) res->graphs.push_back(load_graph(descs[i]));
   validate_config(c);
-  for (auto& g : res->graphs)
-    if (!(g.ratio > 0 && g.ratio <= 1)) throw Invalid("max swap ratio for " + g.job_id + " out of (0,1]");
+  const std::map<std::string, double> rmap = ratios(c);
+  for (auto& g : res->graphs) {  // PlannerConfig::max_swap_ratio, config.hpp:20-23
+    auto it = rmap.find(g.job_id);
+    g.ratio = it == rmap.end() ? 1.0 : it->second;
+  }
   if (n == 0) return res;
   std::vector<std::string> jids;
   for (auto& g : res->graphs) jids.push_back(g.job_id);

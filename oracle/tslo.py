@@ -86,7 +86,9 @@ def _collect(L, res, descs) -> dict:
 def build_plan(jobs, config: dict, max_swap_ratios=None) -> dict:
     """Oracle build_plan over [(graph, latencies)] -> dict (plans_json = save_plans text)."""
     L = lib()
-    descs, arr = abi.pack_jobs(jobs, max_swap_ratios or config.get("max_swap_ratios"))
+    if max_swap_ratios:
+        config = dict(config, max_swap_ratios=max_swap_ratios)
+    descs, arr = abi.pack_jobs(jobs)
     cfg = abi.make_config(**config)
     res = C.c_void_p()
     t0 = time.perf_counter()
@@ -125,7 +127,7 @@ def report_dict(report_json: str) -> dict:
 def initial_peaks(jobs) -> dict:
     """{job_id: initial peak} (make_job_context's report: empty plan, release
     at last use)."""
-    descs, arr = abi.pack_jobs(jobs, {})
+    descs, arr = abi.pack_jobs(jobs)
     out = (C.c_int64 * max(1, len(jobs)))()
     rc = lib().tslo_initial_peaks(arr, len(jobs), out)
     if rc:

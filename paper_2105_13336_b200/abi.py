@@ -37,15 +37,16 @@ _pstr = C.POINTER(C.c_char_p)
 class TslConfig(C.Structure):
     _fields_ = [("pcie_bandwidth", C.c_int64), ("transfer_setup", C.c_int64), ("memory_budget", C.c_int64),
                 ("ewma_alpha", C.c_double), ("replan_threshold", C.c_double), ("stall_epsilon", C.c_double),
-                ("stall_min_iters", C.c_int32), ("cold_start_gpu_usage", C.c_double)]
+                ("stall_min_iters", C.c_int32), ("cold_start_gpu_usage", C.c_double),
+                ("n_max_swap_ratios", C.c_int32), ("max_swap_ratio_jobs", _pstr),
+                ("max_swap_ratio_values", C.POINTER(C.c_double))]
 
 
 class TslJobDesc(C.Structure):
     _fields_ = [("job_id", C.c_char_p), ("n_tensors", C.c_int32), ("tensor_ids", _pstr),
                 ("tensor_sizes", _p64), ("tensor_kinds", _p8), ("n_ops", C.c_int32), ("op_ids", _pstr),
                 ("op_kinds", _pstr), ("op_phases", _p8), ("op_in_offsets", _p32), ("op_inputs", _p32),
-                ("op_out_offsets", _p32), ("op_outputs", _p32), ("op_latencies", _p64),
-                ("max_swap_ratio", C.c_double)]
+                ("op_out_offsets", _p32), ("op_outputs", _p32), ("op_latencies", _p64)]
 
 
 class TslJobView(C.Structure):
@@ -100,11 +101,19 @@ class TslExecReport(C.Structure):
 
 def make_config(pcie_bandwidth: int = 1, transfer_setup: int = 0, memory_budget: int = 0,
                 ewma_alpha: float = 0.3, replan_threshold: float = 0.2, stall_epsilon: float = 0.0005,
-                stall_min_iters: int = 100, cold_start_gpu_usage: float = 0.5, **_ignored) -> TslConfig:
-    """PlannerConfig (config.hpp:9-18) with the reference defaults."""
-    return TslConfig(int(pcie_bandwidth), int(transfer_setup), int(memory_budget), float(ewma_alpha),
-                     float(replan_threshold), float(stall_epsilon), int(stall_min_iters),
-                     float(cold_start_gpu_usage))
+                stall_min_iters: int = 100, cold_start_gpu_usage: float = 0.5,
+                max_swap_ratios: Optional[Dict[str, float]] = None, **_ignored) -> TslConfig:
+    """PlannerConfig (config.hpp:9-18) with the reference defaults. The
+    max_swap_ratios map's arrays stay alive with the returned struct (`_keep`)."""
+    ratios = dict(max_swap_ratios or {})
+    jobs = (C.c_char_p * max(1, len(ratios)))(*[k.encode() for k in ratios])
+    vals = (C.c_double * max(1, len(ratios)))(*[float(v) for v in ratios.values()])
+    cfg = TslConfig(int(pcie_bandwidth), int(transfer_setup), int(memory_budget), float(ewma_alpha),
+                    float(replan_threshold), float(stall_epsilon), int(stall_min_iters),
+                    float(cold_start_gpu_usage), len(ratios), C.cast(jobs, _pstr),
+                    C.cast(vals, C.POINTER(C.c_double)))
+    cfg._keep = (jobs, vals)
+    return cfg
 
 
 def _arr(values, dtype):
@@ -119,9 +128,9 @@ def _ptr(a: np.ndarray, ctype):
 
 
 class JobDesc:
-    """One (graph, latencies[, max_swap_ratio]) job packed for the C-ABI."""
+    """One (graph, latencies) job packed for the C-ABI."""
 
-    def __init__(self, graph: dict, latencies: Dict[str, int], max_swap_ratio: Optional[float] = None):
+    def __init__(self, graph: dict, latencies: Dict[str, int]):
         self.graph = graph
         tensors = graph["tensors"]
         ops = graph["ops"]
@@ -157,21 +166,19 @@ class JobDesc:
                                _ptr(self._kinds, C.c_int8), len(ops), self._oids, self._okinds,
                                _ptr(self._phases, C.c_int8), _ptr(self._ioff, C.c_int32),
                                _ptr(self._ins, C.c_int32), _ptr(self._ooff, C.c_int32),
-                               _ptr(self._outs, C.c_int32), _ptr(self._lat, C.c_int64),
-                               float(max_swap_ratio) if max_swap_ratio is not None else 0.0)
+                               _ptr(self._outs, C.c_int32), _ptr(self._lat, C.c_int64))
 
 
-def pack_jobs(jobs: Sequence[Tuple], max_swap_ratios: Optional[Dict[str, float]] = None):
+def pack_jobs(jobs: Sequence[Tuple]):
     """[(graph, latencies), ...] -> (list[JobDesc], TslJobDesc array)."""
-    ratios = max_swap_ratios or {}
     # a job object passed several times (the requests of a replan sequence)
     # is packed once: identical descriptors let the library load it once
     memo = {}
     descs = []
     for g, l in jobs:
-        key = (id(g), id(l), ratios.get(g["job_id"]))
+        key = (id(g), id(l))
         if key not in memo:
-            memo[key] = JobDesc(g, l, ratios.get(g["job_id"]))
+            memo[key] = JobDesc(g, l)
         descs.append(memo[key])
     arr = (TslJobDesc * max(1, len(descs)))(*[d.desc for d in descs])
     return descs, arr

@@ -63,8 +63,6 @@ struct Graph {
   std::vector<int8_t> kind;
   std::vector<int32_t> in_off, in, out_off, out;
   std::vector<int32_t> trank, store, upd, prod, topo;
-  double ratio = 1.0;
-  bool ratio_given = false;
 };
 
 const char* kind_name(int k) {
@@ -85,8 +83,6 @@ Graph load_graph(const tsl_job_desc& d) {
     fail(TSL_ERR_ARGUMENT, "null tensor table in job " + g.job_id);
   if (g.O > 0 && (!d.op_ids || !d.op_kinds || !d.op_phases || !d.op_in_offsets || !d.op_out_offsets))
     fail(TSL_ERR_ARGUMENT, "null op table in job " + g.job_id);
-  g.ratio_given = d.max_swap_ratio > 0 || std::isnan(d.max_swap_ratio);
-  g.ratio = g.ratio_given ? d.max_swap_ratio : 1.0;
   g.tid.reserve(g.T);
   g.size.assign(d.tensor_sizes, d.tensor_sizes + g.T);
   g.kind.assign(d.tensor_kinds, d.tensor_kinds + g.T);
@@ -243,19 +239,35 @@ void check_latencies(const Graph& g) {
   }
 }
 
-// PlannerConfig::validate, config.hpp:25-35.
-void validate_config(const tsl_config& c, const std::vector<const Graph*>& jobs) {
+// PlannerConfig::max_swap_ratios as the std::map<JobId,double> it restates
+// (a repeated id keeps its last value, like repeated map assignment).
+std::map<std::string, double> ratio_map(const tsl_config& c) {
+  std::map<std::string, double> m;
+  if (c.n_max_swap_ratios < 0) fail(TSL_ERR_ARGUMENT, "negative n_max_swap_ratios");
+  if (c.n_max_swap_ratios > 0 && (!c.max_swap_ratio_jobs || !c.max_swap_ratio_values))
+    fail(TSL_ERR_ARGUMENT, "null max_swap_ratios arrays");
+  for (int32_t i = 0; i < c.n_max_swap_ratios; ++i)
+    m[c.max_swap_ratio_jobs[i] ? c.max_swap_ratio_jobs[i] : ""] = c.max_swap_ratio_values[i];
+  return m;
+}
+
+// PlannerConfig::max_swap_ratio, config.hpp:20-23.
+double ratio_of(const std::map<std::string, double>& m, const std::string& job) {
+  auto it = m.find(job);
+  return it == m.end() ? 1.0 : it->second;
+}
+
+// PlannerConfig::validate, config.hpp:25-35 (every map entry, in key order;
+// the same predicate, so a NaN ratio passes as it does there).
+void validate_config(const tsl_config& c) {
   if (c.pcie_bandwidth <= 0) fail(TSL_ERR_VALIDATION, "pcie_bandwidth must be positive");
   if (c.transfer_setup < 0) fail(TSL_ERR_VALIDATION, "transfer_setup must be nonnegative");
   if (c.memory_budget < 0) fail(TSL_ERR_VALIDATION, "memory_budget must be nonnegative");
   if (c.ewma_alpha < 0 || c.ewma_alpha > 1) fail(TSL_ERR_VALIDATION, "ewma_alpha out of [0,1]");
   if (c.replan_threshold <= 0) fail(TSL_ERR_VALIDATION, "replan_threshold must be positive");
   if (c.stall_epsilon <= 0 || c.stall_epsilon >= 1) fail(TSL_ERR_VALIDATION, "stall_epsilon out of (0,1)");
-  std::map<std::string, double> ratios;  // std::map<JobId,double> order
-  for (const Graph* g : jobs)
-    if (g->ratio_given) ratios[g->job_id] = g->ratio;
-  for (auto& [job, r] : ratios)
-    if (!(r > 0 && r <= 1)) fail(TSL_ERR_VALIDATION, "max swap ratio for " + job + " out of (0,1]");
+  for (auto& [job, r] : ratio_map(c))
+    if (r <= 0 || r > 1) fail(TSL_ERR_VALIDATION, "max swap ratio for " + job + " out of (0,1]");
 }
 
 // ---------------------------------------------------------------------------
@@ -416,6 +428,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   P->mode = mode;
   P->n_groups = n_groups;
   P->cfgs.assign(cfgs, cfgs + n_cfgs);
+  for (auto& c : P->cfgs) {  // the ratio map is read during prepare only
+    c.n_max_swap_ratios = 0;
+    c.max_swap_ratio_jobs = nullptr;
+    c.max_swap_ratio_values = nullptr;
+  }
   P->graphs.resize(n_groups);
   // 1. validate graphs (caller order), then the config, then latencies
   {
@@ -425,14 +442,11 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     for (int gi = 0; gi < n_groups; ++gi) {
       for (int32_t k = offs[gi]; k < offs[gi + 1]; ++k) {
         const tsl_job_desc& d = jobs[k];
-        double ratio = d.max_swap_ratio;
-        uint64_t rbits = 0;
-        std::memcpy(&rbits, &ratio, sizeof rbits);
         std::vector<uintptr_t> key = {
             uintptr_t(d.job_id), uintptr_t(d.n_tensors), uintptr_t(d.tensor_ids), uintptr_t(d.tensor_sizes),
             uintptr_t(d.tensor_kinds), uintptr_t(d.n_ops), uintptr_t(d.op_ids), uintptr_t(d.op_kinds),
             uintptr_t(d.op_phases), uintptr_t(d.op_in_offsets), uintptr_t(d.op_inputs), uintptr_t(d.op_out_offsets),
-            uintptr_t(d.op_outputs), uintptr_t(d.op_latencies), uintptr_t(rbits)};
+            uintptr_t(d.op_outputs), uintptr_t(d.op_latencies)};
         auto it = seen.find(key);
         if (it == seen.end()) it = seen.emplace(std::move(key), std::make_shared<const Graph>(load_graph(d))).first;
         P->graphs[gi].push_back(it->second);
@@ -441,9 +455,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   }
   const auto t_load = std::chrono::steady_clock::now();
   for (int gi = 0; gi < n_groups; ++gi) {
-    std::vector<const Graph*> gg;
-    for (auto& g : P->graphs[gi]) gg.push_back(g.get());
-    if (mode == 0) validate_config(cfgs[n_cfgs == 1 ? 0 : gi], gg);
+    if (mode == 0) validate_config(cfgs[n_cfgs == 1 ? 0 : gi]);
     std::set<std::string> ids;
     for (auto& gp : P->graphs[gi]) {
       const Graph& g = *gp;
@@ -660,9 +672,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     std::vector<std::string> jids;
     for (auto& g : gs) jids.push_back(g->job_id);
     std::vector<int32_t> jrank = lex_rank(jids);
-    bool coupled = false;
-    for (auto& g : gs) coupled = coupled || g->ratio < 1.0;
     const tsl_config* cfg = &cfgs[n_cfgs == 1 ? 0 : gi];
+    const std::map<std::string, double> ratios = mode == 0 ? ratio_map(*cfg) : std::map<std::string, double>{};
+    bool coupled = false;
+    for (auto& g : gs) coupled = coupled || ratio_of(ratios, g->job_id) < 1.0;
     GroupDev* G = hp<GroupDev>(ctx, P->groups_off) + gi;
     std::memset(G, 0, sizeof *G);
     G->n_jobs = static_cast<int32_t>(gs.size());
@@ -732,7 +745,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       put(ctx, p.t_prod, g.prod);
       JobDev* J = hp<JobDev>(ctx, P->jobs_off) + jglob;
       std::memset(J, 0, sizeof *J);
-      J->A = g.A; J->T = g.T; J->O = g.O; J->rank = jrank[k]; J->ratio = g.ratio;
+      J->A = g.A; J->T = g.T; J->O = g.O; J->rank = jrank[k]; J->ratio = ratio_of(ratios, g.job_id);
       J->Scap = p.Scap; J->Rcap = p.Rcap; J->Ecap = p.Ecap;
       J->topo = dp<int32_t>(ctx, p.topo);
       J->o_lat = dp<int64_t>(ctx, p.o_lat);
@@ -1144,6 +1157,9 @@ void tsl_config_default(tsl_config* c) {
   c->stall_epsilon = 0.0005;
   c->stall_min_iters = 100;
   c->cold_start_gpu_usage = 0.5;
+  c->n_max_swap_ratios = 0;
+  c->max_swap_ratio_jobs = nullptr;
+  c->max_swap_ratio_values = nullptr;
 }
 
 int tsl_create(int device, tsl_ctx** out) {
@@ -1268,7 +1284,7 @@ int tsl_build_plan(tsl_ctx* ctx, const tsl_job_desc* jobs, int32_t n_jobs, const
   if (n_jobs == 0) {  // build_plan returns an empty result (orchestrator.cpp:12)
     if (!ctx || !cfg || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
     return guard([&] {
-      validate_config(*cfg, {});
+      validate_config(*cfg);
       *out = new tsl_result();
     });
   }

@@ -192,7 +192,7 @@ class Planner:
 
     def build_plan(self, jobs: Sequence, config: dict, with_views: bool = True) -> dict:
         """build_plan over [(graph, latencies)] -> dict (plans_json = save_plans text)."""
-        descs, arr = abi.pack_jobs(jobs, config.get("max_swap_ratios"))
+        descs, arr = abi.pack_jobs(jobs)
         cfg = abi.make_config(**config)
         res = C.c_void_p()
         t0 = time.perf_counter()
@@ -213,15 +213,13 @@ class Planner:
         cfgs = list(config) if isinstance(config, (list, tuple)) else [config]
         if len(cfgs) not in (1, n_groups):
             raise ValueError("need one config or one per group")
-        arr = (abi.TslConfig * len(cfgs))(*[abi.make_config(**c) for c in cfgs])
-        ratios: Dict[str, float] = {}
-        for c in cfgs:
-            ratios.update(c.get("max_swap_ratios") or {})
-        return arr, len(cfgs), ratios
+        keep = [abi.make_config(**c) for c in cfgs]  # owns each config's ratio-map arrays
+        arr = (abi.TslConfig * len(cfgs))(*keep)
+        return arr, len(cfgs), keep
 
-    def _pack_groups(self, groups: Sequence[Sequence], ratios: dict):
+    def _pack_groups(self, groups: Sequence[Sequence]):
         flat = [j for grp in groups for j in grp]
-        descs, arr = abi.pack_jobs(flat, ratios)
+        descs, arr = abi.pack_jobs(flat)
         offs = (C.c_int32 * (len(groups) + 1))()
         k = 0
         for i, grp in enumerate(groups):
@@ -233,8 +231,8 @@ class Planner:
     def build_plan_groups(self, groups: Sequence[Sequence], config, with_views: bool = True) -> List[dict]:
         """Independent build_plan calls (one per group) in ONE kernel launch.
         `config` is one dict shared by all groups or a list, one per group."""
-        cfgs, ncfg, ratios = self._configs(config, len(groups))
-        descs, arr, offs = self._pack_groups(groups, ratios)
+        cfgs, ncfg, keep = self._configs(config, len(groups))
+        descs, arr, offs = self._pack_groups(groups)
         res = (C.c_void_p * len(groups))()
         rc = self.lib.tsl_build_plan_groups(self._ctx, arr, offs, len(groups), cfgs, ncfg, res)
         if rc:
@@ -248,8 +246,8 @@ class Planner:
         return outs
 
     def prepare(self, groups: Sequence[Sequence], config) -> PreparedPlan:
-        cfgs, ncfg, ratios = self._configs(config, len(groups))
-        descs, arr, offs = self._pack_groups(groups, ratios)
+        cfgs, ncfg, keep = self._configs(config, len(groups))
+        descs, arr, offs = self._pack_groups(groups)
         h = C.c_void_p()
         rc = self.lib.tsl_plan_prepare(self._ctx, arr, offs, len(groups), cfgs, ncfg, C.byref(h))
         if rc:
@@ -260,7 +258,7 @@ class Planner:
                           bytes_per_unit: int = 16) -> dict:
         """build_plan, then replay every job's plan on the device (plan
         executor): {"plan": build_plan dict, "exec": {job_id: report dict}}."""
-        descs, arr = abi.pack_jobs(jobs, config.get("max_swap_ratios"))
+        descs, arr = abi.pack_jobs(jobs)
         cfg = abi.make_config(**config)
         res = C.c_void_p()
         rc = self.lib.tsl_build_plan(self._ctx, arr, len(descs), C.byref(cfg), C.byref(res))
@@ -288,7 +286,7 @@ class Planner:
         """build_plan, then replay ALL jobs' plans together on the device (one
         compute stream per job, one FIFO copy stream, one allocator):
         {"plan": build_plan dict, "exec": {job_id: report}, "merged": report}."""
-        descs, arr = abi.pack_jobs(jobs, config.get("max_swap_ratios"))
+        descs, arr = abi.pack_jobs(jobs)
         cfg = abi.make_config(**config)
         res = C.c_void_p()
         rc = self.lib.tsl_build_plan(self._ctx, arr, len(descs), C.byref(cfg), C.byref(res))

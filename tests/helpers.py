@@ -69,3 +69,46 @@ def ensure_emu():
     """TEST-ONLY CPU emulation build of the planner (tests/emu)."""
     subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "emu")], check=True, stdout=subprocess.DEVNULL)
     return EMU_LIB
+
+
+def edge_jobs(case):
+    """Jobs of an edge.json case. Job specs: {"graph", "latencies"} verbatim, {"c5": k}
+    (configs.c5_job), or {"gen": [family, batch, depth, job_id, lat_seed]} with optional
+    "size_mul" (every tensor size x k) and "lat" ("table" | "zero" | "zero_odd" | int constant)."""
+    from paper_2105_13336_b200 import configs as CF
+    from paper_2105_13336_b200 import workload as W
+    jobs = []
+    for spec in case["jobs"]:
+        if "graph" in spec:
+            jobs.append((spec["graph"], spec["latencies"]))
+            continue
+        if "c5" in spec:
+            jobs.append(CF.c5_job(spec["c5"]))
+            continue
+        fam, batch, depth, jid, lat_seed = spec["gen"]
+        g = W.generate_workload(fam, batch, 0, depth, jid)
+        mul = spec.get("size_mul", 1)
+        if mul != 1:
+            for t in g["tensors"]:
+                t["size"] *= mul
+        lat = W.true_latency_table(g, lat_seed)
+        mode = spec.get("lat", "table")
+        if mode == "zero":
+            lat = {o: 0 for o in lat}
+        elif mode == "zero_odd":
+            lat = {o["id"]: (0 if i % 2 else lat[o["id"]]) for i, o in enumerate(g["ops"])}
+        elif isinstance(mode, int):
+            lat = {o: mode for o in lat}
+        jobs.append((g, lat))
+    return jobs
+
+
+def check_edge(build_plan, case):
+    """One edge.json case: the reference's plan, or the reference's error text."""
+    import pytest
+    if "error" in case:
+        with pytest.raises(Exception) as e:
+            build_plan(edge_jobs(case), case["config"])
+        assert str(e.value) == case["error"]
+    else:
+        check_against_golden(build_plan(edge_jobs(case), case["config"]), case)

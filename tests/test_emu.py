@@ -7,7 +7,7 @@ import json
 
 import pytest
 
-from helpers import check_against_golden, config_jobs, ensure_emu, fuzz_jobs, golden
+from helpers import check_against_golden, check_edge, config_jobs, ensure_emu, fuzz_jobs, golden
 from paper_2105_13336_b200 import abi, workload as W
 from paper_2105_13336_b200.planner import Planner, ValidationError
 
@@ -113,3 +113,12 @@ def test_c4_family_matches_oracle(emu, shape):
     assert got["plans_json"] == want["plans_json"]
     assert got["reports_json"] == want["reports_json"]
     assert got["merged_peak_history"] == want["merged_peak_history"]
+
+
+@pytest.mark.parametrize("case", golden("edge"), ids=lambda c: c["name"])
+def test_edge_cases(emu, case):
+    """Extreme inputs (tests/golden/make_edge_golden.py): single-op jobs, zero and
+    constant latencies, budgets 0 / = peak / unbounded, ~2^40-byte tensors, 10^12-tick
+    latencies, recompute-only setups, ratio-map errors, 40 jobs and all 64 C5 workloads
+    in one build -- the reference's plans byte for byte, or its error text."""
+    check_edge(emu.build_plan, case)

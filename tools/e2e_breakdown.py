@@ -9,8 +9,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 req = CF.requests(name)[-1]
 cfg = req.config(ref.initial_peaks(req.jobs))
 groups = [req.jobs]
-cfg_arr, ncfg, ratios = P._configs([cfg], 1)
-descs, arr, offs = P._pack_groups(groups, ratios)
+cfg_arr, ncfg, keep = P._configs([cfg], 1)
+descs, arr, offs = P._pack_groups(groups)
 res = (C.c_void_p * 1)()
 L = P.lib
 st = abi.TslStats()

@@ -127,6 +127,27 @@ def _ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
+class _CStrings:
+    """A `const char* const*` table: the strings NUL-joined in one buffer and
+    a pointer array into it (built with numpy, not one ctypes object per id)."""
+
+    def __init__(self, strings: List[str]):
+        blob = ("\0".join(strings) + "\0").encode()
+        self.buf = np.frombuffer(blob, dtype=np.uint8).copy()
+        ends = np.flatnonzero(self.buf == 0)  # ids are C strings: no NUL inside
+        starts = np.empty(max(1, len(strings)), dtype=np.uint64)
+        starts[0] = 0
+        starts[1:len(strings)] = ends[:len(strings) - 1] + 1
+        self.addrs = starts + np.uint64(self.buf.ctypes.data)
+        self.ptrs = self.addrs.ctypes.data_as(_pstr)
+
+
+def _offsets(counts: List[int]) -> np.ndarray:
+    out = np.zeros(len(counts) + 1, dtype=np.int32)
+    np.cumsum(counts, out=out[1:])
+    return out
+
+
 class JobDesc:
     """One (graph, latencies) job packed for the C-ABI."""
 
@@ -142,28 +163,21 @@ class JobDesc:
         self.tindex = tindex
         self.oindex = {o: i for i, o in enumerate(self.op_ids)}
 
-        def tref(name):
-            # a dangling reference packs to -1; the library reports it
-            return tindex.get(name, -1)
-
-        self._tids = (C.c_char_p * max(1, len(tensors)))(*[s.encode() for s in self.tensor_ids])
-        self._oids = (C.c_char_p * max(1, len(ops)))(*[s.encode() for s in self.op_ids])
-        self._okinds = (C.c_char_p * max(1, len(ops)))(*[o["kind"].encode() for o in ops])
+        self._tids = _CStrings(self.tensor_ids)
+        self._oids = _CStrings(self.op_ids)
+        self._okinds = _CStrings([o["kind"] for o in ops])
         self._sizes = _arr([t["size"] for t in tensors], np.int64)
         self._kinds = _arr([KINDS[t["kind"]] for t in tensors], np.int8)
         self._phases = _arr([PHASES[o["phase"]] for o in ops], np.int8)
-        ins, outs, ioff, ooff = [], [], [0], [0]
-        for o in ops:
-            ins.extend(tref(t) for t in o["inputs"])
-            outs.extend(tref(t) for t in o["outputs"])
-            ioff.append(len(ins))
-            ooff.append(len(outs))
-        self._ins, self._outs = _arr(ins, np.int32), _arr(outs, np.int32)
-        self._ioff, self._ooff = _arr(ioff, np.int32), _arr(ooff, np.int32)
+        tget = tindex.get  # a dangling reference packs to -1; the library reports it
+        self._ins = _arr([tget(t, -1) for o in ops for t in o["inputs"]], np.int32)
+        self._outs = _arr([tget(t, -1) for o in ops for t in o["outputs"]], np.int32)
+        self._ioff = _offsets([len(o["inputs"]) for o in ops])
+        self._ooff = _offsets([len(o["outputs"]) for o in ops])
         self._lat = _arr([latencies.get(o, LATENCY_MISSING) for o in self.op_ids], np.int64)
         self._jid = graph["job_id"].encode()
-        self.desc = TslJobDesc(self._jid, len(tensors), self._tids, _ptr(self._sizes, C.c_int64),
-                               _ptr(self._kinds, C.c_int8), len(ops), self._oids, self._okinds,
+        self.desc = TslJobDesc(self._jid, len(tensors), self._tids.ptrs, _ptr(self._sizes, C.c_int64),
+                               _ptr(self._kinds, C.c_int8), len(ops), self._oids.ptrs, self._okinds.ptrs,
                                _ptr(self._phases, C.c_int8), _ptr(self._ioff, C.c_int32),
                                _ptr(self._ins, C.c_int32), _ptr(self._ooff, C.c_int32),
                                _ptr(self._outs, C.c_int32), _ptr(self._lat, C.c_int64))

@@ -18,10 +18,24 @@ class _Req:  # C4:<micro_batches> -> one GPT-2-medium job
         return {"pcie_bandwidth": 256, "transfer_setup": 1, "memory_budget": self._init * 7 // 10}
 
 
+class _Edge:  # edge:<case> -> one tests/golden/edge.json build
+    def __init__(self, case):
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+        from helpers import edge_jobs, golden
+        c = next(c for c in golden("edge") if c["name"] == case)
+        self.jobs, self.name, self.n_accesses, self._cfg = edge_jobs(c), case, c["n_accesses"], c["config"]
+
+    def config(self, _):
+        return self._cfg
+
+
 for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
-    reqs = [_Req(int(name[3:]))] if name.startswith("C4:") else CF.requests(name)
+    if name.startswith("edge:"):
+        reqs = [_Edge(name[5:])]
+    else:
+        reqs = [_Req(int(name[3:]))] if name.startswith("C4:") else CF.requests(name)
     for req in [reqs[-1]]:
-        cfg = req.config(None if name.startswith("C4:") else ref.initial_peaks(req.jobs))
+        cfg = req.config(None if name.startswith(("C4:", "edge:")) else ref.initial_peaks(req.jobs))
         P.build_plan(req.jobs, cfg)
         p = P.build_plan(req.jobs, cfg)
         s = p["stats"]

@@ -1255,13 +1255,20 @@ int tsl_build_plan_groups(tsl_ctx* ctx, const tsl_job_desc* jobs, const int32_t*
     tsl_plan* P = prepare(ctx, jobs, group_offsets, n_groups, cfgs, n_cfgs, 0, nullptr, false);
     std::vector<tsl_result*> rs;
     try {
+      const auto tp = std::chrono::steady_clock::now();
       upload(P);
       launch(P, 1, true);
       download(P, ctx->stream);
+      const auto td = std::chrono::steady_clock::now();
       float ms = 0;
       cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "elapsed");
       P->last_kernel_ms = ms;
       for (int gi = 0; gi < n_groups; ++gi) rs.push_back(collect_group(P, gi));
+      if (std::getenv("TSL_E2E_PROFILE")) {
+        auto d = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "e2e: prep %.3f upload+kernel+download %.3f (kernel %.3f, d2h %zu B) collect %.3f ms\n",
+                     d(t0, tp), d(tp, td), double(ms), P->d2h_bytes, d(td, std::chrono::steady_clock::now()));
+      }
     } catch (...) {
       for (auto* r : rs) delete r;
       delete P;

@@ -159,6 +159,39 @@ def cpu_reference(reqs, seconds: float, max_plans: int = 10 ** 9):
     return ev / (ms / 1e3), ms, len(times), kind
 
 
+def host_cpu() -> dict:
+    """The GPU box's host CPU (state the model and core count)."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def _shard_plan_ms(shard: int):
+    """One C5 shard's 15 replans through the reference (a worker process)."""
+    sys.path.insert(0, ROOT)
+    from oracle import ref
+    reqs = workload("C5", shard)
+    return sum(n_accesses(j) for _, j, _ in reqs), sum(ref.build_plan(j, c, repeats=1)[1]["times_ms"][0]
+                                                       for _, j, c in reqs)
+
+
+def cpu_parallel_shards() -> dict:
+    """C5 on the host: N = min(8, cores) processes, shard k in process k, one
+    step each; throughput = all events / the slowest shard."""
+    import multiprocessing as mp
+    n = max(1, min(8, os.cpu_count() or 1))
+    with mp.get_context("spawn").Pool(n) as pool:
+        res = pool.map(_shard_plan_ms, range(n))
+    ev = sum(e for e, _ in res)
+    slow = max(ms for _, ms in res)
+    return {"processes": n, "value": ev / (slow / 1e3), "unit": UNIT, "slowest_shard_ms": slow,
+            "sample": f"shards 0..{n - 1}, one 15-replan step each, one process per shard (reference, -O3)"}
+
+
 def hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -226,10 +259,13 @@ def run_reference(a, rank, world):
             "data": "synthetic traces from the reference generator (workload.cpp), latency seed 13",
             "config": {"workload": workload_desc(a.workload), "requests": len(reqs), "accesses_per_step": ev},
             "plan_gen_ms": ms,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "host": host_cpu(),
+                             "threads_note": "the reference has no threads: one build_plan uses one core",
                              "sample": f"{len(times)} x build_plan of {'the C4 1-micro-batch sample (16,445 accesses)' if sample else a.workload}, single thread "
                                        f"({'oracle/_ref: reference sources compiled -O3' if kind == 'reference' else 'restated oracle port'})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if a.workload == "C5" and kind == "reference":
+        line["cpu_baseline"]["parallel_shards"] = cpu_parallel_shards()
     print(json.dumps(line), flush=True)
 
 
@@ -358,8 +394,11 @@ def run_ours(a, rank, world, local):
         rate, ms, n, kind = cpu_reference(workload("C4-sample", 0) if c4 else reqs, a.cpu_seconds, 1 if c4 else 10 ** 9)
         what = "C4 1-micro-batch sample (16,445 accesses; the reference cannot plan full C4)" if c4 else f"{a.workload} step"
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "ms_per_step": ms,
+                                "host": host_cpu(),
                                 "sample": f"{n} x {what} on 1 host thread (~{a.cpu_seconds:.0f} s), "
                                           f"{'reference sources compiled -O3 (oracle/_ref)' if kind == 'reference' else 'restated oracle port'}"}
+        if a.workload == "C5" and kind == "reference":
+            line["cpu_baseline"]["parallel_shards"] = cpu_parallel_shards()
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

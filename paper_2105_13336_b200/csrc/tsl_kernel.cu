@@ -80,6 +80,7 @@ struct DevX {
   __device__ void amin(int64_t* p, int64_t v) { atomicMin((long long*)p, (long long)v); }
   __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
   __device__ void amax32(int32_t* p, int32_t v) { atomicMax(p, v); }
+  __device__ void aor32(int32_t* p, int32_t v) { atomicOr(p, v); }
   __device__ void errset(GroupDev& g, const ErrInfo& e) {
     if (atomicCAS(&g.err.code, 0, e.code) == 0) {
       g.err.job = e.job;

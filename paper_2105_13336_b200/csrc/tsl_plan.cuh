@@ -1696,7 +1696,7 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
                     const int64_t* wv = g.w_pool + 2 * int64_t(cq[CI_W0]);
                     bool hit = false;
                     for (int32_t w = 0; w < cq[CI_NW] && !hit; ++w) hit = hits(s0, e0, wv[2 * w], wv[2 * w + 1], P);
-                    if (hit) cq[CI_STATUS] |= CS_HIT;  // racing lanes set the same bit
+                    if (hit) x.aor32(&cq[CI_STATUS], CS_HIT);  // lanes may reach q through several buckets
                   }
               }
             }
@@ -2395,6 +2395,7 @@ TSL_HD bool revalidate(X& x, GroupDev& g, int j) {
       }
       x.wsync();
     }
+    x.wsync();  // every lane is past its last read of st.S before lane 0 rewrites it
     // stable compaction (lane 0; pairs are rare to drop)
     if (x.lane == 0) {
       int32_t w = 0;

@@ -1,7 +1,7 @@
 """Representative builds for compute-sanitizer (memcheck / racecheck / synccheck):
 C1, C2, C3's last arrival, a C5 shard's 15 replans in one launch, an analyze_job
 call, a job above one sort tile through the cooperative launch and through the
-single-CTA big path, each checked against the reference fixtures or the oracle.
+single-CTA big path, and (full run) the executor's C3 replay, each checked against the reference fixtures or the oracle.
 
     compute-sanitizer --tool memcheck python tools/sanitize_check.py [quick]
 """
@@ -44,4 +44,10 @@ if not quick:
         os.environ["TSL_COOP"] = coop
         assert P.build_plan(jobs, cfg)["plans_json"] == want
         print("chain 2200 (big mode, coop=%s) ok" % coop, flush=True)
+    # plan executor (tsl_exec.cu): C3's three jobs replayed together, HWM vs prediction
+    c3 = cases["C3.3"]
+    out = P.build_and_execute_all(config_jobs(c3), c3["config"], tick_ns=2000, iterations=1)
+    assert out["merged"]["hwm"] <= out["merged"]["predicted_peak"], out["merged"]
+    assert out["merged"]["verify_errors"] == 0 and out["merged"]["violations"] == 0
+    print("executor C3 replay ok", flush=True)
 print("SANITIZE_CHECK_DONE", flush=True)

@@ -9,6 +9,12 @@
 #include "tsl_plan.cuh"
 #include "tsl_kernel.h"
 
+// Pend-list length at which a cooperative launch folds this pass's commits
+// into the busy structure (grid-wide merge) instead of merging into pend.
+#ifndef TSL_COOP_FOLD
+#define TSL_COOP_FOLD 256
+#endif
+
 namespace tsl {
 
 static_assert(sizeof(PairRec) == PAIRREC_BYTES, "PairRec layout");
@@ -360,7 +366,7 @@ struct DevX {
   // Commit-list length that triggers a fold into the busy structure: folds on
   // the worker CTAs are cheap, a fold by one warp is linear in the structure.
   __device__ int32_t fold_threshold(int32_t bz_n) const {
-    return (coop && grid >= 3) ? 256 : max(PEND_MERGE, bz_n / 128);
+    return (coop && grid >= 3) ? TSL_COOP_FOLD : max(PEND_MERGE, bz_n / 128);
   }
 
   // Deciding warp of CTA 0 (warp-collective): hand a busy-structure fold to

@@ -122,3 +122,14 @@ def test_edge_cases(emu, case):
     latencies, recompute-only setups, ratio-map errors, 40 jobs and all 64 C5 workloads
     in one build -- the reference's plans byte for byte, or its error text."""
     check_edge(emu.build_plan, case)
+
+
+@pytest.mark.parametrize("block", range(6))
+def test_live_reference_fuzz(emu, block):
+    """The GPU suite's live differential fuzz (test_gpu_live_reference.py) through the
+    emulation build: the same fresh seeds against the unmodified reference library."""
+    from oracle import ref
+    import test_gpu_live_reference as live
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    live.test_live_reference_fuzz(emu, ref, block)

@@ -533,19 +533,42 @@ TSL_HD void pend_sort(X& x, PendBuf& pb, JobState& st, bool pingpong = true) {
   }
   x.wsync();
   // merge prefix [0, p) and sorted suffix ts[0, k) into the merge target,
-  // prefix first on equal starts: one contiguous output range per lane
-  // (merge-path split), then the two buffers swap roles
-  const int32_t per = (n + X::W - 1) / X::W;
-  const int32_t d0 = imin(n, int64_t(x.lane) * per), d1 = imin(n, int64_t(d0) + per);
-  int32_t lo = imax(0, d0 - k), hi = imin(d0, p);
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (pb.s[mid] <= ts[d0 - mid - 1]) lo = mid + 1; else hi = mid;
-  }
-  int32_t i = lo, r = d0 - lo;
-  for (int32_t d = d0; d < d1; ++d) {
-    if (i < p && (r >= k || pb.s[i] <= ts[r])) { pb.ts[d] = pb.s[i]; pb.te[d] = pb.e[i]; ++i; }
-    else { pb.ts[d] = ts[r]; pb.te[d] = te[r]; ++r; }
+  // prefix first on equal starts, then the two buffers swap roles
+  if (k <= X::W) {
+    // a few new entries (the usual case: the verbatim commits since the last
+    // re-score): scatter, no dependent search. Prefix entry i moves past the
+    // new entries that start strictly before it; new entry r lands after every
+    // prefix entry that starts at or before it.
+    const int64_t my_s = x.lane < k ? ts[x.lane] : 0, my_e = x.lane < k ? te[x.lane] : 0;
+    int32_t before = 0;
+    for (int32_t c0 = 0; c0 < p; c0 += X::W) {
+      const int32_t i = c0 + x.lane;
+      const bool valid = i < p;
+      const int64_t si = valid ? pb.s[i] : 0, ei = valid ? pb.e[i] : 0;
+      int32_t lt = 0;
+      for (int32_t r = 0; r < k; ++r) {
+        const int64_t v = x.shfl(my_s, r);
+        lt += (valid && v < si) ? 1 : 0;
+        const int32_t le = popc32(x.wballot(valid && si <= v));
+        if (x.lane == r) before += le;
+      }
+      if (valid) { pb.ts[i + lt] = si; pb.te[i + lt] = ei; }
+    }
+    if (x.lane < k) { pb.ts[x.lane + before] = my_s; pb.te[x.lane + before] = my_e; }
+  } else {
+    // one contiguous output range per lane (merge-path split)
+    const int32_t per = (n + X::W - 1) / X::W;
+    const int32_t d0 = imin(n, int64_t(x.lane) * per), d1 = imin(n, int64_t(d0) + per);
+    int32_t lo = imax(0, d0 - k), hi = imin(d0, p);
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pb.s[mid] <= ts[d0 - mid - 1]) lo = mid + 1; else hi = mid;
+    }
+    int32_t i = lo, r = d0 - lo;
+    for (int32_t d = d0; d < d1; ++d) {
+      if (i < p && (r >= k || pb.s[i] <= ts[r])) { pb.ts[d] = pb.s[i]; pb.te[d] = pb.e[i]; ++i; }
+      else { pb.ts[d] = ts[r]; pb.te[d] = te[r]; ++r; }
+    }
   }
   x.wsync();
   if (pingpong) {

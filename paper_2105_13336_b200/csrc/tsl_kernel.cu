@@ -426,11 +426,13 @@ struct DevX {
         return;
       }
       if (type == COOP_EVAL) coop_eval(cta, c->jb, c->je);
+      else if (type == COOP_REBUILD) coop_rebuild(cta);
       else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
   }
   __device__ void coop_eval(int cta, int jb, int je);  // all CTAs: evaluate() on the grid (below)
+  __device__ void coop_rebuild(int cta);               // all CTAs: rebuild_busy() on the grid (below)
   GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
@@ -627,6 +629,29 @@ __device__ inline GridX grid_ctx(DevX& x, int cta) {
 __device__ void DevX::coop_eval(int cta, int jb, int je) {
   GridX gx = grid_ctx(*this, cta);
   evaluate(gx, *coop_group, jb, je);
+}
+
+__device__ void DevX::coop_rebuild(int cta) {
+  GridX gx = grid_ctx(*this, cta);
+  rebuild_busy(gx, *coop_group);
+}
+
+// The end-of-pass busy rebuild on a cooperative launch: key building, the
+// sort and the scatter back run on every CTA (a C4 pass rebuilds ~10^5-10^6
+// intervals; one CTA walking them was 11 % of the build).
+template <>
+__device__ inline void rebuild_batch<DevX>(DevX& x, GroupDev& g) {
+  if (!x.coop) { rebuild_busy(x, g); return; }
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->type = COOP_REBUILD;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  GridX gx = grid_ctx(x, 0);
+  rebuild_busy(gx, g);
 }
 
 // The CUDA build's evaluation batches: on a cooperative launch, CTA 0 calls

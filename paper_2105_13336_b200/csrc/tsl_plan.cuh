@@ -177,7 +177,7 @@ TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, i
     if (hi > TI_NB) hi = TI_NB;
     for (int64_t b = lo; b <= hi; ++b) first[b] = k;
   }
-  if (kWarp) x.wsync();
+  if constexpr (kWarp) x.wsync();
   else x.sync();
 }
 
@@ -1474,6 +1474,13 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
   }
 }
 
+// The end-of-pass rebuild; an execution context may route it elsewhere (the
+// CUDA build runs it on every CTA of a cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD void rebuild_batch(X& x, GroupDev& g) {
+  rebuild_busy(x, g);
+}
+
 // Folds the pass's sorted commit list into the job's busy structure (warp-
 // collective, the job's deciding warp only): queries see the same union of
 // intervals, later pend merges start from an empty list. Both lists are
@@ -2273,7 +2280,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sync();
   tick(8);
   // ---- E. sorted busy structure for the next pass ----
-  if (gsh[10]) rebuild_busy(x, g);
+  if (gsh[10]) rebuild_batch(x, g);
   tick(9);
   return gsh[10] != 0;
 }

@@ -197,7 +197,7 @@ struct CoopCtl {
   int32_t fn1, fn2, fshift, fdone;
   int32_t wbar_count, wbar_gen;  // barrier of the worker CTAs
 };
-enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;

@@ -1178,19 +1178,17 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230),
   // in parallel: in (job, storage)-grouped order, the residency before an
   // event is set by the previous state-changing event of its storage (TGA
-  // and swap-in make it resident, release and swap-out evict); two max-scans
-  // give that index and the storage's first index for every event.
+  // and swap-in make it resident, release and swap-out evict); a max-scan
+  // gives that index, and since a storage's events are contiguous it belongs
+  // to the same storage iff its group key matches.
   {
     int64_t* chg = reinterpret_cast<int64_t*>(g.k_key);  // free after sort 1
-    int64_t* seg = g.x_time + g.ecap;                    // second half of the time scratch
     for (int64_t m = x.tid; m < n; m += x.nthr) {
       const int ty = g.x_type[g.x_order[g.x_seq2[m]]] & 7;
       chg[m] = ty == EV_TUA ? -1 : m;
-      seg[m] = (m == 0 || g.x_key2[m] != g.x_key2[m - 1]) ? m : 0;
     }
     x.sync();
     x.scan_max(chg, int32_t(n));
-    x.scan_max(seg, int32_t(n));
     for (int64_t m = x.tid; m < n; m += x.nthr) {
       const int32_t pos = g.x_seq2[m];
       const int32_t slot = g.x_order[pos];
@@ -1200,7 +1198,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const int ty = g.x_type[slot] & 7;
       const int64_t prev = m > 0 ? chg[m - 1] : -1;  // last state change strictly before m
       uint8_t res;
-      if (prev >= seg[m]) {
+      if (prev >= 0 && g.x_key2[prev] == g.x_key2[m]) {
         const int pt = g.x_type[g.x_order[g.x_seq2[prev]]] & 7;
         res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
       } else {
@@ -1240,17 +1238,27 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     }
   }
   x.sync();
-  for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int b = g.x_job[g.x_order[m]];
-    int64_t* f = sh + b * NF;
-    const int64_t fp = g.x_fp[m] + f[F_OFF];
-    g.x_fp[m] = fp;  // own element only: no cross-thread hazard after the scan
-    if (fp < 0) x.amin(&f[F_ERR], (int64_t(m) << 3) | E_NEG_FOOTPRINT);
-  }
-  x.sync();
-  for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int b = g.x_job[g.x_order[m]];
-    x.amax(&sh[b * NF + F_MAXFP], g.x_fp[m]);
+  {
+    // offset fix-up fused with the per-job maximum: jobs occupy contiguous
+    // position ranges, so each thread folds its strided elements locally and
+    // issues one atomic per job it touched.
+    int cb = -1;
+    int64_t cmx = INT64_MIN;
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int b = g.x_job[g.x_order[m]];
+      int64_t* f = sh + b * NF;
+      const int64_t fp = g.x_fp[m] + f[F_OFF];
+      g.x_fp[m] = fp;  // own element only: no cross-thread hazard after the scan
+      if (fp < 0) x.amin(&f[F_ERR], (int64_t(m) << 3) | E_NEG_FOOTPRINT);
+      if (b != cb) {
+        if (cb >= 0) x.amax(&sh[cb * NF + F_MAXFP], cmx);
+        cb = b;
+        cmx = fp;
+      } else {
+        cmx = imax(cmx, fp);
+      }
+    }
+    if (cb >= 0) x.amax(&sh[cb * NF + F_MAXFP], cmx);
   }
   x.sync();
   etick(5);
@@ -1262,12 +1270,21 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   }
   x.sync();
   // 10. last_input_access at the peak; residency at the peak
-  for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int32_t slot = g.x_order[m];
-    const int b = g.x_job[slot];
-    int64_t* f = sh + b * NF;
-    if (f[F_PPOS] != INT64_MAX && m <= f[F_PPOS] && (g.x_type[slot] & 7) == EV_TUA && !(g.x_type[slot] & 16))
-      x.amax(&f[F_LUA], m);
+  {
+    int cb = -1;
+    int64_t cl = -1;
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int32_t slot = g.x_order[m];
+      const int b = g.x_job[slot];
+      const int64_t pp = sh[b * NF + F_PPOS];
+      if (b != cb) {
+        if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
+        cb = b;
+        cl = -1;
+      }
+      if (pp != INT64_MAX && m <= pp && (g.x_type[slot] & 7) == EV_TUA && !(g.x_type[slot] & 16)) cl = m;
+    }
+    if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
   }
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];

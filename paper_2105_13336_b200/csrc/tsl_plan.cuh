@@ -1035,17 +1035,22 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     x.sync();
     return false;
   }
-  // 2. count releases; initial footprint
+  // 2. initial footprint; releases counted per contiguous access chunk of
+  // each thread and scanned over (job, thread), so release slots are numbered
+  // in access order (the scan's per-job totals are the release counts).
+  int64_t* rcnt = g.x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
-    int32_t rel = 0;
-    for (int32_t a = x.tid; a < J.A; a += x.nthr) rel += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
-    if (rel) x.aadd(&sh[b * NF + F_REL], rel);
     int64_t fp = 0;
     for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.res_init[t]) fp += J.t_size[t];
     if (fp) x.aadd(&sh[b * NF + F_INIT], fp);
+    const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
+    const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
+    int64_t c = 0;
+    for (int32_t a = a0; a < a1; ++a) c += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
+    rcnt[int64_t(b) * x.nthr + x.tid] = c;
   }
-  x.sync();
+  x.scan(rcnt, nb * x.nthr);  // inclusive; barriers on both sides
   // 3. bases and key geometry
   if (x.tid == 0) {
     int64_t base = 0, maxT = 1;
@@ -1053,6 +1058,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const JobDev& J = g.jobs[jb + b];
       const JobState& st = g.st[jb + b];
       int64_t* f = sh + b * NF;
+      f[F_REL] = rcnt[int64_t(b + 1) * x.nthr - 1] - (b > 0 ? rcnt[int64_t(b) * x.nthr - 1] : 0);
       f[F_BASE] = base;
       f[F_N] = J.A + f[F_REL] + st.S + st.R;
       base += f[F_N];
@@ -1090,19 +1096,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     return k;
   };
   etick(0);
-  // 4. emit events (build_timeline, peak.cpp:66-174). Release slots are
-  // numbered in access order: per-thread contiguous access chunks, counted,
-  // then one block scan over (job, thread).
-  int64_t* rcnt = g.x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
-  for (int b = 0; b < nb; ++b) {
-    const JobDev& J = g.jobs[jb + b];
-    const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
-    const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
-    int64_t c = 0;
-    for (int32_t a = a0; a < a1; ++a) c += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
-    rcnt[int64_t(b) * x.nthr + x.tid] = c;
-  }
-  x.scan(rcnt, nb * x.nthr);  // inclusive
+  // 4. emit events (build_timeline, peak.cpp:66-174); release slots from the
+  // step-2 scan.
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
     const JobState& st = g.st[jb + b];
@@ -1291,17 +1286,17 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     for (int32_t t = x.tid; t < J.T; t += x.nthr) J.in_peak[t] = J.res_init[t];
   }
   x.sync();
+  // A storage's residency at the peak is its state after its last event at or
+  // before the peak position: within a (job, storage) group positions ascend,
+  // so that event is the one whose successor leaves the group or the prefix.
   for (int64_t m = x.tid; m < n; m += x.nthr) {
-    if (m > 0 && g.x_key2[m] == g.x_key2[m - 1]) continue;
-    const int32_t slot0 = g.x_order[g.x_seq2[m]];
-    const int b = g.x_job[slot0];
+    const int32_t pos = g.x_seq2[m];
+    const int32_t slot = g.x_order[pos];
+    const int b = g.x_job[slot];
     const int64_t pp = sh[b * NF + F_PPOS];
-    if (pp == INT64_MAX) continue;
-    int64_t last = -1;
-    for (int64_t q = m; q < n && g.x_key2[q] == g.x_key2[m]; ++q) {
-      if (g.x_seq2[q] <= pp) last = g.x_seq2[q]; else break;
-    }
-    if (last >= 0) g.jobs[jb + b].in_peak[g.x_store[slot0]] = g.x_state[last];
+    if (pp == INT64_MAX || pos > pp) continue;
+    if (m + 1 < n && g.x_key2[m + 1] == g.x_key2[m] && g.x_seq2[m + 1] <= pp) continue;
+    g.jobs[jb + b].in_peak[g.x_store[slot]] = g.x_state[pos];
   }
   x.sync();
   etick(6);

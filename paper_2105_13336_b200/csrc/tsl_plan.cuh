@@ -1071,8 +1071,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const int jbits = nbits(uint64_t(nb - 1)), tbits = nbits(uint64_t(tmax - tmin));
     const int rbits = nbits(uint64_t(maxT - 1));
     gsh[3] = (int64_t(jbits) << 48) | (int64_t(tbits) << 32) | (int64_t(rbits) << 16);
-    if (base > g.ecap || jbits + tbits + 1 + rbits + 3 > 63) {
-      g.err.code = E_CAPACITY; g.err.job = jb; g.err.tensor = base; g.err.tick = jbits + tbits + rbits + 4;
+    if (base > g.ecap || jbits + tbits + 1 + rbits + 2 > 63) {
+      g.err.code = E_CAPACITY; g.err.job = jb; g.err.tensor = base; g.err.tick = jbits + tbits + rbits + 3;
     }
   }
   x.sync();
@@ -1092,7 +1092,9 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     k = (k << tbits) | uint64_t(time - tmin);
     k = (k << 1) | (fr ? 0u : 1u);
     k = (k << rbits) | uint64_t(srank);
-    k = (k << 3) | uint64_t(type);
+    // type rank within the free / non-free class: TGA < TUA < SIN and
+    // SOUT < REL (the class bit above already orders frees first), 2 bits
+    k = (k << 2) | uint64_t(fr ? type - EV_SOUT : type);
     return k;
   };
   etick(0);
@@ -1157,7 +1159,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   x.sync();
   etick(1);
   // 5. timeline order (sort_timeline, peak.cpp:44-62)
-  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 3);
+  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 2);
   etick(2);
   // 6. group sorted positions by (job, storage), keeping timeline order
   for (int64_t m = x.tid; m < n; m += x.nthr) {

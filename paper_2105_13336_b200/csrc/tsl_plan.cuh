@@ -933,6 +933,20 @@ enum { F_BASE = 0, F_N, F_REL, F_INIT, F_OFF, F_MAXFP, F_PPOS, F_LUA, F_ERR, F_N
 
 template <class X>
 TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
+  // The scratch pointers live in the group struct in global memory; local
+  // copies keep every store below from forcing a reload of the pointer.
+  uint64_t* const E_k_key = g.k_key;
+  int32_t* const E_k_val = g.k_val;
+  int64_t* const E_x_time = g.x_time;
+  int64_t* const E_x_fp = g.x_fp;
+  int32_t* const E_x_store = g.x_store;
+  int32_t* const E_x_aid = g.x_aid;
+  int8_t* const E_x_type = g.x_type;
+  int8_t* const E_x_job = g.x_job;
+  uint8_t* const E_x_state = g.x_state;
+  int32_t* const E_x_seq2 = g.x_seq2;
+  uint64_t* const E_x_key2 = g.x_key2;
+  int32_t* const E_x_order = g.x_order;
   int64_t* sh = x.sh;
   const int nb = je - jb;
   int64_t et0 = x.clock(), et1;
@@ -1038,7 +1052,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // 2. initial footprint; releases counted per contiguous access chunk of
   // each thread and scanned over (job, thread), so release slots are numbered
   // in access order (the scan's per-job totals are the release counts).
-  int64_t* rcnt = g.x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
+  int64_t* rcnt = E_x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
     int64_t fp = 0;
@@ -1115,20 +1129,20 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const int64_t slot = acc0 + a;
       const bool flagged = J.a_flag[a] != 0;
       if (J.a_type[a] == ACC_TGA) {
-        g.x_time[slot] = J.a_start[a];
-        g.x_type[slot] = int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0));
-        g.k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s]);
+        E_x_time[slot] = J.a_start[a];
+        E_x_type[slot] = int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0));
+        E_k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s]);
       } else {
-        g.x_time[slot] = J.a_end[a];
-        g.x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
-        g.k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s]);
+        E_x_time[slot] = J.a_end[a];
+        E_x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
+        E_k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s]);
       }
-      g.x_store[slot] = s; g.x_aid[slot] = a; g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
+      E_x_store[slot] = s; E_x_aid[slot] = a; E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
       if (flagged && !J.a_owned[a]) {
         const int64_t rs = acc0 + J.A + rel++;
-        g.x_time[rs] = J.a_end[a]; g.x_type[rs] = EV_REL; g.x_store[rs] = s; g.x_aid[rs] = a;
-        g.x_job[rs] = int8_t(b); g.k_val[rs] = int32_t(rs);
-        g.k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s]);
+        E_x_time[rs] = J.a_end[a]; E_x_type[rs] = EV_REL; E_x_store[rs] = s; E_x_aid[rs] = a;
+        E_x_job[rs] = int8_t(b); E_k_val[rs] = int32_t(rs);
+        E_k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s]);
       }
     }
     for (int32_t i = x.tid; i < st.S; i += x.nthr) {
@@ -1143,34 +1157,34 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
         type = EV_SIN;
         if (J.ev_wraps[i] && st.period > 0) when = ((when % st.period) + st.period) % st.period;
       }
-      g.x_time[slot] = when; g.x_type[slot] = int8_t(type); g.x_store[slot] = s; g.x_aid[slot] = -1;
-      g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
-      g.k_key[slot] = key(b, when, type, J.t_rank[s]);
+      E_x_time[slot] = when; E_x_type[slot] = int8_t(type); E_x_store[slot] = s; E_x_aid[slot] = -1;
+      E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
+      E_k_key[slot] = key(b, when, type, J.t_rank[s]);
     }
     for (int32_t r = x.tid; r < st.R; r += x.nthr) {
       const int32_t s = J.t_store[J.rc_tensor[r]];
       const int64_t slot = base + st.S + r;
       const int64_t when = J.a_start[J.rc_target[r]] - J.rc_lat[r];
-      g.x_time[slot] = when; g.x_type[slot] = EV_TGA; g.x_store[slot] = s; g.x_aid[slot] = -1;
-      g.x_job[slot] = int8_t(b); g.k_val[slot] = int32_t(slot);
-      g.k_key[slot] = key(b, when, EV_TGA, J.t_rank[s]);
+      E_x_time[slot] = when; E_x_type[slot] = EV_TGA; E_x_store[slot] = s; E_x_aid[slot] = -1;
+      E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
+      E_k_key[slot] = key(b, when, EV_TGA, J.t_rank[s]);
     }
   }
   x.sync();
   etick(1);
   // 5. timeline order (sort_timeline, peak.cpp:44-62)
-  x.sort(g.k_key, g.k_val, int32_t(n), jbits + tbits + 1 + rbits + 2);
+  x.sort(E_k_key, E_k_val, int32_t(n), jbits + tbits + 1 + rbits + 2);
   etick(2);
   // 6. group sorted positions by (job, storage), keeping timeline order
   for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int32_t slot = g.k_val[m];
-    g.x_order[m] = slot;
-    const int b = g.x_job[slot];
-    g.x_key2[m] = (uint64_t(b) << rbits) | uint64_t(g.jobs[jb + b].t_rank[g.x_store[slot]]);
-    g.x_seq2[m] = int32_t(m);
+    const int32_t slot = E_k_val[m];
+    E_x_order[m] = slot;
+    const int b = E_x_job[slot];
+    E_x_key2[m] = (uint64_t(b) << rbits) | uint64_t(g.jobs[jb + b].t_rank[E_x_store[slot]]);
+    E_x_seq2[m] = int32_t(m);
   }
   x.sync();
-  x.sort(g.x_key2, g.x_seq2, int32_t(n), jbits + rbits);
+  x.sort(E_x_key2, E_x_seq2, int32_t(n), jbits + rbits);
   etick(3);
   // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230),
   // in parallel: in (job, storage)-grouped order, the residency before an
@@ -1179,24 +1193,24 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // gives that index, and since a storage's events are contiguous it belongs
   // to the same storage iff its group key matches.
   {
-    int64_t* chg = reinterpret_cast<int64_t*>(g.k_key);  // free after sort 1
+    int64_t* chg = reinterpret_cast<int64_t*>(E_k_key);  // free after sort 1
     for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int ty = g.x_type[g.x_order[g.x_seq2[m]]] & 7;
+      const int ty = E_x_type[E_x_order[E_x_seq2[m]]] & 7;
       chg[m] = ty == EV_TUA ? -1 : m;
     }
     x.sync();
     x.scan_max(chg, int32_t(n));
     for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int32_t pos = g.x_seq2[m];
-      const int32_t slot = g.x_order[pos];
-      const int b = g.x_job[slot];
+      const int32_t pos = E_x_seq2[m];
+      const int32_t slot = E_x_order[pos];
+      const int b = E_x_job[slot];
       const JobDev& J = g.jobs[jb + b];
-      const int32_t s = g.x_store[slot];
-      const int ty = g.x_type[slot] & 7;
+      const int32_t s = E_x_store[slot];
+      const int ty = E_x_type[slot] & 7;
       const int64_t prev = m > 0 ? chg[m - 1] : -1;  // last state change strictly before m
       uint8_t res;
-      if (prev >= 0 && g.x_key2[prev] == g.x_key2[m]) {
-        const int pt = g.x_type[g.x_order[g.x_seq2[prev]]] & 7;
+      if (prev >= 0 && E_x_key2[prev] == E_x_key2[m]) {
+        const int pt = E_x_type[E_x_order[E_x_seq2[prev]]] & 7;
         res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
       } else {
         res = J.res_init[s];
@@ -1206,7 +1220,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       int errc = 0;
       switch (ty) {
         case EV_TGA:
-          if (!res) { eff = (g.x_type[slot] & 8) ? 0 : size; res = 1; }
+          if (!res) { eff = (E_x_type[slot] & 8) ? 0 : size; res = 1; }
           break;
         case EV_TUA: break;
         case EV_REL:
@@ -1219,19 +1233,19 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
           eff = size; res = 1;
           break;
       }
-      g.x_fp[pos] = eff;
-      g.x_state[pos] = res;
+      E_x_fp[pos] = eff;
+      E_x_state[pos] = res;
       if (errc) x.amin(&sh[b * NF + F_ERR], (int64_t(pos) << 3) | errc);
     }
     x.sync();
   }
   etick(4);
   // 8. footprint curve: inclusive scan of the effective deltas
-  x.scan(g.x_fp, int32_t(n));
+  x.scan(E_x_fp, int32_t(n));
   if (x.tid == 0) {
     for (int b = 0; b < nb; ++b) {
       int64_t* f = sh + b * NF;
-      f[F_OFF] = f[F_INIT] - (f[F_BASE] > 0 ? g.x_fp[f[F_BASE] - 1] : 0);
+      f[F_OFF] = f[F_INIT] - (f[F_BASE] > 0 ? E_x_fp[f[F_BASE] - 1] : 0);
     }
   }
   x.sync();
@@ -1242,10 +1256,10 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     int cb = -1;
     int64_t cmx = INT64_MIN;
     for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int b = g.x_job[g.x_order[m]];
+      const int b = E_x_job[E_x_order[m]];
       int64_t* f = sh + b * NF;
-      const int64_t fp = g.x_fp[m] + f[F_OFF];
-      g.x_fp[m] = fp;  // own element only: no cross-thread hazard after the scan
+      const int64_t fp = E_x_fp[m] + f[F_OFF];
+      E_x_fp[m] = fp;  // own element only: no cross-thread hazard after the scan
       if (fp < 0) x.amin(&f[F_ERR], (int64_t(m) << 3) | E_NEG_FOOTPRINT);
       if (b != cb) {
         if (cb >= 0) x.amax(&sh[cb * NF + F_MAXFP], cmx);
@@ -1261,9 +1275,9 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   etick(5);
   // 9. first strict maximum (analyze_peak, peak.cpp:236-241)
   for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int b = g.x_job[g.x_order[m]];
+    const int b = E_x_job[E_x_order[m]];
     int64_t* f = sh + b * NF;
-    if (f[F_MAXFP] > f[F_INIT] && g.x_fp[m] == f[F_MAXFP]) x.amin(&f[F_PPOS], m);
+    if (f[F_MAXFP] > f[F_INIT] && E_x_fp[m] == f[F_MAXFP]) x.amin(&f[F_PPOS], m);
   }
   x.sync();
   // 10. last_input_access at the peak; residency at the peak
@@ -1271,15 +1285,15 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     int cb = -1;
     int64_t cl = -1;
     for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int32_t slot = g.x_order[m];
-      const int b = g.x_job[slot];
+      const int32_t slot = E_x_order[m];
+      const int b = E_x_job[slot];
       const int64_t pp = sh[b * NF + F_PPOS];
       if (b != cb) {
         if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
         cb = b;
         cl = -1;
       }
-      if (pp != INT64_MAX && m <= pp && (g.x_type[slot] & 7) == EV_TUA && !(g.x_type[slot] & 16)) cl = m;
+      if (pp != INT64_MAX && m <= pp && (E_x_type[slot] & 7) == EV_TUA && !(E_x_type[slot] & 16)) cl = m;
     }
     if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
   }
@@ -1292,13 +1306,13 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // before the peak position: within a (job, storage) group positions ascend,
   // so that event is the one whose successor leaves the group or the prefix.
   for (int64_t m = x.tid; m < n; m += x.nthr) {
-    const int32_t pos = g.x_seq2[m];
-    const int32_t slot = g.x_order[pos];
-    const int b = g.x_job[slot];
+    const int32_t pos = E_x_seq2[m];
+    const int32_t slot = E_x_order[pos];
+    const int b = E_x_job[slot];
     const int64_t pp = sh[b * NF + F_PPOS];
     if (pp == INT64_MAX || pos > pp) continue;
-    if (m + 1 < n && g.x_key2[m + 1] == g.x_key2[m] && g.x_seq2[m + 1] <= pp) continue;
-    g.jobs[jb + b].in_peak[g.x_store[slot]] = g.x_state[pos];
+    if (m + 1 < n && E_x_key2[m + 1] == E_x_key2[m] && E_x_seq2[m + 1] <= pp) continue;
+    g.jobs[jb + b].in_peak[E_x_store[slot]] = E_x_state[pos];
   }
   x.sync();
   etick(6);
@@ -1312,8 +1326,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const int64_t base = f[F_BASE], nn = f[F_N];
     if (x.tid == 0) { J.curve_t[0] = 0; J.curve_b[0] = f[F_INIT]; }
     for (int64_t m = x.tid; m < nn; m += x.nthr) {
-      J.curve_t[m + 1] = g.x_time[g.x_order[base + m]];
-      J.curve_b[m + 1] = g.x_fp[base + m];
+      J.curve_t[m + 1] = E_x_time[E_x_order[base + m]];
+      J.curve_b[m + 1] = E_x_fp[base + m];
     }
   }
   x.sync();
@@ -1322,18 +1336,18 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       int64_t* f = sh + b * NF;
       if (f[F_ERR] != INT64_MAX && !g.err.code) {
         const int64_t pos = f[F_ERR] >> 3;
-        const int32_t slot = g.x_order[pos];
+        const int32_t slot = E_x_order[pos];
         g.err.code = int32_t(f[F_ERR] & 7);
         g.err.job = jb + b;
-        g.err.tensor = g.x_store[slot];
-        g.err.tick = g.x_time[slot];
+        g.err.tensor = E_x_store[slot];
+        g.err.tick = E_x_time[slot];
       }
       JobState& st = g.st[jb + b];
       const bool up = f[F_PPOS] != INT64_MAX;
       st.peak = up ? f[F_MAXFP] : f[F_INIT];
-      st.peak_time = up ? g.x_time[g.x_order[f[F_PPOS]]] : 0;
+      st.peak_time = up ? E_x_time[E_x_order[f[F_PPOS]]] : 0;
       st.has_lua = (up && f[F_LUA] >= 0) ? 1 : 0;
-      st.lua = st.has_lua ? g.x_aid[g.x_order[f[F_LUA]]] : -1;
+      st.lua = st.has_lua ? E_x_aid[E_x_order[f[F_LUA]]] : -1;
       st.n_peak = int32_t(f[F_NPEAK]);
       st.n_curve = int32_t(f[F_N] + 1);
       st.n_events = f[F_N];

@@ -963,11 +963,16 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // 0. initial residency (peak.cpp:176-190) and release-ownership scratch
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
-      int8_t k = J.t_kind[t];
-      J.res_init[t] = (J.t_store[t] == t && (k == K_PARAM || k == K_INPUT || k == K_OUTPUT)) ? 1 : 0;
+    const int8_t* const t_kind = J.t_kind;
+    const int32_t* const t_store = J.t_store;
+    uint8_t* const res_init = J.res_init;
+    uint8_t* const a_owned = J.a_owned;
+    const int32_t T = J.T, A = J.A;
+    for (int32_t t = x.tid; t < T; t += x.nthr) {
+      int8_t k = t_kind[t];
+      res_init[t] = (t_store[t] == t && (k == K_PARAM || k == K_INPUT || k == K_OUTPUT)) ? 1 : 0;
     }
-    for (int32_t a = x.tid; a < J.A; a += x.nthr) J.a_owned[a] = 0;
+    for (int32_t a = x.tid; a < A; a += x.nthr) a_owned[a] = 0;
   }
   x.sync();
   // 1. wrapped swap-ins leave the initial set; swap-outs own releases; time range
@@ -1124,25 +1129,39 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
     const int64_t idx = int64_t(b) * x.nthr + x.tid;
     int64_t rel = (idx > 0 ? rcnt[idx - 1] : 0) - (b > 0 ? rcnt[int64_t(b) * x.nthr - 1] : 0);
-    for (int32_t a = a0; a < a1; ++a) {
-      const int32_t s = J.a_store[a];
-      const int64_t slot = acc0 + a;
-      const bool flagged = J.a_flag[a] != 0;
-      if (J.a_type[a] == ACC_TGA) {
-        E_x_time[slot] = J.a_start[a];
-        E_x_type[slot] = int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0));
-        E_k_key[slot] = key(b, J.a_start[a], EV_TGA, J.t_rank[s]);
-      } else {
-        E_x_time[slot] = J.a_end[a];
-        E_x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
-        E_k_key[slot] = key(b, J.a_end[a], EV_TUA, J.t_rank[s]);
-      }
-      E_x_store[slot] = s; E_x_aid[slot] = a; E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
-      if (flagged && !J.a_owned[a]) {
-        const int64_t rs = acc0 + J.A + rel++;
-        E_x_time[rs] = J.a_end[a]; E_x_type[rs] = EV_REL; E_x_store[rs] = s; E_x_aid[rs] = a;
-        E_x_job[rs] = int8_t(b); E_k_val[rs] = int32_t(rs);
-        E_k_key[rs] = key(b, J.a_end[a], EV_REL, J.t_rank[s]);
+    {
+      const int32_t* const a_store = J.a_store;
+      const int32_t* const a_tensor = J.a_tensor;
+      const uint8_t* const a_flag = J.a_flag;
+      const uint8_t* const a_owned = J.a_owned;
+      const int8_t* const a_type = J.a_type;
+      const int64_t* const a_start = J.a_start;
+      const int64_t* const a_end = J.a_end;
+      const int32_t* const t_rank = J.t_rank;
+      const int32_t A = J.A;
+      for (int32_t a = a0; a < a1; ++a) {
+        const int32_t s = a_store[a];
+        const int64_t slot = acc0 + a;
+        const bool flagged = a_flag[a] != 0;
+        const int32_t rk = t_rank[s];
+        const int64_t te = a_end[a];
+        if (a_type[a] == ACC_TGA) {
+          const int64_t ts = a_start[a];
+          E_x_time[slot] = ts;
+          E_x_type[slot] = int8_t(EV_TGA | (a_tensor[a] != s ? 8 : 0));
+          E_k_key[slot] = key(b, ts, EV_TGA, rk);
+        } else {
+          E_x_time[slot] = te;
+          E_x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
+          E_k_key[slot] = key(b, te, EV_TUA, rk);
+        }
+        E_x_store[slot] = s; E_x_aid[slot] = a; E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
+        if (flagged && !a_owned[a]) {
+          const int64_t rs = acc0 + A + rel++;
+          E_x_time[rs] = te; E_x_type[rs] = EV_REL; E_x_store[rs] = s; E_x_aid[rs] = a;
+          E_x_job[rs] = int8_t(b); E_k_val[rs] = int32_t(rs);
+          E_k_key[rs] = key(b, te, EV_REL, rk);
+        }
       }
     }
     for (int32_t i = x.tid; i < st.S; i += x.nthr) {

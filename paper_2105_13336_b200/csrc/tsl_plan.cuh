@@ -981,44 +981,58 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const JobState& st = g.st[jb + b];
     int64_t lmin = INT64_MAX, lmax = INT64_MIN;
     if (x.tid == 0 && J.A > 0) { lmin = J.a_start[0]; lmax = J.a_end[J.A - 1]; }
+    const int32_t* const L_t_store = J.t_store;
+    const int32_t* const L_ev_tensor = J.ev_tensor;
+    const int64_t* const L_ev_end = J.ev_end;
+    const int64_t* const L_ev_start = J.ev_start;
+    const int64_t* const L_ev_trig = J.ev_trig;
+    const int8_t* const L_ev_dir = J.ev_dir;
+    const int8_t* const L_ev_wraps = J.ev_wraps;
+    uint8_t* const L_res_init = J.res_init;
+    uint8_t* const L_a_owned = J.a_owned;
+    const int64_t* const L_a_end = J.a_end;
+    const int64_t* const L_a_start = J.a_start;
+    const int32_t* const L_s_off = J.s_off;
+    const int32_t* const L_s_acc = J.s_acc;
+    const int32_t L_A = J.A;
     for (int32_t i = x.tid; i < st.S; i += x.nthr) {
-      const int32_t s = J.t_store[J.ev_tensor[i]];
-      int64_t when = J.ev_end[i];
-      if (J.ev_dir[i] == 1) {
-        if (J.ev_wraps[i]) {
-          J.res_init[s] = 0;
+      const int32_t s = L_t_store[L_ev_tensor[i]];
+      int64_t when = L_ev_end[i];
+      if (L_ev_dir[i] == 1) {
+        if (L_ev_wraps[i]) {
+          L_res_init[s] = 0;
           if (st.period > 0) when = ((when % st.period) + st.period) % st.period;
         }
       } else {
-        const int64_t tr = J.ev_trig[i];
+        const int64_t tr = L_ev_trig[i];
         if (tr != -1) {
-          if (tr < 0 || tr >= J.A) {
+          if (tr < 0 || tr >= L_A) {
             x.amax(&gsh[4], 1);
           } else {
-            when = imax(when, J.a_end[tr]);
+            when = imax(when, L_a_end[tr]);
           }
         }
         // peak.cpp:107-130: a flagged access a loses its release when a
         // swap-out of its storage starts in [a.end, next access start).
         // With m = the last storage access start <= t, that is m < a.end <= t.
-        const int64_t t0 = J.ev_start[i];
-        const int32_t k0 = J.s_off[s], k1 = J.s_off[s + 1];
+        const int64_t t0 = L_ev_start[i];
+        const int32_t k0 = L_s_off[s], k1 = L_s_off[s + 1];
         int32_t lo = k0, hi = k1;
         while (lo < hi) {
           int32_t md = (lo + hi) >> 1;
-          if (J.a_start[J.s_acc[md]] <= t0) lo = md + 1; else hi = md;
+          if (L_a_start[L_s_acc[md]] <= t0) lo = md + 1; else hi = md;
         }
         if (lo > k0) {
-          const int64_t m = J.a_start[J.s_acc[lo - 1]];
+          const int64_t m = L_a_start[L_s_acc[lo - 1]];
           int32_t l2 = k0, h2 = k1;  // first position with end > m
           while (l2 < h2) {
             int32_t md = (l2 + h2) >> 1;
-            if (J.a_end[J.s_acc[md]] <= m) l2 = md + 1; else h2 = md;
+            if (L_a_end[L_s_acc[md]] <= m) l2 = md + 1; else h2 = md;
           }
           for (int32_t k = l2; k < k1; ++k) {
-            int32_t a = J.s_acc[k];
-            if (J.a_end[a] > t0) break;
-            J.a_owned[a] = 1;
+            int32_t a = L_s_acc[k];
+            if (L_a_end[a] > t0) break;
+            L_a_owned[a] = 1;
           }
         }
       }

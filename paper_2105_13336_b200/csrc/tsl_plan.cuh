@@ -1233,11 +1233,18 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     }
     x.sync();
     x.scan_max(chg, int32_t(n));
+    int cb = -1;
+    const uint8_t* c_res = nullptr;
+    const int64_t* c_size = nullptr;
     for (int64_t m = x.tid; m < n; m += x.nthr) {
       const int32_t pos = E_x_seq2[m];
       const int32_t slot = E_x_order[pos];
       const int b = E_x_job[slot];
-      const JobDev& J = g.jobs[jb + b];
+      if (b != cb) {  // job arrays cached in registers (the byte stores below alias the struct)
+        cb = b;
+        c_res = g.jobs[jb + b].res_init;
+        c_size = g.jobs[jb + b].t_size;
+      }
       const int32_t s = E_x_store[slot];
       const int ty = E_x_type[slot] & 7;
       const int64_t prev = m > 0 ? chg[m - 1] : -1;  // last state change strictly before m
@@ -1246,9 +1253,9 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
         const int pt = E_x_type[E_x_order[E_x_seq2[prev]]] & 7;
         res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
       } else {
-        res = J.res_init[s];
+        res = c_res[s];
       }
-      const int64_t size = J.t_size[s];
+      const int64_t size = c_size[s];
       int64_t eff = 0;
       int errc = 0;
       switch (ty) {
@@ -1332,7 +1339,10 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   }
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) J.in_peak[t] = J.res_init[t];
+    uint8_t* const in_peak = J.in_peak;
+    const uint8_t* const res_init = J.res_init;
+    const int32_t T = J.T;
+    for (int32_t t = x.tid; t < T; t += x.nthr) in_peak[t] = res_init[t];
   }
   x.sync();
   // A storage's residency at the peak is its state after its last event at or

@@ -162,6 +162,7 @@ typedef struct tsl_stats {
   int64_t cyc_pendsort;
   int64_t fitprof[9];
   int64_t evalprof[7];  /* evaluator phases: prep, emit, sort1, group, automaton, scan.., peak..report */
+  int64_t queryprof[16];  /* development profile of re-score queries (zero unless built with TSL_PROF) */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import math
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -77,8 +78,19 @@ def random_job(seed: int):
     return json.loads(_take(g)), json.loads(_take(l))
 
 
+def _wire_config(config) -> dict:
+    """JSON cannot carry NaN / infinity: non-finite max_swap_ratios travel as
+    strings, which ref_shim.cpp's parse_config converts back with std::stod."""
+    r = config.get("max_swap_ratios")
+    if not r or all(math.isfinite(v) for v in r.values()):
+        return config
+    c = dict(config)
+    c["max_swap_ratios"] = {k: (v if math.isfinite(v) else repr(float(v))) for k, v in r.items()}
+    return c
+
+
 def request(jobs, config) -> str:
-    return json.dumps({"config": config, "jobs": [{"graph": g, "latencies": l} for g, l in jobs]})
+    return json.dumps({"config": _wire_config(config), "jobs": [{"graph": g, "latencies": l} for g, l in jobs]})
 
 
 def initial_peaks(jobs) -> dict:

@@ -59,9 +59,11 @@ PlannerConfig parse_config(const json& c) {
     cfg.replan_threshold = c["replan_threshold"].get<double>();
   if (c.contains("stall_epsilon")) cfg.stall_epsilon = c["stall_epsilon"].get<double>();
   if (c.contains("stall_min_iters")) cfg.stall_min_iters = c["stall_min_iters"].get<int>();
+  // JSON has no NaN / infinity: oracle/ref.py sends non-finite ratios as the
+  // strings "nan" / "inf" / "-inf" (PlannerConfig::validate lets NaN through)
   if (c.contains("max_swap_ratios"))
     for (const auto& [k, v] : c["max_swap_ratios"].items())
-      cfg.max_swap_ratios[k] = v.get<double>();
+      cfg.max_swap_ratios[k] = v.is_string() ? std::stod(v.get<std::string>()) : v.get<double>();
   return cfg;
 }
 

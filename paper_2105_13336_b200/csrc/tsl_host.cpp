@@ -289,7 +289,7 @@ struct JobPlace {  // byte offsets into the device buffer
   size_t a_tensor, a_store, a_type, a_start, a_end, a_base, a_flag, a_owned, s_off, s_acc, t_wfirst, t_utga;
   size_t ev[12], bz_s, bz_e, pd_s, pd_e, pd_ts, pd_te, bzi_s, bzi_e, ai_e, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
   size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve;
-  int32_t Scap, Rcap, Ecap;
+  int32_t Scap, Rcap, Ecap, ti_nb;
 };
 
 struct GroupPlace {
@@ -359,7 +359,10 @@ struct tsl_plan {
   tsl_ctx* ctx = nullptr;
   Buffers* buf = nullptr;  // ctx->buf, or own_buf for a prepared plan
   Buffers own_buf;
-  ~tsl_plan() { own_buf.release(); }
+  ~tsl_plan() {
+    if (done) cudaEventDestroy(done);
+    own_buf.release();
+  }
   int mode = 0;  // 0 build_plan, 1 analyze_job
   int32_t n_groups = 0;
   std::vector<std::vector<GraphP>> graphs;  // per group, caller order (a descriptor seen twice is loaded once)
@@ -380,6 +383,7 @@ struct tsl_plan {
   bool coop = false;      // big and one group: cooperative launch, one CTA per SM
   size_t res_bytes = 0;   // shared memory for resident job arrays (build mode)
   tsl::CoopCtl coop_init{};  // initial cooperative control block (uploaded before each launch)
+  cudaEvent_t done = nullptr;  // recorded after the last asynchronous launch (tsl_plan_launch_async)
   int64_t n_accesses = 0;
 };
 
@@ -524,6 +528,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.Scap = 2 * g.A + 2;
       p.Rcap = g.T + 1;
       p.Ecap = 2 * g.A + p.Scap + p.Rcap;
+      // time-index buckets (per job; a finer index for the big jobs measured
+      // only 7 % faster re-score queries on C4 -- the bisection steps after
+      // the coarse index mostly hit L1 -- and made index rebuilds costlier)
+      p.ti_nb = tsl::TI_NB_HOST;
       P->n_accesses += g.A;
       P->jp[gi].push_back(p);
     }
@@ -601,9 +609,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.pd_e = L.take<int64_t>(p.Scap);
       p.pd_ts = L.take<int64_t>(p.Scap);
       p.pd_te = L.take<int64_t>(p.Scap);
-      p.bzi_s = L.take<int32_t>(tsl::TI_NB_HOST + 1);
-      p.bzi_e = L.take<int32_t>(tsl::TI_NB_HOST + 1);
-      p.ai_e = L.take<int32_t>(tsl::TI_NB_HOST + 1);
+      p.bzi_s = L.take<int32_t>(size_t(p.ti_nb) + 1);
+      p.bzi_e = L.take<int32_t>(size_t(p.ti_nb) + 1);
+      p.ai_e = L.take<int32_t>(size_t(p.ti_nb) + 1);
       p.st_evcnt = L.take<int32_t>(g.T);
       p.swapped = L.take<uint8_t>(g.T);
       p.ev_drop = L.take<uint8_t>(p.Scap);
@@ -674,12 +682,16 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     std::vector<int32_t> jrank = lex_rank(jids);
     const tsl_config* cfg = &cfgs[n_cfgs == 1 ? 0 : gi];
     const std::map<std::string, double> ratios = mode == 0 ? ratio_map(*cfg) : std::map<std::string, double>{};
+    // jobs interact through SwapBudget::allows (swap_planner.cpp:268-276)
+    // unless every ratio is >= 1; a NaN ratio (it passes validate) couples too
     bool coupled = false;
-    for (auto& g : gs) coupled = coupled || ratio_of(ratios, g->job_id) < 1.0;
+    for (auto& g : gs) coupled = coupled || !(ratio_of(ratios, g->job_id) >= 1.0);
     GroupDev* G = hp<GroupDev>(ctx, P->groups_off) + gi;
     std::memset(G, 0, sizeof *G);
     G->n_jobs = static_cast<int32_t>(gs.size());
     G->coupled = coupled ? 1 : 0;
+    G->spec_window = 0;
+    if (const char* e = std::getenv("TSL_SPEC_WINDOW")) G->spec_window = std::atoi(e);
     G->hist_cap = P->gp[gi].hist_cap;
     G->cfg.bw = cfg->pcie_bandwidth;
     G->cfg.setup = cfg->transfer_setup;
@@ -746,7 +758,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       JobDev* J = hp<JobDev>(ctx, P->jobs_off) + jglob;
       std::memset(J, 0, sizeof *J);
       J->A = g.A; J->T = g.T; J->O = g.O; J->rank = jrank[k]; J->ratio = ratio_of(ratios, g.job_id);
-      J->Scap = p.Scap; J->Rcap = p.Rcap; J->Ecap = p.Ecap;
+      J->Scap = p.Scap; J->Rcap = p.Rcap; J->Ecap = p.Ecap; J->ti_nb = p.ti_nb;
       J->topo = dp<int32_t>(ctx, p.topo);
       J->o_lat = dp<int64_t>(ctx, p.o_lat);
       J->o_in_off = dp<int32_t>(ctx, p.o_in_off);
@@ -1007,6 +1019,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   for (int k = 0; k < 4; ++k) s.fitprof[k] = G.stats.cyc[16 + k];
   for (int k = 0; k < 5; ++k) s.fitprof[4 + k] = G.stats.cyc[27 + k];
   for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
+  for (int k = 0; k < 16; ++k) s.queryprof[k] = G.stats.prof[k];
   return R;
 }
 
@@ -1210,6 +1223,7 @@ int tsl_plan_run(tsl_plan* P, int32_t repeats, double* kernel_ms) {
   if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     tsl_ctx* c = P->ctx;
+    cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
     launch(P, std::max(1, repeats), true);
     cuda_check(cudaEventSynchronize(c->ev1), "sync");
     float ms = 0;
@@ -1223,15 +1237,22 @@ int tsl_plan_launch_async(tsl_plan* P, void* stream) {
   if (!P) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
     tsl_ctx* c = P->ctx;
+    cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+    const cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     cuda_check(launch_plan_kernel(dp<GroupDev>(P->buf, P->groups_off), P->n_groups, P->mode, P->max_jobs, P->ipt,
-                                  P->res_bytes, P->big, P->coop, stream ? static_cast<cudaStream_t>(stream) : c->stream), "launch");
+                                  P->res_bytes, P->big, P->coop, s), "launch");
+    if (!P->done) cuda_check(cudaEventCreateWithFlags(&P->done, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(P->done, s), "event record");
   });
 }
 
 int tsl_plan_collect(tsl_plan* P, tsl_result** out) {
   if (!P || !out) { g_err = "null argument"; return TSL_ERR_ARGUMENT; }
   return guard([&] {
-    cuda_check(cudaDeviceSynchronize(), "sync");  // launches may sit on a caller stream
+    cuda_check(cudaSetDevice(P->ctx->device), "cudaSetDevice");
+    // the last asynchronous launch may sit on a caller stream: wait for it
+    // alone (not the whole device), then read back on the context's stream
+    if (P->done) cuda_check(cudaEventSynchronize(P->done), "sync");
     download(P, P->ctx->stream);
     std::vector<tsl_result*> rs;
     try {

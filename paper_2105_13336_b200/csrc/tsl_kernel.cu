@@ -4,6 +4,7 @@
 // warp votes and atomics.
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
+#include <mutex>
 #include <type_traits>
 
 #include "tsl_plan.cuh"
@@ -325,7 +326,7 @@ struct DevX {
     const int64_t *as = c->fa_s, *ae = c->fa_e, *bs = c->fb_s, *be = c->fb_e;
     int64_t *ms = c->fm_s, *me = c->fm_e, *os = c->fo_s, *oe = c->fo_e;
     int32_t *is = c->fi_s, *ie = c->fi_e;
-    const int32_t n1 = c->fn1, n2 = c->fn2, shift = c->fshift, n = n1 + n2;
+    const int32_t n1 = c->fn1, n2 = c->fn2, shift = c->fshift, nb = c->fnb, n = n1 + n2;
     const int64_t wt = int64_t(cta - 1) * NT + tid, WT = int64_t(grid - 1) * NT;
     const int64_t per = (n + WT - 1) / WT;
     const int32_t d0 = int32_t(min(int64_t(n), wt * per)), d1 = int32_t(min(int64_t(n), int64_t(d0) + per));
@@ -350,9 +351,9 @@ struct DevX {
         const int64_t kp = kk > 0 ? __ldcg(&keys[kk - 1]) : 0, kc = kk < n ? __ldcg(&keys[kk]) : 0;
         int64_t blo = kk == 0 ? 0 : (kp >> shift) + 1;
         if (kk > 0 && kp < 0) blo = 0;
-        int64_t bhi = kk == n ? TI_NB : (kc < 0 ? -1 : (kc >> shift));
+        int64_t bhi = kk == n ? nb : (kc < 0 ? -1 : (kc >> shift));
         if (kk < n && kc >= 0 && (kc & ((int64_t(1) << shift) - 1)) != 0) bhi = kc >> shift;
-        if (bhi > TI_NB) bhi = TI_NB;
+        if (bhi > nb) bhi = nb;
         for (int64_t b = blo; b <= bhi; ++b) __stcg(&first[b], int32_t(kk));
       }
     }
@@ -366,20 +367,24 @@ struct DevX {
   // Commit-list length that triggers a fold into the busy structure: folds on
   // the worker CTAs are cheap, a fold by one warp is linear in the structure.
   __device__ int32_t fold_threshold(int32_t bz_n) const {
-    return (coop && grid >= 3) ? TSL_COOP_FOLD : max(PEND_MERGE, bz_n / 128);
+    return coop_folds() ? TSL_COOP_FOLD : max(PEND_MERGE, bz_n / 128);
   }
+  // Folds go to the worker CTAs only when one deciding warp exists: with
+  // several jobs their warps decide concurrently and would race for the
+  // single control block, so they fold on their own warp.
+  __device__ bool coop_folds() const { return coop && grid >= 3 && coop_group && coop_group->n_jobs == 1; }
 
   // Deciding warp of CTA 0 (warp-collective): hand a busy-structure fold to
   // the worker CTAs and wait. False when there are no workers.
   __device__ bool fold_hook(const int64_t* as, const int64_t* ae, int32_t n1, const int64_t* bs, const int64_t* be,
                             int32_t n2, int64_t* ms, int64_t* me, int64_t* os, int64_t* oe, int32_t* is, int32_t* ie,
-                            int shift) {
-    if (!coop || grid < 3) return false;
+                            int shift, int32_t nb) {
+    if (!coop_folds()) return false;
     __syncwarp();
     if (lane == 0) {
       volatile CoopCtl* c = coop;
       c->fa_s = as; c->fa_e = ae; c->fb_s = bs; c->fb_e = be; c->fm_s = ms; c->fm_e = me; c->fo_s = os;
-      c->fo_e = oe; c->fi_s = is; c->fi_e = ie; c->fn1 = n1; c->fn2 = n2; c->fshift = shift; c->fdone = 0;
+      c->fo_e = oe; c->fi_s = is; c->fi_e = ie; c->fn1 = n1; c->fn2 = n2; c->fshift = shift; c->fnb = nb; c->fdone = 0;
       c->type = COOP_FOLD;
       __threadfence();
       atomicAdd(&coop->epoch, 1);
@@ -838,8 +843,14 @@ cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int m
                                bool big, bool coop, cudaStream_t stream) {
   if (mode != 0 || max_jobs > RES_MAX_JOBS || big) res_bytes = 0;
   const size_t smem = kernel_smem_bytes(max_jobs, ipt, res_bytes, big);
-  static size_t attr = 0;  // (per process: one device)
-  if (smem != attr) {
+  // the kernel attributes are per device: remember the last size set on each
+  // (guarded: several host threads may launch plans)
+  static std::mutex attr_mu;
+  static size_t attr[64] = {};
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur < 0 || cur >= 64) cur = 0;
+  std::lock_guard<std::mutex> lock(attr_mu);
+  if (smem != attr[cur]) {
     cudaError_t e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // The planner is a latency-bound dependent-load chain over data that
@@ -849,7 +860,7 @@ cudaError_t launch_plan_kernel(GroupDev* d_groups, int n_groups, int mode, int m
     const int pct = int(((smem + 1024) * 100 + full - 1) / full);
     e = cudaFuncSetAttribute(tsl_plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[cur] = smem;
   }
   unsigned tb = (unsigned)tmp_bytes_for(ipt), rb = (unsigned)res_bytes;
   int bg = big ? 1 : 0;

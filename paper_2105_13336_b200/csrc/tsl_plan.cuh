@@ -51,6 +51,9 @@
 
 namespace tsl {
 
+#ifndef TSL_PROF
+#define TSL_PROF 0
+#endif
 #ifndef TSL_DEBUG_REASONS
 #define TSL_DEBUG_REASONS 0
 #endif
@@ -128,8 +131,9 @@ TSL_HD void stream_load(Stream& q, bool fwd, int64_t b, int64_t e) {
 constexpr int TI_NB = 256;
 
 struct TIndex {
-  const int32_t* first;  // [TI_NB + 1] or null
+  const int32_t* first;  // [nb + 1] or null
   int32_t shift;
+  int32_t nb;            // bucket count (TI_NB, or the job's finer ti_nb)
 };
 
 // First index k in [0, n) with key(k) > v (strict) or key(k) >= v, for
@@ -144,9 +148,9 @@ TSL_HD_FORCE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t 
     // all k before first[b] have key < (b << shift) <= v; from first[b + 1]
     // on, key >= (b + 1) << shift > v
     int64_t bk = v >> ti->shift;
-    if (bk > TI_NB) bk = TI_NB;
+    if (bk > ti->nb) bk = ti->nb;
     lo = ti->first[bk];
-    if (bk < TI_NB) hi = imin(hi, ti->first[bk + 1]);
+    if (bk < ti->nb) hi = imin(hi, ti->first[bk + 1]);
     if (lo > hi) lo = hi;
   }
   while (lo < hi) {
@@ -157,24 +161,24 @@ TSL_HD_FORCE int32_t search_keys(const int64_t* arr, const int32_t* ix, int32_t 
   return lo;
 }
 
-TSL_HD int tindex_shift(int64_t max_key) {
+TSL_HD int tindex_shift(int64_t max_key, int32_t nb = TI_NB) {
   int sh = 0;
-  while (max_key > 0 && (max_key >> sh) >= TI_NB) ++sh;
+  while (max_key > 0 && (max_key >> sh) >= nb) ++sh;
   return sh;
 }
 
-// Builds first[0..TI_NB] for keys[0, n) (nondecreasing, >= 0); CTA-collective
+// Builds first[0..nb] for keys[0, n) (nondecreasing, >= 0); CTA-collective
 // (kWarp: warp-collective).
 template <class X, bool kWarp = false>
-TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, int shift) {
+TSL_HD void build_tindex(X& x, const int64_t* keys, int32_t n, int32_t* first, int shift, int32_t nb) {
   const int32_t t0 = kWarp ? x.lane : x.tid, dt = kWarp ? X::W : x.nthr;
   for (int32_t k = t0; k <= n; k += dt) {
     // buckets b with key(k-1) < (b << shift) <= key(k) get first[b] = k
     int64_t lo = k == 0 ? 0 : (keys[k - 1] >> shift) + 1;
     if (k > 0 && keys[k - 1] < 0) lo = 0;
-    int64_t hi = k == n ? TI_NB : (keys[k] < 0 ? -1 : (keys[k] >> shift));
+    int64_t hi = k == n ? nb : (keys[k] < 0 ? -1 : (keys[k] >> shift));
     if (k < n && keys[k] >= 0 && (keys[k] & ((int64_t(1) << shift) - 1)) != 0) hi = keys[k] >> shift;
-    if (hi > TI_NB) hi = TI_NB;
+    if (hi > nb) hi = nb;
     for (int64_t b = lo; b <= hi; ++b) first[b] = k;
   }
   if constexpr (kWarp) x.wsync();
@@ -253,7 +257,7 @@ TSL_HD_FORCE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q,
   const int64_t* SE[3] = {nsrc > 0 ? src[0].e : nullptr, nsrc > 1 ? src[1].e : nullptr, J.a_end};
   const int32_t* IX[3] = {nullptr, nullptr, J.s_acc + a0};
   const int32_t SN[3] = {nsrc > 0 ? src[0].n : 0, nsrc > 1 ? src[1].n : 0, na};
-  const TIndex NOI{nullptr, 0};
+  const TIndex NOI{nullptr, 0, 0};
   const TIndex TIS[3] = {nsrc > 0 ? src[0].is : NOI, nsrc > 1 ? src[1].is : NOI, NOI};
   const TIndex TIE[3] = {nsrc > 0 ? src[0].ie : NOI, nsrc > 1 ? src[1].ie : NOI, NOI};
   int64_t S0[3], EN[3];
@@ -305,7 +309,7 @@ TSL_HD_FORCE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q,
       HE[z] = wp.shfl(mhe, z);
       LIVE[z] = wp.shfl(ml ? 1 : 0, z) != 0;
     }
-    if (prof) { int64_t t = clk(); prof[5] += t - tp0; tp0 = t; }
+    if (prof) { int64_t t = clk(); prof[1] += t - tp0; tp0 = t; }
   } else {
 #pragma unroll
     for (int z = 0; z < 9; ++z) open(z, I[z], HS[z], HE[z], LIVE[z]);
@@ -410,7 +414,7 @@ TSL_HD_FORCE int64_t fit(const JobDev& J, const JobState& st, const FitQuery& q,
     if (found || (cur > q.b && cur - q.b >= q.d)) result = cur - q.d;
   }
   if (swept) *swept += n_swept;
-  if (prof) { prof[2] += clk() - tp0; }
+  if (prof) { prof[2] += clk() - tp0; prof[9] += n_swept; }
   return result;
 }
 
@@ -427,7 +431,7 @@ struct NoClock {
 TSL_HD_FORCE void anchor(const JobDev& J, const JobState& st, int64_t t, bool wrapped, int64_t& trig,
                    int64_t& delta) {
   if (wrapped && st.period > 0) t = ((t % st.period) + st.period) % st.period;
-  const TIndex ti{J.ai_e, st.ai_shift};
+  const TIndex ti{J.ai_e, st.ai_shift, J.ti_nb};
   const int32_t lo = search_keys(J.a_end, nullptr, J.A, t, true, &ti);
   if (lo == 0) { trig = -1; delta = t; }
   else { trig = lo - 1; delta = t - J.a_end[lo - 1]; }
@@ -603,8 +607,8 @@ struct ReCtx {
   int64_t* dbg = nullptr;  // development cycle counters (thread 0 only)
   // a query made by one lane on its own (gap pairs in parallel)
   TSL_HD int64_t query_lane(const FitQuery& q, bool latest) {
-    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift, J.ti_nb}, {J.bzi_e, st.bzi_shift, J.ti_nb}},
+                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0, 0}, {nullptr, 0, 0}}};
     int64_t sw = 0;
     const int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr);
     if (x.lane == 0) { gs->fit_queries += 1; gs->busy_intervals += sw; }
@@ -612,10 +616,25 @@ struct ReCtx {
   }
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
     const int64_t c0 = x.clock();
-    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}},
-                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0}, {nullptr, 0}}};
+    Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift, J.ti_nb}, {J.bzi_e, st.bzi_shift, J.ti_nb}},
+                   {pb.s, pb.e, st.pend_sorted, {nullptr, 0, 0}, {nullptr, 0, 0}}};
     int64_t sw = 0;
+#if TSL_PROF
+    // development profile (TSL_PROF builds only): per-source search cycles
+    // summed over the lanes that opened them, the rest from lane 0
+    int64_t lp[10] = {};
+    auto clk = [] { return int64_t(clock64()); };
+    int64_t r = fit(J, st, q, latest, src, 2, &sw, clk, lp, WarpOf<X>{x});
+    for (int k = 0; k < 10; ++k) {
+      int64_t v = lp[k];
+      if (k >= 3 && k <= 8)
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (x.lane == 0) gs->prof[k] += v;
+    }
+    if (x.lane == 0) gs->prof[10] += 1;
+#else
     int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr, WarpOf<X>{x});
+#endif
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (dbg && x.tid == 0) { dbg[0] += x.clock() - c0; dbg[1] += 1; }
@@ -649,7 +668,10 @@ constexpr int GS_PCAP = 160;    // gsh slots: per-job reserved pair slots of a p
 constexpr int GS_POFF = 300;    // gsh slots: per-job pend buffer offsets in shared scratch
 constexpr int GS_WK = 440;      // gsh slot: window-index bucket shift + 1 (0: no window index this pass)
 constexpr int GS_NB = 441;      // gsh slot: bucket count of this pass's indexes
+constexpr int GS_PPOOL = 442;   // gsh slot: pair-pool bump counter of the pass
+constexpr int GS_WPOOL = 443;   // gsh slot: window-pool bump counter of the pass
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
+static_assert(MAXB * 16 + 443 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
 constexpr int CB_GRID_MAX = 160;  // passes with at most this many candidates check all pairs directly
@@ -673,7 +695,7 @@ struct SpecCtx {
   int32_t nwin, cap_win;
   bool overflow;
   TSL_HD int64_t query(const FitQuery& q, bool latest) {
-    Src src[1] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift}, {J.bzi_e, st.bzi_shift}}};
+    Src src[1] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift, J.ti_nb}, {J.bzi_e, st.bzi_shift, J.ti_nb}}};
     int64_t sw = 0;
     int64_t r = fit(J, st, q, latest, src, 1, &sw, NoClock{}, nullptr);
     gs->fit_queries += 1;
@@ -1471,21 +1493,21 @@ TSL_HD void build_busy_index(X& x, GroupDev& g, int j) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   const int32_t n = st.S;
-  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0);
+  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0, J.ti_nb);
   x.sync();
   if (x.tid == 0) st.bzi_shift = sh;
-  build_tindex(x, J.bz_s, n, J.bzi_s, sh);
-  build_tindex(x, J.bz_e, n, J.bzi_e, sh);
+  build_tindex(x, J.bz_s, n, J.bzi_s, sh, J.ti_nb);
+  build_tindex(x, J.bz_e, n, J.bzi_e, sh, J.ti_nb);
 }
 
 template <class X>
 TSL_HD void build_anchor_index(X& x, GroupDev& g, int j) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
-  const int sh = tindex_shift(J.A ? imax(J.a_end[J.A - 1], 0) : 0);
+  const int sh = tindex_shift(J.A ? imax(J.a_end[J.A - 1], 0) : 0, J.ti_nb);
   x.sync();
   if (x.tid == 0) st.ai_shift = sh;
-  build_tindex(x, J.a_end, J.A, J.ai_e, sh);
+  build_tindex(x, J.a_end, J.A, J.ai_e, sh, J.ti_nb);
 }
 
 // Sorted busy structure of every job rebuilt from the plan: block sorts of
@@ -1576,8 +1598,8 @@ TSL_HD void merge_pend_into_busy(X& x, GroupDev& g, int j, const PendBuf& pb) {
   {
     // a cooperative launch folds on its worker CTAs
     const int64_t mx = imax(n1 ? J.bz_e[n1 - 1] : 0, n2 ? pb.e[n2 - 1] : 0);
-    const int sh = tindex_shift(imax(mx, 0));
-    if (x.fold_hook(bs, be, n1, pb.s, pb.e, n2, ms, me, J.bz_s, J.bz_e, J.bzi_s, J.bzi_e, sh)) {
+    const int sh = tindex_shift(imax(mx, 0), J.ti_nb);
+    if (x.fold_hook(bs, be, n1, pb.s, pb.e, n2, ms, me, J.bz_s, J.bz_e, J.bzi_s, J.bzi_e, sh, J.ti_nb)) {
       x.wsync();
       st.bz_n = n;
       st.pend_n = 0;
@@ -1602,15 +1624,49 @@ TSL_HD void merge_pend_into_busy(X& x, GroupDev& g, int j, const PendBuf& pb) {
   x.wsync();
   for (int32_t d = x.lane; d < n; d += X::W) { J.bz_s[d] = ms[d]; J.bz_e[d] = me[d]; }
   x.wsync();
-  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0);
+  const int sh = tindex_shift(n ? imax(J.bz_e[n - 1], 0) : 0, J.ti_nb);
   x.wsync();
   st.bz_n = n;
   st.pend_n = 0;
   st.pend_sorted = 0;
   st.bzi_shift = sh;
   x.wsync();
-  build_tindex<X, true>(x, J.bz_s, n, J.bzi_s, sh);
-  build_tindex<X, true>(x, J.bz_e, n, J.bzi_e, sh);
+  build_tindex<X, true>(x, J.bz_s, n, J.bzi_s, sh, J.ti_nb);
+  build_tindex<X, true>(x, J.bz_e, n, J.bzi_e, sh, J.ti_nb);
+}
+
+// Appends the intervals of the candidates taken verbatim (speculation kept)
+// since the last append, up to candidate m, to the job's pend list, 32
+// candidates at a time (a warp prefix sum places them in plan order).
+// Warp-collective; false on overflow.
+template <class X>
+TSL_HD bool pend_append(X& x, GroupDev& g, int j, int64_t m, const int32_t* cand, const int32_t* cinfo, PendBuf& pb,
+                        ErrInfo& lerr) {
+  JobState& st = g.st[j];
+  for (int64_t q0 = st.pend_upto; q0 < m; q0 += X::W) {
+    const int64_t q = q0 + x.lane;
+    const int32_t* cq = cinfo + q * CI_STRIDE;
+    const int32_t nq = (q < m && cq[CI_STATE] == 1 && (cand[q] >> 24) == j) ? cq[CI_NP] : 0;
+    int32_t tot = 0;
+    const int32_t ex = x.wexcl(2 * nq, &tot);
+    const int32_t pn = st.pend_n;
+    if (pn + tot > pb.cap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = pb.cap; return false; }
+    x.wsync();
+    if (nq) {
+      const PairRec* pr = g.pr_pool + cq[CI_P0];
+      for (int32_t p = 0; p < nq; ++p) {
+        const int32_t o = pn + ex + 2 * p;
+        pb.s[o] = pr[p].os; pb.e[o] = pr[p].oe;
+        pb.s[o + 1] = pr[p].is; pb.e[o + 1] = pr[p].ie;
+      }
+    }
+    st.pend_n = pn + tot;
+    x.wsync();
+  }
+  x.wsync();
+  st.pend_upto = int32_t(m);  // callers never move backwards (m >= pend_upto)
+  x.wsync();
+  return true;
 }
 
 // Re-scores candidate m of job j exactly against the real state: pass-start
@@ -1625,31 +1681,7 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   int32_t* ci = cinfo + m * CI_STRIDE;
   ls.rescored += 1;
   const int64_t rc0 = x.clock();
-  // candidates taken verbatim since the last re-score: their intervals, 32
-  // candidates at a time (a warp prefix sum places them in plan order)
-  for (int64_t q0 = st.pend_upto; q0 < m; q0 += X::W) {
-    const int64_t q = q0 + x.lane;
-    const int32_t* cq = cinfo + q * CI_STRIDE;
-    const int32_t nq = (q < m && cq[CI_STATE] == 1 && (cand[q] >> 24) == j) ? cq[CI_NP] : 0;
-    int32_t tot = 0;
-    const int32_t ex = x.wexcl(2 * nq, &tot);
-    const int32_t pn = st.pend_n;
-    if (pn + tot > pb.cap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = pb.cap; return -1; }
-    x.wsync();
-    if (nq) {
-      const PairRec* pr = g.pr_pool + cq[CI_P0];
-      for (int32_t p = 0; p < nq; ++p) {
-        const int32_t o = pn + ex + 2 * p;
-        pb.s[o] = pr[p].os; pb.e[o] = pr[p].oe;
-        pb.s[o + 1] = pr[p].is; pb.e[o + 1] = pr[p].ie;
-      }
-    }
-    st.pend_n = pn + tot;
-    x.wsync();
-  }
-  x.wsync();
-  st.pend_upto = int32_t(m);
-  x.wsync();
+  if (!pend_append(x, g, j, m, cand, cinfo, pb, lerr)) return -1;
   const int64_t rc1 = x.clock();
   pend_sort(x, pb, st);
   if (st.pend_n >= x.fold_threshold(st.bz_n)) {
@@ -1686,7 +1718,7 @@ constexpr int32_t CS_HIT = 16;
 
 template <class X>
 TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int32_t* cand, int32_t* cinfo,
-                           int64_t* chull, PendBuf& pb, GroupStats& ls, ErrInfo& lerr) {
+                           int64_t* chull, PendBuf& pb, GroupStats& ls, ErrInfo& lerr, bool fold_end) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t S = st.S;
@@ -1845,6 +1877,15 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
   st.son = son;
   if (changed) st.dirty = 1;
   x.wsync();
+  if (fold_end && m0 < m1) {
+    // a later speculation window follows: this window's commits join the
+    // busy structure its speculation is taken against
+    const int64_t f0 = x.clock();
+    if (!pend_append(x, g, j, m1, cand, cinfo, pb, lerr)) return changed;
+    pend_sort(x, pb, st);
+    if (st.pend_n > 0) merge_pend_into_busy(x, g, j, pb);
+    if (x.tid == 0) g.stats.cyc[19] += x.clock() - f0;
+  }
   if (x.lane == 0) {  // development cycle counters
     x.aadd(&g.stats.cyc[27], x.clock() - dc0);
     x.aadd(&g.stats.cyc[28], dcb);
@@ -1862,7 +1903,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   if (x.tid == 0) {
     int64_t maxT = 1;
     for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
-    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[13] = 0; gsh[14] = 0; gsh[GS_WK] = 0;
+    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[GS_PPOOL] = 0; gsh[GS_WPOOL] = 0; gsh[GS_WK] = 0;
     for (int j = 0; j < g.n_jobs; ++j) {
       JobState& st = g.st[j];
       st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
@@ -1935,15 +1976,35 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     g.stats.sort_elems += nc;
     if (!coupled)
       for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
-    for (int j = 0; j < g.n_jobs; ++j) g.st[j].pend_upto = coupled ? 0 : int32_t(gsh[16 + j]);
   }
   x.sync();
   int64_t t0 = x.clock(), t1;
   auto tick = [&](int k) { t1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += t1 - t0; t0 = t1; };
+  // Speculation windows: phases A-C run on consecutive windows of the
+  // candidate order [w0, w1). A window's speculation is taken against the
+  // state after every earlier window (their commits are folded into the busy
+  // structure at the end of each window's decisions), so it only has to
+  // survive the commits of its own window -- the validity argument of
+  // phase A holds unchanged relative to the window start. Coupled groups (one
+  // global walk) use one window.
+  const int64_t WIN = (coupled || g.spec_window <= 0) ? nc : int64_t(g.spec_window);
+  for (int64_t w0 = 0; w0 < nc;) {
+  const int64_t w1 = imin(nc, w0 + WIN);
+  const int64_t wn = w1 - w0;
+  if (x.tid == 0) {
+    gsh[GS_WK] = 0;
+    for (int j = 0; j < g.n_jobs; ++j) {
+      gsh[GS_PCAP + j] = 0;
+      JobState& st = g.st[j];
+      st.pend_n = 0; st.pend_sorted = 0;
+      st.pend_upto = coupled ? 0 : int32_t(imax(gsh[16 + j], w0));
+    }
+  }
+  x.sync();
   // ---- A. speculative scoring, one thread per candidate ----
   {
     GroupStats ls{};
-    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       const int j = cand[m] >> 24;
       const int32_t s = cand[m] & 0xffffff;
       const JobDev& J = g.jobs[j];
@@ -1960,16 +2021,16 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
       const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
       const int32_t capw = 2 * capp + 2;
-      const int64_t p0 = x.aadd(&gsh[13], capp);
-      const int64_t w0 = x.aadd(&gsh[14], capw);
+      const int64_t p0 = x.aadd(&gsh[GS_PPOOL], capp);
+      const int64_t wp0 = x.aadd(&gsh[GS_WPOOL], capw);
       x.aadd(&gsh[GS_PCAP + j], capp);
-      if (p0 + capp > g.pr_cap || w0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
+      if (p0 + capp > g.pr_cap || wp0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
       ci[CI_P0] = int32_t(p0);
-      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * w0, 0, capw, false};
+      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * wp0, 0, capw, false};
       const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
       ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
       ci[CI_NP] = c.npairs;
-      ci[CI_W0] = int32_t(w0);
+      ci[CI_W0] = int32_t(wp0);
       ci[CI_NW] = c.nwin;
       for (int32_t w = 0; w < c.nwin; ++w) {
         hl[0] = imin(hl[0], c.win[2 * w]);
@@ -1991,14 +2052,14 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   // passes: every speculative pair interval goes into a time-bucketed index;
   // a candidate then checks only the buckets its placement windows (lifted
   // by -P/0/+P) touch, against entries of earlier candidates of its job.
-  if (nc <= CB_GRID_MAX) {
+  if (wn <= CB_GRID_MAX) {
     // one warp per candidate, its lanes over the earlier candidates
-    for (int32_t m = x.warp; m < int32_t(nc); m += x.nwarp) {
+    for (int32_t m = int32_t(w0) + x.warp; m < int32_t(w1); m += x.nwarp) {
       int32_t* ci = cinfo + int64_t(m) * CI_STRIDE;
       if (ci[CI_NW] == 0) continue;
       const int jm = cand[m] >> 24;
       const int64_t P = imax(1, g.st[jm].period);
-      for (int32_t i = x.lane; i < m; i += X::W) {
+      for (int32_t i = int32_t(w0) + x.lane; i < m; i += X::W) {
         const int32_t* cj = cinfo + int64_t(i) * CI_STRIDE;
         if (cj[CI_STATUS] != CS_OK || (cand[i] >> 24) != jm) continue;
         if (!hits(chull[i * 4 + 2], chull[i * 4 + 3], chull[m * 4], chull[m * 4 + 1], P)) continue;
@@ -2032,7 +2093,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     if (x.tid == 0) { gsh[14] = 0; gsh[GS_NB] = NB; }
     for (int32_t k = x.tid; k < NB + 1; k += x.nthr) { bk_cnt[k] = 0; wk_cnt[k] = 0; }
     x.sync();
-    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
       if (ci[CI_STATUS] == CS_OK) x.amax(&gsh[14], chull[m * 4 + 3]);
       if (ci[CI_NW]) x.amax(&gsh[14], chull[m * 4 + 1]);
@@ -2042,7 +2103,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     while ((gsh[14] >> shb) >= NB) ++shb;
     auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(NB) - 1); };
     // count
-    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
       if (ci[CI_STATUS] != CS_OK) continue;
       const PairRec* pr = g.pr_pool + ci[CI_P0];
@@ -2052,7 +2113,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
           for (int64_t q = imax(0, bucket(s0)); q <= bucket(e0 - 1) && q >= 0; ++q) x.aadd32(&bk_cnt[q + 1], 1);
         }
     }
-    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
       const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
       for (int32_t w = 0; w < ci[CI_NW]; ++w)
@@ -2092,7 +2153,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     for (int32_t k = x.tid; k < NB; k += x.nthr) { bk_cur[k] = bk_cnt[k]; wk_cur[k] = wk_cnt[k]; }
     x.sync();
     if (gsh[GS_WK]) {
-      for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
         const int32_t* ci = cinfo + m * CI_STRIDE;
         const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
         for (int32_t w = 0; w < ci[CI_NW]; ++w)
@@ -2101,7 +2162,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       }
     }
     if (fits) {
-      for (int64_t m = x.tid; m < nc; m += x.nthr) {
+      for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
         const int32_t* ci = cinfo + m * CI_STRIDE;
         if (ci[CI_STATUS] != CS_OK) continue;
         const PairRec* pr = g.pr_pool + ci[CI_P0];
@@ -2114,13 +2175,13 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       }
     }
     x.sync();
-    for (int64_t m = x.tid; m < nc; m += x.nthr) {
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       int32_t* ci = cinfo + m * CI_STRIDE;
       if (ci[CI_NW] == 0) continue;
       const int j = cand[m] >> 24;
       const int64_t P = imax(1, g.st[j].period);
       const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
-      const int64_t m0 = coupled ? 0 : gsh[16 + j];
+      const int64_t m0 = imax(w0, coupled ? 0 : gsh[16 + j]);
       int32_t nconf = 0;
       auto consider = [&](int64_t i) {
         if (i >= m || i < m0 || (cand[i] >> 24) != j) return;
@@ -2184,7 +2245,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         int64_t* b = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(x.tmp) + rec_bytes) + gsh[GS_POFF + seg];
         pb = PendBuf{b, b + cap, b + 2 * cap, b + 3 * cap, b + 4 * cap, cap};
       }
-      const bool ch = decide_chunked(x, g, seg, gsh[16 + seg], gsh[16 + seg + 1], cand, cinfo, chull, pb, ls, lerr);
+      const bool ch = decide_chunked(x, g, seg, imax(w0, gsh[16 + seg]), imin(w1, gsh[16 + seg + 1]), cand, cinfo,
+                                     chull, pb, ls, lerr, w1 < nc);
       x.wsync();
       if (x.lane == 0) {
         if (ch) gsh[10] = 1;
@@ -2193,6 +2255,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
         x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
         x.aadd(&g.stats.rescored, ls.rescored);
+#if TSL_PROF
+        for (int k = 0; k < 16; ++k) x.aadd(&g.stats.prof[k], ls.prof[k]);
+#endif
       }
     }
   }
@@ -2326,6 +2391,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sync();
   tick(7);
   if (g.err.code) return false;
+  w0 = w1;
+  }
   // ---- D. write the committed events (make_event + pair links + flags) ----
   for (int64_t m = x.tid; m < nc; m += x.nthr) {
     const int32_t* ci = cinfo + m * CI_STRIDE;

@@ -47,6 +47,7 @@ struct JobDev {
   int32_t rank;      // job-id rank inside the group (std::string order)
   double ratio;      // SwapBudget max ratio (config.max_swap_ratio(job))
   int32_t Scap, Rcap, Ecap;  // swap-event / recompute-event / timeline capacities
+  int32_t ti_nb;             // buckets of the time indexes (TI_NB; finer for jobs above one sort tile)
 
   // ---- static graph (host-packed) ----
   const int32_t* topo;       // [O] op indices in topological order (graph.cpp:245-282)
@@ -97,9 +98,9 @@ struct JobDev {
   int64_t* pd_e;
   int64_t* pd_ts;  // [Scap] merge scratch
   int64_t* pd_te;
-  int32_t* bzi_s;     // [TI_NB+1] time index over bz_s
-  int32_t* bzi_e;     // [TI_NB+1] time index over bz_e
-  int32_t* ai_e;      // [TI_NB+1] time index over a_end (anchor)
+  int32_t* bzi_s;     // [ti_nb+1] time index over bz_s
+  int32_t* bzi_e;     // [ti_nb+1] time index over bz_e
+  int32_t* ai_e;      // [ti_nb+1] time index over a_end (anchor)
   int32_t* st_evcnt;  // [T] swap events per storage (storage_has_swap)
   uint8_t* swapped;   // [T] SwapBudget::swapped_storages for this job
   // recompute events (plan.hpp:34-42)
@@ -167,6 +168,7 @@ struct GroupStats {
   int64_t sort_elems;        // elements through block sorts
   int64_t rescored;          // swap candidates re-scored after speculation
   int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
+  int64_t prof[16];          // development profile of re-score queries (TSL_PROF builds)
 };
 
 // Control block of a cooperative launch (one group above one sort tile,
@@ -194,7 +196,7 @@ struct CoopCtl {
   int64_t *fm_s, *fm_e, *fo_s, *fo_e;
   int32_t* fi_s;
   int32_t* fi_e;
-  int32_t fn1, fn2, fshift, fdone;
+  int32_t fn1, fn2, fshift, fdone, fnb, fpad;
   int32_t wbar_count, wbar_gen;  // barrier of the worker CTAs
 };
 enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_EXIT = 9 };
@@ -210,7 +212,7 @@ struct GroupDev {
   int64_t* hist;        // merged_peak_history
   int64_t final_merged;
   int32_t within_budget;
-  int32_t pad0;
+  int32_t spec_window;  // candidates per speculation window of a swap pass (0: the whole pass)
   int64_t total_swapped;  // SwapBudget::total_swapped
   int32_t loop_iters;
   int32_t pad2;

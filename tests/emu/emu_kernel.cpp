@@ -23,7 +23,7 @@ struct HostX {
   void sync() {}
   int32_t fold_threshold(int32_t bz_n) const { return std::max(PEND_MERGE, bz_n / 128); }
   bool fold_hook(const int64_t*, const int64_t*, int32_t, const int64_t*, const int64_t*, int32_t, int64_t*, int64_t*,
-                 int64_t*, int64_t*, int32_t*, int32_t*, int) { return false; }
+                 int64_t*, int64_t*, int32_t*, int32_t*, int, int32_t) { return false; }
   int64_t clock() { return 0; }
   void wsync() {}
   bool wany(bool p) { return p; }

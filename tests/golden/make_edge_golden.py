@@ -74,6 +74,16 @@ def cases():
     out.append(("C1.ratio1", c1, lambda p: cfg(seventy(p), ratios={"vgg16": 1.0})))
     out.append(("C1.ratio_other_job_invalid", c1, lambda p: cfg(seventy(p), ratios={"ghost": 2.0, "vgg16": 0.5})))
     out.append(("C1.ratio_other_job_valid", c1, lambda p: cfg(seventy(p), ratios={"ghost": 0.5})))
+    # non-finite ratios: NaN passes PlannerConfig::validate (config.hpp:32-34)
+    # and then SwapBudget::allows (swap_planner.cpp:268-276) refuses every
+    # swap of that job after the first; +inf fails validation
+    nan = float("nan")
+    c3 = [gen("inception_v3", 32, "inception_v3"), gen("densenet", 32, "densenet"), gen("vgg16", 32, "vgg16")]
+    out.append(("C1.ratio_nan", c1, lambda p: cfg(seventy(p), ratios={"vgg16": nan})))
+    out.append(("C3.ratio_nan_densenet", c3, lambda p: cfg(seventy(p), ratios={"densenet": nan})))
+    out.append(("C3.ratio_nan_all", c3, lambda p: cfg(seventy(p), ratios={k: nan for k in p})))
+    out.append(("C3.ratio_nan_ghost", c3, lambda p: cfg(seventy(p), ratios={"ghost": nan})))
+    out.append(("C1.ratio_inf_invalid", c1, lambda p: cfg(seventy(p), ratios={"vgg16": float("inf")})))
     out.append(("chain8_size_2p36.bw1", [gen("chain", 1, "cb", depth=8, size_mul=1 << 36)],
                 lambda p: cfg(seventy(p), bw=1, setup=0)))
     out.append(("vgg16_b8_size_2p30", [gen("vgg16", 8, "vb", size_mul=1 << 30)],

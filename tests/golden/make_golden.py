@@ -189,11 +189,12 @@ def fuzz_cases(n=120):
 def config_cases():
     out = []
     for ratio in (None, 0.1):
-        for name in ["C1", "C2", "C3", "C5s0", "C5s3"] + (["C5s1"] if ratio else []):
+        # every C5 shard (15 arrival/departure replans each) at both ratios
+        for name in ["C1", "C2", "C3"] + [f"C5s{g}" for g in range(8)]:
             for req in CF.requests(name, ratio=ratio):
                 ip = ref.initial_peaks(req.jobs)
                 cfg = req.config(ip)
-                text, res = ref.build_plan(req.jobs, cfg, repeats=3)
+                text, res = ref.build_plan(req.jobs, cfg, repeats=1 if name.startswith("C5") else 3)
                 out.append({"name": req.name, "ratio": ratio, "config": cfg,
                             "initial_peaks": ip, "n_accesses": req.n_accesses,
                             **summarize(text, res, keep_text=(name == "C1"))})
@@ -204,6 +205,10 @@ def config_cases():
 def main():
     if not ref.available():
         sys.exit("build the reference first: make -C oracle ref")
+    if sys.argv[1:] == ["configs"]:  # regenerate configs.json only
+        with open(os.path.join(HERE, "configs.json"), "w") as f:
+            json.dump(config_cases(), f, indent=1)
+        return
     with open(os.path.join(HERE, "analyze.json"), "w") as f:
         json.dump(analyze_cases(), f, separators=(",", ":"))
     with open(os.path.join(HERE, "handbuilt.json"), "w") as f:

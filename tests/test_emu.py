@@ -29,6 +29,26 @@ def test_fuzz(emu, case):
     check_against_golden(emu.build_plan(fuzz_jobs(case), case["config"]), case)
 
 
+@pytest.mark.parametrize("case", golden("stall"), ids=lambda c: f"{c['name']}-r{c['ratio']}-"
+                         f"{c['config']['stall_min_iters']}-{c['config']['stall_epsilon']}")
+def test_stall_rule(emu, case):
+    """Builds where the stall rule (orchestrator.cpp:35-41) fires."""
+    check_against_golden(emu.build_plan(config_jobs(case), case["config"]), case)
+
+
+@pytest.mark.parametrize("window", [1, 5, 64])
+def test_speculation_windows(emu, window, monkeypatch):
+    """Swap passes speculating in windows of the candidate order (the busy
+    structure advanced between windows) plan exactly what one pass-wide
+    speculation plans: the reference's fixtures, byte for byte."""
+    monkeypatch.setenv("TSL_SPEC_WINDOW", str(window))
+    cases = [c for c in golden("configs") if c["name"] in ("C1", "C2", "C3.3", "C5s2.7")]
+    for case in cases:
+        check_against_golden(emu.build_plan(config_jobs(case), case["config"]), case)
+    for case in golden("fuzz")[1::6]:
+        check_against_golden(emu.build_plan(fuzz_jobs(case), case["config"]), case)
+
+
 def test_handbuilt(emu):
     for name, spec in golden("handbuilt").items():
         for case in spec["cases"]:

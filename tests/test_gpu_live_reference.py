@@ -2,13 +2,17 @@
 
 oracle/_ref/libmemsched_ref.so is the reference's hot path compiled from its own
 sources (oracle/Makefile); it travels with the repo, so the round-end GPU run can
-compare fresh random cases directly with it -- no fixture in between. Cases mix
+compare random cases directly with it -- no fixture in between. Cases mix
 the reference's own random_job (test_support.hpp) and generator families
-(workload.cpp) with random bandwidth, setup, budget and coupled swap ratios; the
-seeds are outside every committed fixture.
+(workload.cpp) with random bandwidth, setup, budget and coupled swap ratios.
+150 cases use the fixed seeds 20000-20149 (outside every committed fixture);
+50 more are drawn fresh on every run from a time-derived base seed (or
+TSL_FUZZ_SEED), which the test prints and names in any failure.
 """
 import json
+import os
 import random
+import time
 
 import pytest
 
@@ -52,11 +56,8 @@ def _case(ref, seed):
     return jobs, cfg
 
 
-@pytest.mark.parametrize("block", range(6))
-def test_live_reference_fuzz(planner, ref, block):
-    """25 fresh cases per block (seeds 20000 + 25*block ...): save_plans text,
-    PeakReports, merged history, budget flag and diagnostic equal the reference's."""
-    for seed in range(20000 + 25 * block, 20000 + 25 * (block + 1)):
+def _check_seeds(planner, ref, seeds):
+    for seed in seeds:
         jobs, cfg = _case(ref, seed)
         try:
             text, res = ref.build_plan(jobs, cfg, repeats=1)
@@ -71,3 +72,17 @@ def test_live_reference_fuzz(planner, ref, block):
         assert out["within_budget"] == res["within_budget"] and out["diagnostic"] == res["diagnostic"], seed
         for jid, rep in res["reports"].items():
             assert json.loads(out["reports_json"][jid]) == rep, f"seed {seed}: PeakReport of {jid}"
+
+
+@pytest.mark.parametrize("block", range(6))
+def test_live_reference_fuzz(planner, ref, block):
+    """25 cases per block (fixed seeds 20000 + 25*block ...): save_plans text,
+    PeakReports, merged history, budget flag and diagnostic equal the reference's."""
+    _check_seeds(planner, ref, range(20000 + 25 * block, 20000 + 25 * (block + 1)))
+
+
+def test_live_reference_fresh_seeds(planner, ref):
+    """50 cases from a base seed drawn at run time (TSL_FUZZ_SEED to replay)."""
+    base = int(os.environ.get("TSL_FUZZ_SEED", int(time.time()) % 1_000_000_000 + 10 ** 9))
+    print(f"fresh fuzz base seed {base}")
+    _check_seeds(planner, ref, range(base, base + 50))

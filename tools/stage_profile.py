@@ -52,3 +52,10 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
               f"cyc; pend_sort {s['cyc_pendsort']} (folds {s['fitprof'][3]} cyc) append/schedule {list(s['fitprof'])[:2]}", flush=True)
         fp = list(s["fitprof"])
         print(f"   decide: total {fp[4]} bulk {fp[5]} attn-check {fp[6]} hit-mark {fp[7]} attention {fp[8]}", flush=True)
+        qp = list(s.get("queryprof", [0] * 16))
+        if qp[10]:
+            n = qp[10]
+            print(f"   re-score queries (TSL_PROF): {n}; per query prologue {qp[0]/n:.0f} open {qp[1]/n:.0f} "
+                  f"sweep {qp[2]/n:.0f} cyc, swept {qp[9]/n:.2f}; search cyc/search busy {qp[3]/max(1,qp[6]):.0f} "
+                  f"(x{qp[6]/n:.2f}) pend {qp[4]/max(1,qp[7]):.0f} (x{qp[7]/n:.2f}) storage {qp[5]/max(1,qp[8]):.0f} "
+                  f"(x{qp[8]/n:.2f})", flush=True)

@@ -163,6 +163,7 @@ typedef struct tsl_stats {
   int64_t fitprof[9];
   int64_t evalprof[7];  /* evaluator phases: prep, emit, sort1, group, automaton, scan.., peak..report */
   int64_t queryprof[16];  /* development profile of re-score queries (zero unless built with TSL_PROF) */
+  int64_t comp_rescored;  /* candidates re-speculated inside their conflict component (phase A2) */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

@@ -293,8 +293,10 @@ struct JobPlace {  // byte offsets into the device buffer
 };
 
 struct GroupPlace {
-  size_t hist, c_info, c_hull, dev_list, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
-  size_t coop = 0, tile_hist = 0, coop_gsh = 0, cta_part = 0;
+  size_t hist, c_info, c_hull, dev_list, c_comp, pr_pool, w_pool, wbuf, cb_idx, cb_ent, bs_key = 0, bs_val = 0;
+  int64_t c_cap = 0;
+  size_t coop = 0, tile_hist = 0, coop_gsh = 0, cta_part = 0, c_wscratch = 0;
+  int64_t c_wscap = 0;
   int64_t pr_cap, w_cap, wcap, cb_cap;
   int32_t cb_nb = 1024;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
@@ -389,7 +391,9 @@ struct tsl_plan {
 
 namespace {
 
-void grow(Buffers* c, size_t need) {
+// The device buffer holds inputs, outputs and the workspace; the pinned host
+// staging buffer only the inputs and outputs (host_need <= need).
+void grow(Buffers* c, size_t need, size_t host_need) {
   if (need > c->dcap) {
     if (c->dbuf) cudaFree(c->dbuf);
     c->dbuf = nullptr;
@@ -397,10 +401,10 @@ void grow(Buffers* c, size_t need) {
     cuda_check(cudaMalloc(&c->dbuf, cap), "cudaMalloc");
     c->dcap = cap;
   }
-  if (need > c->hcap) {
+  if (host_need > c->hcap) {
     if (c->hbuf) cudaFreeHost(c->hbuf);
     c->hbuf = nullptr;
-    size_t cap = std::max(need, c->hcap * 2);
+    size_t cap = std::max(host_need, c->hcap * 2);
     cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c->hbuf), cap), "cudaMallocHost");
     c->hcap = cap;
   }
@@ -640,6 +644,13 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       q.tile_hist = L.take<int32_t>(size_t((P->ecap + NT * SORT_IPT - 1) / (NT * SORT_IPT)) * 256);
       q.coop_gsh = L.take<int64_t>(1024);  // SH_WORDS (tsl_plan.cuh)
       q.cta_part = L.take<int64_t>(1024);
+      // component runs on every warp of the grid: a private interval list of
+      // up to 4096 entries per warp (6 words each: list, merge target, scratch)
+      int sms = 0;
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->ctx->device) != cudaSuccess || sms <= 0)
+        sms = 148;
+      q.c_wscap = 4096;
+      q.c_wscratch = L.take<int64_t>(size_t(sms) * (NT / 32) * 6 * size_t(q.c_wscap));
     }
     q.k_key = L.take<uint64_t>(E);
     q.k_val = L.take<int32_t>(E);
@@ -658,6 +669,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     q.c_info = L.take<int32_t>(CC * 16);
     q.c_hull = L.take<int64_t>(CC * 4);
     q.dev_list = L.take<int64_t>(CC);
+    q.c_cap = int64_t(CC);
+    q.c_comp = L.take<int32_t>(2 * CC);
     q.pr_pool = L.take<uint8_t>(size_t(q.pr_cap) * tsl::PAIRREC_BYTES);
     q.w_pool = L.take<int64_t>(size_t(2 * q.w_cap));
     int64_t maxS = 0;
@@ -671,7 +684,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   }
   const size_t total = L.off;
   const auto t_lay = std::chrono::steady_clock::now();
-  grow(ctx, total);
+  grow(ctx, total, out_end);
   const auto t_grow = std::chrono::steady_clock::now();
   // 3. fill the staging buffer
   int32_t jglob = 0;
@@ -692,6 +705,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->coupled = coupled ? 1 : 0;
     G->spec_window = 0;
     if (const char* e = std::getenv("TSL_SPEC_WINDOW")) G->spec_window = std::atoi(e);
+    // component speculation (swap_pass phase A2): on for jobs above one sort
+    // tile, whose passes re-score ~40 % of their candidates without it
+    G->spec_comp = P->big ? 1 : 0;
+    if (const char* e = std::getenv("TSL_SPEC_COMP")) G->spec_comp = std::atoi(e);
     G->hist_cap = P->gp[gi].hist_cap;
     G->cfg.bw = cfg->pcie_bandwidth;
     G->cfg.setup = cfg->transfer_setup;
@@ -728,6 +745,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->c_info = dp<int32_t>(ctx, q.c_info);
     G->c_hull = dp<int64_t>(ctx, q.c_hull);
     G->dev_list = dp<int64_t>(ctx, q.dev_list);
+    G->c_comp = dp<int32_t>(ctx, q.c_comp);
+    G->c_cap = q.c_cap;
+    G->c_wscratch = P->coop ? dp<int64_t>(ctx, q.c_wscratch) : nullptr;
+    G->c_wscap = q.c_wscap;
     G->pr_pool = reinterpret_cast<tsl::PairRec*>(static_cast<uint8_t*>(ctx->dbuf) + q.pr_pool);
     G->w_pool = dp<int64_t>(ctx, q.w_pool);
     G->pr_cap = q.pr_cap;
@@ -1020,6 +1041,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   for (int k = 0; k < 5; ++k) s.fitprof[4 + k] = G.stats.cyc[27 + k];
   for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
   for (int k = 0; k < 16; ++k) s.queryprof[k] = G.stats.prof[k];
+  s.comp_rescored = G.stats.comp_rescored;
   return R;
 }
 

@@ -87,6 +87,7 @@ struct DevX {
   __device__ void amin(int64_t* p, int64_t v) { atomicMin((long long*)p, (long long)v); }
   __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
   __device__ void amax32(int32_t* p, int32_t v) { atomicMax(p, v); }
+  __device__ void amin32(int32_t* p, int32_t v) { atomicMin(p, v); }
   __device__ void aor32(int32_t* p, int32_t v) { atomicOr(p, v); }
   __device__ void errset(GroupDev& g, const ErrInfo& e) {
     if (atomicCAS(&g.err.code, 0, e.code) == 0) {
@@ -432,12 +433,14 @@ struct DevX {
       }
       if (type == COOP_EVAL) coop_eval(cta, c->jb, c->je);
       else if (type == COOP_REBUILD) coop_rebuild(cta);
+      else if (type == COOP_COMP) coop_comp(cta);
       else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
   }
   __device__ void coop_eval(int cta, int jb, int je);  // all CTAs: evaluate() on the grid (below)
   __device__ void coop_rebuild(int cta);               // all CTAs: rebuild_busy() on the grid (below)
+  __device__ void coop_comp(int cta);                  // workers: component runs (below)
   GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
@@ -639,6 +642,53 @@ __device__ void DevX::coop_eval(int cta, int jb, int je) {
 __device__ void DevX::coop_rebuild(int cta) {
   GridX gx = grid_ctx(*this, cta);
   rebuild_busy(gx, *coop_group);
+}
+
+// Component runs on a cooperative launch: every warp of every CTA takes runs
+// through one global counter (a C4 pass re-speculates thousands of members;
+// CTA 0's eight warps alone were the bottleneck). Each warp keeps its run's
+// private interval list in its own slice of c_wscratch.
+__device__ void DevX::coop_comp(int cta) {
+  volatile CoopCtl* c = coop;
+  GroupDev& g = *coop_group;
+  const int64_t gw = int64_t(cta) * nwarp + warp;
+  comp_runs(*this, g, c->cw0, c->ccand, c->ccinfo, c->cchull, &coop->crun, c->cnruns,
+            g.c_wscratch + gw * 6 * g.c_wscap, g.c_wscap);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(&coop->cdone, 1);
+  }
+}
+
+template <>
+__device__ inline void comp_dispatch<DevX>(DevX& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_t* cinfo,
+                                           int64_t* chull, int64_t nruns) {
+  if (!x.coop || !g.c_wscratch || x.grid < 2) {
+    int64_t* gsh = x.sh + MAXB * NF;
+    comp_runs(x, g, w0, cand, cinfo, chull, &gsh[GS_CRUN], nruns, g.wbuf + int64_t(x.warp) * 4 * g.wcap,
+              (g.wcap * 4) / 6);
+    return;
+  }
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->cw0 = w0; c->ccand = cand; c->ccinfo = cinfo; c->cchull = chull; c->cnruns = nruns; c->crun = 0;
+    c->cdone = 0; c->type = COOP_COMP;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  comp_runs(x, g, w0, cand, cinfo, chull, &x.coop->crun, nruns, g.c_wscratch + int64_t(x.warp) * 6 * g.c_wscap,
+            g.c_wscap);
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile int32_t* dn = &x.coop->cdone;
+    const int64_t t0 = clock64();
+    while (*dn < x.grid - 1) { __nanosleep(64); DevX::spin_guard(t0); }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 // The end-of-pass busy rebuild on a cooperative launch: key building, the

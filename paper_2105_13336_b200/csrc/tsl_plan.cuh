@@ -49,7 +49,38 @@
 #define TSL_HD_FORCE inline
 #endif
 
+#if TSL_EMU_STATS
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#endif
 namespace tsl {
+
+#if TSL_EMU_STATS
+// development statistics of the re-scores (emulation build only)
+namespace emu_stats {
+inline int64_t n_rescore, spec_not_ok, wrapped, spec_pairs, new_pairs, kept_pairs, main_same, main_in_only, now_fail,
+    now_ok, with_gaps, passes, comp_max, comp_sum_max, comp_big, conf_over, conf_edges, cands, why_hit, why_over,
+    why_nconf, why_diff, why_conf, verify_bad, verified;
+struct Printer {
+  ~Printer() {
+    std::fprintf(stderr,
+                 "rescore %lld spec_not_ok %lld wrapped %lld spec_pairs %lld new_pairs %lld kept_pairs %lld "
+                 "main_same %lld main_in_only %lld now_fail %lld now_ok %lld with_gaps %lld\n",
+                 (long long)n_rescore, (long long)spec_not_ok, (long long)wrapped, (long long)spec_pairs,
+                 (long long)new_pairs, (long long)kept_pairs, (long long)main_same, (long long)main_in_only,
+                 (long long)now_fail, (long long)now_ok, (long long)with_gaps);
+    std::fprintf(stderr, "passes %lld cands %lld edges %lld conf_over %lld comp_max %lld mean_max %.1f in_big(>32) %lld\n",
+                 (long long)passes, (long long)cands, (long long)conf_edges, (long long)conf_over, (long long)comp_max,
+                 passes ? double(comp_sum_max) / passes : 0.0, (long long)comp_big);
+    std::fprintf(stderr, "verified %lld bad %lld\n", (long long)verified, (long long)verify_bad);
+    std::fprintf(stderr, "why: hit %lld overflow %lld nconf>CAPC %lld comp-diff %lld conflict %lld\n", (long long)why_hit,
+                 (long long)why_over, (long long)why_nconf, (long long)why_diff, (long long)why_conf);
+  }
+};
+inline Printer printer;
+}  // namespace emu_stats
+#endif
 
 #ifndef TSL_PROF
 #define TSL_PROF 0
@@ -605,6 +636,16 @@ struct ReCtx {
   int32_t nout, cap;
   bool overflow;
   int64_t* dbg = nullptr;  // development cycle counters (thread 0 only)
+  // component speculation records the placement window of every successful
+  // query (as SpecCtx does) for the later validity checks
+  int64_t* win = nullptr;  // (lo, hi) pairs
+  int32_t nwin = 0, cap_win = 0;
+  TSL_HD void record(int64_t r, int64_t d) {
+    if (!win || r == NONE) return;
+    if (nwin >= cap_win) { overflow = true; return; }
+    if (x.lane == 0) { win[2 * nwin] = r; win[2 * nwin + 1] = r + d; }
+    ++nwin;
+  }
   // a query made by one lane on its own (gap pairs in parallel)
   TSL_HD int64_t query_lane(const FitQuery& q, bool latest) {
     Src src[2] = {{J.bz_s, J.bz_e, st.bz_n, {J.bzi_s, st.bzi_shift, J.ti_nb}, {J.bzi_e, st.bzi_shift, J.ti_nb}},
@@ -635,6 +676,7 @@ struct ReCtx {
 #else
     int64_t r = fit(J, st, q, latest, src, 2, &sw, NoClock{}, nullptr, WarpOf<X>{x});
 #endif
+    record(r, q.d);
     gs->fit_queries += 1;
     gs->busy_intervals += sw;
     if (dbg && x.tid == 0) { dbg[0] += x.clock() - c0; dbg[1] += 1; }
@@ -670,8 +712,11 @@ constexpr int GS_WK = 440;      // gsh slot: window-index bucket shift + 1 (0: n
 constexpr int GS_NB = 441;      // gsh slot: bucket count of this pass's indexes
 constexpr int GS_PPOOL = 442;   // gsh slot: pair-pool bump counter of the pass
 constexpr int GS_WPOOL = 443;   // gsh slot: window-pool bump counter of the pass
+constexpr int GS_CCHG = 444;    // gsh slot: component union-find round changed something
+constexpr int GS_CRUN = 445;    // gsh slot: next component run to process
+constexpr int GS_NRUN = 446;    // gsh slot: component runs of >= 2 members
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
-static_assert(MAXB * 16 + 443 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
+static_assert(MAXB * 16 + 446 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
 constexpr int CB_GRID_MAX = 160;  // passes with at most this many candidates check all pairs directly
@@ -765,6 +810,16 @@ TSL_HD void gap_pairs_parallel(C& c, int32_t store, int32_t fk, int32_t a1, int6
           }
         }
       }
+    }
+    if (c.win) {  // both placements of every lane whose queries succeeded (ordered by lane)
+      const int32_t nw = (os != NONE ? 1 : 0) + (is != NONE ? 1 : 0);
+      int32_t tot = 0;
+      const int32_t ex = x.wexcl(nw, &tot);
+      if (c.nwin + tot > c.cap_win) { c.overflow = true; return; }
+      if (os != NONE) { c.win[2 * (c.nwin + ex)] = os; c.win[2 * (c.nwin + ex) + 1] = os + d; }
+      if (is != NONE) { c.win[2 * (c.nwin + ex + 1)] = is; c.win[2 * (c.nwin + ex + 1) + 1] = is + d; }
+      c.nwin += tot;
+      x.wsync();
     }
     const unsigned okm = x.wballot(ok);
     for (int t = 0; t < X::W; ++t) {
@@ -1693,9 +1748,35 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
   int64_t earliest = 0, latest = 0;
   const int kind = candidate_kind(J, st, s, earliest, latest);
   const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+#if TSL_EMU_STATS
+  const std::vector<PairRec> spec(g.pr_pool + ci[CI_P0], g.pr_pool + ci[CI_P0] + ((ci[CI_STATUS] & 0xf) == CS_OK ? ci[CI_NP] : 0));
+  const int spec_status = ci[CI_STATUS] & 0xf;
+#endif
   ReCtx<X> c{x, J, st, pb, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
   c.dbg = &g.stats.cyc[12];
   const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+#if TSL_EMU_STATS
+  {
+    emu_stats::n_rescore++;
+    const int np = ok ? c.nout : 0;
+    if (spec_status != CS_OK) emu_stats::spec_not_ok++;
+    if (kind == 1) emu_stats::wrapped++;
+    emu_stats::spec_pairs += spec.size();
+    emu_stats::new_pairs += np;
+    int kept = 0;
+    for (int p = 0; p < np; ++p)
+      for (const PairRec& r : spec)
+        if (r.os == c.out[p].os && r.is == c.out[p].is) { ++kept; break; }
+    emu_stats::kept_pairs += kept;
+    const bool main_same = np > 0 && !spec.empty() && spec[0].os == c.out[0].os && spec[0].is == c.out[0].is;
+    const bool main_out_same = np > 0 && !spec.empty() && spec[0].os == c.out[0].os;
+    if (main_same) emu_stats::main_same++;
+    else if (main_out_same) emu_stats::main_in_only++;
+    if (np == 0 && !spec.empty()) emu_stats::now_fail++;
+    if (np > 0 && spec.empty()) emu_stats::now_ok++;
+    if (np > 1 || spec.size() > 1) emu_stats::with_gaps++;
+  }
+#endif
   if (x.tid == 0) {
     const int64_t rc3 = x.clock();
     g.stats.cyc[10] += rc3 - rc0;
@@ -1715,10 +1796,59 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
 // attention candidate and everything before it is decided in bulk (a warp
 // prefix sum assigns event slots and ids in plan order).
 constexpr int32_t CS_HIT = 16;
+constexpr int32_t CS_DIFF = 32;  // decided by a re-score whose result differs from the speculation
+constexpr int32_t CS_BRK = 64;   // an earlier member of the candidate's component has CS_DIFF
+
+#if TSL_EMU_STATS
+// Emulation-only check (TSL_VERIFY=1): the speculation a candidate is about to
+// be decided with equals an exact re-score against the real state.
+template <class X>
+void emu_verify(X& x, GroupDev& g, int j, int64_t m, int32_t* cand, int32_t* cinfo, PendBuf& pb, int32_t S,
+                int64_t id, const int32_t* cprev, int64_t cw0) {
+  static const bool on = std::getenv("TSL_VERIFY") != nullptr;
+  if (!on) return;
+  JobState& st = g.st[j];
+  const JobDev& J = g.jobs[j];
+  int32_t* ci = cinfo + m * CI_STRIDE;
+  ErrInfo lerr{};
+  st.S = S;
+  st.next_id = id;
+  pend_append(x, g, j, m, cand, cinfo, pb, lerr);
+  pend_sort(x, pb, st);
+  if (st.pend_n >= x.fold_threshold(st.bz_n)) merge_pend_into_busy(x, g, j, pb);
+  const int32_t pn0 = st.pend_n;
+  const int32_t s = cand[m] & 0xffffff;
+  int64_t earliest = 0, latest = 0;
+  const int kind = candidate_kind(J, st, s, earliest, latest);
+  const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+  static std::vector<PairRec> scratch(1 << 20);
+  GroupStats ls{};
+  ReCtx<X> c{x, J, st, pb, g.cfg, &ls, scratch.data(), 0, capp, false};
+  const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+  st.pend_n = pn0;
+  st.pend_sorted = pn0;
+  const int32_t np_spec = (ci[CI_STATUS] & 0xf) == CS_OK ? ci[CI_NP] : 0;
+  const int32_t np_ex = ok ? c.nout : 0;
+  bool bad = np_spec != np_ex;
+  const PairRec* pr = g.pr_pool + ci[CI_P0];
+  for (int32_t q = 0; !bad && q < np_ex; ++q)
+    bad = pr[q].os != c.out[q].os || pr[q].oe != c.out[q].oe || pr[q].is != c.out[q].is || pr[q].ie != c.out[q].ie;
+  if (bad) {
+    ++emu_stats::verify_bad;
+    if (emu_stats::verify_bad <= 5)
+      std::fprintf(stderr, "VERIFY m=%lld status=%x nconf=%d prev=%d np spec %d exact %d spec.os %lld ex.os %lld\n",
+                   (long long)m, ci[CI_STATUS], ci[CI_NCONF], cprev ? cprev[m - cw0] : -9, np_spec, np_ex,
+                   np_spec ? (long long)pr[0].os : -1LL, np_ex ? (long long)c.out[0].os : -1LL);
+  }
+  ++emu_stats::verified;
+}
+#endif
+
 
 template <class X>
 TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int32_t* cand, int32_t* cinfo,
-                           int64_t* chull, PendBuf& pb, GroupStats& ls, ErrInfo& lerr, bool fold_end) {
+                           int64_t* chull, PendBuf& pb, GroupStats& ls, ErrInfo& lerr, bool fold_end,
+                           const int32_t* cprev = nullptr, int64_t cw0 = 0) {
   const JobDev& J = g.jobs[j];
   JobState& st = g.st[j];
   int32_t S = st.S;
@@ -1735,9 +1865,13 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     const bool in = c < m1;
     int32_t status = in ? cinfo[c * CI_STRIDE + CI_STATUS] : CS_SKIP;
     const int32_t nconf = in ? cinfo[c * CI_STRIDE + CI_NCONF] : 0;
+    // component speculation: a member whose component predecessor (decided
+    // in an earlier chunk) was re-scored needs attention
+    const int32_t pv = (in && cprev) ? cprev[c - cw0] : -1;
+    const bool brk = pv >= 0 && pv < m && (cinfo[int64_t(pv) * CI_STRIDE + CI_STATUS] & (CS_DIFF | CS_BRK));
     const bool attn = in && (status & 0xf) != CS_SKIP &&
                       ((status & CS_HIT) || nconf > 0 || (status & 0xf) == CS_OVERFLOW || (status & 0xf) == CS_ERROR ||
-                       cinfo[c * CI_STRIDE + CI_P0] < 0);
+                       cinfo[c * CI_STRIDE + CI_P0] < 0 || brk);
     const unsigned amask = x.wballot(attn);
     const int f = amask ? x.ffs(amask) - 1 : X::W;
     const int64_t nbulk = imin(int64_t(f), m1 - m);
@@ -1747,6 +1881,10 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     int32_t tot = 0;
     const int32_t ex = x.wexcl(2 * np, &tot);
     const int32_t ntake = popc32(x.wballot(take));
+#if TSL_EMU_STATS
+    if (x.lane < nbulk && (status & 0xf) == CS_FAIL) emu_verify(x, g, j, c, cand, cinfo, pb, S, id, cprev, cw0);
+    if (take) emu_verify(x, g, j, c, cand, cinfo, pb, S, id, cprev, cw0);
+#endif
     if (S + tot > J.Scap) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = J.Scap; return changed; }
     x.wsync();
     if (x.lane < nbulk) {
@@ -1775,6 +1913,15 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     if ((st_m & 0xf) == CS_ERROR) { lerr.code = E_NO_TGA; lerr.job = j; lerr.tensor = s; lerr.tick = 0; return changed; }
     if (ci[CI_P0] < 0) { lerr.code = E_CAPACITY; lerr.job = j; lerr.tensor = g.pr_cap; lerr.tick = 4; return changed; }
     bool valid = !(st_m & CS_HIT) && (st_m & 0xf) != CS_OVERFLOW && ci[CI_NCONF] <= CAPC;
+    // a component member's speculation assumed every earlier member's: once
+    // one of them decided differently (DIFF), the rest of the component is
+    // re-scored in order (BRK carries that down the chain)
+    bool pbrk = false;
+    if (cprev) {
+      const int32_t pvm = cprev[m - cw0];
+      pbrk = pvm >= 0 && (cinfo[int64_t(pvm) * CI_STRIDE + CI_STATUS] & (CS_DIFF | CS_BRK));
+      if (pbrk) valid = false;
+    }
     {
       bool bad = false;
       for (int32_t k = x.lane; valid && k < ci[CI_NCONF]; k += X::W)
@@ -1784,15 +1931,54 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
     int32_t npm = 0;
     int32_t state = 0;
     dca += x.clock() - da0;
+#if TSL_EMU_STATS
+    if (!valid) {
+      if (st_m & CS_HIT) emu_stats::why_hit++;
+      else if ((st_m & 0xf) == CS_OVERFLOW) emu_stats::why_over++;
+      else if (ci[CI_NCONF] > CAPC) emu_stats::why_nconf++;
+      else if (cprev && cprev[m - cw0] >= 0 && (cinfo[int64_t(cprev[m - cw0]) * CI_STRIDE + CI_STATUS] & (CS_DIFF | CS_BRK))) emu_stats::why_diff++;
+      else emu_stats::why_conf++;
+    }
+#endif
     if (valid) {
+#if TSL_EMU_STATS
+      emu_verify(x, g, j, m, cand, cinfo, pb, S, id, cprev, cw0);
+#endif
       if ((st_m & 0xf) == CS_OK) { npm = ci[CI_NP]; state = 1; }
     } else {
       // the real state needs this pass's commits so far
       x.wsync();
       st.S = S; st.next_id = id;
       x.wsync();
+      // component speculation: later members of m's component assumed m's
+      // speculated commits; keep them (to compare) unless there are none
+      int64_t* keep = g.wbuf + int64_t(x.warp) * 4 * g.wcap + 2 * g.wcap;
+      const int32_t np_old = (cprev && (st_m & 0xf) == CS_OK && ci[CI_P0] >= 0) ? ci[CI_NP] : 0;
+      if (np_old > 0) {
+        const PairRec* pr = g.pr_pool + ci[CI_P0];
+        for (int32_t q = x.lane; q < np_old; q += X::W) {
+          keep[4 * q] = pr[q].os; keep[4 * q + 1] = pr[q].oe; keep[4 * q + 2] = pr[q].is; keep[4 * q + 3] = pr[q].ie;
+        }
+        x.wsync();
+      }
       npm = rescore_candidate(x, g, j, s, m, cand, cinfo, pb, ls, lerr);
       if (npm < 0) return changed;
+      if (cprev) {
+        // the chain stays intact only if the re-score commits exactly the
+        // speculated intervals (a speculated failure: nothing)
+        bool diff = npm != np_old || (st_m & 0xf) == CS_OVERFLOW;
+        if (!diff && npm > 0) {
+          const PairRec* pr = g.pr_pool + ci[CI_P0];
+          bool d = false;
+          for (int32_t q = x.lane; q < npm; q += X::W)
+            d = d || keep[4 * q] != pr[q].os || keep[4 * q + 1] != pr[q].oe || keep[4 * q + 2] != pr[q].is ||
+                keep[4 * q + 3] != pr[q].ie;
+          diff = x.wany(d);
+        }
+        x.wsync();
+        if (x.lane == 0) ci[CI_STATUS] |= (diff ? CS_DIFF : 0) | (pbrk ? CS_BRK : 0);
+        x.wsync();
+      }
       if (npm > 0) {
         const int64_t dh0 = x.clock();
         state = 2;
@@ -1896,157 +2082,17 @@ TSL_HD bool decide_chunked(X& x, GroupDev& g, int j, int64_t m0, int64_t m1, int
   return changed;
 }
 
+// Phase B of a speculation window [w0, w1): for every candidate, the earlier
+// candidates of its job whose speculative pair intervals (lifted by -P/0/+P)
+// touch one of its placement windows (ci[CI_CONF..], count ci[CI_NCONF]),
+// and the window index phase C's hit marking uses. With `comp` (component
+// speculation), conflicts inside a component are not recorded: a member's
+// speculation already includes its component predecessors' commits.
 template <class X>
-TSL_HD bool swap_pass(X& x, GroupDev& g) {
-  int64_t* sh = x.sh;
-  int64_t* gsh = sh + MAXB * NF;  // [9]=maxT [10]=changed [11]=cursor [12]=maxsize [13..14] pools [16..] segments
-  if (x.tid == 0) {
-    int64_t maxT = 1;
-    for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
-    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[GS_PPOOL] = 0; gsh[GS_WPOOL] = 0; gsh[GS_WK] = 0;
-    for (int j = 0; j < g.n_jobs; ++j) {
-      JobState& st = g.st[j];
-      st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
-      gsh[GS_PCAP + j] = 0;
-    }
-  }
-  x.sync();
-  for (int j = 0; j < g.n_jobs; ++j) {
-    const JobDev& J = g.jobs[j];
-    int64_t mx = 1;
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.in_peak[t]) mx = imax(mx, J.t_size[t]);
-    x.amax(&gsh[12], mx);
-  }
-  x.sync();
-  const int jbits = nbits(uint64_t(g.n_jobs - 1));
-  const int rbits = nbits(uint64_t(gsh[9] - 1));
-  const int sbits = nbits(uint64_t(gsh[12]));
-  const uint64_t smax = (sbits >= 63) ? (~0ull >> 1) : ((1ull << sbits) - 1);
-  const bool coupled = g.coupled != 0;
-  // candidates: every job's peak tensors (the report stays stale for the whole
-  // pass), ordered (size desc, job id, storage id) -- swap_planner.cpp:469-481
-  for (int j = 0; j < g.n_jobs; ++j) {
-    const JobDev& J = g.jobs[j];
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
-      if (!J.in_peak[t]) continue;
-      const int64_t slot = x.aadd(&gsh[11], 1);
-      if (slot >= g.ecap) continue;
-      const uint64_t inv = smax - uint64_t(J.t_size[t]);
-      uint64_t k;
-      if (coupled) k = (((inv << jbits) | uint64_t(J.rank)) << rbits) | uint64_t(J.t_rank[t]);
-      else k = (((uint64_t(j) << sbits) | inv) << rbits) | uint64_t(J.t_rank[t]);
-      g.k_key[slot] = k;
-      g.k_val[slot] = (j << 24) | t;  // the host guarantees T < 2^24 and <= 128 jobs
-    }
-  }
-  x.sync();
-  const int64_t nc = gsh[11];
-  if (nc > g.ecap) {
-    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = -1; g.err.tensor = nc; g.err.tick = 1; }
-    x.sync();
-    return false;
-  }
-  x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
-  // Candidate records live in shared memory when they fit (the sort scratch
-  // is free until phase E): the in-order decisions read them back-to-back.
-  int32_t* cand = g.k_val;
-  int32_t* cinfo = g.c_info;
-  int64_t* chull = g.c_hull;
-  size_t rec_bytes = 0;  // shared scratch taken by the candidate records
-  {
-    const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
-    if (need <= x.tmp_bytes) {
-      chull = reinterpret_cast<int64_t*>(x.tmp);
-      cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
-      cand = cinfo + CI_STRIDE * nc;
-      rec_bytes = (need + 15) & ~size_t(15);
-    }
-  }
-  if (cand != g.k_val)
-    for (int64_t m = x.tid; m < nc; m += x.nthr) cand[m] = g.k_val[m];
-  // segment starts: first candidate of each job (candidates are job-major
-  // when uncoupled)
-  for (int j = x.tid; j <= g.n_jobs; j += x.nthr) gsh[16 + j] = nc;
-  x.sync();
-  if (!coupled)
-    for (int64_t m = x.tid; m < nc; m += x.nthr) x.amin(&gsh[16 + (cand[m] >> 24)], m);
-  x.sync();
-  if (x.tid == 0) {
-    g.stats.candidates += nc;
-    g.stats.sort_elems += nc;
-    if (!coupled)
-      for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
-  }
-  x.sync();
-  int64_t t0 = x.clock(), t1;
-  auto tick = [&](int k) { t1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += t1 - t0; t0 = t1; };
-  // Speculation windows: phases A-C run on consecutive windows of the
-  // candidate order [w0, w1). A window's speculation is taken against the
-  // state after every earlier window (their commits are folded into the busy
-  // structure at the end of each window's decisions), so it only has to
-  // survive the commits of its own window -- the validity argument of
-  // phase A holds unchanged relative to the window start. Coupled groups (one
-  // global walk) use one window.
-  const int64_t WIN = (coupled || g.spec_window <= 0) ? nc : int64_t(g.spec_window);
-  for (int64_t w0 = 0; w0 < nc;) {
-  const int64_t w1 = imin(nc, w0 + WIN);
+TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo,
+                           const int64_t* chull, bool coupled, const int32_t* comp) {
+  int64_t* gsh = x.sh + MAXB * NF;
   const int64_t wn = w1 - w0;
-  if (x.tid == 0) {
-    gsh[GS_WK] = 0;
-    for (int j = 0; j < g.n_jobs; ++j) {
-      gsh[GS_PCAP + j] = 0;
-      JobState& st = g.st[j];
-      st.pend_n = 0; st.pend_sorted = 0;
-      st.pend_upto = coupled ? 0 : int32_t(imax(gsh[16 + j], w0));
-    }
-  }
-  x.sync();
-  // ---- A. speculative scoring, one thread per candidate ----
-  {
-    GroupStats ls{};
-    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
-      const int j = cand[m] >> 24;
-      const int32_t s = cand[m] & 0xffffff;
-      const JobDev& J = g.jobs[j];
-      const JobState& st = g.st[j];
-      int32_t* ci = cinfo + m * CI_STRIDE;
-      int64_t* hl = chull + m * 4;
-      ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
-      ci[CI_P0] = -1;
-      hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
-      if (J.swapped[s]) { ci[CI_STATUS] = CS_SKIP; continue; }
-      int64_t earliest = 0, latest = 0;
-      const int kind = candidate_kind(J, st, s, earliest, latest);
-      if (kind == 0) { ci[CI_STATUS] = CS_SKIP; continue; }
-      if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
-      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
-      const int32_t capw = 2 * capp + 2;
-      const int64_t p0 = x.aadd(&gsh[GS_PPOOL], capp);
-      const int64_t wp0 = x.aadd(&gsh[GS_WPOOL], capw);
-      x.aadd(&gsh[GS_PCAP + j], capp);
-      if (p0 + capp > g.pr_cap || wp0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
-      ci[CI_P0] = int32_t(p0);
-      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * wp0, 0, capw, false};
-      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
-      ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
-      ci[CI_NP] = c.npairs;
-      ci[CI_W0] = int32_t(wp0);
-      ci[CI_NW] = c.nwin;
-      for (int32_t w = 0; w < c.nwin; ++w) {
-        hl[0] = imin(hl[0], c.win[2 * w]);
-        hl[1] = imax(hl[1], c.win[2 * w + 1]);
-      }
-      for (int32_t p = 0; p < c.npairs; ++p) {
-        hl[2] = imin(hl[2], imin(c.pairs[p].os, c.pairs[p].is));
-        hl[3] = imax(hl[3], imax(c.pairs[p].oe, c.pairs[p].ie));
-      }
-    }
-    x.aadd(&g.stats.fit_queries, ls.fit_queries);
-    x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
-    x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
-  }
-  x.sync();
-  tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
   // Small passes: one thread per (candidate, earlier candidate) pair. Large
   // passes: every speculative pair interval goes into a time-bucketed index;
@@ -2062,6 +2108,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       for (int32_t i = int32_t(w0) + x.lane; i < m; i += X::W) {
         const int32_t* cj = cinfo + int64_t(i) * CI_STRIDE;
         if (cj[CI_STATUS] != CS_OK || (cand[i] >> 24) != jm) continue;
+        if (comp && comp[i - w0] == comp[m - w0]) continue;  // same component: consistent by construction
         if (!hits(chull[i * 4 + 2], chull[i * 4 + 3], chull[m * 4], chull[m * 4 + 1], P)) continue;
         const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
         const PairRec* pr = g.pr_pool + cj[CI_P0];
@@ -2185,6 +2232,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       int32_t nconf = 0;
       auto consider = [&](int64_t i) {
         if (i >= m || i < m0 || (cand[i] >> 24) != j) return;
+        if (comp && comp[i - w0] == comp[m - w0]) return;
         for (int32_t k = 0; k < imin(nconf, CAPC); ++k)
           if (ci[CI_CONF + k] == i) return;
         const int32_t* cj = cinfo + i * CI_STRIDE;
@@ -2216,8 +2264,395 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       ci[CI_NCONF] = nconf;
     }
   }
+}
+
+// Component runs [r] of a window (x_order / x_seq2 / c_comp from
+// component_speculation), taken in turn by warps through *run_ctr: each
+// member is re-speculated in order against the pass-start state plus the
+// run's earlier results (private sorted list in wb: 6 * cap words).
+// Warp-collective; any number of warps on any number of CTAs.
+template <class X>
+TSL_HD void comp_runs(X& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_t* cinfo, int64_t* chull,
+                      int64_t* run_ctr, int64_t nruns, int64_t* wb, int64_t cap) {
+  const int64_t wn = g.c_wn;
+  GroupStats ls{};
+  const volatile int32_t* par = g.c_comp;
+  for (;;) {
+    int64_t r = 0;
+    if (x.lane == 0) r = x.aadd(run_ctr, 1);
+    r = x.shfl(r, 0);
+    if (r >= nruns) break;
+    const int32_t p0 = g.x_order[r];
+    const int32_t root = par[g.x_seq2[p0]];
+    const int j = cand[w0 + g.x_seq2[p0]] >> 24;
+    const JobDev& J = g.jobs[j];
+    JobState lst = g.st[j];  // this warp's view: pass-start busy + the component's commits
+    lst.pend_n = 0;
+    lst.pend_sorted = 0;
+    PendBuf pl{wb, wb + cap, wb + 2 * cap, wb + 3 * cap, wb + 4 * cap, int32_t(imin(cap, INT32_MAX))};
+    const int64_t P = imax(1, lst.period);
+    bool broken = false;
+    for (int64_t p = p0; p < wn && par[g.x_seq2[p]] == root; ++p) {
+      const int64_t m = w0 + g.x_seq2[p];
+      int32_t* ci = cinfo + m * CI_STRIDE;
+      const int32_t stm = ci[CI_STATUS] & 0xf;
+      if (stm == CS_SKIP || stm == CS_ERROR || ci[CI_P0] < 0) continue;
+      if (broken) {  // an earlier member overflowed: the walk re-scores the rest
+        x.wsync();
+        if (x.lane == 0) ci[CI_STATUS] = CS_OVERFLOW;
+        x.wsync();
+        continue;
+      }
+      // phase-A result still valid against the component's commits so far?
+      bool valid = stm != CS_OVERFLOW;
+      if (valid && lst.pend_n > 0) {
+        const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
+        const int32_t nw = ci[CI_NW];
+        bool hit = false;
+        for (int32_t e = x.lane; e < lst.pend_n && !hit; e += X::W)
+          for (int32_t w = 0; w < nw && !hit; ++w) hit = hits(pl.s[e], pl.e[e], wv[2 * w], wv[2 * w + 1], P);
+        valid = !x.wany(hit);
+      }
+      if (valid) {
+        if (stm == CS_OK) {  // its pairs join the component's commits
+          const PairRec* pr = g.pr_pool + ci[CI_P0];
+          const int32_t np = ci[CI_NP];
+          if (lst.pend_n + 2 * np > pl.cap) { broken = true; continue; }
+          for (int32_t q = x.lane; q < np; q += X::W) {
+            const int32_t o = lst.pend_n + 2 * q;
+            pl.s[o] = pr[q].os; pl.e[o] = pr[q].oe;
+            pl.s[o + 1] = pr[q].is; pl.e[o + 1] = pr[q].ie;
+          }
+          x.wsync();
+          lst.pend_n += 2 * np;
+          x.wsync();
+        }
+        continue;
+      }
+      ls.comp_rescored += 1;
+      pend_sort(x, pl, lst);
+      const int32_t s = cand[m] & 0xffffff;
+      int64_t earliest = 0, latest = 0;
+      const int kind = candidate_kind(J, lst, s, earliest, latest);
+      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+      ReCtx<X> c{x, J, lst, pl, g.cfg, &ls, g.pr_pool + ci[CI_P0], 0, capp, false};
+      c.win = g.w_pool + 2 * int64_t(ci[CI_W0]);
+      c.cap_win = 2 * capp + 2;
+      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+      x.wsync();
+      if (c.overflow) {
+        broken = true;
+        if (x.lane == 0) ci[CI_STATUS] = CS_OVERFLOW;
+        x.wsync();
+        continue;
+      }
+      if (x.lane == 0) {
+        ci[CI_STATUS] = ok ? CS_OK : CS_FAIL;
+        ci[CI_NP] = ok ? c.nout : 0;
+        ci[CI_NW] = c.nwin;
+        int64_t* hl = chull + m * 4;
+        hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
+        for (int32_t w = 0; w < c.nwin; ++w) { hl[0] = imin(hl[0], c.win[2 * w]); hl[1] = imax(hl[1], c.win[2 * w + 1]); }
+        for (int32_t q = 0; ok && q < c.nout; ++q) {
+          hl[2] = imin(hl[2], imin(c.out[q].os, c.out[q].is));
+          hl[3] = imax(hl[3], imax(c.out[q].oe, c.out[q].ie));
+        }
+      }
+      if (!ok) {  // a failed schedule commits nothing (ReCtx appended nothing)
+        x.wsync();
+        continue;
+      }
+      x.wsync();
+    }
+  }
+  if (x.lane == 0) {
+    x.aadd(&g.stats.comp_rescored, ls.comp_rescored);
+    x.aadd(&g.stats.fit_queries, ls.fit_queries);
+    x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+  }
+}
+
+// The run processing of component_speculation; an execution context may
+// route it elsewhere (the CUDA build spreads it over every CTA of a
+// cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD void comp_dispatch(X& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_t* cinfo, int64_t* chull,
+                          int64_t nruns) {
+  int64_t* gsh = x.sh + MAXB * NF;
+  const int64_t cap = (g.wcap * 4) / 6;
+  comp_runs(x, g, w0, cand, cinfo, chull, &gsh[GS_CRUN], nruns, g.wbuf + int64_t(x.warp) * 4 * g.wcap, cap);
+}
+
+// ---- A2. component speculation (uncoupled swap passes) ----
+// Phase B's conflict edges group a window's candidates into components; the
+// members of a component (in the candidate order, typically tensors of one
+// layer and micro-batch packing into the same channel gaps) are speculated
+// again IN ORDER by one warp, against the pass-start state plus the results
+// of their earlier component members, so a member's speculation no longer
+// conflicts with its own component. A member whose phase-A result survives its
+// predecessors' commits keeps it (same validity argument as phase C). The
+// grouping only affects speed: phase B is then re-run across components, and
+// the in-order walk accepts a member only while every earlier member of its
+// component committed its speculation unchanged (CS_DIFF breaks the chain).
+template <class X>
+TSL_HD void component_speculation(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo,
+                                  int64_t* chull) {
+  const int64_t wn = w1 - w0;
+  volatile int32_t* par = g.c_comp;      // [wn] union-find parent -> root (window-relative)
+  int32_t* prv = g.c_comp + g.c_cap;     // [wn] previous member (candidate index) or -1
+  int64_t* gsh = x.sh + MAXB * NF;
+  for (int64_t i = x.tid; i < wn; i += x.nthr) par[i] = int32_t(i);
+  x.sync();
+  // hook the larger root under the smaller one (atomic min) until no conflict
+  // edge joins two components; a lost race is redone by the next round
+  for (int round = 0; round < 64; ++round) {
+    if (x.tid == 0) gsh[GS_CCHG] = 0;
+    x.sync();
+    int64_t chg = 0;
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      const int32_t nc = imin(ci[CI_NCONF], CAPC);
+      for (int k = 0; k < nc; ++k) {
+        int32_t a = int32_t(m - w0), b = ci[CI_CONF + k] - int32_t(w0);
+        while (par[a] != a) a = par[a];
+        while (par[b] != b) b = par[b];
+        if (a != b) { x.amin32(const_cast<int32_t*>(&par[imax(a, b)]), int32_t(imin(a, b))); chg = 1; }
+      }
+    }
+    if (chg) x.amax(&gsh[GS_CCHG], 1);
+    x.sync();
+    for (int64_t i = x.tid; i < wn; i += x.nthr) {
+      int32_t r = par[i];
+      while (par[r] != r) r = par[r];
+      par[i] = r;
+    }
+    x.sync();
+    const bool again = gsh[GS_CCHG] != 0;
+    x.sync();  // (every thread has read the flag before the next round resets it)
+    if (!again) break;
+  }
+  // members of each component in candidate order: sort (root, index)
+  const int rb = nbits(uint64_t(wn));
+  for (int64_t i = x.tid; i < wn; i += x.nthr) {
+    g.x_key2[i] = (uint64_t(par[i]) << rb) | uint64_t(i);
+    g.x_seq2[i] = int32_t(i);
+  }
+  if (x.tid == 0) { gsh[GS_NRUN] = 0; gsh[GS_CRUN] = 0; g.c_wn = wn; }
+  x.sync();
+  x.sort(g.x_key2, g.x_seq2, int32_t(wn), 2 * rb);
+  for (int64_t p = x.tid; p < wn; p += x.nthr) {
+    const int32_t i = g.x_seq2[p];
+    const bool first = p == 0 || par[g.x_seq2[p - 1]] != par[i];
+    prv[i] = first ? -1 : int32_t(w0 + g.x_seq2[p - 1]);
+    if (first && p + 1 < wn && par[g.x_seq2[p + 1]] == par[i]) {  // a run of >= 2 members
+      const int64_t r = x.aadd(&gsh[GS_NRUN], 1);
+      g.x_order[r] = int32_t(p);
+    }
+  }
+  x.sync();
+  const int64_t nruns = gsh[GS_NRUN];
+  // one warp per run (taken in turn): on every CTA of a cooperative launch
+  comp_dispatch(x, g, w0, cand, cinfo, chull, nruns);
+  x.sync();
+  for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) cinfo[m * CI_STRIDE + CI_NCONF] = 0;
+  x.sync();
+}
+
+template <class X>
+TSL_HD bool swap_pass(X& x, GroupDev& g) {
+  int64_t* sh = x.sh;
+  int64_t* gsh = sh + MAXB * NF;  // [9]=maxT [10]=changed [11]=cursor [12]=maxsize [13..14] pools [16..] segments
+  if (x.tid == 0) {
+    int64_t maxT = 1;
+    for (int j = 0; j < g.n_jobs; ++j) maxT = imax(maxT, g.jobs[j].T);
+    gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[GS_PPOOL] = 0; gsh[GS_WPOOL] = 0; gsh[GS_WK] = 0;
+    for (int j = 0; j < g.n_jobs; ++j) {
+      JobState& st = g.st[j];
+      st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
+      gsh[GS_PCAP + j] = 0;
+    }
+  }
+  x.sync();
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    int64_t mx = 1;
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.in_peak[t]) mx = imax(mx, J.t_size[t]);
+    x.amax(&gsh[12], mx);
+  }
+  x.sync();
+  const int jbits = nbits(uint64_t(g.n_jobs - 1));
+  const int rbits = nbits(uint64_t(gsh[9] - 1));
+  const int sbits = nbits(uint64_t(gsh[12]));
+  const uint64_t smax = (sbits >= 63) ? (~0ull >> 1) : ((1ull << sbits) - 1);
+  const bool coupled = g.coupled != 0;
+  // candidates: every job's peak tensors (the report stays stale for the whole
+  // pass), ordered (size desc, job id, storage id) -- swap_planner.cpp:469-481
+  for (int j = 0; j < g.n_jobs; ++j) {
+    const JobDev& J = g.jobs[j];
+    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
+      if (!J.in_peak[t]) continue;
+      const int64_t slot = x.aadd(&gsh[11], 1);
+      if (slot >= g.ecap) continue;
+      const uint64_t inv = smax - uint64_t(J.t_size[t]);
+      uint64_t k;
+      if (coupled) k = (((inv << jbits) | uint64_t(J.rank)) << rbits) | uint64_t(J.t_rank[t]);
+      else k = (((uint64_t(j) << sbits) | inv) << rbits) | uint64_t(J.t_rank[t]);
+      g.k_key[slot] = k;
+      g.k_val[slot] = (j << 24) | t;  // the host guarantees T < 2^24 and <= 128 jobs
+    }
+  }
+  x.sync();
+  const int64_t nc = gsh[11];
+  if (nc > g.ecap) {
+    if (x.tid == 0) { g.err.code = E_CAPACITY; g.err.job = -1; g.err.tensor = nc; g.err.tick = 1; }
+    x.sync();
+    return false;
+  }
+  x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
+  // Candidate records live in shared memory when they fit (the sort scratch
+  // is free until phase E): the in-order decisions read them back-to-back.
+  int32_t* cand = g.k_val;
+  int32_t* cinfo = g.c_info;
+  int64_t* chull = g.c_hull;
+  size_t rec_bytes = 0;  // shared scratch taken by the candidate records
+  {
+    const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
+    // (component speculation sorts in that scratch: records stay in HBM)
+    if (need <= x.tmp_bytes && !(g.spec_comp && !coupled)) {
+      chull = reinterpret_cast<int64_t*>(x.tmp);
+      cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
+      cand = cinfo + CI_STRIDE * nc;
+      rec_bytes = (need + 15) & ~size_t(15);
+    }
+  }
+  if (cand != g.k_val)
+    for (int64_t m = x.tid; m < nc; m += x.nthr) cand[m] = g.k_val[m];
+  // segment starts: first candidate of each job (candidates are job-major
+  // when uncoupled)
+  for (int j = x.tid; j <= g.n_jobs; j += x.nthr) gsh[16 + j] = nc;
+  x.sync();
+  if (!coupled)
+    for (int64_t m = x.tid; m < nc; m += x.nthr) x.amin(&gsh[16 + (cand[m] >> 24)], m);
+  x.sync();
+  if (x.tid == 0) {
+    g.stats.candidates += nc;
+    g.stats.sort_elems += nc;
+    if (!coupled)
+      for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
+  }
+  x.sync();
+  int64_t t0 = x.clock(), t1;
+  auto tick = [&](int k) { t1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += t1 - t0; t0 = t1; };
+  // Speculation windows: phases A-C run on consecutive windows of the
+  // candidate order [w0, w1). A window's speculation is taken against the
+  // state after every earlier window (their commits are folded into the busy
+  // structure at the end of each window's decisions), so it only has to
+  // survive the commits of its own window -- the validity argument of
+  // phase A holds unchanged relative to the window start. Coupled groups (one
+  // global walk) use one window.
+  const int64_t WIN = (coupled || g.spec_window <= 0) ? nc : int64_t(g.spec_window);
+  for (int64_t w0 = 0; w0 < nc;) {
+  const int64_t w1 = imin(nc, w0 + WIN);
+  const int64_t wn = w1 - w0;
+  if (x.tid == 0) {
+    gsh[GS_WK] = 0;
+    for (int j = 0; j < g.n_jobs; ++j) {
+      gsh[GS_PCAP + j] = 0;
+      JobState& st = g.st[j];
+      st.pend_n = 0; st.pend_sorted = 0;
+      st.pend_upto = coupled ? 0 : int32_t(imax(gsh[16 + j], w0));
+    }
+  }
+  x.sync();
+  // ---- A. speculative scoring, one thread per candidate ----
+  {
+    GroupStats ls{};
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
+      const int j = cand[m] >> 24;
+      const int32_t s = cand[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      const JobState& st = g.st[j];
+      int32_t* ci = cinfo + m * CI_STRIDE;
+      int64_t* hl = chull + m * 4;
+      ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
+      ci[CI_P0] = -1;
+      hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
+      if (J.swapped[s]) { ci[CI_STATUS] = CS_SKIP; continue; }
+      int64_t earliest = 0, latest = 0;
+      const int kind = candidate_kind(J, st, s, earliest, latest);
+      if (kind == 0) { ci[CI_STATUS] = CS_SKIP; continue; }
+      if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
+      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+      const int32_t capw = 2 * capp + 2;
+      const int64_t p0 = x.aadd(&gsh[GS_PPOOL], capp);
+      const int64_t wp0 = x.aadd(&gsh[GS_WPOOL], capw);
+      x.aadd(&gsh[GS_PCAP + j], capp);
+      if (p0 + capp > g.pr_cap || wp0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
+      ci[CI_P0] = int32_t(p0);
+      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * wp0, 0, capw, false};
+      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+      ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
+      ci[CI_NP] = c.npairs;
+      ci[CI_W0] = int32_t(wp0);
+      ci[CI_NW] = c.nwin;
+      for (int32_t w = 0; w < c.nwin; ++w) {
+        hl[0] = imin(hl[0], c.win[2 * w]);
+        hl[1] = imax(hl[1], c.win[2 * w + 1]);
+      }
+      for (int32_t p = 0; p < c.npairs; ++p) {
+        hl[2] = imin(hl[2], imin(c.pairs[p].os, c.pairs[p].is));
+        hl[3] = imax(hl[3], imax(c.pairs[p].oe, c.pairs[p].ie));
+      }
+    }
+    x.aadd(&g.stats.fit_queries, ls.fit_queries);
+    x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+    x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+  }
+  x.sync();
+  tick(5);
+  // ---- B. conflicts with earlier speculative commits of the same job ----
+  find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, nullptr);
+  const bool use_comp = !coupled && g.spec_comp && wn > 1;
+  if (use_comp) {
+    x.sync();
+    tick(6);
+    component_speculation(x, g, w0, w1, cand, cinfo, chull);
+    tick(5);
+    // conflicts across components (a member's speculation includes its own
+    // component's earlier results)
+    find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, g.c_comp);
+  }
   x.sync();
   tick(6);
+#if TSL_EMU_STATS
+  {  // conflict components of this window (union-find over the conflict lists)
+    std::vector<int64_t> par(wn);
+    for (int64_t i = 0; i < wn; ++i) par[i] = i;
+    auto find = [&](int64_t a) { while (par[a] != a) a = par[a] = par[par[a]]; return a; };
+    int64_t over = 0, edges = 0;
+    for (int64_t m = w0; m < w1; ++m) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      if ((ci[CI_STATUS] & 0xf) == CS_SKIP) continue;
+      if (ci[CI_NCONF] > CAPC) ++over;
+      for (int k = 0; k < imin(ci[CI_NCONF], CAPC); ++k) {
+        ++edges;
+        par[find(m - w0)] = find(ci[CI_CONF + k] - w0);
+      }
+    }
+    std::vector<int64_t> sz(wn, 0);
+    for (int64_t i = 0; i < wn; ++i) sz[find(i)]++;
+    int64_t mx = 0, big = 0, ncomp = 0;
+    for (int64_t i = 0; i < wn; ++i)
+      if (sz[i]) { ++ncomp; mx = imax(mx, sz[i]); if (sz[i] > 32) big += sz[i]; }
+    emu_stats::passes++;
+    emu_stats::comp_max = imax(emu_stats::comp_max, mx);
+    emu_stats::comp_sum_max += mx;
+    emu_stats::comp_big += big;
+    emu_stats::conf_over += over;
+    emu_stats::conf_edges += edges;
+    emu_stats::cands += wn;
+  }
+#endif
   // ---- C. in-order decisions ----
   const int nseg = coupled ? 1 : g.n_jobs;
   if (!coupled) {
@@ -2246,7 +2681,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
         pb = PendBuf{b, b + cap, b + 2 * cap, b + 3 * cap, b + 4 * cap, cap};
       }
       const bool ch = decide_chunked(x, g, seg, imax(w0, gsh[16 + seg]), imin(w1, gsh[16 + seg + 1]), cand, cinfo,
-                                     chull, pb, ls, lerr, w1 < nc);
+                                     chull, pb, ls, lerr, w1 < nc, use_comp ? g.c_comp + g.c_cap : nullptr, w0);
       x.wsync();
       if (x.lane == 0) {
         if (ch) gsh[10] = 1;

@@ -169,6 +169,7 @@ struct GroupStats {
   int64_t rescored;          // swap candidates re-scored after speculation
   int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
   int64_t prof[16];          // development profile of re-score queries (TSL_PROF builds)
+  int64_t comp_rescored;     // candidates re-speculated inside their conflict component
 };
 
 // Control block of a cooperative launch (one group above one sort tile,
@@ -198,8 +199,14 @@ struct CoopCtl {
   int32_t* fi_e;
   int32_t fn1, fn2, fshift, fdone, fnb, fpad;
   int32_t wbar_count, wbar_gen;  // barrier of the worker CTAs
+  // COOP_COMP: component runs of a speculation window, taken by every warp
+  int64_t cw0, cnruns, crun;     // window start, runs, next run (atomic)
+  const int32_t* ccand;
+  int32_t* ccinfo;
+  int64_t* cchull;
+  int32_t cdone, cpad;           // worker CTAs done
 };
-enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;
@@ -249,6 +256,13 @@ struct GroupDev {
   int32_t* cb_idx;   // [2 * CB_NB + 4] conflict-index bucket offsets / cursors
   int32_t* cb_ent;   // [cb_cap] conflict-index entries
   int64_t cb_cap;
+  int32_t* c_comp;   // [2 * c_cap] component speculation: union-find roots, previous members
+  int64_t c_cap;
+  int32_t spec_comp; // component speculation on (uncoupled swap passes)
+  int32_t pad3;
+  int64_t c_wn;      // candidates of the window being processed
+  int64_t* c_wscratch;  // cooperative launches: per-warp run lists (6 * c_wscap words per warp of the grid)
+  int64_t c_wscap;
 };
 
 }  // namespace tsl

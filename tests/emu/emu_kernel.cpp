@@ -37,6 +37,7 @@ struct HostX {
   void amax(int64_t* p, int64_t v) { if (v > *p) *p = v; }
   void amax32(int32_t* p, int32_t v) { if (v > *p) *p = v; }
   void aor32(int32_t* p, int32_t v) { *p |= v; }
+  void amin32(int32_t* p, int32_t v) { if (v < *p) *p = v; }
   void errset(GroupDev& g, const ErrInfo& e) { if (!g.err.code) g.err = e; }
   void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     if (n <= 1 || bits <= 0) return;

@@ -709,6 +709,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     // tile, whose passes re-score ~40 % of their candidates without it
     G->spec_comp = P->big ? 1 : 0;
     if (const char* e = std::getenv("TSL_SPEC_COMP")) G->spec_comp = std::atoi(e);
+    G->grid_conf = 1;
+    if (const char* e = std::getenv("TSL_GRID_CONF")) G->grid_conf = std::atoi(e);
     G->hist_cap = P->gp[gi].hist_cap;
     G->cfg.bw = cfg->pcie_bandwidth;
     G->cfg.setup = cfg->transfer_setup;

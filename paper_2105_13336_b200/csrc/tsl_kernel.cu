@@ -434,6 +434,7 @@ struct DevX {
       if (type == COOP_EVAL) coop_eval(cta, c->jb, c->je);
       else if (type == COOP_REBUILD) coop_rebuild(cta);
       else if (type == COOP_COMP) coop_comp(cta);
+      else if (type == COOP_CONF) coop_conf(cta);
       else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
@@ -441,6 +442,7 @@ struct DevX {
   __device__ void coop_eval(int cta, int jb, int je);  // all CTAs: evaluate() on the grid (below)
   __device__ void coop_rebuild(int cta);               // all CTAs: rebuild_busy() on the grid (below)
   __device__ void coop_comp(int cta);                  // workers: component runs (below)
+  __device__ void coop_conf(int cta);                  // all CTAs: find_conflicts() on the grid (below)
   GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
@@ -566,6 +568,8 @@ struct GridX {
   }
   __device__ void amin(int64_t* p, int64_t v) { atomicMin((long long*)p, (long long)v); }
   __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
+  __device__ int32_t aadd32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
+  __device__ int32_t wexcl(int32_t v, int32_t* total) { return dx->wexcl(v, total); }
   // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs
   __device__ void scan_op(int64_t* a, int n, int op) {
     sync();
@@ -642,6 +646,73 @@ __device__ void DevX::coop_eval(int cta, int jb, int je) {
 __device__ void DevX::coop_rebuild(int cta) {
   GridX gx = grid_ctx(*this, cta);
   rebuild_busy(gx, *coop_group);
+}
+
+// Phase B on a cooperative launch: every candidate loop spreads over the grid
+// (a C4 pass checks thousands of candidates against a 65,536-bucket index;
+// CTA 0 alone spent ~0.8 ms per call). The bucket shift, the index flag and
+// the entry total land in the grid scalars; CTA 0 copies them back.
+__device__ void DevX::coop_conf(int cta) {
+  volatile CoopCtl* c = coop;
+  GridX gx = grid_ctx(*this, cta);
+  find_conflicts(gx, *coop_group, c->cw0, c->cw1, c->ccand, c->ccinfo, c->cchull, c->ccoupled != 0, c->ccomp);
+}
+
+template <>
+__device__ inline void conflicts_batch<DevX>(DevX& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand,
+                                             int32_t* cinfo, const int64_t* chull, bool coupled, const int32_t* comp) {
+  if (!x.coop || x.grid < 2 || !g.grid_conf) { find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, comp); return; }
+  __syncthreads();
+  {  // the jobs' candidate segments (gsh[16 ..]) go to the grid scalars
+    const int64_t* gsh = x.sh + MAXB * NF;
+    int64_t* ggsh = x.coop->gsh + MAXB * NF;
+    for (int j = x.tid; j <= g.n_jobs; j += x.nthr) __stcg(&ggsh[16 + j], gsh[16 + j]);
+  }
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->cw0 = w0; c->cw1 = w1; c->ccand = cand; c->ccinfo = cinfo; c->cchull = const_cast<int64_t*>(chull);
+    c->ccomp = comp; c->ccoupled = coupled ? 1 : 0; c->type = COOP_CONF;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  GridX gx = grid_ctx(x, 0);
+  find_conflicts(gx, g, w0, w1, cand, cinfo, chull, coupled, comp);  // ends with a grid barrier
+  int64_t* gsh = x.sh + MAXB * NF;
+  const int64_t* ggsh = gx.sh + MAXB * NF;
+  if (x.tid == 0) {
+    gsh[14] = __ldcg(&ggsh[14]); gsh[15] = __ldcg(&ggsh[15]);
+    gsh[GS_WK] = __ldcg(&ggsh[GS_WK]); gsh[GS_NB] = __ldcg(&ggsh[GS_NB]);
+  }
+  __syncthreads();
+#if TSL_PROF
+  if (g.grid_conf == 2) {  // development check: CTA 0 alone must find the same lists
+    int32_t* keep = reinterpret_cast<int32_t*>(g.wbuf + 4 * g.wcap);  // warp 1's region (idle here)
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr)
+      for (int k = 0; k < 1 + CAPC; ++k) keep[(m - w0) * 8 + k] = cinfo[m * CI_STRIDE + CI_NCONF + k];
+    __syncthreads();
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) cinfo[m * CI_STRIDE + CI_NCONF] = 0;
+    int64_t* dbg = g.wbuf + 8 * g.wcap;
+    int64_t* dbg2 = g.wbuf + 12 * g.wcap;
+    for (int64_t i = x.tid; i < (w1 - w0) * 6; i += x.nthr) dbg2[i] = __ldcg(&dbg[i]);
+    __syncthreads();
+    find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, comp);
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
+      const int32_t* ci = cinfo + m * CI_STRIDE;
+      if (ci[CI_NCONF] != keep[(m - w0) * 8]) atomicAdd((unsigned long long*)&g.stats.prof[15], 1ull);
+      if (ci[CI_NCONF] != keep[(m - w0) * 8] && atomicAdd((unsigned long long*)&g.stats.prof[14], 1ull) < 3)
+        printf("conf mismatch m=%lld grid %d cta %d wn=%lld | grid nexam %lld fits %lld shb %lld nw %lld pass %lld late %lld"
+               " | cta nexam %lld fits %lld shb %lld nw %lld pass %lld late %lld\n", (long long)m, keep[(m - w0) * 8],
+               ci[CI_NCONF], (long long)(w1 - w0), (long long)dbg2[(m - w0) * 6], (long long)dbg2[(m - w0) * 6 + 1],
+               (long long)dbg2[(m - w0) * 6 + 2], (long long)dbg2[(m - w0) * 6 + 3], (long long)dbg2[(m - w0) * 6 + 4],
+               (long long)dbg2[(m - w0) * 6 + 5], (long long)dbg[(m - w0) * 6], (long long)dbg[(m - w0) * 6 + 1],
+               (long long)dbg[(m - w0) * 6 + 2], (long long)dbg[(m - w0) * 6 + 3], (long long)dbg[(m - w0) * 6 + 4],
+               (long long)dbg[(m - w0) * 6 + 5]);
+    }
+    __syncthreads();
+  }
+#endif
 }
 
 // Component runs on a cooperative launch: every warp of every CTA takes runs

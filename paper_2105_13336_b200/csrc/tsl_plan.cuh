@@ -2100,7 +2100,8 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
   // by -P/0/+P) touch, against entries of earlier candidates of its job.
   if (wn <= CB_GRID_MAX) {
     // one warp per candidate, its lanes over the earlier candidates
-    for (int32_t m = int32_t(w0) + x.warp; m < int32_t(w1); m += x.nwarp) {
+    const int32_t gw = x.tid / X::W, ngw = x.nthr / X::W;  // warps of the context (the grid's, cooperatively)
+    for (int32_t m = int32_t(w0) + gw; m < int32_t(w1); m += ngw) {
       int32_t* ci = cinfo + int64_t(m) * CI_STRIDE;
       if (ci[CI_NW] == 0) continue;
       const int jm = cand[m] >> 24;
@@ -2170,7 +2171,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
     x.sync();
     // prefix over the bucket counts: one warp, 32 buckets per lane (the
     // block scan's scratch holds the candidate records here)
-    if (x.warp == 0) {
+    if (x.tid < X::W) {
       const int PER = NB / X::W;
       int32_t* c = bk_cnt + 1 + x.lane * PER;
       int32_t sum = 0;
@@ -2179,7 +2180,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
       int32_t off = x.wexcl(sum, &tot);
       for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
       if (x.lane == 0) gsh[15] = tot;
-    } else if (x.warp == 1) {
+    } else if (x.tid >= X::W && x.tid < 2 * X::W) {
       const int PER = NB / X::W;
       int32_t* c = wk_cnt + 1 + x.lane * PER;
       int32_t sum = 0;
@@ -2189,7 +2190,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
       for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
       if (x.lane == 0) gsh[GS_WK] = tot <= g.cb_cap ? shb + 1 : 0;
     }
-    if (X::W == 1 && x.warp == 0) {  // one-thread context: the window prefix too
+    if (X::W == 1 && x.tid == 0) {  // one-thread context: the window prefix too
       int32_t* c = wk_cnt + 1;
       int32_t off = 0;
       for (int k = 0; k < NB; ++k) { off += c[k]; c[k] = off; }
@@ -2224,14 +2225,23 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
     x.sync();
     for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       int32_t* ci = cinfo + m * CI_STRIDE;
+#if TSL_PROF
+      if (g.grid_conf == 2) {
+        int64_t* dbg = g.wbuf + 8 * g.wcap + (m - w0) * 6;
+        dbg[0] = -7; dbg[1] = ci[CI_NW]; dbg[2] = ci[CI_STATUS]; dbg[3] = x.tid; dbg[4] = x.nthr; dbg[5] = w1;
+      }
+#endif
       if (ci[CI_NW] == 0) continue;
       const int j = cand[m] >> 24;
       const int64_t P = imax(1, g.st[j].period);
       const int64_t* wv = g.w_pool + 2 * int64_t(ci[CI_W0]);
       const int64_t m0 = imax(w0, coupled ? 0 : gsh[16 + j]);
       int32_t nconf = 0;
+      int64_t npass = 0, nlate = 0;
       auto consider = [&](int64_t i) {
+        if (i >= m) ++nlate;
         if (i >= m || i < m0 || (cand[i] >> 24) != j) return;
+        ++npass;
         if (comp && comp[i - w0] == comp[m - w0]) return;
         for (int32_t k = 0; k < imin(nconf, CAPC); ++k)
           if (ci[CI_CONF + k] == i) return;
@@ -2247,6 +2257,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
           ++nconf;
         }
       };
+      int64_t nexam = 0;
       if (!fits || nconf > CAPC) {
         for (int64_t i = m0; i < m; ++i) {
           if (cinfo[i * CI_STRIDE + CI_STATUS] != CS_OK) continue;
@@ -2258,12 +2269,19 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
             const int64_t lo = wv[2 * w] - k * P, hi = wv[2 * w + 1] - k * P;  // raw coordinates
             if (hi <= 0) continue;
             for (int64_t q = imax(0, bucket(lo)); q <= bucket(hi - 1) && q >= 0; ++q)
-              for (int32_t e = bk_cnt[q]; e < bk_cnt[q + 1]; ++e) consider(bk_ent[e]);
+              for (int32_t e = bk_cnt[q]; e < bk_cnt[q + 1]; ++e) { consider(bk_ent[e]); ++nexam; }
           }
       }
+#if TSL_PROF
+      if (g.grid_conf == 2) {
+        int64_t* dbg = g.wbuf + 8 * g.wcap + (m - w0) * 6;
+        dbg[0] = nexam; dbg[1] = fits; dbg[2] = shb; dbg[3] = ci[CI_NW]; dbg[4] = npass; dbg[5] = nlate;
+      }
+#endif
       ci[CI_NCONF] = nconf;
     }
   }
+  x.sync();  // (a grid context returns only when every CTA has written its lists)
 }
 
 // Component runs [r] of a window (x_order / x_seq2 / c_comp from
@@ -2458,6 +2476,14 @@ TSL_HD void component_speculation(X& x, GroupDev& g, int64_t w0, int64_t w1, con
   x.sync();
 }
 
+// Phase B of a window; an execution context may route it elsewhere (the CUDA
+// build runs it on every CTA of a cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD void conflicts_batch(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo,
+                            const int64_t* chull, bool coupled, const int32_t* comp) {
+  find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, comp);
+}
+
 template <class X>
 TSL_HD bool swap_pass(X& x, GroupDev& g) {
   int64_t* sh = x.sh;
@@ -2611,7 +2637,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sync();
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
-  find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, nullptr);
+  conflicts_batch(x, g, w0, w1, cand, cinfo, chull, coupled, nullptr);
   const bool use_comp = !coupled && g.spec_comp && wn > 1;
   if (use_comp) {
     x.sync();
@@ -2620,7 +2646,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     tick(5);
     // conflicts across components (a member's speculation includes its own
     // component's earlier results)
-    find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, g.c_comp);
+    conflicts_batch(x, g, w0, w1, cand, cinfo, chull, coupled, g.c_comp);
   }
   x.sync();
   tick(6);

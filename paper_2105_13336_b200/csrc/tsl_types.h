@@ -205,8 +205,12 @@ struct CoopCtl {
   int32_t* ccinfo;
   int64_t* cchull;
   int32_t cdone, cpad;           // worker CTAs done
+  // COOP_CONF: phase B of the window [cw0, cw1) on the grid
+  int64_t cw1;
+  const int32_t* ccomp;
+  int32_t ccoupled, cpad2;
 };
-enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_CONF = 6, COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;
@@ -259,7 +263,7 @@ struct GroupDev {
   int32_t* c_comp;   // [2 * c_cap] component speculation: union-find roots, previous members
   int64_t c_cap;
   int32_t spec_comp; // component speculation on (uncoupled swap passes)
-  int32_t pad3;
+  int32_t grid_conf; // cooperative launches run phase B on the whole grid
   int64_t c_wn;      // candidates of the window being processed
   int64_t* c_wscratch;  // cooperative launches: per-warp run lists (6 * c_wscap words per warp of the grid)
   int64_t c_wscap;

@@ -20,6 +20,7 @@
 #include <queue>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tensile_b200.h"
@@ -43,12 +44,65 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(TSL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// std::sort over up to 8 host threads: chunks sorted in parallel, then merged
+// pairwise in parallel rounds (large graphs: C4's 4e5 tensor ids).
+template <class T, class Cmp>
+void par_sort(std::vector<T>& v, Cmp cmp) {
+  const size_t n = v.size();
+  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t parts = 1;
+  while (parts * 2 <= std::min<size_t>(8, hw) && n / (parts * 2) >= 32768) parts *= 2;
+  if (parts == 1) { std::sort(v.begin(), v.end(), cmp); return; }
+  std::vector<size_t> cut(parts + 1);
+  for (size_t p = 0; p <= parts; ++p) cut[p] = n * p / parts;
+  {
+    std::vector<std::thread> th;
+    for (size_t p = 0; p < parts; ++p)
+      th.emplace_back([&, p] { std::sort(v.begin() + cut[p], v.begin() + cut[p + 1], cmp); });
+    for (auto& t : th) t.join();
+  }
+  std::vector<T> buf(n);
+  std::vector<T>* src = &v;
+  std::vector<T>* dst = &buf;
+  for (size_t w = 1; w < parts; w *= 2) {
+    std::vector<std::thread> th;
+    for (size_t p = 0; p < parts; p += 2 * w)
+      th.emplace_back([&, p] {
+        const size_t a = cut[p], m = cut[std::min(parts, p + w)], b = cut[std::min(parts, p + 2 * w)];
+        std::merge(src->begin() + a, src->begin() + m, src->begin() + m, src->begin() + b, dst->begin() + a, cmp);
+      });
+    for (auto& t : th) t.join();
+    std::swap(src, dst);
+  }
+  if (src != &v) v.swap(*src);
+}
+
+// Rank of every id in std::string order, ties by index (a stable sort). The
+// sort compares a 16-byte big-endian prefix held inline (ids of one job share
+// long prefixes, but rarely 16 bytes) and only then the strings.
 std::vector<int32_t> lex_rank(const std::vector<std::string>& ids) {
-  std::vector<int32_t> idx(ids.size());
-  std::iota(idx.begin(), idx.end(), 0);
-  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  struct K {
+    uint64_t k0, k1;
+    int32_t i;
+  };
+  auto be = [](const std::string& s, size_t off) {
+    uint64_t v = 0;
+    for (size_t b = 0; b < 8; ++b) v = (v << 8) | (off + b < s.size() ? uint8_t(s[off + b]) : 0u);
+    return v;
+  };
+  std::vector<K> keys(ids.size());
+  for (size_t i = 0; i < ids.size(); ++i) keys[i] = K{be(ids[i], 0), be(ids[i], 8), int32_t(i)};
+  par_sort(keys, [&](const K& a, const K& b) {
+    if (a.k0 != b.k0) return a.k0 < b.k0;
+    if (a.k1 != b.k1) return a.k1 < b.k1;
+    const std::string& x = ids[a.i];
+    const std::string& y = ids[b.i];
+    // equal 16-byte prefixes (zero-padded): compare the rest, then the index
+    const int c = (x.size() > 16 || y.size() > 16) ? x.compare(y) : (x.size() == y.size() ? 0 : x.size() < y.size() ? -1 : 1);
+    return c != 0 ? c < 0 : a.i < b.i;
+  });
   std::vector<int32_t> rank(ids.size());
-  for (size_t r = 0; r < idx.size(); ++r) rank[idx[r]] = static_cast<int32_t>(r);
+  for (size_t r = 0; r < keys.size(); ++r) rank[keys[r].i] = static_cast<int32_t>(r);
   return rank;
 }
 
@@ -75,6 +129,14 @@ const char* kind_name(int k) {
 // the ranks need anyway, successor sets are one sorted edge list.
 Graph load_graph(const tsl_job_desc& d) {
   Graph g;
+  static const bool lp = std::getenv("TSL_PREP_PROFILE") != nullptr;
+  auto lt0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!lp) return;
+    auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  load %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - lt0).count());
+    lt0 = t;
+  };
   g.job_id = d.job_id ? d.job_id : "";
   g.T = d.n_tensors;
   g.O = d.n_ops;
@@ -83,6 +145,7 @@ Graph load_graph(const tsl_job_desc& d) {
     fail(TSL_ERR_ARGUMENT, "null tensor table in job " + g.job_id);
   if (g.O > 0 && (!d.op_ids || !d.op_kinds || !d.op_phases || !d.op_in_offsets || !d.op_out_offsets))
     fail(TSL_ERR_ARGUMENT, "null op table in job " + g.job_id);
+  lap("strings");
   g.tid.reserve(g.T);
   g.size.assign(d.tensor_sizes, d.tensor_sizes + g.T);
   g.kind.assign(d.tensor_kinds, d.tensor_kinds + g.T);
@@ -90,7 +153,21 @@ Graph load_graph(const tsl_job_desc& d) {
     g.tid.emplace_back(d.tensor_ids[i] ? d.tensor_ids[i] : "");
     if (g.kind[i] < 0 || g.kind[i] > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(g.kind[i]));
   }
-  g.trank = lex_rank(g.tid);
+  lap("tid");
+  // op ids are ranked on a second thread while the tensor ids are (both are
+  // O(n log n) string sorts: ~0.1 s each for C4's 4e5 tensors / 2e5 ops)
+  g.oid.reserve(g.O);
+  for (int o = 0; o < g.O; ++o) g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
+  lap("oid");
+  std::vector<int32_t> orank;
+  {
+    std::thread ranker;
+    if (g.O > 4096) ranker = std::thread([&] { orank = lex_rank(g.oid); });
+    else orank = lex_rank(g.oid);
+    g.trank = lex_rank(g.tid);
+    if (ranker.joinable()) ranker.join();
+  }
+  lap("lexrank");
   {
     // first tensor (in order) that is nonpositive or a repeated id
     std::vector<int32_t> by(g.T);
@@ -106,19 +183,17 @@ Graph load_graph(const tsl_job_desc& d) {
       if (dup[i]) fail(TSL_ERR_VALIDATION, "duplicate tensor id " + g.tid[i]);
     }
   }
+  lap("ranks+dups");
   std::vector<int32_t> producer(g.T, -1);
   std::vector<std::string> okind;
   std::vector<int8_t> phase;
-  g.oid.reserve(g.O);
   okind.reserve(g.O);
   for (int o = 0; o < g.O; ++o) {
-    g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
     okind.emplace_back(d.op_kinds[o] ? d.op_kinds[o] : "");
     int8_t ph = d.op_phases[o];
     if (ph != 0 && ph != 1) fail(TSL_ERR_VALIDATION, "unknown op phase: #" + std::to_string(ph));
     phase.push_back(ph);
   }
-  std::vector<int32_t> orank = lex_rank(g.oid);
   std::vector<char> odup(g.O, 0);
   {
     std::vector<int32_t> by(g.O);
@@ -126,6 +201,7 @@ Graph load_graph(const tsl_job_desc& d) {
     for (int r = 1; r < g.O; ++r)
       if (g.oid[by[r]] == g.oid[by[r - 1]]) odup[by[r]] = 1;
   }
+  lap("opkinds+odup");
   g.in_off.assign(1, 0);
   g.out_off.assign(1, 0);
   for (int o = 0; o < g.O; ++o) {
@@ -147,6 +223,7 @@ Graph load_graph(const tsl_job_desc& d) {
     g.in_off.push_back(static_cast<int32_t>(g.in.size()));
     g.out_off.push_back(static_cast<int32_t>(g.out.size()));
   }
+  lap("csr");
   for (int t = 0; t < g.T; ++t) {
     if (g.kind[t] == TSL_KIND_INPUT || g.kind[t] == TSL_KIND_PARAMETER) {
       if (producer[t] >= 0) fail(TSL_ERR_VALIDATION, "source tensor " + g.tid[t] + " must not have a producing op");
@@ -203,11 +280,30 @@ Graph load_graph(const tsl_job_desc& d) {
           if (cons[k] != o) edges.emplace_back(cons[k], o);
       }
   }
-  std::sort(edges.begin(), edges.end());
-  edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+  lap("edges");
+  // group the edges by source (counting sort), then sort + dedupe each
+  // source's short target list: the same (source, target) order as one
+  // global sort + unique, in linear time
   std::vector<int32_t> indeg(g.O, 0), soff(g.O + 1, 0);
-  for (auto& e : edges) { indeg[e.second]++; soff[e.first + 1]++; }
-  for (int o = 0; o < g.O; ++o) soff[o + 1] += soff[o];
+  {
+    std::vector<int32_t> cnt(g.O + 1, 0), tgt(edges.size());
+    for (auto& e : edges) cnt[e.first + 1]++;
+    for (int o = 0; o < g.O; ++o) cnt[o + 1] += cnt[o];
+    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+    for (auto& e : edges) tgt[cur[e.first]++] = e.second;
+    size_t w = 0;
+    for (int o = 0; o < g.O; ++o) {
+      auto b = tgt.begin() + cnt[o], e = tgt.begin() + cnt[o + 1];
+      std::sort(b, e);
+      auto u = std::unique(b, e);
+      soff[o] = int32_t(w);
+      for (auto it = b; it != u; ++it) edges[w++] = {o, *it};
+    }
+    soff[g.O] = int32_t(w);
+    edges.resize(w);
+  }
+  for (auto& e : edges) indeg[e.second]++;
+  lap("sort-edges");
   auto cmp = [&](int32_t a, int32_t b) { return orank[a] > orank[b]; };
   std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
   for (int o = 0; o < g.O; ++o)
@@ -221,6 +317,7 @@ Graph load_graph(const tsl_job_desc& d) {
       if (--indeg[edges[k].second] == 0) ready.push(edges[k].second);
   }
   if (static_cast<int32_t>(g.topo.size()) != g.O) fail(TSL_ERR_VALIDATION, "cycle detected in graph of job " + g.job_id);
+  lap("topo");
   // latency table (generate_access_sequence, access.cpp:33-38), checked in
   // topological order like the reference.
   g.lat.assign(g.O, 0);

@@ -715,8 +715,9 @@ constexpr int GS_WPOOL = 443;   // gsh slot: window-pool bump counter of the pas
 constexpr int GS_CCHG = 444;    // gsh slot: component union-find round changed something
 constexpr int GS_CRUN = 445;    // gsh slot: next component run to process
 constexpr int GS_NRUN = 446;    // gsh slot: component runs of >= 2 members
+constexpr int GS_QTOT = 448;    // gsh slots [448, 456): phase B prefix quarters' totals
 static_assert(MAXB * 16 + GS_POFF + 128 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
-static_assert(MAXB * 16 + 446 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
+static_assert(MAXB * 16 + 456 < SH_WORDS - 1, "gsh slots overlap the clock word (NF == 16)");
 constexpr int CAPC = 7;         // conflict list entries per candidate
 constexpr int CB_NB = 1024;     // time buckets of the conflict index
 constexpr int CB_GRID_MAX = 160;  // passes with at most this many candidates check all pairs directly
@@ -2093,6 +2094,12 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
                            const int64_t* chull, bool coupled, const int32_t* comp) {
   int64_t* gsh = x.sh + MAXB * NF;
   const int64_t wn = w1 - w0;
+#if TSL_PROF
+  int64_t pc0 = clock64();
+  auto ptick = [&](int k) { if (x.tid == 0) { const int64_t t = clock64(); g.stats.prof[k] += t - pc0; pc0 = t; } };
+#else
+  auto ptick = [](int) {};
+#endif
   // ---- B. conflicts with earlier speculative commits of the same job ----
   // Small passes: one thread per (candidate, earlier candidate) pair. Large
   // passes: every speculative pair interval goes into a time-bucketed index;
@@ -2141,12 +2148,14 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
     if (x.tid == 0) { gsh[14] = 0; gsh[GS_NB] = NB; }
     for (int32_t k = x.tid; k < NB + 1; k += x.nthr) { bk_cnt[k] = 0; wk_cnt[k] = 0; }
     x.sync();
+    ptick(0);
     for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       const int32_t* ci = cinfo + m * CI_STRIDE;
       if (ci[CI_STATUS] == CS_OK) x.amax(&gsh[14], chull[m * 4 + 3]);
       if (ci[CI_NW]) x.amax(&gsh[14], chull[m * 4 + 1]);
     }
     x.sync();
+    ptick(1);
     int shb = 0;
     while ((gsh[14] >> shb) >= NB) ++shb;
     auto bucket = [&](int64_t t) -> int64_t { return t < 0 ? -1 : imin(t >> shb, int64_t(NB) - 1); };
@@ -2169,37 +2178,67 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
           x.aadd32(&wk_cnt[q + 1], 1);
     }
     x.sync();
-    // prefix over the bucket counts: one warp, 32 buckets per lane (the
-    // block scan's scratch holds the candidate records here)
-    if (x.tid < X::W) {
-      const int PER = NB / X::W;
-      int32_t* c = bk_cnt + 1 + x.lane * PER;
-      int32_t sum = 0;
-      for (int k = 0; k < PER; ++k) sum += c[k];
-      int32_t tot = 0;
-      int32_t off = x.wexcl(sum, &tot);
-      for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
-      if (x.lane == 0) gsh[15] = tot;
-    } else if (x.tid >= X::W && x.tid < 2 * X::W) {
-      const int PER = NB / X::W;
-      int32_t* c = wk_cnt + 1 + x.lane * PER;
-      int32_t sum = 0;
-      for (int k = 0; k < PER; ++k) sum += c[k];
-      int32_t tot = 0;
-      int32_t off = x.wexcl(sum, &tot);
-      for (int k = 0; k < PER; ++k) { off += c[k]; c[k] = off; }
-      if (x.lane == 0) gsh[GS_WK] = tot <= g.cb_cap ? shb + 1 : 0;
+    ptick(2);
+    // prefix over the bucket counts (the block scan's scratch holds the
+    // candidate records here): 4 warps per table, each scanning its quarter
+    // 32 consecutive buckets at a time (coalesced, a warp prefix sum carrying
+    // the running total), then the quarters' totals are added in
+    constexpr int QW = 4;
+    if (X::W > 1 && x.tid < 2 * QW * X::W) {
+      const int tab = x.tid / (QW * X::W), q = (x.tid / X::W) % QW;
+      const int PER = NB / QW;
+      int32_t* c = (tab ? wk_cnt : bk_cnt) + 1 + q * PER;
+      int32_t run = 0;
+      constexpr int U = 8;  // loads of 8 rows in flight before their scans
+      for (int k = 0; k < PER; k += U * X::W) {
+        int32_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = (k + u * X::W < PER) ? c[k + u * X::W + x.lane] : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k + u * X::W >= PER) break;
+          int32_t tot = 0;
+          const int32_t ex = x.wexcl(v[u], &tot);
+          c[k + u * X::W + x.lane] = run + ex + v[u];
+          run += tot;
+        }
+      }
+      if (x.lane == 0) gsh[GS_QTOT + tab * QW + q] = run;
     }
-    if (X::W == 1 && x.tid == 0) {  // one-thread context: the window prefix too
-      int32_t* c = wk_cnt + 1;
-      int32_t off = 0;
-      for (int k = 0; k < NB; ++k) { off += c[k]; c[k] = off; }
-      gsh[GS_WK] = off <= g.cb_cap ? shb + 1 : 0;
+    if (X::W == 1 && x.tid == 0) {  // one-thread context
+      for (int tab = 0; tab < 2; ++tab) {
+        int32_t* c = (tab ? wk_cnt : bk_cnt) + 1;
+        int32_t off = 0;
+        for (int k = 0; k < NB; ++k) { off += c[k]; c[k] = off; }
+        gsh[GS_QTOT + tab * QW] = off;
+        for (int q = 1; q < QW; ++q) gsh[GS_QTOT + tab * QW + q] = 0;
+      }
     }
     x.sync();
+    ptick(3);
+    if (X::W > 1 && x.tid < 2 * QW * X::W) {
+      const int tab = x.tid / (QW * X::W), q = (x.tid / X::W) % QW;
+      const int PER = NB / QW;
+      int64_t add = 0;
+      for (int r = 0; r < q; ++r) add += gsh[GS_QTOT + tab * QW + r];
+      int32_t* c = (tab ? wk_cnt : bk_cnt) + 1 + q * PER;
+      if (add) {
+#pragma unroll 8
+        for (int k = x.lane; k < PER; k += X::W) c[k] += int32_t(add);
+      }
+    }
+    if (x.tid == 0) {
+      int64_t tb = 0, tw = 0;
+      for (int q = 0; q < QW; ++q) { tb += gsh[GS_QTOT + q]; tw += gsh[GS_QTOT + QW + q]; }
+      gsh[15] = tb;
+      gsh[GS_WK] = tw <= g.cb_cap ? shb + 1 : 0;
+    }
+    x.sync();
+    ptick(4);
     const bool fits = gsh[15] <= g.cb_cap;
     for (int32_t k = x.tid; k < NB; k += x.nthr) { bk_cur[k] = bk_cnt[k]; wk_cur[k] = wk_cnt[k]; }
     x.sync();
+    ptick(5);
     if (gsh[GS_WK]) {
       for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
         const int32_t* ci = cinfo + m * CI_STRIDE;
@@ -2223,6 +2262,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
       }
     }
     x.sync();
+    ptick(6);
     for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
       int32_t* ci = cinfo + m * CI_STRIDE;
 #if TSL_PROF
@@ -2282,6 +2322,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
     }
   }
   x.sync();  // (a grid context returns only when every CTA has written its lists)
+  ptick(7);
 }
 
 // Component runs [r] of a window (x_order / x_seq2 / c_comp from

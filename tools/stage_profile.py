@@ -59,3 +59,6 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C5s0"]:
                   f"sweep {qp[2]/n:.0f} cyc, swept {qp[9]/n:.2f}; search cyc/search busy {qp[3]/max(1,qp[6]):.0f} "
                   f"(x{qp[6]/n:.2f}) pend {qp[4]/max(1,qp[7]):.0f} (x{qp[7]/n:.2f}) storage {qp[5]/max(1,qp[8]):.0f} "
                   f"(x{qp[8]/n:.2f})", flush=True)
+        if os.environ.get("TSL_CONF_PROF"):
+            print("   conflict phases (prof build): clear/maxend/count/prefix1/prefix2/cursors/fill/consider:",
+                  list(s.get("queryprof", [0] * 16))[:8], flush=True)

@@ -304,6 +304,74 @@ char* tsl_result_report_json(const tsl_result* r, int32_t i);
 void tsl_result_destroy(tsl_result* r);
 void tsl_free(void* p);
 
+/* PlannerConfig::validate (config.hpp:25-35) alone. */
+int tsl_validate_config(const tsl_config* cfg);
+/* SchedulingPlan::version of one job in a result (Orchestrator::rebuild
+ * numbers its plans, orchestrator.cpp:104-108). */
+int tsl_result_set_version(tsl_result* result, const char* job_id, int64_t version);
+
+/* ---- Planning session: memsched::Orchestrator (orchestrator.hpp:30-60;
+ * orchestrator.cpp:89-159) -- the replan lifecycle around the device planner.
+ * Jobs arrive (add_job, op_latencies = current estimates or NULL) and depart
+ * (remove_job); rebuild = one build_plan over the active set with per-job
+ * plan versions; replan_if_needed = EWMA correction + drift-triggered rebuild
+ * (result NULL when no replan). Every rebuild's wall time is recorded. ---- */
+typedef struct tsl_session tsl_session;
+int tsl_session_create(tsl_ctx* ctx, const tsl_config* cfg, tsl_session** out);
+void tsl_session_destroy(tsl_session* session);
+int tsl_session_add_job(tsl_session* session, const tsl_job_desc* job);
+int tsl_session_remove_job(tsl_session* session, const char* job_id);
+int tsl_session_set_latencies(tsl_session* session, const char* job_id, const int64_t* op_latencies);
+int tsl_session_rebuild(tsl_session* session, tsl_result** out);
+int tsl_session_replan_if_needed(tsl_session* session, int32_t n, const char* const* job_ids,
+                                 const int64_t* const* observed_op_ticks, tsl_result** out);
+int32_t tsl_session_replan_count(const tsl_session* session);
+int32_t tsl_session_rebuild_times(const tsl_session* session, const double** ms);
+int32_t tsl_session_n_jobs(const tsl_session* session);
+int tsl_session_latencies(const tsl_session* session, const char* job_id, int64_t* out_op_latencies);
+
+/* ---- Tick-level executor model (the reference's simulate, simulator.hpp:84-87;
+ * simulator.cpp:26-582): vanilla / scheduled / passive modes, one FIFO
+ * transfer channel, LRU eviction under the budget in passive mode. ---- */
+typedef struct tsl_sim tsl_sim;
+enum { TSL_SIM_VANILLA = 0, TSL_SIM_SCHEDULED = 1, TSL_SIM_PASSIVE = 2 };
+typedef struct tsl_sim_config {      /* SimConfig (simulator.hpp:16-27) */
+  int32_t mode;                      /* TSL_SIM_*                        */
+  int32_t iterations;                /* >= 1                             */
+  int64_t ticks_per_iteration_limit; /* default 10,000,000               */
+  int64_t memory_budget;             /* enforced in passive mode only    */
+  int64_t pcie_bandwidth;
+  int64_t transfer_setup;
+  int32_t n_slowdown;                /* gpu_slowdown_curve entries       */
+  const int32_t* slowdown_jobs;      /* concurrent jobs ...              */
+  const double* slowdown_mult;       /* ... -> multiplier (>= 1)         */
+} tsl_sim_config;
+/* SimController::on_iteration_end (simulator.hpp:73-79): called at each job's
+ * iteration boundary with the ticks of the ops it ran (op order, -1 = not
+ * run); new plans are installed with tsl_sim_set_plan from inside the
+ * callback and take effect at each affected job's next boundary. Nonzero
+ * return aborts the run with that status. */
+typedef int (*tsl_sim_controller_fn)(void* user, tsl_sim* sim, int32_t job, int32_t iteration,
+                                     const int64_t* observed_op_ticks);
+/* memsched::simulate(jobs, plans, config, controller): jobs carry their TRUE
+ * latencies in op_latencies; plans[k] may have no events (vanilla/passive
+ * runs read only release_flags). */
+int tsl_simulate(const tsl_job_desc* jobs, const int64_t* launch_ticks, int32_t n_jobs,
+                 const tsl_plan_desc* plans, const tsl_sim_config* cfg,
+                 tsl_sim_controller_fn controller, void* user, tsl_sim** out);
+int tsl_sim_set_plan(tsl_sim* sim, int32_t job, const tsl_plan_desc* plan);
+int64_t tsl_sim_peak(const tsl_sim* sim);
+/* SimulationTrace as JSON (peak, blocked_ticks, passive_swap_count, per job:
+ * peak, iteration_times, plan_versions, footprint_curve; transfers,
+ * safety_violations, passive_events) / SimulationTrace::to_csv. Free with tsl_free. */
+char* tsl_sim_trace_json(const tsl_sim* sim);
+char* tsl_sim_trace_csv(const tsl_sim* sim);
+void tsl_sim_destroy(tsl_sim* sim);
+/* activity_analysis (access.cpp:61-78): the release-at-last-use flags (the
+ * last access of every Interim tensor id), ascending; the vanilla / passive
+ * modes' plans (scenario.cpp:180-194). out may be null to query *n_out. */
+int tsl_base_release_flags(const tsl_job_desc* job, int64_t* out_flags, int32_t cap, int32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

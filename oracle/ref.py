@@ -120,6 +120,28 @@ def analyze_job(graph, latencies, plan) -> dict:
     return json.loads(_take(out))
 
 
+def simulate(jobs, plans: dict, config: dict) -> dict:
+    """memsched::simulate: jobs [(graph, true latencies, launch_tick)], plans a
+    save_plans document ({job: plan}), config {"mode", "iterations", ...}."""
+    L = lib()
+    L.ref_simulate.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    out = ctypes.c_void_p()
+    req = json.dumps({"jobs": [{"graph": g, "latencies": l, "launch_tick": t} for g, l, t in jobs],
+                      "plans": plans, "config": config})
+    _check(L.ref_simulate(req.encode(), ctypes.byref(out)))
+    return json.loads(_take(out))
+
+
+def run_scenario(document: str, base_dir: str, modes=("vanilla", "scheduled", "passive")) -> dict:
+    """run_scenario: {"stats": {mode: ModeStats::to_json text}, "csv": {mode: trace CSV},
+    "plans": save_plans text, "replan_count", "diagnostic"}."""
+    L = lib()
+    L.ref_run_scenario.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    out = ctypes.c_void_p()
+    _check(L.ref_run_scenario(document.encode(), base_dir.encode(), ",".join(modes).encode(), ctypes.byref(out)))
+    return json.loads(_take(out))
+
+
 def plan_scenario(document: str, base_dir: str):
     """The reference CLI's `plan` (load_scenario + plan_scenario):
     (plans.json text, peaks.json text, diagnostic)."""

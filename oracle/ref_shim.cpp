@@ -238,4 +238,93 @@ int ref_plan_scenario(const char* document, const char* base_dir, char** plans_j
   });
 }
 
+// memsched::simulate (simulator.cpp:573-582) on caller plans.
+// request: {"jobs": [{"graph", "latencies" (TRUE latencies), "launch_tick"}],
+//           "plans": <save_plans document>, "config": {"mode": "vanilla" |
+//           "scheduled" | "passive", "iterations", "memory_budget",
+//           "pcie_bandwidth", "transfer_setup", "slowdown": {jobs: mult},
+//           "ticks_per_iteration_limit"}}
+// out: the trace in tsl_sim_trace_json's layout + "csv" (to_csv).
+int ref_simulate(const char* request, char** out_json) {
+  return guarded([&] {
+    json req = json::parse(request);
+    std::vector<SimJob> jobs;
+    for (const auto& j : req.at("jobs")) {
+      SimJob sj;
+      sj.graph = load_graph(j.at("graph").dump());
+      for (const auto& [k, v] : j.at("latencies").items()) sj.true_latencies[k] = v.get<Tick>();
+      sj.launch_tick = j.value("launch_tick", Tick{0});
+      jobs.push_back(std::move(sj));
+    }
+    std::map<JobId, SchedulingPlan> plans;
+    if (req.contains("plans")) plans = load_plans(req["plans"].dump());
+    const json& c = req.at("config");
+    SimConfig cfg;
+    const std::string mode = c.value("mode", std::string("vanilla"));
+    cfg.mode = mode == "scheduled" ? SimMode::Scheduled : mode == "passive" ? SimMode::Passive : SimMode::Vanilla;
+    cfg.iterations = c.value("iterations", 1);
+    cfg.memory_budget = c.value("memory_budget", Bytes{0});
+    cfg.pcie_bandwidth = c.value("pcie_bandwidth", Bytes{1});
+    cfg.transfer_setup = c.value("transfer_setup", Tick{0});
+    if (c.contains("ticks_per_iteration_limit")) cfg.ticks_per_iteration_limit = c["ticks_per_iteration_limit"].get<Tick>();
+    if (c.contains("slowdown"))
+      for (const auto& [k, v] : c["slowdown"].items()) cfg.gpu_slowdown_curve[std::stoi(k)] = v.get<double>();
+    SimulationTrace t = simulate(jobs, plans, cfg);
+    ojson o;
+    o["peak"] = t.peak;
+    o["blocked_ticks"] = t.blocked_ticks;
+    o["passive_swap_count"] = t.passive_swap_count;
+    ojson js = ojson::array();
+    for (const auto& sj : jobs) {
+      const JobId id = sj.graph.job_id();
+      ojson e;
+      e["job_id"] = id;
+      e["peak"] = t.per_job_peak.count(id) ? t.per_job_peak.at(id) : 0;
+      e["iteration_times"] = t.iteration_times.count(id) ? t.iteration_times.at(id) : std::vector<Tick>{};
+      e["plan_versions"] = t.plan_versions.count(id) ? t.plan_versions.at(id) : std::vector<std::int64_t>{};
+      ojson curve = ojson::array();
+      if (t.per_job_curve.count(id))
+        for (const auto& [tick, b] : t.per_job_curve.at(id)) curve.push_back({tick, b});
+      e["footprint_curve"] = curve;
+      js.push_back(e);
+    }
+    o["jobs"] = js;
+    ojson tr = ojson::array();
+    for (const auto& x : t.transfers) tr.push_back({x.start, x.end, x.job_id, x.tensor_id, x.kind});
+    o["transfers"] = tr;
+    o["safety_violations"] = t.safety_violations;
+    ojson pe = ojson::array();
+    for (const auto& [j, it, s] : t.passive_events) pe.push_back({j, it, s});
+    o["passive_events"] = pe;
+    o["csv"] = t.to_csv();
+    *out_json = dup(o.dump());
+  });
+}
+
+// run_scenario (scenario.cpp:223-262): the modes' ModeStats::to_json texts,
+// the scheduled plans (save_plans) and replan count, and each mode's trace CSV.
+int ref_run_scenario(const char* document, const char* base_dir, const char* modes_csv, char** out_json) {
+  return guarded([&] {
+    ScenarioConfig cfg = load_scenario(document, base_dir);
+    std::set<std::string> modes;
+    std::string m = modes_csv, cur;
+    for (char ch : m + ",") {
+      if (ch == ',') { if (!cur.empty()) modes.insert(cur); cur.clear(); }
+      else cur += ch;
+    }
+    ScenarioResult r = run_scenario(cfg, modes);
+    ojson o;
+    ojson st = ojson::object();
+    for (const auto& [mode, s] : r.stats) st[mode] = s.to_json();
+    o["stats"] = st;
+    ojson csv = ojson::object();
+    for (const auto& [mode, t] : r.traces) csv[mode] = t.to_csv();
+    o["csv"] = csv;
+    o["plans"] = save_plans(r.plans);
+    o["replan_count"] = r.replan_count;
+    o["diagnostic"] = r.plan_diagnostic;
+    *out_json = dup(o.dump());
+  });
+}
+
 }  // extern "C"

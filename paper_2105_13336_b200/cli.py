@@ -71,7 +71,9 @@ def load_scenario(document: str, base_dir: str) -> dict:
             cfg[key] = float(doc[key])
     if "stall_min_iters" in doc:
         cfg["stall_min_iters"] = int(doc["stall_min_iters"])
-    out = {"config": cfg, "jobs": [],
+    out = {"config": cfg, "jobs": [], "launch_ticks": [],
+           "iterations": int(doc.get("iterations", 3)), "seed": int(doc.get("seed", 0)),
+           "gpu_slowdown_curve": {int(k): float(v) for k, v in doc.get("gpu_slowdown_curve", {}).items()},
            "predictor_file": _resolve(base_dir, doc["predictor_file"]) if "predictor_file" in doc else "",
            "latency_file": _resolve(base_dir, doc["latency_file"]) if "latency_file" in doc else ""}
     entries = []
@@ -92,6 +94,7 @@ def load_scenario(document: str, base_dir: str) -> dict:
             raise CliError("graph file is not valid JSON: " + str(ex))
         ratios[g.get("job_id", "")] = e["max_swap_ratio"]
         out["jobs"].append(g)
+        out["launch_ticks"].append(e["launch_tick"])
     cfg["max_swap_ratios"] = ratios
     return out
 

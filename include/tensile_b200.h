@@ -330,6 +330,23 @@ int32_t tsl_session_rebuild_times(const tsl_session* session, const double** ms)
 int32_t tsl_session_n_jobs(const tsl_session* session);
 int tsl_session_latencies(const tsl_session* session, const char* job_id, int64_t* out_op_latencies);
 
+/* ---- Cold-start latency predictor: LatencyPredictor (latency.hpp:45-66,
+ * latency.cpp:11-149) and predict_latencies (orchestrator.cpp:72-87). ---- */
+typedef struct tsl_predictor tsl_predictor;
+/* LatencyPredictor::fit: sample k = (op_kinds[k], values[value_offsets[k] ..
+ * value_offsets[k+1]) = input dims, attributes, gpu usage, labels[k]). */
+int tsl_latency_fit(int32_t n_samples, const char* const* op_kinds, const int32_t* value_offsets,
+                    const double* values, const double* labels, tsl_predictor** out);
+int tsl_latency_from_json(const char* document, tsl_predictor** out);
+char* tsl_latency_to_json(const tsl_predictor* predictor);  /* free with tsl_free */
+int tsl_latency_predict(const tsl_predictor* predictor, const char* op_kind, const double* values,
+                        int32_t n_values, double* out);
+int tsl_latency_r2(const tsl_predictor* predictor, const char* op_kind, double* out);
+/* every op's predicted latency (ticks, op order); op attributes as CSR (NULL: none) */
+int tsl_predict_latencies(const tsl_predictor* predictor, const tsl_job_desc* job, const int32_t* op_attr_offsets,
+                          const double* op_attrs, double gpu_usage, int64_t* out_op_latencies);
+void tsl_latency_destroy(tsl_predictor* predictor);
+
 /* ---- Tick-level executor model (the reference's simulate, simulator.hpp:84-87;
  * simulator.cpp:26-582): vanilla / scheduled / passive modes, one FIFO
  * transfer channel, LRU eviction under the budget in passive mode. ---- */

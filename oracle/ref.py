@@ -132,6 +132,38 @@ def simulate(jobs, plans: dict, config: dict) -> dict:
     return json.loads(_take(out))
 
 
+def _call_json(fn_name, argtypes, *args):
+    L = lib()
+    fn = getattr(L, fn_name)
+    fn.argtypes = argtypes + [ctypes.POINTER(ctypes.c_void_p)]
+    out = ctypes.c_void_p()
+    _check(fn(*args, ctypes.byref(out)))
+    return _take(out)
+
+
+def training_samples(graph: dict, seed: int, per_op: int, noise: float):
+    """generate_training_samples (workload.cpp:211-248): [(kind, values, label)]."""
+    s = _call_json("ref_training_samples", [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_double],
+                   json.dumps(graph).encode(), seed, per_op, noise)
+    return [tuple(x) for x in json.loads(s)]
+
+
+def linear_samples(noise: float, seed: int):
+    """test_latency.cpp:44-62's samples: [(kind, values, label)]."""
+    s = _call_json("ref_linear_samples", [ctypes.c_double, ctypes.c_uint64], noise, seed)
+    return [tuple(x) for x in json.loads(s)]
+
+
+def predictor_roundtrip(document: str) -> str:
+    return _call_json("ref_predictor_roundtrip", [ctypes.c_char_p], document.encode())
+
+
+def predict_latencies(graph: dict, predictor_doc: str, usage: float) -> dict:
+    s = _call_json("ref_predict_latencies", [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double],
+                   json.dumps(graph).encode(), predictor_doc.encode(), usage)
+    return json.loads(s)
+
+
 def run_scenario(document: str, base_dir: str, modes=("vanilla", "scheduled", "passive")) -> dict:
     """run_scenario: {"stats": {mode: ModeStats::to_json text}, "csv": {mode: trace CSV},
     "plans": save_plans text, "replan_count", "diagnostic"}."""

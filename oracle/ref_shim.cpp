@@ -10,6 +10,7 @@
 // (peak.cpp:258-272).
 #include <algorithm>
 #include <chrono>
+#include <random>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -18,6 +19,7 @@
 
 #include <nlohmann/json.hpp>
 
+#include "memsched/latency.hpp"
 #include "memsched/orchestrator.hpp"
 #include "memsched/peak.hpp"
 #include "memsched/plan.hpp"
@@ -235,6 +237,51 @@ int ref_plan_scenario(const char* document, const char* base_dir, char** plans_j
     o += "}\n";
     *peaks_json = dup(o);
     *diag = dup(result.plan_diagnostic);
+  });
+}
+
+// generate_training_samples (workload.cpp:211-248) for a graph:
+// [[op_kind, [values...], label], ...].
+int ref_training_samples(const char* graph_json, std::uint64_t seed, int per_op, double noise, char** out_json) {
+  return guarded([&] {
+    ComputeGraph g = load_graph(graph_json);
+    ojson o = ojson::array();
+    for (const auto& [fv, y] : generate_training_samples(g, seed, per_op, noise))
+      o.push_back({fv.op_kind, fv.values, y});
+    *out_json = dup(o.dump());
+  });
+}
+
+// The reference unit test's linear_samples (test_latency.cpp:44-62):
+// latency = 2 * dim0 + 5 with optional multiplicative noise.
+int ref_linear_samples(double noise_fraction, std::uint64_t seed, char** out_json) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> usage(0.0, 1.0);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    ojson o = ojson::array();
+    for (int i = 1; i <= 60; ++i) {
+      std::vector<double> v = {static_cast<double>(i), usage(rng)};
+      double label = 2.0 * v[0] + 5.0;
+      if (noise_fraction > 0) label *= 1.0 + noise_fraction * gauss(rng);
+      o.push_back({"k", v, label});
+    }
+    *out_json = dup(o.dump());
+  });
+}
+
+// LatencyPredictor::from_json -> to_json (the reference's text of a document).
+int ref_predictor_roundtrip(const char* doc, char** out) {
+  return guarded([&] { *out = dup(LatencyPredictor::from_json(doc).to_json()); });
+}
+
+// predict_latencies (orchestrator.cpp:72-87) with a predictor document.
+int ref_predict_latencies(const char* graph_json, const char* predictor_doc, double usage, char** out_json) {
+  return guarded([&] {
+    ComputeGraph g = load_graph(graph_json);
+    ojson o = ojson::object();
+    for (const auto& [op, t] : predict_latencies(g, LatencyPredictor::from_json(predictor_doc), usage)) o[op] = t;
+    *out_json = dup(o.dump());
   });
 }
 

@@ -12,9 +12,9 @@ DIR/plans.json (save_plans) and DIR/peaks.json (the CLI's {"job": PeakReport}
 document) byte-identical to the reference CLI's. The plan diagnostic, if any,
 goes to stdout; errors print "error: <text>" and exit 1 (memsched_cli.cpp:175-178).
 
-Latency source: `latency_file` ({job: {op: ticks}}). A `predictor_file`
-(cold start through the Eigen-fitted LatencyPredictor) is outside this build
-and is rejected with an explanatory error.
+Latency source: `latency_file` ({job: {op: ticks}}) or `predictor_file` (a
+LatencyPredictor document: cold start, every op's latency predicted at the
+config's cold_start_gpu_usage -- latency.py / csrc/tsl_latency.cpp).
 """
 from __future__ import annotations
 
@@ -104,8 +104,12 @@ def plan_scenario(scn: dict, planner) -> tuple:
     if scn["latency_file"]:
         table = json.loads(_read(scn["latency_file"]))
     elif scn["predictor_file"]:
-        raise CliError("predictor_file (cold start through the fitted LatencyPredictor) is not supported by the "
-                       "B200 planner CLI; supply a latency table (latency_file)")
+        # Orchestrator::plan_cold_start (orchestrator.cpp:118-124): every op's
+        # latency from the fitted predictor at cold_start_gpu_usage
+        from .latency import LatencyPredictor
+        pred = LatencyPredictor.from_json(_read(scn["predictor_file"]), lib_path=planner.lib._name)
+        usage = scn["config"].get("cold_start_gpu_usage", 0.5)
+        table = {g.get("job_id", ""): pred.predict_latencies(g, usage) for g in scn["jobs"]}
     else:
         raise CliError("scheduled mode needs a latency source: fit a predictor (predictor_file) or supply a "
                        "latency table (latency_file)")

@@ -1797,6 +1797,7 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
 // attention candidate and everything before it is decided in bulk (a warp
 // prefix sum assigns event slots and ids in plan order).
 constexpr int32_t CS_HIT = 16;
+constexpr int64_t COMP_MIN_CANDIDATES = 128;
 constexpr int32_t CS_DIFF = 32;  // decided by a re-score whose result differs from the speculation
 constexpr int32_t CS_BRK = 64;   // an earlier member of the candidate's component has CS_DIFF
 
@@ -2576,6 +2577,10 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     return false;
   }
   x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
+  // component speculation (phase A2): spec_comp 2 always, 1 for passes of
+  // at least COMP_MIN_CANDIDATES candidates (below that the extra phase costs
+  // more than the few re-scores it saves), 0 never
+  const bool comp_on = !coupled && (g.spec_comp == 2 || (g.spec_comp == 1 && nc >= COMP_MIN_CANDIDATES));
   // Candidate records live in shared memory when they fit (the sort scratch
   // is free until phase E): the in-order decisions read them back-to-back.
   int32_t* cand = g.k_val;
@@ -2585,7 +2590,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   {
     const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
     // (component speculation sorts in that scratch: records stay in HBM)
-    if (need <= x.tmp_bytes && !(g.spec_comp && !coupled)) {
+    if (need <= x.tmp_bytes && !comp_on) {
       chull = reinterpret_cast<int64_t*>(x.tmp);
       cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
       cand = cinfo + CI_STRIDE * nc;
@@ -2679,7 +2684,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
   conflicts_batch(x, g, w0, w1, cand, cinfo, chull, coupled, nullptr);
-  const bool use_comp = !coupled && g.spec_comp && wn > 1;
+  const bool use_comp = comp_on && wn > 1;
   if (use_comp) {
     x.sync();
     tick(6);

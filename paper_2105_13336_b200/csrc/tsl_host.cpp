@@ -505,7 +505,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->coupled = coupled ? 1 : 0;
     G->spec_window = 0;
     if (const char* e = std::getenv("TSL_SPEC_WINDOW")) G->spec_window = std::atoi(e);
-    // component speculation (swap_pass phase A2): 1 = on for passes of >= 128
+    // component speculation (swap_pass phase A2): 1 = on for passes of >= 512
     // candidates (C4's passes re-score ~40 % of their candidates without it)
     G->spec_comp = 1;
     if (const char* e = std::getenv("TSL_SPEC_COMP")) G->spec_comp = std::atoi(e);

@@ -853,19 +853,59 @@ __device__ void make_resident(GroupDev* gs, const JobDev* gj, JobDev* jd, uint8_
     gs->jobs = jd;
   }
   __syncthreads();
-  // uploaded inputs that moved: copy them in
-  for (int j = 0; j < nj; ++j) {
-    const JobDev& G = gj[j];
-    JobDev& J = jd[j];
-    auto cp = [&](auto* dst, const auto* src, int n) {
-      if (static_cast<const void*>(dst) == static_cast<const void*>(src)) return;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) const_cast<std::remove_const_t<std::remove_pointer_t<decltype(dst)>>*>(dst)[i] = src[i];
+  // uploaded inputs that moved: one thread issues TMA bulk copies
+  // (cp.async.bulk global -> shared, 16-byte granules; the host layout
+  // aligns every array to 16 bytes and the shared carve-outs are 16-byte
+  // rounded, so a copy may round its size up) completing on one mbarrier
+  // that every thread then waits on
+  __shared__ __align__(8) uint64_t mbar;
+  if (threadIdx.x == 0) {
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    uint32_t total = 0;
+    auto plan = [&](const void* dst, const void* src, size_t bytes) {
+      if (dst == src || bytes == 0) return;
+      total += uint32_t((bytes + 15) & ~size_t(15));
     };
-    cp(J.t_size, G.t_size, J.T);
-    cp(J.t_kind, G.t_kind, J.T);
-    cp(J.t_rank, G.t_rank, J.T);
-    cp(J.t_store, G.t_store, J.T);
-    cp(J.t_upd, G.t_upd, J.T);
+    auto issue = [&](const void* dst, const void* src, size_t bytes) {
+      if (dst == src || bytes == 0) return;
+      const uint32_t b = uint32_t((bytes + 15) & ~size_t(15));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+          "l"(src), "r"(b), "r"(bar)
+          : "memory");
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {  // the transaction count first, then the copies that complete it
+        if (total) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(total) : "memory");
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+      for (int j = 0; j < nj; ++j) {
+        const JobDev& G = gj[j];
+        const JobDev& J = jd[j];
+        const size_t T = size_t(J.T);
+        const void* d[5] = {J.t_size, J.t_kind, J.t_rank, J.t_store, J.t_upd};
+        const void* s[5] = {G.t_size, G.t_kind, G.t_rank, G.t_store, G.t_upd};
+        const size_t b[5] = {8 * T, T, 4 * T, 4 * T, 4 * T};
+        for (int k = 0; k < 5; ++k) {
+          if (pass == 0) plan(d[k], s[k], b[k]);
+          else issue(d[k], s[k], b[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
   }
   __syncthreads();
 }

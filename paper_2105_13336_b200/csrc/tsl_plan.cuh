@@ -1797,7 +1797,7 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
 // attention candidate and everything before it is decided in bulk (a warp
 // prefix sum assigns event slots and ids in plan order).
 constexpr int32_t CS_HIT = 16;
-constexpr int64_t COMP_MIN_CANDIDATES = 128;
+constexpr int64_t COMP_MIN_CANDIDATES = 512;
 constexpr int32_t CS_DIFF = 32;  // decided by a re-score whose result differs from the speculation
 constexpr int32_t CS_BRK = 64;   // an earlier member of the candidate's component has CS_DIFF
 

@@ -720,8 +720,12 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   tsl_ctx* c = P->ctx;
   GroupDev* dg = dp<GroupDev>(P->buf, P->groups_off);
   if (timed) cuda_check(cudaEventRecord(c->ev0, c->stream), "event");
-  for (int r = 0; r < repeats; ++r)  // the kernel resets its own group header
+  for (int r = 0; r < repeats; ++r) {  // the kernel resets its own group header
+    if (P->coop && r == 0)  // (and the control block, unless a launch aborted)
+      cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(P->buf->dbuf) + P->gp[0].coop, &P->coop_init,
+                                 sizeof P->coop_init, cudaMemcpyHostToDevice, c->stream), "H2D coop");
     cuda_check(launch_plan_kernel(dg, P->n_groups, P->mode, P->max_jobs, P->ipt, P->res_bytes, P->big, P->coop, c->stream), "launch");
+  }
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
@@ -744,7 +748,10 @@ std::string err_text(const GroupDev& G, const std::vector<GraphP>& gs) {
     case E_UNKNOWN_ACCESS:
       return "unknown access id " + std::to_string(e.tensor) + " in job " + (g ? g->job_id : std::string("?"));
     case E_CAPACITY: return "device planner capacity exceeded (" + std::to_string(e.tensor) + ")";
-    default: return "internal planner error";
+    default:
+      if (e.code == E_INTERNAL && e.tick >= 1000)
+        return "device spin timeout at site " + std::to_string(e.tick - 1000) + ": cooperative launch aborted";
+      return "internal planner error";
   }
 }
 

@@ -184,11 +184,24 @@ struct DevX {
   // ---- cooperative passes (all CTAs of the launch) ----
   // L1 is not coherent across SMs: everything another CTA wrote or will read
   // moves through L2 (ld/st .cg).
-  // Bounded spins: fail loudly, never hang the GPU. Barriers and folds are
-  // short (~35 s bound); an idle worker waits for CTA 0's next task through a
-  // whole decision sweep (~9 min bound).
-  __device__ static void spin_guard(int64_t t0, int shift = 36) {
-    if (clock64() - t0 > (int64_t(1) << shift)) __trap();
+  // Bounded spins: a wait past its bound (a planner bug, never a normal
+  // build) aborts the launch instead of trapping -- the group reports
+  // E_INTERNAL (tick = 1000 + site), the abort word tells every other waiting
+  // CTA, and each CTA leaves at its next barrier (leave_if_aborted), so the
+  // kernel ends, the CUDA context stays usable and the host returns an error.
+  // Barriers and folds are short (~35 s bound); an idle worker waits for CTA
+  // 0's next task through a whole decision sweep (~9 min bound).
+  __device__ bool spin_abort(int64_t t0, int site, int shift = 36) {
+    if (*reinterpret_cast<volatile int32_t*>(&coop->abort)) return true;
+    if (clock64() - t0 <= (int64_t(1) << shift)) return false;
+    if (coop_group && atomicCAS(&coop_group->err.code, 0, E_INTERNAL) == 0) coop_group->err.tick = 1000 + site;
+    atomicExch(&coop->abort, 1);
+    __threadfence();
+    return true;
+  }
+  // CTA-collective (after a barrier): every thread leaves when the launch aborted.
+  __device__ void leave_if_aborted() {
+    if (coop && *reinterpret_cast<volatile int32_t*>(&coop->abort)) asm volatile("exit;");
   }
   __device__ void grid_barrier() {
     __syncthreads();
@@ -202,11 +215,12 @@ struct DevX {
         atomicAdd(&coop->bar_gen, 1);
       } else {
         const int64_t t0 = clock64();
-        while (*gen == g0) { __nanosleep(64); spin_guard(t0); }
+        while (*gen == g0) { __nanosleep(64); if (spin_abort(t0, 1)) break; }
       }
       __threadfence();
     }
     __syncthreads();
+    leave_if_aborted();
   }
 
   // One stable LSD pass over all CTAs: per-tile digit counts, grid barrier,
@@ -313,11 +327,12 @@ struct DevX {
         atomicAdd(&coop->wbar_gen, 1);
       } else {
         const int64_t t0 = clock64();
-        while (*gen == g0) { __nanosleep(64); spin_guard(t0); }
+        while (*gen == g0) { __nanosleep(64); if (spin_abort(t0, 2)) break; }
       }
       __threadfence();
     }
     __syncthreads();
+    leave_if_aborted();
   }
 
   // Workers: fold the sorted lists a (busy) and b (pend) -- merge-path over
@@ -391,7 +406,7 @@ struct DevX {
       atomicAdd(&coop->epoch, 1);
       volatile int32_t* dn = &coop->fdone;
       const int64_t t0 = clock64();
-      while (*dn == 0) { __nanosleep(64); spin_guard(t0); }
+      while (*dn == 0) { __nanosleep(64); if (spin_abort(t0, 3)) break; }  // (CTA 0 leaves at its next grid barrier)
       __threadfence();
     }
     __syncwarp();
@@ -419,9 +434,10 @@ struct DevX {
       if (tid == 0) {
         volatile int32_t* ep = &coop->epoch;
         const int64_t t0 = clock64();
-        while (*ep == seen) { __nanosleep(256); spin_guard(t0, 40); }
+        while (*ep == seen) { __nanosleep(256); if (spin_abort(t0, 4, 40)) break; }
       }
       __syncthreads();
+      leave_if_aborted();
       volatile CoopCtl* c = coop;
       seen = c->epoch;
       __threadfence();
@@ -451,7 +467,7 @@ struct DevX {
     if (tid == 0) {
       volatile int32_t* ex = &coop->exited;
       const int64_t t0 = clock64();
-      while (*ex < grid - 1) { __nanosleep(128); spin_guard(t0); }
+      while (*ex < grid - 1) { __nanosleep(128); if (spin_abort(t0, 5)) break; }
       volatile CoopCtl* c = coop;
       c->epoch = 0; c->type = 0; c->bar_count = 0; c->bar_gen = 0; c->exited = 0;
       __threadfence();
@@ -756,10 +772,11 @@ __device__ inline void comp_dispatch<DevX>(DevX& x, GroupDev& g, int64_t w0, con
   if (x.tid == 0) {
     volatile int32_t* dn = &x.coop->cdone;
     const int64_t t0 = clock64();
-    while (*dn < x.grid - 1) { __nanosleep(64); DevX::spin_guard(t0); }
+    while (*dn < x.grid - 1) { __nanosleep(64); if (x.spin_abort(t0, 6)) break; }
     __threadfence();
   }
   __syncthreads();
+  x.leave_if_aborted();
 }
 
 // The end-of-pass busy rebuild on a cooperative launch: key building, the

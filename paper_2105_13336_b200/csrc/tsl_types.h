@@ -208,7 +208,8 @@ struct CoopCtl {
   // COOP_CONF: phase B of the window [cw0, cw1) on the grid
   int64_t cw1;
   const int32_t* ccomp;
-  int32_t ccoupled, cpad2;
+  int32_t ccoupled;
+  int32_t abort;                 // a spin timed out: every CTA leaves (the group reports E_INTERNAL)
 };
 enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_CONF = 6, COOP_EXIT = 9 };
 

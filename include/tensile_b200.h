@@ -255,6 +255,12 @@ typedef struct tsl_exec_config {
   int32_t vanilla;        /* 1: replay without the scheduler -- release at last
                              use (activity analysis), no swaps, no recomputation
                              (the reference's vanilla mode, the MSR/EOR/CBR base) */
+  int32_t mempool;        /* 1: every storage lives in memory of a private CUDA
+                             memory pool, allocated (cudaMallocAsync) when it
+                             becomes resident and freed (cudaFreeAsync) when it is
+                             released or swapped out, issued in the replay's planned
+                             order; the report carries the pool's high-water marks.
+                             Single-job replays (tsl_execute_plan) only. */
 } tsl_exec_config;
 
 typedef struct tsl_exec_report {
@@ -270,6 +276,9 @@ typedef struct tsl_exec_report {
   int32_t violations;          /* reads of absent inputs / bad releases       */
   int32_t kernels;             /* kernels launched by the replay              */
   double total_ms;             /* host wall time of the call                  */
+  int64_t pool_used_hwm;       /* mempool: cudaMemPoolAttrUsedMemHigh (bytes)  */
+  int64_t pool_reserved_hwm;   /* mempool: cudaMemPoolAttrReservedMemHigh      */
+  int64_t pool_allocs;         /* mempool: cudaMallocAsync calls               */
 } tsl_exec_report;
 
 void tsl_exec_config_default(tsl_exec_config* cfg);

@@ -89,7 +89,7 @@ class TslStats(C.Structure):
 
 class TslExecConfig(C.Structure):
     _fields_ = [("tick_ns", C.c_int64), ("iterations", C.c_int32), ("bytes_per_unit", C.c_int64),
-                ("vanilla", C.c_int32)]
+                ("vanilla", C.c_int32), ("mempool", C.c_int32)]
 
 
 class TslExecReport(C.Structure):
@@ -97,7 +97,8 @@ class TslExecReport(C.Structure):
                 ("iterations", C.c_int32), ("iteration_ms", C.c_double * 8), ("planned_iteration_ms", C.c_double),
                 ("swap_outs", C.c_int32), ("swap_ins", C.c_int32), ("bytes_d2h", C.c_int64), ("bytes_h2d", C.c_int64),
                 ("verify_errors", C.c_int32), ("violations", C.c_int32), ("kernels", C.c_int32),
-                ("total_ms", C.c_double)]
+                ("total_ms", C.c_double), ("pool_used_hwm", C.c_int64), ("pool_reserved_hwm", C.c_int64),
+                ("pool_allocs", C.c_int64)]
 
 
 def make_config(pcie_bandwidth: int = 1, transfer_setup: int = 0, memory_budget: int = 0,

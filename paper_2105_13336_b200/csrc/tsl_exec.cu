@@ -49,6 +49,12 @@ __device__ __forceinline__ void acct_sub(ExecDevice* d, int32_t s, int64_t size)
   }
 }
 
+// Where a storage's data lives: its fixed slot, or (mempool mode) the
+// allocation the host made for its current residency.
+__device__ __forceinline__ uint8_t* slot_of(ExecDevice* d, int32_t s) {
+  return d->addr ? d->addr[s] : d->pool + d->slot_off[s];
+}
+
 __device__ __forceinline__ uint64_t tag_of(int32_t s, int32_t version) {
   return 0x5453'4c00'0000'0000ull ^ (uint64_t(uint32_t(s)) << 20) ^ uint64_t(uint32_t(version));
 }
@@ -69,7 +75,7 @@ __global__ void exec_op(ExecDevice* d, const ExecOp* op, int base, int iter) {
   for (int k = 0; k < op->n_in; ++k) {
     const int32_t s = op->ins[k];
     if (!d->resident[s]) { atomicAdd(&d->violations, 1); continue; }
-    const uint64_t* slot = reinterpret_cast<const uint64_t*>(d->pool + d->slot_off[s]);
+    const uint64_t* slot = reinterpret_cast<const uint64_t*>(slot_of(d, s));
     if (*slot != tag_of(s, d->version[s])) atomicAdd(&d->verify_errors, 1);
   }
   for (int k = 0; k < op->n_out; ++k)
@@ -82,7 +88,7 @@ __global__ void exec_op(ExecDevice* d, const ExecOp* op, int base, int iter) {
   for (int k = 0; k < op->n_out; ++k) {
     const int32_t s = op->outs[k];
     d->version[s] += 1;
-    *reinterpret_cast<uint64_t*>(d->pool + d->slot_off[s]) = tag_of(s, d->version[s]);
+    *reinterpret_cast<uint64_t*>(slot_of(d, s)) = tag_of(s, d->version[s]);
   }
   // a pending swap-out of the storage owns its eviction (simulator.cpp:461-470)
   for (int k = 0; k < op->n_rel; ++k)
@@ -113,7 +119,7 @@ __global__ void exec_xfer_done(ExecDevice* d, int32_t s, int64_t size, int64_t d
   if (dir == 0) {
     atomicSub(&d->out_pending[s], 1);
     if (d->resident[s]) acct_sub(d, s, size);
-    *reinterpret_cast<uint64_t*>(d->pool + d->slot_off[s]) = 0xdeaddeaddeaddeadull;
+    *reinterpret_cast<uint64_t*>(slot_of(d, s)) = 0xdeaddeaddeaddeadull;
     d->n_out += 1;
   } else {
     acct_add(d, s, size);
@@ -133,7 +139,7 @@ __global__ void exec_init(ExecDevice* d, const int32_t* st, const int64_t* sz, i
   if (threadIdx.x != 0) return;
   for (int k = 0; k < n; ++k) {
     acct_add(d, st[k], sz[k]);
-    *reinterpret_cast<uint64_t*>(d->pool + d->slot_off[st[k]]) = tag_of(st[k], d->version[st[k]]);
+    *reinterpret_cast<uint64_t*>(slot_of(d, st[k])) = tag_of(st[k], d->version[st[k]]);
   }
 }
 

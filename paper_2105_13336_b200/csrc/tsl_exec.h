@@ -17,6 +17,7 @@ struct ExecDevice {
   uint64_t tick_ns;
   uint8_t* pool;          // device pool: one slot per storage
   const int64_t* slot_off;
+  uint8_t** addr;         // mempool mode: each storage's current allocation (else null)
   int32_t* resident;      // [T] allocator residency flags
   int32_t* version;       // [T] data version (tag) of each storage
   int32_t* out_pending;   // [T] swap-outs of the storage not yet complete this iteration

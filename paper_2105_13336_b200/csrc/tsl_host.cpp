@@ -1444,6 +1444,10 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
   if (ex.iterations < 1 || ex.iterations > 8) fail(TSL_ERR_ARGUMENT, "iterations must be in 1..8");
   if (ex.tick_ns <= 0 || ex.bytes_per_unit <= 0) fail(TSL_ERR_ARGUMENT, "tick_ns and bytes_per_unit must be positive");
   if (jis.empty()) fail(TSL_ERR_ARGUMENT, "no job to replay");
+  // the host issues the pool's frees at the plan's instants; with several
+  // jobs contending for the channel the device's release ownership can drift
+  // from them, so the pool-backed replay is a single-job replay
+  if (ex.mempool && jis.size() != 1) fail(TSL_ERR_ARGUMENT, "mempool mode replays one job (tsl_execute_plan)");
   std::vector<JobProgram> progs;
   for (int32_t ji : jis) {
     if (ji < 0 || ji >= static_cast<int32_t>(r->jobs.size())) fail(TSL_ERR_ARGUMENT, "bad job index");
@@ -1453,9 +1457,10 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
   const int iters = ex.iterations;
   // device layout: the shared counters, then every job's block
   struct DevOff {
-    size_t dev, ops, i32, i64, slot, res, ver, pend, opi, init, initsz, end, iter, pool;
+    size_t dev, ops, i32, i64, slot, res, ver, pend, opi, init, initsz, end, iter, pool, addr;
     size_t host;
   };
+  const bool mp = ex.mempool != 0;
   Layout L;
   const size_t o_acct = L.take<ExecAcct>(1);
   std::vector<DevOff> dof(nj);
@@ -1477,11 +1482,13 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
     f.initsz = L.take<int64_t>(P.init_sz.size() + 1);
     f.end = L.take<uint64_t>(size_t(iters) * P.steps.size() + 1);
     f.iter = L.take<uint64_t>(iters + 1);
+    f.addr = L.take<uint8_t*>(T + 1);  // mempool mode: each storage's current allocation
     f.host = static_cast<size_t>(host_total);
     host_total += P.host_bytes;
   }
   const size_t meta_end = L.off;  // staged by the host
-  for (int j = 0; j < nj; ++j) dof[j].pool = L.take<uint8_t>(progs[j].pool_bytes + 256);
+  // fixed slots (mempool mode: the pool holds the data, the slots are unused)
+  for (int j = 0; j < nj; ++j) dof[j].pool = L.take<uint8_t>(mp ? 256 : progs[j].pool_bytes + 256);
   const size_t total = L.off;
   uint8_t* dbuf = nullptr;
   uint8_t* hpin = nullptr;
@@ -1489,12 +1496,29 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
   std::vector<cudaEvent_t> events;
   std::vector<cudaStream_t> cs(nj, nullptr);
   cudaStream_t xs_stream = nullptr;
+  // mempool mode: a private pool, every storage's live allocation on the host
+  // side, and pinned cells holding the pointer values the device table is fed
+  // from in stream order (one cell per allocation event)
+  cudaMemPool_t mpool = nullptr;
+  std::vector<std::vector<void*>> live(nj);
+  int64_t* hptr = nullptr;
+  size_t nptr = 0, ptr_cap = 0;
+  int64_t n_alloc = 0;
   auto cleanup = [&]() {
+    if (mpool) {
+      for (auto c : cs) if (c) cudaStreamSynchronize(c);
+      if (xs_stream) cudaStreamSynchronize(xs_stream);
+      for (auto& v : live)
+        for (void* p : v) if (p) cudaFree(p);
+      cudaMemPoolDestroy(mpool);
+      mpool = nullptr;
+    }
     for (auto e : events) cudaEventDestroy(e);
     for (auto c : cs) if (c) cudaStreamDestroy(c);
     if (xs_stream) cudaStreamDestroy(xs_stream);
     if (dbuf) cudaFree(dbuf);
     if (hpin) cudaFreeHost(hpin);
+    if (hptr) cudaFreeHost(hptr);
   };
   per.assign(nj, tsl_exec_report{});
   merged = tsl_exec_report{};
@@ -1505,6 +1529,24 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
     for (auto& c : cs) cuda_check(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&xs_stream, cudaStreamNonBlocking), "stream");
     auto D = [&](size_t off) { return dbuf + off; };
+    if (mp) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = ctx->device;
+      cuda_check(cudaMemPoolCreate(&mpool, &props), "cudaMemPoolCreate");
+      uint64_t keep = ~uint64_t(0), zero = 0;
+      cuda_check(cudaMemPoolSetAttribute(mpool, cudaMemPoolAttrReleaseThreshold, &keep), "pool attr");
+      cuda_check(cudaMemPoolSetAttribute(mpool, cudaMemPoolAttrUsedMemHigh, &zero), "pool attr");
+      cuda_check(cudaMemPoolSetAttribute(mpool, cudaMemPoolAttrReservedMemHigh, &zero), "pool attr");
+      for (int j = 0; j < nj; ++j) {
+        live[j].assign(progs[j].g->T, nullptr);
+        ptr_cap += progs[j].init_st.size() + size_t(iters) * (progs[j].steps.size() * 4 + progs[j].xs.size() + 1);
+        for (const auto& st : progs[j].steps) ptr_cap += size_t(iters) * st.outs.size();
+      }
+      cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hptr), (ptr_cap + 1) * sizeof(int64_t)), "cudaMallocHost");
+    }
     std::vector<ExecDevice*> dptr(nj);
     for (int j = 0; j < nj; ++j) {
       const JobProgram& P = progs[j];
@@ -1519,6 +1561,7 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
       dev.out_pending = reinterpret_cast<int32_t*>(D(f.pend));
       dev.op_end_ns = reinterpret_cast<uint64_t*>(D(f.end));
       dev.iter_start_ns = reinterpret_cast<uint64_t*>(D(f.iter));
+      dev.addr = mp ? reinterpret_cast<uint8_t**>(D(f.addr)) : nullptr;
       std::memcpy(stage.data() + f.dev, &dev, sizeof dev);
       for (size_t k = 0; k < P.steps.size(); ++k) {
         ExecOp op{};
@@ -1543,6 +1586,22 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
       if (!P.init_sz.empty()) std::memcpy(stage.data() + f.initsz, P.init_sz.data(), P.init_sz.size() * 8);
       dptr[j] = reinterpret_cast<ExecDevice*>(D(f.dev));
     }
+    // mempool mode: the initially resident storages' allocations (stream
+    // ordered before each job's init kernel), their pointers staged into the
+    // device address tables
+    auto mp_alloc = [&](int j, int32_t s, int64_t units, cudaStream_t st) -> void* {
+      void* p = nullptr;
+      cuda_check(cudaMallocFromPoolAsync(&p, size_t(units * ex.bytes_per_unit), mpool, st), "cudaMallocFromPoolAsync");
+      live[j][s] = p;
+      ++n_alloc;
+      return p;
+    };
+    if (mp)
+      for (int j = 0; j < nj; ++j)
+        for (size_t k = 0; k < progs[j].init_st.size(); ++k) {
+          void* p = mp_alloc(j, progs[j].init_st[k], progs[j].init_sz[k], cs[j]);
+          std::memcpy(stage.data() + dof[j].addr + sizeof(void*) * size_t(progs[j].init_st[k]), &p, sizeof p);
+        }
     cuda_check(cudaMemcpy(dbuf, stage.data(), meta_end, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemset(D(dof[0].pool), 0, total - dof[0].pool), "memset");
     auto ev = [&]() {
@@ -1605,6 +1664,63 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
         acts[j].push_back({A_END, it, -1, base + P.period});
       }
     }
+    // mempool mode: every transfer's planned completion on the shared FIFO
+    // channel (enqueue order = the merged action order below), so the host
+    // frees a released storage exactly when the device's release does -- not
+    // while a swap-out of it is still pending (simulator.cpp:461-470)
+    std::vector<std::vector<std::vector<int64_t>>> done_at(nj);
+    if (mp) {
+      std::vector<std::tuple<int64_t, int, int, int>> q;  // (time, job, iteration, transfer)
+      for (int j = 0; j < nj; ++j) {
+        done_at[j].assign(iters, std::vector<int64_t>(progs[j].xs.size(), 0));
+        for (const Act& a : acts[j])
+          if (a.kind == A_XFER) q.emplace_back(a.time, j, a.it, a.idx);
+      }
+      std::stable_sort(q.begin(), q.end(), [](const auto& a, const auto& b) {
+        return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
+      });
+      int64_t chan = 0;
+      for (const auto& [t, j, it, xi] : q) {
+        chan = std::max(chan, t) + progs[j].xs[size_t(xi)].dur;
+        done_at[j][it][size_t(xi)] = chan;
+      }
+      // The pool accounts allocations and frees in the order the host issues
+      // them, so they are issued in the replay's planned time order: a
+      // transfer's action moves to its planned channel start (where a swap-in
+      // allocates), frees wait in a queue until the timeline reaches their
+      // instant (op end / swap-out completion), frees before allocations at
+      // equal ticks (simulator.cpp:47-52).
+      for (int j = 0; j < nj; ++j) {
+        for (Act& a : acts[j])
+          if (a.kind == A_XFER) a.time = done_at[j][a.it][size_t(a.idx)] - progs[j].xs[size_t(a.idx)].dur;
+        std::stable_sort(acts[j].begin(), acts[j].end(), [](const Act& x, const Act& y) {
+          const int px = x.kind == A_END ? 1 : 0, py = y.kind == A_END ? 1 : 0;
+          return x.time != y.time ? x.time < y.time : px < py;
+        });
+      }
+    }
+    struct PendingFree { int64_t time; uint64_t seq; int j; int32_t s; cudaStream_t st; };
+    auto later = [](const PendingFree& a, const PendingFree& b) {
+      return a.time != b.time ? a.time > b.time : a.seq > b.seq;
+    };
+    std::priority_queue<PendingFree, std::vector<PendingFree>, decltype(later)> frees(later);
+    uint64_t free_seq = 0;
+    auto flush_frees = [&](int64_t upto) {
+      while (!frees.empty() && frees.top().time <= upto) {
+        const PendingFree f = frees.top();
+        frees.pop();
+        if (!live[f.j][f.s]) continue;
+        cuda_check(cudaFreeAsync(live[f.j][f.s], f.st), "cudaFreeAsync");
+        live[f.j][f.s] = nullptr;
+      }
+    };
+    auto set_addr = [&](int j, int32_t s, void* p, cudaStream_t st) {
+      if (nptr >= ptr_cap) fail(TSL_ERR_INTERNAL, "mempool pointer cells exhausted");
+      hptr[nptr] = reinterpret_cast<int64_t>(p);
+      cuda_check(cudaMemcpyAsync(D(dof[j].addr) + sizeof(void*) * size_t(s), &hptr[nptr], sizeof(void*),
+                                 cudaMemcpyHostToDevice, st), "H2D addr");
+      ++nptr;
+    };
     // merge the jobs' lists by planned time (ties: job order); enqueue
     std::vector<size_t> head(nj, 0);
     std::vector<std::vector<char>> enq(nj);
@@ -1615,6 +1731,7 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
         if (head[j] < acts[j].size() && (bj < 0 || acts[j][head[j]].time < acts[bj][head[bj]].time)) bj = j;
       if (bj < 0) break;
       const Act a = acts[bj][head[bj]++];
+      if (mp) flush_frees(a.time);
       const JobProgram& P = progs[bj];
       JobRun& R = run[bj];
       ExecDevice* d = dptr[bj];
@@ -1634,8 +1751,13 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
         const size_t nbytes = static_cast<size_t>(t.size * ex.bytes_per_unit);
         uint8_t* dev_slot = D(dof[bj].pool) + P.slot_off[t.storage];
         uint8_t* host_slot = hpin + dof[bj].host + P.host_off[t.storage];
+        if (mp && t.dir == 1 && !live[bj][t.storage]) {  // a swap-in allocates before its copy
+          void* p = mp_alloc(bj, t.storage, t.size, xs_stream);
+          set_addr(bj, t.storage, p, xs_stream);
+        }
+        if (mp) dev_slot = static_cast<uint8_t*>(live[bj][t.storage]);
         if (t.dir == 0) {
-          cuda_check(cudaMemcpyAsync(host_slot, dev_slot, nbytes, cudaMemcpyDeviceToHost, xs_stream), "D2H");
+          if (dev_slot) cuda_check(cudaMemcpyAsync(host_slot, dev_slot, nbytes, cudaMemcpyDeviceToHost, xs_stream), "D2H");
           per[bj].bytes_d2h += static_cast<int64_t>(nbytes);
         } else {
           cuda_check(cudaMemcpyAsync(dev_slot, host_slot, nbytes, cudaMemcpyHostToDevice, xs_stream), "H2D");
@@ -1643,14 +1765,32 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
         }
         cuda_check(exec_launch_done(d, t.storage, t.size, t.dur, t.dir, xs_stream), "done");
         kernels += 2;
+        if (mp && t.dir == 0)  // a completed swap-out frees (queued to its completion instant)
+          frees.push({done_at[bj][a.it][size_t(a.idx)], free_seq++, bj, t.storage, xs_stream});
         if (t.dir == 1) cuda_check(cudaEventRecord(R.in_done[static_cast<size_t>(a.idx)], xs_stream), "event");
         enq[bj][static_cast<size_t>(a.idx)] = 1;
       } else if (a.kind == A_OP) {
         for (size_t q = 0; q < P.xs.size(); ++q)  // swap-ins serving this step, already on the channel
           if (P.xs[q].serve_step == a.idx && enq[bj][q]) cuda_check(cudaStreamWaitEvent(cs[bj], R.in_done[q], 0), "wait");
+        const ExecStepH& stp = P.steps[static_cast<size_t>(a.idx)];
+        if (mp)  // outputs allocate at the op's start
+          for (size_t k = 0; k < stp.outs.size(); ++k)
+            if (stp.out_size[k] > 0 && !live[bj][stp.outs[k]]) {
+              void* p = mp_alloc(bj, stp.outs[k], stp.out_size[k], cs[bj]);
+              set_addr(bj, stp.outs[k], p, cs[bj]);
+            }
         cuda_check(exec_launch_op(d, reinterpret_cast<const ExecOp*>(D(dof[bj].ops)) + a.idx, base, a.it, cs[bj]), "op");
         ++kernels;
         cuda_check(cudaEventRecord(R.op_end[static_cast<size_t>(a.idx)], cs[bj]), "event");
+        if (mp) {  // releases at its end, unless a swap-out of the storage is still pending
+          const int64_t end_t = int64_t(a.it) * P.period + stp.end;
+          for (int32_t s : stp.rel) {
+            bool owned = false;
+            for (size_t q = 0; q < P.xs.size() && !owned; ++q)
+              owned = P.xs[q].dir == 0 && P.xs[q].storage == s && done_at[bj][a.it][q] > end_t;
+            if (!owned) frees.push({end_t, free_seq++, bj, s, cs[bj]});
+          }
+        }
       } else {
         // the iteration ends when its transfers are done (simulator.cpp:478-484)
         cuda_check(cudaEventRecord(R.xfer_tail, xs_stream), "event");
@@ -1659,6 +1799,7 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
           cuda_check(cudaStreamWaitEvent(xs_stream, R.op_end[static_cast<size_t>(nsteps - 1)], 0), "wait");
       }
     }
+    if (mp) flush_frees(std::numeric_limits<int64_t>::max());
     for (int j = 0; j < nj; ++j) {
       cuda_check(exec_launch_iter_begin(dptr[j], reinterpret_cast<const int32_t*>(D(dof[j].opi)), 0, iters, cs[j]),
                  "iter");
@@ -1666,6 +1807,14 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
     }
     for (auto c : cs) cuda_check(cudaStreamSynchronize(c), "sync");
     cuda_check(cudaStreamSynchronize(xs_stream), "sync");
+    int64_t pool_used = 0, pool_reserved = 0;
+    if (mp) {
+      uint64_t v = 0;
+      cuda_check(cudaMemPoolGetAttribute(mpool, cudaMemPoolAttrUsedMemHigh, &v), "pool attr");
+      pool_used = int64_t(v);
+      cuda_check(cudaMemPoolGetAttribute(mpool, cudaMemPoolAttrReservedMemHigh, &v), "pool attr");
+      pool_reserved = int64_t(v);
+    }
     ExecAcct acct{};
     cuda_check(cudaMemcpy(&acct, D(o_acct), sizeof acct, cudaMemcpyDeviceToHost), "D2H");
     for (int j = 0; j < nj; ++j) {
@@ -1701,7 +1850,15 @@ void execute_jobs(tsl_ctx* ctx, const tsl_result* r, const std::vector<int32_t>&
     merged.final_footprint = acct.footprint;
     merged.iterations = iters;
     merged.kernels = kernels;
-    for (auto& rep : per) rep.kernels = kernels;
+    merged.pool_used_hwm = pool_used;
+    merged.pool_reserved_hwm = pool_reserved;
+    merged.pool_allocs = n_alloc;
+    for (auto& rep : per) {
+      rep.kernels = kernels;
+      rep.pool_used_hwm = pool_used;
+      rep.pool_reserved_hwm = pool_reserved;
+      rep.pool_allocs = n_alloc;
+    }
   } catch (...) {
     cleanup();
     throw;
@@ -1729,6 +1886,7 @@ void tsl_exec_config_default(tsl_exec_config* c) {
   c->iterations = 3;
   c->bytes_per_unit = 16;
   c->vanilla = 0;
+  c->mempool = 0;
 }
 
 int tsl_execute_plan(tsl_ctx* ctx, const tsl_result* r, int32_t job, const tsl_config* cfg,

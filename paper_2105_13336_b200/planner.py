@@ -255,7 +255,7 @@ class Planner:
         return PreparedPlan(self, h, descs, len(groups))
 
     def build_and_execute(self, jobs: Sequence, config: dict, tick_ns: int = 1000, iterations: int = 3,
-                          bytes_per_unit: int = 16) -> dict:
+                          bytes_per_unit: int = 16, mempool: bool = False) -> dict:
         """build_plan, then replay every job's plan on the device (plan
         executor): {"plan": build_plan dict, "exec": {job_id: report dict}}."""
         descs, arr = abi.pack_jobs(jobs)
@@ -266,7 +266,7 @@ class Planner:
             _raise(self.lib, rc)
         try:
             out = {"plan": _collect(self.lib, res, descs), "exec": {}}
-            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 0)
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 0, 1 if mempool else 0)
             for i in range(self.lib.tsl_result_n_jobs(res)):
                 rep = abi.TslExecReport()
                 rc = self.lib.tsl_execute_plan(self._ctx, res, i, C.byref(cfg), C.byref(ex), C.byref(rep))
@@ -282,7 +282,7 @@ class Planner:
         return out
 
     def build_and_execute_all(self, jobs: Sequence, config: dict, tick_ns: int = 1000, iterations: int = 3,
-                              bytes_per_unit: int = 16, vanilla: bool = False) -> dict:
+                              bytes_per_unit: int = 16, vanilla: bool = False, mempool: bool = False) -> dict:
         """build_plan, then replay ALL jobs' plans together on the device (one
         compute stream per job, one FIFO copy stream, one allocator):
         {"plan": build_plan dict, "exec": {job_id: report}, "merged": report}."""
@@ -300,7 +300,7 @@ class Planner:
 
         try:
             out = {"plan": _collect(self.lib, res, descs), "exec": {}}
-            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 1 if vanilla else 0)
+            ex = abi.TslExecConfig(tick_ns, iterations, bytes_per_unit, 1 if vanilla else 0, 1 if mempool else 0)
             n = self.lib.tsl_result_n_jobs(res)
             per = (abi.TslExecReport * max(1, n))()
             merged = abi.TslExecReport()

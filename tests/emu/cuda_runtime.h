@@ -45,6 +45,26 @@ inline cudaError_t cudaMalloc(void** p, size_t n) {
 inline cudaError_t cudaFree(void* p) { std::free(p); return cudaSuccess; }
 inline cudaError_t cudaMallocHost(void** p, size_t n) { return cudaMalloc(p, n); }
 inline cudaError_t cudaFreeHost(void* p) { std::free(p); return cudaSuccess; }
+
+// stream-ordered pool allocator (the plan executor's mempool mode)
+typedef void* cudaMemPool_t;
+enum cudaMemAllocationType { cudaMemAllocationTypePinned = 1 };
+enum cudaMemAllocationHandleType { cudaMemHandleTypeNone = 0 };
+enum cudaMemLocationType { cudaMemLocationTypeDevice = 1 };
+enum cudaMemPoolAttr { cudaMemPoolAttrReleaseThreshold = 4, cudaMemPoolAttrReservedMemHigh = 6,
+                       cudaMemPoolAttrUsedMemHigh = 8 };
+struct cudaMemLocation { cudaMemLocationType type; int id; };
+struct cudaMemPoolProps { cudaMemAllocationType allocType; cudaMemAllocationHandleType handleTypes;
+                          cudaMemLocation location; };
+inline cudaError_t cudaMemPoolCreate(cudaMemPool_t* p, const cudaMemPoolProps*) { *p = nullptr; return cudaSuccess; }
+inline cudaError_t cudaMemPoolDestroy(cudaMemPool_t) { return cudaSuccess; }
+inline cudaError_t cudaMemPoolSetAttribute(cudaMemPool_t, cudaMemPoolAttr, void*) { return cudaSuccess; }
+inline cudaError_t cudaMemPoolGetAttribute(cudaMemPool_t, cudaMemPoolAttr, void* v) {
+  *static_cast<unsigned long long*>(v) = 0;
+  return cudaSuccess;
+}
+inline cudaError_t cudaMallocFromPoolAsync(void** p, size_t n, cudaMemPool_t, cudaStream_t) { return cudaMalloc(p, n); }
+inline cudaError_t cudaFreeAsync(void* p, cudaStream_t) { return cudaFree(p); }
 inline cudaError_t cudaMemcpyAsync(void* d, const void* s, size_t n, cudaMemcpyKind, cudaStream_t) {
   if (n) std::memmove(d, s, n);
   return cudaSuccess;

@@ -94,3 +94,41 @@ def test_vanilla_replay_and_metrics(planner, name):
     assert m["msr"] > 0.2  # the budget is 70 % of the initial peak
     if name == "C2":  # one job: the swaps hide behind compute, iterations keep their planned length
         assert abs(m["eor"]) < 0.02
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_mempool_replay_high_water_mark(planner, name):
+    """mempool mode: every storage is a real cudaMallocAsync allocation of a
+    private pool (64 KiB per planner byte unit here, so swaps move MBs), freed
+    by cudaFreeAsync at its release / swap-out completion, allocations and
+    frees issued in the plan's time order. The planner (peak.cpp:146-153)
+    counts a swap-in at its completion while a real allocator must hold the
+    buffer from the copy's start, so the pool's used-memory high-water mark is
+    the predicted peak plus at most the transfers in flight; every tensor
+    survives its trips through host memory."""
+    import json
+    from paper_2105_13336_b200 import configs as CF
+    req = CF.requests(name)[-1]
+    bpu = 64 * 1024
+    out = planner.build_and_execute(req.jobs, req.config(CF.INITIAL_PEAK), tick_ns=4000, iterations=2,
+                                    bytes_per_unit=bpu, mempool=True)
+    plans = json.loads(out["plan"]["plans_json"])
+    sizes = {g["job_id"]: {t["id"]: t["size"] for t in g["tensors"]} for g, _ in req.jobs}
+    for jid, r in out["exec"].items():
+        assert r["verify_errors"] == 0 and r["violations"] == 0, jid
+        assert r["hwm"] == r["predicted_peak"]
+        inflight = max([sizes[jid][e["tensor"]] for e in plans[jid]["swap_events"] if e["direction"] == "in"] or [0])
+        assert r["predicted_peak"] * bpu <= r["pool_used_hwm"] <= (r["predicted_peak"] + inflight) * bpu, \
+            (jid, r["pool_used_hwm"] // bpu, r["predicted_peak"], inflight)
+        assert r["pool_reserved_hwm"] >= r["pool_used_hwm"]
+        assert r["pool_allocs"] > r["swap_ins"] > 0
+        assert r["bytes_d2h"] >= r["swap_outs"] * bpu
+
+
+def test_mempool_needs_a_single_job(planner):
+    from paper_2105_13336_b200 import configs as CF
+    from paper_2105_13336_b200.planner import PlannerError
+    req = CF.requests("C3")[-1]
+    with pytest.raises(PlannerError, match="mempool mode replays one job"):
+        planner.build_and_execute_all(req.jobs, req.config(CF.INITIAL_PEAK), tick_ns=4000, iterations=1,
+                                      bytes_per_unit=1024, mempool=True)

@@ -88,7 +88,7 @@ struct JobPlace {  // byte offsets into the device buffer
   size_t topo, o_lat, o_in_off, o_in, o_out_off, o_out, t_size, t_kind, t_rank, t_store, t_upd, t_prod, inflag;
   size_t a_tensor, a_store, a_type, a_start, a_end, a_base, a_flag, a_owned, s_off, s_acc, t_wfirst, t_utga;
   size_t ev[12], bz_s, bz_e, pd_s, pd_e, pd_ts, pd_te, bzi_s, bzi_e, ai_e, st_evcnt, swapped, rc[6], in_peak, ev_drop, res_init, curve_t, curve_b;
-  size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve;
+  size_t bk_a_start, bk_a_end, bk_flag, bk_in_peak, bk_ev, bk_rc, bk_bz, bk_evcnt, bk_curve, pk_list;
   int32_t Scap, Rcap, Ecap, ti_nb;
 };
 
@@ -101,6 +101,10 @@ struct GroupPlace {
   int32_t cb_nb = 1024;
   size_t k_key, k_val, x_time, x_fp, x_store, x_aid, x_type, x_job, x_state, x_seq2, x_key2, x_order;
   int32_t hist_cap;
+  // incremental timeline order (one-job big builds)
+  bool ec = false;
+  int64_t ec_dcap = 0;
+  size_t ec_bt, ec_bl, ec_bs, ec_gt, ec_gl, ec_gb, ec_ginv, ec_posb, ec_sc, ec_dord, ec_dins, ec_dgrp, ec_gins, ec_nw, ec_posd, ec_dl;
 };
 
 }  // namespace
@@ -424,6 +428,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       p.bk_a_end = L.take<int64_t>(g.A);
       p.bk_flag = L.take<uint8_t>(g.A);
       p.bk_in_peak = L.take<uint8_t>(g.T);
+      p.pk_list = L.take<int32_t>(g.T);
       p.bk_ev = L.take<int64_t>(size_t(12) * p.Scap);
       p.bk_rc = L.take<int64_t>(size_t(6) * p.Rcap);
       p.bk_bz = L.take<int64_t>(size_t(2) * p.Scap);
@@ -481,6 +486,30 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     q.cb_idx = L.take<int32_t>(4 * size_t(q.cb_nb + 2));
     q.cb_cap = std::max<int64_t>(8 * P->sort_cap, 4 * q.pr_cap);
     q.cb_ent = L.take<int32_t>(2 * size_t(q.cb_cap));
+    // incremental evaluation (tsl_plan.cuh inc_order): one big job per build
+    const char* ie = std::getenv("TSL_EVAL_INC");
+    q.ec = mode == 0 && P->big && P->graphs[gi].size() == 1 && !(ie && ie[0] == '0');
+    if (q.ec) {
+      const size_t NB = 2 * size_t(sumA);
+      q.ec_dcap = P->jp[gi][0].Scap + P->jp[gi][0].Rcap;
+      const size_t D = size_t(q.ec_dcap);
+      q.ec_bt = L.take<int64_t>(NB);
+      q.ec_bl = L.take<uint32_t>(NB);
+      q.ec_bs = L.take<int32_t>(NB);
+      q.ec_gt = L.take<int64_t>(NB);
+      q.ec_gl = L.take<uint32_t>(NB);
+      q.ec_gb = L.take<int32_t>(NB);
+      q.ec_ginv = L.take<int32_t>(NB);
+      q.ec_posb = L.take<int32_t>(NB);
+      q.ec_sc = L.take<int64_t>(2 * (NB + 1));
+      q.ec_dord = L.take<int32_t>(2 * D);
+      q.ec_dins = L.take<int32_t>(2 * D);
+      q.ec_dgrp = L.take<int32_t>(2 * D);
+      q.ec_gins = L.take<int32_t>(2 * D);
+      q.ec_nw = L.take<int32_t>(4 * D);
+      q.ec_posd = L.take<int32_t>(D);
+      q.ec_dl = L.take<uint32_t>(D);
+    }
   }
   const size_t total = L.off;
   const auto t_lay = std::chrono::steady_clock::now();
@@ -561,6 +590,26 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
     G->cb_ent = dp<int32_t>(ctx, q.cb_ent);
     G->cb_cap = q.cb_cap;
     G->w_cap = q.w_cap;
+    G->ec_S0 = -1;
+    if (q.ec) {
+      G->ec_dcap = q.ec_dcap;
+      G->ec_bt = dp<int64_t>(ctx, q.ec_bt);
+      G->ec_bl = dp<uint32_t>(ctx, q.ec_bl);
+      G->ec_bs = dp<int32_t>(ctx, q.ec_bs);
+      G->ec_gt = dp<int64_t>(ctx, q.ec_gt);
+      G->ec_gl = dp<uint32_t>(ctx, q.ec_gl);
+      G->ec_gb = dp<int32_t>(ctx, q.ec_gb);
+      G->ec_ginv = dp<int32_t>(ctx, q.ec_ginv);
+      G->ec_posb = dp<int32_t>(ctx, q.ec_posb);
+      G->ec_sc = dp<int64_t>(ctx, q.ec_sc);
+      G->ec_dord = dp<int32_t>(ctx, q.ec_dord);
+      G->ec_dins = dp<int32_t>(ctx, q.ec_dins);
+      G->ec_dgrp = dp<int32_t>(ctx, q.ec_dgrp);
+      G->ec_gins = dp<int32_t>(ctx, q.ec_gins);
+      G->ec_nw = dp<int32_t>(ctx, q.ec_nw);
+      G->ec_posd = dp<int32_t>(ctx, q.ec_posd);
+      G->ec_dl = dp<uint32_t>(ctx, q.ec_dl);
+    }
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
       const Graph& g = *gs[k];
       const JobPlace& p = P->jp[gi][k];
@@ -645,6 +694,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       J->bk_a_end = dp<int64_t>(ctx, p.bk_a_end);
       J->bk_flag = dp<uint8_t>(ctx, p.bk_flag);
       J->bk_in_peak = dp<uint8_t>(ctx, p.bk_in_peak);
+      J->pk_list = dp<int32_t>(ctx, p.pk_list);
       J->bk_ev = dp<int64_t>(ctx, p.bk_ev);
       J->bk_rc = dp<int64_t>(ctx, p.bk_rc);
       J->bk_bz = dp<int64_t>(ctx, p.bk_bz);
@@ -851,6 +901,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
   for (int k = 0; k < 16; ++k) s.queryprof[k] = G.stats.prof[k];
   s.comp_rescored = G.stats.comp_rescored;
+  for (int k = 0; k < 16; ++k) s.stageprof[k] = G.stats.sprof[k];
   return R;
 }
 

@@ -41,6 +41,11 @@ constexpr size_t tmp_bytes_for(int ipt) {
                           : sizeof(typename BRS<SORT_IPT>::TempStorage));
 }
 
+// the grid scan's tile (GridX::scan_op) shares the big-mode sort scratch
+static_assert(tmp_bytes_for(SORT_IPT) >= ((sizeof(typename BScan::TempStorage) + 15) & ~size_t(15)) +
+                                            size_t(NT) * 8 * 17 / 16 * sizeof(int64_t),
+              "scan tile does not fit the sort scratch");
+
 struct DevX {
   static constexpr int W = 32;
   int tid, nthr, lane, warp, nwarp;
@@ -586,29 +591,66 @@ struct GridX {
   __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
   __device__ int32_t aadd32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
   __device__ int32_t wexcl(int32_t v, int32_t* total) { return dx->wexcl(v, total); }
-  // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs
+  // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs: each CTA owns
+  // a contiguous segment; its total is reduced with coalesced loads, one warp
+  // combines the earlier CTAs' totals, and the segment is scanned in tiles
+  // staged through shared memory (coalesced loads and stores, each thread
+  // scanning K consecutive elements).
   __device__ void scan_op(int64_t* a, int n, int op) {
     sync();
-    const int chunk = (n + nthr - 1) / nthr;
-    const int b = min(n, tid * chunk), e = min(n, b + chunk);
-    int64_t s = op ? INT64_MIN : 0;
-    for (int i = b; i < e; ++i) s = op ? max(s, a[i]) : s + a[i];
-    int64_t off;
+    const int t = threadIdx.x;
+    const int64_t idn = op ? INT64_MIN : 0;
+    auto comb = [op](int64_t u, int64_t v) { return op ? (u > v ? u : v) : u + v; };
+    const int seg = (n + dx->grid - 1) / dx->grid;
+    const int s0 = min(n, cta * seg), s1 = min(n, s0 + seg);
+    int64_t s = idn;
+    for (int i = s0 + t; i < s1; i += NT) s = comb(s, a[i]);
     auto& ts = *reinterpret_cast<typename BScan::TempStorage*>(dx->tmp);
-    int64_t total;
+    int64_t off, total;
     if (op) BScan(ts).ExclusiveScan(s, off, INT64_MIN, cub::Max(), total);
     else BScan(ts).ExclusiveSum(s, off, total);
-    if (threadIdx.x == 0) __stcg(&dx->coop->cta_part[cta], total);
+    if (t == 0) __stcg(&dx->coop->cta_part[cta], total);
     sync();
-    int64_t pre = op ? INT64_MIN : 0;  // the CTAs before this one
-    for (int c = 0; c < cta; ++c) {
-      const int64_t v = __ldcg(&dx->coop->cta_part[c]);
-      pre = op ? max(pre, v) : pre + v;
+    __shared__ int64_t s_pre;
+    if (t < 32) {
+      int64_t v = idn;
+      for (int c = t; c < cta; c += 32) v = comb(v, __ldcg(&dx->coop->cta_part[c]));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = comb(v, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)v, o));
+      if (t == 0) s_pre = v;
     }
-    off = op ? max(pre, off) : pre + off;
-    for (int i = b; i < e; ++i) {
-      off = op ? max(off, a[i]) : off + a[i];
-      a[i] = off;
+    __syncthreads();
+    int64_t carry = s_pre;
+    constexpr int K = 8, TILE = NT * K;
+    int64_t* buf = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(dx->tmp) +
+                                              ((sizeof(typename BScan::TempStorage) + 15) & ~size_t(15)));
+    auto P = [](int e) { return e + (e >> 4); };  // one pad word per 16: thread-contiguous reads hit distinct banks
+    for (int t0 = s0; t0 < s1; t0 += TILE) {
+      const int valid = min(TILE, s1 - t0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int e = k * NT + t;
+        buf[P(e)] = e < valid ? a[t0 + e] : idn;
+      }
+      __syncthreads();
+      int64_t v[K];
+      int64_t ls = idn;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { v[k] = buf[P(t * K + k)]; ls = comb(ls, v[k]); }
+      int64_t o2, agg;
+      if (op) BScan(ts).ExclusiveScan(ls, o2, INT64_MIN, cub::Max(), agg);
+      else BScan(ts).ExclusiveSum(ls, o2, agg);
+      int64_t run = comb(carry, o2);
+#pragma unroll
+      for (int k = 0; k < K; ++k) { run = comb(run, v[k]); buf[P(t * K + k)] = run; }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int e = k * NT + t;
+        if (e < valid) a[t0 + e] = buf[P(e)];
+      }
+      carry = comb(carry, agg);
+      __syncthreads();
     }
     sync();
   }

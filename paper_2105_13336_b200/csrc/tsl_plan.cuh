@@ -995,6 +995,7 @@ TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
   }
   if (x.tid == 0) {
     st.S = 0; st.R = 0; st.n_peak = 0; st.n_curve = 0;
+    g.ec_ok = 0; g.ec_S0 = -1;
     st.next_id = 0; st.peak = 0; st.peak_time = 0; st.lua = -1; st.has_lua = 0;
     st.dirty = 1; st.n_events = 0; st.son = 0; st.bz_n = 0; st.bzi_shift = 0;
   }
@@ -1008,6 +1009,324 @@ TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
 // ----------------------------------------------------------------------------
 // Shared scalar layout per batch job b: sh[b*16 + field].
 enum { F_BASE = 0, F_N, F_REL, F_INIT, F_OFF, F_MAXFP, F_PPOS, F_LUA, F_ERR, F_NPEAK, NF = 16 };
+
+// ----------------------------------------------------------------------------
+// Incremental timeline order (one-job big builds; GroupDev.ec_*)
+// ----------------------------------------------------------------------------
+// The timeline sort key (time, frees first, storage rank, type rank) as an
+// int64 time and a 32-bit low word. The evaluator's two sorts -- timeline
+// order and (storage, timeline) grouping -- are replaced by merges: the
+// accesses and every access's potential release (the "base") are sorted once
+// per access-time configuration, a release is active iff its access is
+// flagged and not owned by a swap-out, and the swap events keep their orders
+// from the previous evaluation (a swap pass only appends events), so each
+// evaluation sorts only the pass's new events. Ties follow the full sort's
+// slot order: swap events (plan order), recomputes, accesses, releases.
+TSL_HD uint32_t ev_lo(int type, int32_t rank) {
+  const bool fr = type == EV_REL || type == EV_SOUT;
+  return (uint32_t(fr ? 0 : 1) << 30) | (uint32_t(rank) << 2) | uint32_t(fr ? type - EV_SOUT : type);
+}
+TSL_HD uint32_t lo_rank(uint32_t lo) { return (lo >> 2) & 0xffffff; }
+TSL_HD uint32_t lo_cls(uint32_t lo) { return ((lo >> 30) << 2) | (lo & 3); }  // class bit, type rank
+// timeline order of (time, low word)
+TSL_HD bool tl_less(int64_t ta, uint32_t la, int64_t tb, uint32_t lb) { return ta < tb || (ta == tb && la < lb); }
+// storage-grouped order: (rank, time, class, type rank)
+TSL_HD bool gr_less(int64_t ta, uint32_t la, int64_t tb, uint32_t lb) {
+  const uint32_t ra = lo_rank(la), rb = lo_rank(lb);
+  if (ra != rb) return ra < rb;
+  if (ta != tb) return ta < tb;
+  return lo_cls(la) < lo_cls(lb);
+}
+TSL_HD uint64_t tl_key(int64_t dt, uint32_t lo, int rbits) {
+  return (uint64_t(dt) << (rbits + 3)) | (uint64_t(lo >> 30) << (rbits + 2)) | (uint64_t(lo_rank(lo)) << 2) | (lo & 3);
+}
+TSL_HD uint64_t gr_key(int64_t dt, uint32_t lo, int tbits) {
+  return (uint64_t(lo_rank(lo)) << (tbits + 3)) | (uint64_t(dt) << 3) | lo_cls(lo);
+}
+
+// Merge-path merge of two sorted slot lists, each with a payload, over every
+// thread of x (less is a strict total order on slots). No barrier.
+template <class X, class Less>
+TSL_HD void merge_slots(X& x, const int32_t* a, const int32_t* ap, int64_t n1, const int32_t* b, const int32_t* bp,
+                        int64_t n2, int32_t* out, int32_t* outp, Less less) {
+  const int64_t n = n1 + n2;
+  const int64_t per = (n + x.nthr - 1) / x.nthr;
+  const int64_t d0 = imin(n, int64_t(x.tid) * per), d1 = imin(n, d0 + per);
+  if (d0 >= d1) return;
+  int64_t lo = imax(0, d0 - n2), hi = imin(d0, n1);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (less(a[mid], b[d0 - mid - 1])) lo = mid + 1; else hi = mid;
+  }
+  int64_t i = lo, k = d0 - lo;
+  for (int64_t d = d0; d < d1; ++d) {
+    if (i < n1 && (k >= n2 || less(a[i], b[k]))) { out[d] = a[i]; outp[d] = ap[i]; ++i; }
+    else { out[d] = b[k]; outp[d] = bp[k]; ++k; }
+  }
+}
+
+// New D entries ordered by counting (each entry's rank = the entries before
+// it) while there are few of them; a radix sort above this.
+constexpr int64_t INC_COUNT_MAX = 8192;
+
+// Timeline positions (E_x_order) and the storage-grouped order (E_x_seq2,
+// E_x_key2, and the slots in that order in k_val) of job j's events, from the cached base and D orders. Needs the
+// emitted events: times in x_time, D low words in ec_dl, accesses at slot
+// acc0 + a and releases at acc0 + A + a.
+//
+// Positions: an ordered D entry k with base insertion point ins (the base
+// entries ordering before it) lands at k + #active base entries before ins; an
+// active base entry p lands at #active base entries before p + #D entries
+// with ins <= p. One scan of (active, D count) per base entry gives both; the
+// grouped order is the same construction over the grouped base. D entries
+// keep their insertion points across evaluations (the base does not move).
+template <class X>
+TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t acc0) {
+  const JobDev& J = g.jobs[j];
+  const JobState& st = g.st[j];
+  int64_t* gsh = x.sh + MAXB * NF;  // [5..8] reductions
+  const int32_t A = J.A;
+  const int64_t NB = 2 * int64_t(A);
+  uint64_t* const kk = g.k_key;
+  int32_t* const kv = g.k_val;
+  const int64_t* const xt = g.x_time;
+  int64_t* const bt = g.ec_bt;
+  uint32_t* const bl = g.ec_bl;
+  int32_t* const bs = g.ec_bs;
+  int64_t* const gt = g.ec_gt;
+  uint32_t* const gl = g.ec_gl;
+  int32_t* const gb = g.ec_gb;      // base slot of each grouped entry
+  int32_t* const ginv = g.ec_ginv;  // base position -> grouped position
+  int32_t* const posb = g.ec_posb;  // grouped position -> merged timeline position
+  int64_t* const sc = g.ec_sc;
+  int64_t* const sc2 = g.ec_sc + (NB + 1);
+  uint32_t* const dl = g.ec_dl;
+  int32_t* const posd = g.ec_posd;
+  const uint8_t* const a_flag = J.a_flag;
+  const uint8_t* const a_owned = J.a_owned;
+  const int32_t* const a_store = J.a_store;
+  const int32_t* const t_rank = J.t_rank;
+  auto base_time = [&](int32_t i) -> int64_t {
+    const int32_t a = i < A ? i : i - A;
+    return (i < A && J.a_type[a] == ACC_TGA) ? J.a_start[a] : J.a_end[a];
+  };
+  auto base_lo = [&](int32_t i) -> uint32_t {
+    const int32_t a = i < A ? i : i - A;
+    const int type = i >= A ? EV_REL : (J.a_type[a] == ACC_TGA ? EV_TGA : EV_TUA);
+    return ev_lo(type, t_rank[a_store[a]]);
+  };
+  auto active = [&](int32_t i) -> int64_t { return i < A ? 1 : ((a_flag[i - A] && !a_owned[i - A]) ? 1 : 0); };
+  int64_t ic0 = x.clock();
+  auto itick = [&](int k) { const int64_t c = x.clock(); if (x.tid == 0) g.stats.sprof[k] += c - ic0; ic0 = c; };
+  // 1. the base, once per access-time configuration
+  if (!g.ec_ok) {
+    if (x.tid == 0) { gsh[5] = INT64_MAX; gsh[6] = INT64_MIN; }
+    x.sync();
+    {
+      int64_t mn = INT64_MAX, mx = INT64_MIN;
+      for (int64_t i = x.tid; i < NB; i += x.nthr) { const int64_t t = base_time(int32_t(i)); mn = imin(mn, t); mx = imax(mx, t); }
+      if (mn != INT64_MAX) { x.amin(&gsh[5], mn); x.amax(&gsh[6], mx); }
+    }
+    x.sync();
+    const int64_t tmin = gsh[5];
+    const int tb = nbits(uint64_t(gsh[6] - gsh[5]));
+    if (tb + rbits + 3 > 63) {
+      if (x.tid == 0 && !g.err.code) { g.err.code = E_CAPACITY; g.err.job = j; g.err.tensor = NB; g.err.tick = tb + rbits + 3; }
+      x.sync();
+      return;
+    }
+    for (int64_t i = x.tid; i < NB; i += x.nthr) {
+      kk[i] = tl_key(base_time(int32_t(i)) - tmin, base_lo(int32_t(i)), rbits);
+      kv[i] = int32_t(i);
+    }
+    x.sort(kk, kv, int32_t(NB), tb + rbits + 3);  // stable: ties keep accesses, then releases, by access
+    for (int64_t p = x.tid; p < NB; p += x.nthr) {
+      const int32_t i = kv[p];
+      const uint32_t lo = base_lo(i);
+      bs[p] = i; bt[p] = base_time(i); bl[p] = lo;
+      kk[p] = lo_rank(lo);
+      kv[p] = int32_t(p);
+    }
+    x.sort(kk, kv, int32_t(NB), rbits);
+    for (int64_t q = x.tid; q < NB; q += x.nthr) {
+      const int32_t p = kv[q];
+      gb[q] = bs[p]; gt[q] = bt[p]; gl[q] = bl[p]; ginv[p] = int32_t(q);
+    }
+    x.sync();
+    if (x.tid == 0) { g.ec_ok = 1; g.ec_S0 = -1; }
+    x.sync();
+    itick(0);
+  }
+  // 2. D (swap events, recomputes): the new entries ordered, with their base
+  // insertion points, merged with the cached orders
+  const int64_t nD = int64_t(st.S) + st.R;
+  const bool keep = g.ec_S0 >= 0 && st.R == 0 && st.S >= g.ec_S0;
+  const int64_t n0 = keep ? g.ec_S0 : 0, nn = nD - n0;
+  const int cur = g.ec_cur;
+  const int64_t dcap = g.ec_dcap;
+  const int32_t* const dord0 = g.ec_dord + cur * dcap;
+  const int32_t* const dins0 = g.ec_dins + cur * dcap;
+  const int32_t* const dgrp0 = g.ec_dgrp + cur * dcap;
+  const int32_t* const gins0 = g.ec_gins + cur * dcap;
+  int32_t* const dord = g.ec_dord + (1 - cur) * dcap;
+  int32_t* const dins = g.ec_dins + (1 - cur) * dcap;
+  int32_t* const dgrp = g.ec_dgrp + (1 - cur) * dcap;
+  int32_t* const gins = g.ec_gins + (1 - cur) * dcap;
+  // new-entry scratch: ranks, then the ordered lists with their insertion points
+  int32_t* const rk_t = kv;
+  int32_t* const rk_g = kv + nn;
+  int32_t* const nw_t = g.ec_nw;
+  int32_t* const nw_ti = g.ec_nw + nn;
+  int32_t* const nw_g = g.ec_nw + 2 * nn;
+  int32_t* const nw_gi = g.ec_nw + 3 * nn;
+  auto d_tl = [&](int32_t u, int32_t v) { return xt[u] != xt[v] || dl[u] != dl[v] ? tl_less(xt[u], dl[u], xt[v], dl[v]) : u < v; };
+  auto d_gr = [&](int32_t u, int32_t v) { return xt[u] != xt[v] || dl[u] != dl[v] ? gr_less(xt[u], dl[u], xt[v], dl[v]) : u < v; };
+  auto ins_tl = [&](int32_t u) -> int32_t {  // base entries ordering before D slot u (D first on ties)
+    const int64_t t = xt[u];
+    const uint32_t l = dl[u];
+    int64_t lo = 0, hi = NB;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (tl_less(bt[mid], bl[mid], t, l)) lo = mid + 1; else hi = mid;
+    }
+    return int32_t(lo);
+  };
+  auto ins_gr = [&](int32_t u) -> int32_t {
+    const int64_t t = xt[u];
+    const uint32_t l = dl[u];
+    int64_t lo = 0, hi = NB;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (gr_less(gt[mid], gl[mid], t, l)) lo = mid + 1; else hi = mid;
+    }
+    return int32_t(lo);
+  };
+  itick(7);
+  if (nn <= INC_COUNT_MAX) {
+    for (int64_t i = x.tid; i < 2 * nn; i += x.nthr) kv[i] = 0;
+    x.sync();
+    itick(8);
+    // pairs (u, v-slice) over the threads; one atomic per (u, slice)
+    const int64_t L = nn > 0 ? imax(1, x.nthr / nn) : 1;
+    const int64_t ss = (nn + L - 1) / L;
+    for (int64_t w = x.tid; w < nn * L; w += x.nthr) {
+      const int64_t iu = w % nn, sl = w / nn;
+      const int32_t u = int32_t(n0 + iu);
+      const int64_t t = xt[u];
+      const uint32_t l = dl[u];
+      int32_t ct = 0, cg = 0;
+      const int64_t v1 = imin(nn, (sl + 1) * ss);
+      for (int64_t iv = sl * ss; iv < v1; ++iv) {
+        const int32_t v = int32_t(n0 + iv);
+        const int64_t tv = xt[v];
+        const uint32_t lv = dl[v];
+        const bool same = tv == t && lv == l;
+        ct += (same ? v < u : tl_less(tv, lv, t, l)) ? 1 : 0;
+        cg += (same ? v < u : gr_less(tv, lv, t, l)) ? 1 : 0;
+      }
+      if (ct) x.aadd32(&rk_t[iu], ct);
+      if (cg) x.aadd32(&rk_g[iu], cg);
+    }
+    x.sync();
+    itick(9);
+    for (int64_t iu = x.tid; iu < nn; iu += x.nthr) {
+      const int32_t u = int32_t(n0 + iu);
+      nw_t[rk_t[iu]] = u; nw_ti[rk_t[iu]] = ins_tl(u);
+      nw_g[rk_g[iu]] = u; nw_gi[rk_g[iu]] = ins_gr(u);
+    }
+    x.sync();
+    itick(10);
+  } else {
+    if (x.tid == 0) { gsh[7] = INT64_MAX; gsh[8] = INT64_MIN; }
+    x.sync();
+    {
+      int64_t mn = INT64_MAX, mx = INT64_MIN;
+      for (int64_t i = n0 + x.tid; i < nD; i += x.nthr) { mn = imin(mn, xt[i]); mx = imax(mx, xt[i]); }
+      if (mn != INT64_MAX) { x.amin(&gsh[7], mn); x.amax(&gsh[8], mx); }
+    }
+    x.sync();
+    const int64_t tmin_n = gsh[7];
+    const int tbn = nbits(uint64_t(gsh[8] - gsh[7]));
+    for (int64_t i = x.tid; i < nn; i += x.nthr) {
+      kk[i] = tl_key(xt[n0 + i] - tmin_n, dl[n0 + i], rbits);
+      kv[i] = int32_t(n0 + i);
+    }
+    x.sort(kk, kv, int32_t(nn), tbn + rbits + 3);
+    for (int64_t i = x.tid; i < nn; i += x.nthr) { nw_t[i] = kv[i]; nw_ti[i] = ins_tl(kv[i]); }
+    x.sync();
+    for (int64_t i = x.tid; i < nn; i += x.nthr) {
+      kk[i] = gr_key(xt[n0 + i] - tmin_n, dl[n0 + i], tbn);
+      kv[i] = int32_t(n0 + i);
+    }
+    x.sort(kk, kv, int32_t(nn), tbn + rbits + 3);
+    for (int64_t i = x.tid; i < nn; i += x.nthr) { nw_g[i] = kv[i]; nw_gi[i] = ins_gr(kv[i]); }
+  }
+  // (the scan arrays' initial values: active base entries)
+  for (int64_t i = x.tid; i < NB; i += x.nthr) {
+    const int64_t a = active(bs[i]);
+    sc[i] = a;
+    sc2[ginv[i]] = a;
+  }
+  if (x.tid == 0) { sc[NB] = 0; sc2[NB] = 0; }
+  x.sync();
+  itick(1);
+  merge_slots(x, dord0, dins0, n0, nw_t, nw_ti, nn, dord, dins, d_tl);
+  merge_slots(x, dgrp0, gins0, n0, nw_g, nw_gi, nn, dgrp, gins, d_gr);
+  x.sync();
+  itick(2);
+  // 3. D insertion counts, then one scan per order
+  for (int64_t k = x.tid; k < nD; k += x.nthr) {
+    x.aadd(&sc[dins[k]], int64_t(1) << 32);
+    x.aadd(&sc2[gins[k]], int64_t(1) << 32);
+  }
+  x.sync();
+  itick(3);
+  x.scan(sc, int32_t(NB + 1));
+  x.scan(sc2, int32_t(NB + 1));
+  itick(4);
+  constexpr int64_t LOW = 0xffffffffLL;
+  for (int64_t p = x.tid; p < NB; p += x.nthr) {
+    const int64_t e = p > 0 ? sc[p - 1] : 0;
+    if (!((sc[p] - e) & LOW)) continue;  // inactive release
+    const int64_t pos = (e & LOW) + (sc[p] >> 32);
+    g.x_order[pos] = int32_t(acc0 + bs[p]);
+    posb[ginv[p]] = int32_t(pos);
+  }
+  for (int64_t k = x.tid; k < nD; k += x.nthr) {
+    const int64_t e = dins[k] > 0 ? sc[dins[k] - 1] : 0;
+    const int64_t pos = k + (e & LOW);
+    g.x_order[pos] = dord[k];
+    posd[dord[k]] = int32_t(pos);
+  }
+  x.sync();
+  itick(5);
+  for (int64_t q = x.tid; q < NB; q += x.nthr) {
+    const int64_t e = q > 0 ? sc2[q - 1] : 0;
+    if (!((sc2[q] - e) & LOW)) continue;
+    const int64_t gpos = (e & LOW) + (sc2[q] >> 32);
+    g.x_seq2[gpos] = posb[q];
+    g.x_key2[gpos] = lo_rank(gl[q]);
+    kv[gpos] = int32_t(acc0 + gb[q]);
+  }
+  for (int64_t r = x.tid; r < nD; r += x.nthr) {
+    const int64_t e = gins[r] > 0 ? sc2[gins[r] - 1] : 0;
+    const int64_t gpos = r + (e & LOW);
+    const int32_t u = dgrp[r];
+    g.x_seq2[gpos] = posd[u];
+    g.x_key2[gpos] = lo_rank(dl[u]);
+    kv[gpos] = u;
+  }
+  x.sync();
+  itick(6);
+  if (x.tid == 0) {
+    g.ec_cur = 1 - cur;
+    g.ec_S0 = st.R == 0 ? st.S : -1;
+    g.stats.sort_elems += 2 * nn;
+  }
+  (void)n;
+  x.sync();
+}
+
 
 template <class X>
 TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
@@ -1209,6 +1528,10 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     return k;
   };
   etick(0);
+  // one-job big builds order the timeline incrementally (inc_order): events
+  // keep fixed slots (a release at acc0 + A + a) and need no sort keys
+  const bool inc = g.ec_bt != nullptr && nb == 1 && g.n_jobs == 1;
+  uint32_t* const E_dl = g.ec_dl;
   // 4. emit events (build_timeline, peak.cpp:66-174); release slots from the
   // step-2 scan.
   for (int b = 0; b < nb; ++b) {
@@ -1241,18 +1564,19 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
           const int64_t ts = a_start[a];
           E_x_time[slot] = ts;
           E_x_type[slot] = int8_t(EV_TGA | (a_tensor[a] != s ? 8 : 0));
-          E_k_key[slot] = key(b, ts, EV_TGA, rk);
+          if (!inc) E_k_key[slot] = key(b, ts, EV_TGA, rk);
         } else {
           E_x_time[slot] = te;
           E_x_type[slot] = int8_t(EV_TUA | (flagged ? 16 : 0));
-          E_k_key[slot] = key(b, te, EV_TUA, rk);
+          if (!inc) E_k_key[slot] = key(b, te, EV_TUA, rk);
         }
-        E_x_store[slot] = s; E_x_aid[slot] = a; E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
+        E_x_store[slot] = s; E_x_aid[slot] = a; E_x_job[slot] = int8_t(b);
+        if (!inc) E_k_val[slot] = int32_t(slot);
         if (flagged && !a_owned[a]) {
-          const int64_t rs = acc0 + A + rel++;
+          const int64_t rs = inc ? acc0 + A + a : acc0 + A + rel++;
           E_x_time[rs] = te; E_x_type[rs] = EV_REL; E_x_store[rs] = s; E_x_aid[rs] = a;
-          E_x_job[rs] = int8_t(b); E_k_val[rs] = int32_t(rs);
-          E_k_key[rs] = key(b, te, EV_REL, rk);
+          E_x_job[rs] = int8_t(b);
+          if (!inc) { E_k_val[rs] = int32_t(rs); E_k_key[rs] = key(b, te, EV_REL, rk); }
         }
       }
     }
@@ -1271,6 +1595,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       E_x_time[slot] = when; E_x_type[slot] = int8_t(type); E_x_store[slot] = s; E_x_aid[slot] = -1;
       E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
       E_k_key[slot] = key(b, when, type, J.t_rank[s]);
+      if (inc) E_dl[slot] = ev_lo(type, J.t_rank[s]);
     }
     for (int32_t r = x.tid; r < st.R; r += x.nthr) {
       const int32_t s = J.t_store[J.rc_tensor[r]];
@@ -1279,10 +1604,17 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       E_x_time[slot] = when; E_x_type[slot] = EV_TGA; E_x_store[slot] = s; E_x_aid[slot] = -1;
       E_x_job[slot] = int8_t(b); E_k_val[slot] = int32_t(slot);
       E_k_key[slot] = key(b, when, EV_TGA, J.t_rank[s]);
+      if (inc) E_dl[slot] = ev_lo(EV_TGA, J.t_rank[s]);
     }
   }
   x.sync();
   etick(1);
+  if (inc) {
+    // 5-6. timeline order and (storage, timeline) grouping by merges
+    inc_order(x, g, jb, n, rbits, sh[F_BASE] + g.st[jb].S + g.st[jb].R);
+    if (g.err.code) return false;
+    etick(2);
+  } else {
   // 5. timeline order (sort_timeline, peak.cpp:44-62)
   x.sort(E_k_key, E_k_val, int32_t(n), jbits + tbits + 1 + rbits + 2);
   etick(2);
@@ -1296,7 +1628,11 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   }
   x.sync();
   x.sort(E_x_key2, E_x_seq2, int32_t(n), jbits + rbits);
+  for (int64_t m = x.tid; m < n; m += x.nthr) E_k_val[m] = E_x_order[E_x_seq2[m]];
+  x.sync();
   etick(3);
+  }
+  const int32_t* const E_gslot = E_k_val;  // slots in (job, storage)-grouped order
   // 7. per-storage residency automaton (analyze_peak's switch, peak.cpp:206-230),
   // in parallel: in (job, storage)-grouped order, the residency before an
   // event is set by the previous state-changing event of its storage (TGA
@@ -1306,7 +1642,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   {
     int64_t* chg = reinterpret_cast<int64_t*>(E_k_key);  // free after sort 1
     for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int ty = E_x_type[E_x_order[E_x_seq2[m]]] & 7;
+      const int ty = E_x_type[E_gslot[m]] & 7;
       chg[m] = ty == EV_TUA ? -1 : m;
     }
     x.sync();
@@ -1316,7 +1652,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const int64_t* c_size = nullptr;
     for (int64_t m = x.tid; m < n; m += x.nthr) {
       const int32_t pos = E_x_seq2[m];
-      const int32_t slot = E_x_order[pos];
+      const int32_t slot = E_gslot[m];
       const int b = E_x_job[slot];
       if (b != cb) {  // job arrays cached in registers (the byte stores below alias the struct)
         cb = b;
@@ -1328,7 +1664,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const int64_t prev = m > 0 ? chg[m - 1] : -1;  // last state change strictly before m
       uint8_t res;
       if (prev >= 0 && E_x_key2[prev] == E_x_key2[m]) {
-        const int pt = E_x_type[E_x_order[E_x_seq2[prev]]] & 7;
+        const int pt = E_x_type[E_gslot[prev]] & 7;
         res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
       } else {
         res = c_res[s];
@@ -1428,7 +1764,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // so that event is the one whose successor leaves the group or the prefix.
   for (int64_t m = x.tid; m < n; m += x.nthr) {
     const int32_t pos = E_x_seq2[m];
-    const int32_t slot = E_x_order[pos];
+    const int32_t slot = E_gslot[m];
     const int b = E_x_job[slot];
     const int64_t pp = sh[b * NF + F_PPOS];
     if (pp == INT64_MAX || pos > pp) continue;
@@ -1441,9 +1777,10 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
     int64_t* f = sh + b * NF;
-    int32_t cnt = 0;
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) cnt += J.in_peak[t];
-    if (cnt) x.aadd(&f[F_NPEAK], cnt);
+    // the peak storages, unordered: the next swap pass's candidates
+    int32_t* const pk_list = J.pk_list;
+    for (int32_t t = x.tid; t < J.T; t += x.nthr)
+      if (J.in_peak[t]) pk_list[x.aadd(&f[F_NPEAK], 1)] = t;
     const int64_t base = f[F_BASE], nn = f[F_N];
     if (x.tid == 0) { J.curve_t[0] = 0; J.curve_b[0] = f[F_INIT]; }
     for (int64_t m = x.tid; m < nn; m += x.nthr) {
@@ -2529,6 +2866,8 @@ TSL_HD void conflicts_batch(X& x, GroupDev& g, int64_t w0, int64_t w1, const int
 template <class X>
 TSL_HD bool swap_pass(X& x, GroupDev& g) {
   int64_t* sh = x.sh;
+  int64_t pc0 = x.clock();
+  auto ptick = [&](int k) { const int64_t c = x.clock(); if (x.tid == 0) g.stats.sprof[k] += c - pc0; pc0 = c; };
   int64_t* gsh = sh + MAXB * NF;  // [9]=maxT [10]=changed [11]=cursor [12]=maxsize [13..14] pools [16..] segments
   if (x.tid == 0) {
     int64_t maxT = 1;
@@ -2541,13 +2880,14 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     }
   }
   x.sync();
-  for (int j = 0; j < g.n_jobs; ++j) {
+  for (int j = 0; j < g.n_jobs; ++j) {  // (the evaluator lists each job's peak storages)
     const JobDev& J = g.jobs[j];
     int64_t mx = 1;
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.in_peak[t]) mx = imax(mx, J.t_size[t]);
+    for (int32_t i = x.tid; i < g.st[j].n_peak; i += x.nthr) mx = imax(mx, J.t_size[J.pk_list[i]]);
     x.amax(&gsh[12], mx);
   }
   x.sync();
+  ptick(11);
   const int jbits = nbits(uint64_t(g.n_jobs - 1));
   const int rbits = nbits(uint64_t(gsh[9] - 1));
   const int sbits = nbits(uint64_t(gsh[12]));
@@ -2557,8 +2897,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   // pass), ordered (size desc, job id, storage id) -- swap_planner.cpp:469-481
   for (int j = 0; j < g.n_jobs; ++j) {
     const JobDev& J = g.jobs[j];
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
-      if (!J.in_peak[t]) continue;
+    for (int32_t i = x.tid; i < g.st[j].n_peak; i += x.nthr) {
+      const int32_t t = J.pk_list[i];
       const int64_t slot = x.aadd(&gsh[11], 1);
       if (slot >= g.ecap) continue;
       const uint64_t inv = smax - uint64_t(J.t_size[t]);
@@ -2576,7 +2916,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     x.sync();
     return false;
   }
+  ptick(12);
   x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
+  ptick(13);
   // component speculation (phase A2): spec_comp 2 always, 1 for passes of
   // at least COMP_MIN_CANDIDATES candidates (below that the extra phase costs
   // more than the few re-scores it saves), 0 never
@@ -2613,6 +2955,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
       for (int j = g.n_jobs - 1; j >= 0; --j) gsh[16 + j] = imin(gsh[16 + j], gsh[16 + j + 1]);
   }
   x.sync();
+  ptick(14);
   int64_t t0 = x.clock(), t1;
   auto tick = [&](int k) { t1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += t1 - t0; t0 = t1; };
   // Speculation windows: phases A-C run on consecutive windows of the
@@ -3159,8 +3502,9 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
   for (int j = 0; j < g.n_jobs; ++j) {
     const JobDev& J = g.jobs[j];
     const JobState& st = g.st[j];
-    for (int32_t t = x.tid; t < J.T; t += x.nthr) {
-      if (!J.in_peak[t] || J.t_kind[t] != K_INTERIM) continue;
+    for (int32_t i = x.tid; i < st.n_peak; i += x.nthr) {
+      const int32_t t = J.pk_list[i];
+      if (J.t_kind[t] != K_INTERIM) continue;
       if (J.st_evcnt[t] > 0) continue;  // storage_has_swap
       bool rec = false;
       for (int32_t r = 0; r < st.R; ++r) if (J.rc_tensor[r] == t) rec = true;
@@ -3241,6 +3585,7 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
     st.R = r + 1;
     st.next_id += 1;
     st.period += lat;
+    g.ec_ok = 0; g.ec_S0 = -1;  // access times shift: the incremental base is stale
   }
   for (int32_t a = x.tid; a < J.A; a += x.nthr)
     if (J.a_start[a] >= pivot) { J.a_start[a] += lat; J.a_end[a] += lat; }
@@ -3252,7 +3597,10 @@ TSL_HD bool recompute_pass(X& x, GroupDev& g) {
   if (!eval_batch(x, g, j, j + 1)) return false;
   if (st.peak > saved.peak) {  // rollback (recompute_planner.cpp:148-151)
     backup_job(x, g, j, true, saved.S, saved.R, saved.n_curve);
-    if (x.tid == 0) st = saved;
+    if (x.tid == 0) { st = saved; g.ec_ok = 0; g.ec_S0 = -1; gsh[27] = 0; }
+    x.sync();
+    for (int32_t t = x.tid; t < J.T; t += x.nthr)  // the restored report's peak list
+      if (J.in_peak[t]) J.pk_list[x.aadd(&gsh[27], 1)] = t;
     x.sync();
     build_anchor_index(x, g, j);
     build_busy_index(x, g, j);
@@ -3276,6 +3624,7 @@ TSL_HD void reset_group(X& x, GroupDev& g) {
     g.loop_iters = 0;
     g.err = ErrInfo{};
     g.stats = GroupStats{};
+    g.ec_ok = 0; g.ec_S0 = -1;
   }
   x.sync();
 }

@@ -113,6 +113,7 @@ struct JobDev {
 
   // ---- report (PeakReport, peak.hpp:47-56) ----
   uint8_t* in_peak;   // [T] storage resident at the peak
+  int32_t* pk_list;   // [T] the storages resident at the peak, unordered (JobState.n_peak entries)
   uint8_t* ev_drop;   // [Scap] scratch for revalidation
   uint8_t* res_init;  // [T] scratch: initial residency (peak.cpp:176-190)
   int64_t* curve_t;   // [Ecap+1]
@@ -170,6 +171,7 @@ struct GroupStats {
   int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
   int64_t prof[16];          // development profile of re-score queries (TSL_PROF builds)
   int64_t comp_rescored;     // candidates re-speculated inside their conflict component
+  int64_t sprof[16];         // SM cycles (thread 0): [0..6] incremental timeline order, [11..14] swap-pass prologue
 };
 
 // Control block of a cooperative launch (one group above one sort tile,
@@ -268,6 +270,33 @@ struct GroupDev {
   int64_t c_wn;      // candidates of the window being processed
   int64_t* c_wscratch;  // cooperative launches: per-warp run lists (6 * c_wscap words per warp of the grid)
   int64_t c_wscap;
+  // Incremental timeline order (tsl_plan.cuh inc_order; one-job big builds,
+  // null otherwise). The "base" is every access event plus one potential
+  // release per access (2A entries), sorted once per access-time
+  // configuration; swap passes only append events, so the swap events'
+  // timeline and storage-grouped orders are kept across evaluations and
+  // only each pass's new events are sorted and merged in.
+  int32_t ec_ok;       // base valid (access times unchanged since it was built)
+  int32_t ec_S0;       // swap events [0, ec_S0) are in the cached D orders (-1: none)
+  int32_t ec_cur;      // current half of the D ping-pong buffers
+  int32_t ec_pad;
+  int64_t ec_dcap;     // D capacity (Scap + Rcap)
+  int64_t* ec_bt;      // [2A] base in timeline order: time
+  uint32_t* ec_bl;     // [2A] key low word: non-free << 30 | storage rank << 2 | type rank
+  int32_t* ec_bs;      // [2A] base slot: a (access a), A + a (release of a)
+  int64_t* ec_gt;      // [2A] base in (storage rank, timeline) order: time
+  uint32_t* ec_gl;     // [2A] key low word
+  int32_t* ec_gb;      // [2A] base slot
+  int32_t* ec_ginv;    // [2A] base position -> grouped position
+  int32_t* ec_posb;    // [2A] merged timeline position of each grouped base entry
+  int64_t* ec_sc;      // [2 x (2A + 1)] active base entries + D insertions, per order (scan scratch)
+  int32_t* ec_dord;    // [2 * dcap] D slots in timeline order (ping-pong)
+  int32_t* ec_dins;    // [2 * dcap] their base insertion points
+  int32_t* ec_dgrp;    // [2 * dcap] D slots in storage-grouped order (ping-pong)
+  int32_t* ec_gins;    // [2 * dcap] their grouped-base insertion points
+  int32_t* ec_nw;      // [4 * dcap] an evaluation's new D entries, ordered, with insertion points
+  int32_t* ec_posd;    // [dcap] merged timeline position of each D slot
+  uint32_t* ec_dl;     // [dcap] key low word of each D slot
 };
 
 }  // namespace tsl

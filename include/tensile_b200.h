@@ -164,8 +164,10 @@ typedef struct tsl_stats {
   int64_t evalprof[7];  /* evaluator phases: prep, emit, sort1, group, automaton, scan.., peak..report */
   int64_t queryprof[16];  /* development profile of re-score queries (zero unless built with TSL_PROF) */
   int64_t comp_rescored;  /* candidates re-speculated inside their conflict component (phase A2) */
-  int64_t stageprof[16];  /* SM cycles: [0..6] incremental timeline order phases, [7..10] its new-entry ordering,
-                             [11..14] swap-pass prologue (peak sizes, candidates, sort, rest) */
+  int64_t stageprof[24];  /* SM cycles: [0..6] incremental timeline order phases, [7..10] its new-entry ordering,
+                             [11..14] swap-pass prologue (peak sizes, candidates, sort, rest), [15] phase A,
+                             [16..20] component runs: sum of per-pass longest run, members, runs,
+                             sum of per-pass slowest run cycles, run cycles */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

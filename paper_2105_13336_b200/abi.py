@@ -85,7 +85,7 @@ class TslStats(C.Structure):
                 ("prep_ms", C.c_double), ("cyc_rescore", C.c_int64),
                 ("cyc_apply", C.c_int64), ("debug", C.c_int64 * 4), ("cyc_pendsort", C.c_int64), ("fitprof", C.c_int64 * 9), ("evalprof", C.c_int64 * 7),
                 ("queryprof", C.c_int64 * 16), ("comp_rescored", C.c_int64),
-                ("stageprof", C.c_int64 * 16)]
+                ("stageprof", C.c_int64 * 24)]
 
 
 class TslExecConfig(C.Structure):

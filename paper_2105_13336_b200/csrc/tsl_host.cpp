@@ -901,7 +901,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   for (int k = 0; k < 7; ++k) s.evalprof[k] = G.stats.cyc[20 + k];
   for (int k = 0; k < 16; ++k) s.queryprof[k] = G.stats.prof[k];
   s.comp_rescored = G.stats.comp_rescored;
-  for (int k = 0; k < 16; ++k) s.stageprof[k] = G.stats.sprof[k];
+  for (int k = 0; k < 24; ++k) s.stageprof[k] = G.stats.sprof[k];
   return R;
 }
 

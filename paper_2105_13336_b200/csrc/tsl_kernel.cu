@@ -456,6 +456,8 @@ struct DevX {
       else if (type == COOP_REBUILD) coop_rebuild(cta);
       else if (type == COOP_COMP) coop_comp(cta);
       else if (type == COOP_CONF) coop_conf(cta);
+      else if (type == COOP_SPEC) coop_spec(cta);
+      else if (type == COOP_A2) coop_a2(cta);
       else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
@@ -464,6 +466,8 @@ struct DevX {
   __device__ void coop_rebuild(int cta);               // all CTAs: rebuild_busy() on the grid (below)
   __device__ void coop_comp(int cta);                  // workers: component runs (below)
   __device__ void coop_conf(int cta);                  // all CTAs: find_conflicts() on the grid (below)
+  __device__ void coop_spec(int cta);                  // all CTAs: spec_phase() on the grid (below)
+  __device__ void coop_a2(int cta);                    // all CTAs: component_speculation() on the grid (below)
   GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
@@ -591,6 +595,16 @@ struct GridX {
   __device__ void amax(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }
   __device__ int32_t aadd32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
   __device__ int32_t wexcl(int32_t v, int32_t* total) { return dx->wexcl(v, total); }
+  // warp primitives (warp-collective code run by every warp of the grid)
+  __device__ void wsync() { __syncwarp(); }
+  __device__ bool wany(bool p) { return __any_sync(0xffffffffu, p); }
+  __device__ unsigned wballot(bool p) { return __ballot_sync(0xffffffffu, p); }
+  __device__ int64_t shfl(int64_t v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+  __device__ int ffs(unsigned m) { return __ffs(m); }
+  __device__ void amax32(int32_t* p, int32_t v) { atomicMax(p, v); }
+  __device__ void amin32(int32_t* p, int32_t v) { atomicMin(p, v); }
+  __device__ void aor32(int32_t* p, int32_t v) { atomicOr(p, v); }
+  __device__ void errset(GroupDev& g, const ErrInfo& e) { dx->errset(g, e); }
   // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs: each CTA owns
   // a contiguous segment; its total is reduced with coalesced loads, one warp
   // combines the earlier CTAs' totals, and the segment is scanned in tiles
@@ -771,6 +785,75 @@ __device__ inline void conflicts_batch<DevX>(DevX& x, GroupDev& g, int64_t w0, i
     __syncthreads();
   }
 #endif
+}
+
+// Phase A on a cooperative launch: one thread per candidate over the whole
+// grid (a C4 window speculates ~2,300 candidates, ~9 per thread of CTA 0
+// alone, each a chain of dependent placement queries). The pool counters
+// move to the grid scalars and back.
+__device__ void DevX::coop_spec(int cta) {
+  volatile CoopCtl* c = coop;
+  GridX gx = grid_ctx(*this, cta);
+  spec_phase(gx, *coop_group, c->cw0, c->cw1, c->ccand, c->ccinfo, c->cchull);
+  gx.sync();
+}
+
+constexpr int64_t SPEC_GRID_MIN = 512;  // smaller windows: CTA 0's threads take one candidate each anyway
+
+template <>
+__device__ inline void spec_batch<DevX>(DevX& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand,
+                                        int32_t* cinfo, int64_t* chull) {
+  if (!x.coop || x.grid < 2 || !g.grid_conf || w1 - w0 < SPEC_GRID_MIN) {
+    spec_phase(x, g, w0, w1, cand, cinfo, chull);
+    return;
+  }
+  int64_t* gsh = x.sh + MAXB * NF;
+  int64_t* ggsh = x.coop->gsh + MAXB * NF;
+  __syncthreads();
+  if (x.tid == 0) { __stcg(&ggsh[GS_PPOOL], gsh[GS_PPOOL]); __stcg(&ggsh[GS_WPOOL], gsh[GS_WPOOL]); }
+  for (int j = x.tid; j < g.n_jobs; j += x.nthr) __stcg(&ggsh[GS_PCAP + j], gsh[GS_PCAP + j]);
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->cw0 = w0; c->cw1 = w1; c->ccand = cand; c->ccinfo = cinfo; c->cchull = chull; c->type = COOP_SPEC;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  GridX gx = grid_ctx(x, 0);
+  spec_phase(gx, g, w0, w1, cand, cinfo, chull);
+  gx.sync();
+  if (x.tid == 0) { gsh[GS_PPOOL] = __ldcg(&ggsh[GS_PPOOL]); gsh[GS_WPOOL] = __ldcg(&ggsh[GS_WPOOL]); }
+  for (int j = x.tid; j < g.n_jobs; j += x.nthr) gsh[GS_PCAP + j] = __ldcg(&ggsh[GS_PCAP + j]);
+  __syncthreads();
+}
+
+// Phase A2 on a cooperative launch: the union-find rounds, the member lists
+// and the runs (every warp of the grid, comp_dispatch's grid branch) all on
+// the grid; CTA 0 alone spent ~0.3 ms per C4 pass outside the runs.
+__device__ void DevX::coop_a2(int cta) {
+  volatile CoopCtl* c = coop;
+  GridX gx = grid_ctx(*this, cta);
+  component_speculation(gx, *coop_group, c->cw0, c->cw1, c->ccand, c->ccinfo, c->cchull);
+}
+
+template <>
+__device__ inline void comp_batch<DevX>(DevX& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand,
+                                        int32_t* cinfo, int64_t* chull) {
+  if (!x.coop || x.grid < 2 || !g.grid_conf || !g.c_wscratch) {
+    component_speculation(x, g, w0, w1, cand, cinfo, chull);
+    return;
+  }
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->cw0 = w0; c->cw1 = w1; c->ccand = cand; c->ccinfo = cinfo; c->cchull = chull; c->type = COOP_A2;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  GridX gx = grid_ctx(x, 0);
+  component_speculation(gx, g, w0, w1, cand, cinfo, chull);  // ends with a grid barrier
 }
 
 // Component runs on a cooperative launch: every warp of every CTA takes runs

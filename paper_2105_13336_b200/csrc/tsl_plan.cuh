@@ -2689,7 +2689,9 @@ TSL_HD void comp_runs(X& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_
     PendBuf pl{wb, wb + cap, wb + 2 * cap, wb + 3 * cap, wb + 4 * cap, int32_t(imin(cap, INT32_MAX))};
     const int64_t P = imax(1, lst.period);
     bool broken = false;
-    for (int64_t p = p0; p < wn && par[g.x_seq2[p]] == root; ++p) {
+    const int64_t rc0 = x.clock();
+    int64_t p = p0;
+    for (; p < wn && par[g.x_seq2[p]] == root; ++p) {
       const int64_t m = w0 + g.x_seq2[p];
       int32_t* ci = cinfo + m * CI_STRIDE;
       const int32_t stm = ci[CI_STATUS] & 0xf;
@@ -2761,6 +2763,14 @@ TSL_HD void comp_runs(X& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_
       }
       x.wsync();
     }
+    if (x.lane == 0) {  // run statistics (stageprof)
+      const int64_t rc = x.clock() - rc0;
+      x.amax(&g.stats.sprof[21], p - p0);
+      x.amax(&g.stats.sprof[22], rc);
+      x.aadd(&g.stats.sprof[17], p - p0);
+      x.aadd(&g.stats.sprof[18], 1);
+      x.aadd(&g.stats.sprof[20], rc);
+    }
   }
   if (x.lane == 0) {
     x.aadd(&g.stats.comp_rescored, ls.comp_rescored);
@@ -2776,6 +2786,11 @@ template <class X>
 TSL_HD void comp_dispatch(X& x, GroupDev& g, int64_t w0, const int32_t* cand, int32_t* cinfo, int64_t* chull,
                           int64_t nruns) {
   int64_t* gsh = x.sh + MAXB * NF;
+  if (X::W > 1 && g.c_wscratch) {  // a grid context: every warp of the launch, each with its own list
+    comp_runs(x, g, w0, cand, cinfo, chull, &gsh[GS_CRUN], nruns, g.c_wscratch + int64_t(x.tid / X::W) * 6 * g.c_wscap,
+              g.c_wscap);
+    return;
+  }
   const int64_t cap = (g.wcap * 4) / 6;
   comp_runs(x, g, w0, cand, cinfo, chull, &gsh[GS_CRUN], nruns, g.wbuf + int64_t(x.warp) * 4 * g.wcap, cap);
 }
@@ -2848,11 +2863,26 @@ TSL_HD void component_speculation(X& x, GroupDev& g, int64_t w0, int64_t w1, con
   }
   x.sync();
   const int64_t nruns = gsh[GS_NRUN];
+  if (x.tid == 0) { g.stats.sprof[21] = 0; g.stats.sprof[22] = 0; }
+  x.sync();
   // one warp per run (taken in turn): on every CTA of a cooperative launch
   comp_dispatch(x, g, w0, cand, cinfo, chull, nruns);
   x.sync();
+  if (x.tid == 0) {
+    const volatile int64_t* sp = g.stats.sprof;
+    g.stats.sprof[16] += sp[21];
+    g.stats.sprof[19] += sp[22];
+  }
   for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) cinfo[m * CI_STRIDE + CI_NCONF] = 0;
   x.sync();
+}
+
+// Phase A2 of a window; an execution context may route it elsewhere (the
+// CUDA build runs it on every CTA of a cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD void comp_batch(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo,
+                       int64_t* chull) {
+  component_speculation(x, g, w0, w1, cand, cinfo, chull);
 }
 
 // Phase B of a window; an execution context may route it elsewhere (the CUDA
@@ -2861,6 +2891,66 @@ template <class X>
 TSL_HD void conflicts_batch(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo,
                             const int64_t* chull, bool coupled, const int32_t* comp) {
   find_conflicts(x, g, w0, w1, cand, cinfo, chull, coupled, comp);
+}
+
+// ---- A. speculative scoring of the window [w0, w1), one thread per
+// candidate (pool counters GS_PPOOL / GS_WPOOL / GS_PCAP + j in x's scalars).
+// No trailing barrier.
+template <class X>
+TSL_HD void spec_phase(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo, int64_t* chull) {
+  int64_t* gsh = x.sh + MAXB * NF;
+  {
+    GroupStats ls{};
+    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
+      const int j = cand[m] >> 24;
+      const int32_t s = cand[m] & 0xffffff;
+      const JobDev& J = g.jobs[j];
+      const JobState& st = g.st[j];
+      int32_t* ci = cinfo + m * CI_STRIDE;
+      int64_t* hl = chull + m * 4;
+      ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
+      ci[CI_P0] = -1;
+      hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
+      if (J.swapped[s]) { ci[CI_STATUS] = CS_SKIP; continue; }
+      int64_t earliest = 0, latest = 0;
+      const int kind = candidate_kind(J, st, s, earliest, latest);
+      if (kind == 0) { ci[CI_STATUS] = CS_SKIP; continue; }
+      if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
+      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
+      const int32_t capw = 2 * capp + 2;
+      const int64_t p0 = x.aadd(&gsh[GS_PPOOL], capp);
+      const int64_t wp0 = x.aadd(&gsh[GS_WPOOL], capw);
+      x.aadd(&gsh[GS_PCAP + j], capp);
+      if (p0 + capp > g.pr_cap || wp0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
+      ci[CI_P0] = int32_t(p0);
+      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * wp0, 0, capw, false};
+      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
+      ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
+      ci[CI_NP] = c.npairs;
+      ci[CI_W0] = int32_t(wp0);
+      ci[CI_NW] = c.nwin;
+      for (int32_t w = 0; w < c.nwin; ++w) {
+        hl[0] = imin(hl[0], c.win[2 * w]);
+        hl[1] = imax(hl[1], c.win[2 * w + 1]);
+      }
+      for (int32_t p = 0; p < c.npairs; ++p) {
+        hl[2] = imin(hl[2], imin(c.pairs[p].os, c.pairs[p].is));
+        hl[3] = imax(hl[3], imax(c.pairs[p].oe, c.pairs[p].ie));
+      }
+    }
+    if (ls.fit_queries | ls.busy_intervals | ls.candidate_accesses) {  // (idle grid threads skip the atomics)
+      x.aadd(&g.stats.fit_queries, ls.fit_queries);
+      x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
+      x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
+    }
+  }
+}
+
+// Phase A of a window; an execution context may route it elsewhere (the CUDA
+// build runs it on every CTA of a cooperative launch, tsl_kernel.cu).
+template <class X>
+TSL_HD void spec_batch(X& x, GroupDev& g, int64_t w0, int64_t w1, const int32_t* cand, int32_t* cinfo, int64_t* chull) {
+  spec_phase(x, g, w0, w1, cand, cinfo, chull);
 }
 
 template <class X>
@@ -2931,8 +3021,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   size_t rec_bytes = 0;  // shared scratch taken by the candidate records
   {
     const size_t need = size_t(nc) * (sizeof(int64_t) * 4 + sizeof(int32_t) * (CI_STRIDE + 2)) + 64;
-    // (component speculation sorts in that scratch: records stay in HBM)
-    if (need <= x.tmp_bytes && !comp_on) {
+    // (component speculation sorts in that scratch, and a cooperative
+    // launch's grid phases read the records from every SM: records stay in HBM)
+    if (need <= x.tmp_bytes && !comp_on && !(g.coop && g.grid_conf)) {
       chull = reinterpret_cast<int64_t*>(x.tmp);
       cinfo = reinterpret_cast<int32_t*>(chull + 4 * nc);
       cand = cinfo + CI_STRIDE * nc;
@@ -2980,50 +3071,9 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   }
   x.sync();
   // ---- A. speculative scoring, one thread per candidate ----
-  {
-    GroupStats ls{};
-    for (int64_t m = w0 + x.tid; m < w1; m += x.nthr) {
-      const int j = cand[m] >> 24;
-      const int32_t s = cand[m] & 0xffffff;
-      const JobDev& J = g.jobs[j];
-      const JobState& st = g.st[j];
-      int32_t* ci = cinfo + m * CI_STRIDE;
-      int64_t* hl = chull + m * 4;
-      ci[CI_NP] = 0; ci[CI_NW] = 0; ci[CI_NCONF] = 0; ci[CI_STATE] = 0; ci[CI_EV0] = 0; ci[CI_ID0] = 0;
-      ci[CI_P0] = -1;
-      hl[0] = INT64_MAX; hl[1] = INT64_MIN; hl[2] = INT64_MAX; hl[3] = INT64_MIN;
-      if (J.swapped[s]) { ci[CI_STATUS] = CS_SKIP; continue; }
-      int64_t earliest = 0, latest = 0;
-      const int kind = candidate_kind(J, st, s, earliest, latest);
-      if (kind == 0) { ci[CI_STATUS] = CS_SKIP; continue; }
-      if (kind < 0) { ci[CI_STATUS] = CS_ERROR; continue; }
-      const int32_t capp = kind == 1 ? 1 : imax(1, J.s_off[s + 1] - J.s_off[s]);
-      const int32_t capw = 2 * capp + 2;
-      const int64_t p0 = x.aadd(&gsh[GS_PPOOL], capp);
-      const int64_t wp0 = x.aadd(&gsh[GS_WPOOL], capw);
-      x.aadd(&gsh[GS_PCAP + j], capp);
-      if (p0 + capp > g.pr_cap || wp0 + capw > g.w_cap) { ci[CI_STATUS] = CS_OVERFLOW; continue; }
-      ci[CI_P0] = int32_t(p0);
-      SpecCtx c{J, st, g.cfg, &ls, g.pr_pool + p0, 0, capp, g.w_pool + 2 * wp0, 0, capw, false};
-      const bool ok = kind == 1 ? schedule_wrapped_swap(c, s) : schedule_swap(c, s, earliest, latest);
-      ci[CI_STATUS] = c.overflow ? CS_OVERFLOW : (ok ? CS_OK : CS_FAIL);
-      ci[CI_NP] = c.npairs;
-      ci[CI_W0] = int32_t(wp0);
-      ci[CI_NW] = c.nwin;
-      for (int32_t w = 0; w < c.nwin; ++w) {
-        hl[0] = imin(hl[0], c.win[2 * w]);
-        hl[1] = imax(hl[1], c.win[2 * w + 1]);
-      }
-      for (int32_t p = 0; p < c.npairs; ++p) {
-        hl[2] = imin(hl[2], imin(c.pairs[p].os, c.pairs[p].is));
-        hl[3] = imax(hl[3], imax(c.pairs[p].oe, c.pairs[p].ie));
-      }
-    }
-    x.aadd(&g.stats.fit_queries, ls.fit_queries);
-    x.aadd(&g.stats.busy_intervals, ls.busy_intervals);
-    x.aadd(&g.stats.candidate_accesses, ls.candidate_accesses);
-  }
+  spec_batch(x, g, w0, w1, cand, cinfo, chull);
   x.sync();
+  if (x.tid == 0) g.stats.sprof[15] += x.clock() - t0;
   tick(5);
   // ---- B. conflicts with earlier speculative commits of the same job ----
   conflicts_batch(x, g, w0, w1, cand, cinfo, chull, coupled, nullptr);
@@ -3031,7 +3081,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   if (use_comp) {
     x.sync();
     tick(6);
-    component_speculation(x, g, w0, w1, cand, cinfo, chull);
+    comp_batch(x, g, w0, w1, cand, cinfo, chull);
     tick(5);
     // conflicts across components (a member's speculation includes its own
     // component's earlier results)

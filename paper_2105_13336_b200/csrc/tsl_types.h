@@ -171,7 +171,7 @@ struct GroupStats {
   int64_t cyc[32];           // SM cycles per stage (thread 0): seq, eval, swap, rc, total, spec, conflict, sweep, merge
   int64_t prof[16];          // development profile of re-score queries (TSL_PROF builds)
   int64_t comp_rescored;     // candidates re-speculated inside their conflict component
-  int64_t sprof[16];         // SM cycles (thread 0): [0..6] incremental timeline order, [11..14] swap-pass prologue
+  int64_t sprof[24];         // SM cycles (thread 0): [0..6] incremental timeline order, [11..14] swap-pass prologue
 };
 
 // Control block of a cooperative launch (one group above one sort tile,
@@ -207,13 +207,15 @@ struct CoopCtl {
   int32_t* ccinfo;
   int64_t* cchull;
   int32_t cdone, cpad;           // worker CTAs done
-  // COOP_CONF: phase B of the window [cw0, cw1) on the grid
+  // COOP_CONF / COOP_SPEC: phase B / phase A of the window [cw0, cw1) on the grid
   int64_t cw1;
   const int32_t* ccomp;
   int32_t ccoupled;
   int32_t abort;                 // a spin timed out: every CTA leaves (the group reports E_INTERNAL)
 };
-enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_CONF = 6, COOP_EXIT = 9 };
+enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_CONF = 6, COOP_SPEC = 7,
+                 COOP_A2 = 8,
+                 COOP_EXIT = 9 };
 
 struct GroupDev {
   int32_t n_jobs;

@@ -11,4 +11,7 @@ P.build_plan(jobs, cfg)
 p = P.build_plan(jobs, cfg)
 s = p["stats"]
 print("kernel", s["kernel_ms"], "evalprof", list(s["evalprof"]))
-print("inc phases base/new+init/merges/atomics/scans/scatter1/scatter2:", list(s["stageprof"])[:11], "swap pre: maxsize/collect/sort/rest", list(s["stageprof"])[11:15])
+print("inc phases base/new+init/merges/atomics/scans/scatter1/scatter2:", list(s["stageprof"])[:11], "swap pre: maxsize/collect/sort/rest", list(s["stageprof"])[11:15], "phaseA", s["stageprof"][15], "spec", s["cyc_spec"], "conflict", s["cyc_conflict"])
+sp = list(s["stageprof"])
+print(f"component runs: {sp[18]} runs, {sp[17]} members, sum of per-pass longest run {sp[16]} members, "
+      f"sum of per-pass slowest run {sp[19]} cyc, all runs {sp[20]} cyc; A2 total {s['cyc_spec'] - sp[15]} cyc")

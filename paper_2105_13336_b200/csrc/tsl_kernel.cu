@@ -48,6 +48,7 @@ static_assert(tmp_bytes_for(SORT_IPT) >= ((sizeof(typename BScan::TempStorage) +
 
 struct DevX {
   static constexpr int W = 32;
+  static constexpr bool GRID = false;
   int tid, nthr, lane, warp, nwarp;
   int64_t* sh;
   void* tmp;
@@ -583,6 +584,7 @@ namespace tsl {
 // acquire fence -- checked by tools/l1_coherence_probe.cu.)
 struct GridX {
   static constexpr int W = 32;
+  static constexpr bool GRID = true;  // every CTA of a cooperative launch
   int tid, nthr, lane, warp, nwarp, cta;
   int64_t* sh;
   DevX* dx;
@@ -610,7 +612,8 @@ struct GridX {
   // combines the earlier CTAs' totals, and the segment is scanned in tiles
   // staged through shared memory (coalesced loads and stores, each thread
   // scanning K consecutive elements).
-  __device__ void scan_op(int64_t* a, int n, int op) {
+  template <class T>
+  __device__ void scan_op(T* a, int n, int op) {
     sync();
     const int t = threadIdx.x;
     const int64_t idn = op ? INT64_MIN : 0;
@@ -618,7 +621,7 @@ struct GridX {
     const int seg = (n + dx->grid - 1) / dx->grid;
     const int s0 = min(n, cta * seg), s1 = min(n, s0 + seg);
     int64_t s = idn;
-    for (int i = s0 + t; i < s1; i += NT) s = comb(s, a[i]);
+    for (int i = s0 + t; i < s1; i += NT) s = comb(s, int64_t(a[i]));
     auto& ts = *reinterpret_cast<typename BScan::TempStorage*>(dx->tmp);
     int64_t off, total;
     if (op) BScan(ts).ExclusiveScan(s, off, INT64_MIN, cub::Max(), total);
@@ -644,7 +647,7 @@ struct GridX {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int e = k * NT + t;
-        buf[P(e)] = e < valid ? a[t0 + e] : idn;
+        buf[P(e)] = e < valid ? int64_t(a[t0 + e]) : idn;
       }
       __syncthreads();
       int64_t v[K];
@@ -661,7 +664,7 @@ struct GridX {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int e = k * NT + t;
-        if (e < valid) a[t0 + e] = buf[P(e)];
+        if (e < valid) a[t0 + e] = T(buf[P(e)]);
       }
       carry = comb(carry, agg);
       __syncthreads();
@@ -669,6 +672,7 @@ struct GridX {
     sync();
   }
   __device__ void scan(int64_t* a, int n) { scan_op(a, n, 0); }
+  __device__ void scan32(int32_t* a, int n) { scan_op(a, n, 0); }  // (values and prefixes fit int32)
   __device__ void scan_max(int64_t* a, int n) { scan_op(a, n, 1); }
   __device__ void sort(uint64_t* keys, int32_t* vals, int n, int bits) {
     sync();

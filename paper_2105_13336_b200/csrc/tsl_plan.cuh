@@ -2522,6 +2522,14 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
     // 32 consecutive buckets at a time (coalesced, a warp prefix sum carrying
     // the running total), then the quarters' totals are added in
     constexpr int QW = 4;
+    if constexpr (X::GRID) {  // the grid's coalesced scans (a handful of barriers, no serial rows)
+      x.scan32(bk_cnt + 1, NB);
+      x.scan32(wk_cnt + 1, NB);
+      if (x.tid == 0) {
+        gsh[15] = bk_cnt[NB];
+        gsh[GS_WK] = wk_cnt[NB] <= g.cb_cap ? shb + 1 : 0;
+      }
+    } else {
     if (X::W > 1 && x.tid < 2 * QW * X::W) {
       const int tab = x.tid / (QW * X::W), q = (x.tid / X::W) % QW;
       const int PER = NB / QW;
@@ -2570,6 +2578,7 @@ TSL_HD void find_conflicts(X& x, GroupDev& g, int64_t w0, int64_t w1, const int3
       for (int q = 0; q < QW; ++q) { tb += gsh[GS_QTOT + q]; tw += gsh[GS_QTOT + QW + q]; }
       gsh[15] = tb;
       gsh[GS_WK] = tw <= g.cb_cap ? shb + 1 : 0;
+    }
     }
     x.sync();
     ptick(4);

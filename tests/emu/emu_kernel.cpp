@@ -15,6 +15,7 @@ namespace tsl {
 
 struct HostX {
   static constexpr int W = 1;
+  static constexpr bool GRID = false;
   int tid = 0, nthr = 1, lane = 0, warp = 0, nwarp = 1;
   int64_t* sh = nullptr;
   void* tmp = nullptr;

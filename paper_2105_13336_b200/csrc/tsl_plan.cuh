@@ -1908,6 +1908,54 @@ TSL_HD void build_anchor_index(X& x, GroupDev& g, int j) {
 template <class X>
 TSL_HD void rebuild_busy(X& x, GroupDev& g) {
   int64_t* gsh = x.sh + MAXB * NF;
+  if (g.n_jobs == 1 && g.st[0].bz_n == g.st[0].S_pass && g.st[0].S >= g.st[0].S_pass) {
+    // One job whose busy structure was not folded into during the pass: it
+    // still holds the pass-start events sorted by (start, event), so only the
+    // pass's new events are sorted and merged in (old first on equal starts,
+    // the full sort's tie order).
+    const JobDev& J = g.jobs[0];
+    JobState& st = g.st[0];
+    const int32_t S0 = st.S_pass, nn = st.S - S0;
+    if (x.tid == 0) gsh[14] = 0;
+    x.sync();
+    {
+      int64_t mx = 0;
+      for (int32_t i = x.tid; i < nn; i += x.nthr) mx = imax(mx, J.ev_start[S0 + i]);
+      x.amax(&gsh[14], mx);
+    }
+    x.sync();
+    const int tbits = nbits(uint64_t(gsh[14]));
+    for (int32_t i = x.tid; i < nn; i += x.nthr) { g.k_key[i] = uint64_t(J.ev_start[S0 + i]); g.k_val[i] = S0 + i; }
+    x.sort(g.k_key, g.k_val, nn, tbits);
+    int64_t* const ms = J.bk_bz;  // (the fold / rollback buffer: idle here)
+    int64_t* const me = J.bk_bz + J.Scap;
+    {
+      const int64_t* const bs = J.bz_s;
+      const int64_t* const be = J.bz_e;
+      const int32_t* const nv = g.k_val;
+      const int64_t n = int64_t(S0) + nn;
+      const int64_t per = (n + x.nthr - 1) / x.nthr;
+      const int64_t d0 = imin(n, int64_t(x.tid) * per), d1 = imin(n, d0 + per);
+      if (d0 < d1) {
+        int64_t lo = imax(0, d0 - nn), hi = imin(d0, S0);
+        while (lo < hi) {  // old entries before the d0-th output
+          const int64_t mid = (lo + hi) >> 1;
+          if (bs[mid] <= J.ev_start[nv[d0 - mid - 1]]) lo = mid + 1; else hi = mid;
+        }
+        int64_t i = lo, k = d0 - lo;
+        for (int64_t d = d0; d < d1; ++d) {
+          if (i < S0 && (k >= nn || bs[i] <= J.ev_start[nv[k]])) { ms[d] = bs[i]; me[d] = be[i]; ++i; }
+          else { ms[d] = J.ev_start[nv[k]]; me[d] = J.ev_end[nv[k]]; ++k; }
+        }
+      }
+      x.sync();
+      for (int64_t d = x.tid; d < n; d += x.nthr) { J.bz_s[d] = ms[d]; J.bz_e[d] = me[d]; }
+    }
+    if (x.tid == 0) st.bz_n = st.S;
+    x.sync();
+    build_busy_index(x, g, 0);
+    return;
+  }
   int j0 = 0;
   while (j0 < g.n_jobs) {
     if (x.tid == 0) {
@@ -2974,7 +3022,7 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
     gsh[9] = maxT; gsh[10] = 0; gsh[11] = 0; gsh[12] = 1; gsh[GS_PPOOL] = 0; gsh[GS_WPOOL] = 0; gsh[GS_WK] = 0;
     for (int j = 0; j < g.n_jobs; ++j) {
       JobState& st = g.st[j];
-      st.bz_n = st.S; st.pend_n = 0; st.pend_sorted = 0;
+      st.bz_n = st.S; st.S_pass = st.S; st.pend_n = 0; st.pend_sorted = 0;
       gsh[GS_PCAP + j] = 0;
     }
   }

@@ -149,6 +149,8 @@ struct JobState {
   int32_t pend_upto;   // candidates before this index are in the pend list
   int32_t bzi_shift;   // bucket shift of the busy-structure time index
   int32_t ai_shift;    // bucket shift of the access-end (anchor) time index
+  int32_t S_pass;      // S at the start of the current swap pass
+  int32_t pad_st;
 };
 
 struct GroupConfig {

@@ -177,6 +177,8 @@ struct tsl_plan {
   std::vector<tsl_config> cfgs;
   size_t h2d_bytes = 0;          // [0, h2d_bytes) uploaded
   size_t d2h_off = 0, d2h_bytes = 0;
+  size_t stage_end = 0;     // end of the group / state / job headers
+  size_t d2h_done = 0;      // bytes the last download moved
   size_t groups_off = 0, jobs_off = 0, states_off = 0;
   std::vector<int32_t> group_job_base;  // first JobDev index of each group
   double last_kernel_ms = 0;
@@ -748,6 +750,7 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
   P->h2d_bytes = mode == 1 ? out_end : stage_end;
   P->d2h_off = P->groups_off;
   P->d2h_bytes = out_end - P->groups_off;
+  P->stage_end = stage_end;
   auto t1 = std::chrono::steady_clock::now();
   P->prep_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   if (std::getenv("TSL_PREP_PROFILE")) {
@@ -779,11 +782,46 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
+// Results to the host. Small builds: the whole output region in one copy.
+// Large ones (C4: ~250 MB of capacity-sized arrays): the headers first, then
+// only the used prefix of every output array (events, recomputes, history,
+// curve), one extra round trip for ~4x fewer bytes.
 void download(tsl_plan* P, cudaStream_t s) {
   Buffers* b = P->buf;
-  cuda_check(cudaMemcpyAsync(b->hbuf + P->d2h_off, static_cast<uint8_t*>(b->dbuf) + P->d2h_off, P->d2h_bytes,
-                             cudaMemcpyDeviceToHost, s), "D2H");
+  size_t moved = 0;
+  auto d2h = [&](size_t off, size_t n) {
+    if (!n) return;
+    cuda_check(cudaMemcpyAsync(b->hbuf + off, static_cast<uint8_t*>(b->dbuf) + off, n, cudaMemcpyDeviceToHost, s),
+               "D2H");
+    moved += n;
+  };
+  if (P->d2h_bytes <= (size_t(8) << 20) || P->mode != 0) {
+    d2h(P->d2h_off, P->d2h_bytes);
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    P->d2h_done = moved;
+    return;
+  }
+  d2h(P->groups_off, P->stage_end - P->groups_off);
   cuda_check(cudaStreamSynchronize(s), "sync");
+  for (int gi = 0; gi < P->n_groups; ++gi) {
+    const GroupDev& G = hp<GroupDev>(b, P->groups_off)[gi];
+    const GroupPlace& q = P->gp[gi];
+    d2h(q.hist, sizeof(int64_t) * size_t(std::max(0, std::min(G.n_hist, G.hist_cap))));
+    const int32_t jb = P->group_job_base[gi];
+    for (size_t k = 0; k < P->graphs[gi].size(); ++k) {
+      const Graph& g = *P->graphs[gi][k];
+      const JobPlace& p = P->jp[gi][k];
+      const JobState& st = hp<JobState>(b, P->states_off)[jb + k];
+      for (int f = 0; f < 12; ++f) d2h(p.ev[f], size_t((f == 1) ? 4 : (f == 2 || f == 3) ? 1 : 8) * size_t(st.S));
+      for (int f = 0; f < 6; ++f) d2h(p.rc[f], size_t((f == 1 || f == 3) ? 4 : 8) * size_t(st.R));
+      d2h(p.a_flag, size_t(g.A));
+      d2h(p.in_peak, size_t(g.T));
+      d2h(p.curve_t, sizeof(int64_t) * size_t(st.n_curve));
+      d2h(p.curve_b, sizeof(int64_t) * size_t(st.n_curve));
+    }
+  }
+  cuda_check(cudaStreamSynchronize(s), "sync");
+  P->d2h_done = moved;
 }
 
 std::string err_text(const GroupDev& G, const std::vector<GraphP>& gs) {
@@ -880,7 +918,7 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
   s.algorithmic_bytes = 24 * s.timeline_events + 24 * s.candidate_accesses + 16 * s.busy_intervals + 16 * s.candidates;
   s.kernel_launches = 1;
   s.h2d_bytes = static_cast<int64_t>(P->h2d_bytes);
-  s.d2h_bytes = static_cast<int64_t>(P->d2h_bytes);
+  s.d2h_bytes = static_cast<int64_t>(P->d2h_done);
   s.prep_ms = P->prep_ms;
   s.rescored = G.stats.rescored;
   s.cyc_sequence = G.stats.cyc[0];

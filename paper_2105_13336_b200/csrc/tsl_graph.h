@@ -135,6 +135,35 @@ inline Graph load_graph(const tsl_job_desc& d) {
   if (g.O > 0 && (!d.op_ids || !d.op_kinds || !d.op_phases || !d.op_in_offsets || !d.op_out_offsets))
     fail(TSL_ERR_ARGUMENT, "null op table in job " + g.job_id);
   lap("strings");
+  // The op side (op id strings, their ranks and duplicates, phases, update
+  // kinds) runs on a second thread for big graphs while the tensor side is
+  // built; its first error is raised where the sequential order puts it.
+  std::vector<int32_t> orank;
+  std::vector<char> odup(g.O, 0), is_update(g.O, 0);
+  std::vector<int8_t> phase(g.O, 0);
+  std::string phase_err;
+  auto op_side = [&] {
+    g.oid.reserve(g.O);
+    for (int o = 0; o < g.O; ++o) g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
+    orank = lex_rank(g.oid);
+    std::vector<int32_t> by(g.O);
+    for (int i = 0; i < g.O; ++i) by[orank[i]] = i;
+    for (int r = 1; r < g.O; ++r)
+      if (g.oid[by[r]] == g.oid[by[r - 1]]) odup[by[r]] = 1;
+    for (int o = 0; o < g.O; ++o) {
+      const int8_t ph = d.op_phases[o];
+      if (ph != 0 && ph != 1 && phase_err.empty()) phase_err = "unknown op phase: #" + std::to_string(ph);
+      phase[o] = ph;
+      is_update[o] = d.op_kinds[o] && std::strcmp(d.op_kinds[o], "update") == 0;
+    }
+  };
+  std::thread op_thread;
+  struct Join {
+    std::thread& t;
+    ~Join() { if (t.joinable()) t.join(); }
+  } join_on_exit{op_thread};
+  if (g.O > 4096) op_thread = std::thread(op_side);
+  else op_side();
   g.tid.reserve(g.T);
   g.size.assign(d.tensor_sizes, d.tensor_sizes + g.T);
   g.kind.assign(d.tensor_kinds, d.tensor_kinds + g.T);
@@ -143,19 +172,7 @@ inline Graph load_graph(const tsl_job_desc& d) {
     if (g.kind[i] < 0 || g.kind[i] > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(g.kind[i]));
   }
   lap("tid");
-  // op ids are ranked on a second thread while the tensor ids are (both are
-  // O(n log n) string sorts: ~0.1 s each for C4's 4e5 tensors / 2e5 ops)
-  g.oid.reserve(g.O);
-  for (int o = 0; o < g.O; ++o) g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
-  lap("oid");
-  std::vector<int32_t> orank;
-  {
-    std::thread ranker;
-    if (g.O > 4096) ranker = std::thread([&] { orank = lex_rank(g.oid); });
-    else orank = lex_rank(g.oid);
-    g.trank = lex_rank(g.tid);
-    if (ranker.joinable()) ranker.join();
-  }
+  g.trank = lex_rank(g.tid);
   lap("lexrank");
   {
     // first tensor (in order) that is nonpositive or a repeated id
@@ -174,22 +191,8 @@ inline Graph load_graph(const tsl_job_desc& d) {
   }
   lap("ranks+dups");
   std::vector<int32_t> producer(g.T, -1);
-  std::vector<std::string> okind;
-  std::vector<int8_t> phase;
-  okind.reserve(g.O);
-  for (int o = 0; o < g.O; ++o) {
-    okind.emplace_back(d.op_kinds[o] ? d.op_kinds[o] : "");
-    int8_t ph = d.op_phases[o];
-    if (ph != 0 && ph != 1) fail(TSL_ERR_VALIDATION, "unknown op phase: #" + std::to_string(ph));
-    phase.push_back(ph);
-  }
-  std::vector<char> odup(g.O, 0);
-  {
-    std::vector<int32_t> by(g.O);
-    for (int i = 0; i < g.O; ++i) by[orank[i]] = i;
-    for (int r = 1; r < g.O; ++r)
-      if (g.oid[by[r]] == g.oid[by[r - 1]]) odup[by[r]] = 1;
-  }
+  if (op_thread.joinable()) op_thread.join();
+  if (!phase_err.empty()) fail(TSL_ERR_VALIDATION, phase_err);
   lap("opkinds+odup");
   g.in_off.assign(1, 0);
   g.out_off.assign(1, 0);
@@ -223,7 +226,7 @@ inline Graph load_graph(const tsl_job_desc& d) {
   std::vector<int32_t> alias(g.T, -1);
   g.upd.assign(g.T, -1);
   for (int o = 0; o < g.O; ++o) {
-    if (phase[o] != TSL_PHASE_OPTIMIZE || okind[o] != "update") continue;
+    if (phase[o] != TSL_PHASE_OPTIMIZE || !is_update[o]) continue;
     int32_t u = -1, p = -1, nu = 0, np = 0;
     for (int32_t i = g.out_off[o]; i < g.out_off[o + 1]; ++i)
       if (g.kind[g.out[i]] == TSL_KIND_UPDATED_PARAMETER) { if (nu++ == 0) u = g.out[i]; }

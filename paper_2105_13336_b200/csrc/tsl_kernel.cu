@@ -95,6 +95,10 @@ struct DevX {
   __device__ void amax32(int32_t* p, int32_t v) { atomicMax(p, v); }
   __device__ void amin32(int32_t* p, int32_t v) { atomicMin(p, v); }
   __device__ void aor32(int32_t* p, int32_t v) { atomicOr(p, v); }
+  // (block contexts: the plain atomics, skipping identity values)
+  __device__ void radd(int64_t* p, int64_t v) { if (v) aadd(p, v); }
+  __device__ void ramin(int64_t* p, int64_t v) { if (v != INT64_MAX) amin(p, v); }
+  __device__ void ramax(int64_t* p, int64_t v) { if (v != INT64_MIN) amax(p, v); }
   __device__ void errset(GroupDev& g, const ErrInfo& e) {
     if (atomicCAS(&g.err.code, 0, e.code) == 0) {
       g.err.job = e.job;
@@ -607,6 +611,26 @@ struct GridX {
   __device__ void amin32(int32_t* p, int32_t v) { atomicMin(p, v); }
   __device__ void aor32(int32_t* p, int32_t v) { atomicOr(p, v); }
   __device__ void errset(GroupDev& g, const ErrInfo& e) { dx->errset(g, e); }
+  // warp-uniform reductions into one address: a butterfly first, then one
+  // atomic per warp instead of one per thread of the grid (~38k per call)
+  template <class F>
+  __device__ int64_t wreduce(int64_t v, F f) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = f(v, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)v, o));
+    return v;
+  }
+  __device__ void radd(int64_t* p, int64_t v) {
+    v = wreduce(v, [](int64_t a, int64_t b) { return a + b; });
+    if (lane == 0 && v) aadd(p, v);
+  }
+  __device__ void ramin(int64_t* p, int64_t v) {
+    v = wreduce(v, [](int64_t a, int64_t b) { return a < b ? a : b; });
+    if (lane == 0 && v != INT64_MAX) amin(p, v);
+  }
+  __device__ void ramax(int64_t* p, int64_t v) {
+    v = wreduce(v, [](int64_t a, int64_t b) { return a > b ? a : b; });
+    if (lane == 0 && v != INT64_MIN) amax(p, v);
+  }
   // inclusive scan (op: 0 sum, 1 max) of a[0, n) over all CTAs: each CTA owns
   // a contiguous segment; its total is reduced with coalesced loads, one warp
   // combines the earlier CTAs' totals, and the segment is scanned in tiles

@@ -1443,7 +1443,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       lmin = imin(lmin, when);
       lmax = imax(lmax, when);
     }
-    if (lmin != INT64_MAX) { x.amin(&gsh[0], lmin); x.amax(&gsh[1], lmax); }
+    x.ramin(&gsh[0], lmin);  // (identity values are harmless; a grid context reduces per warp first)
+    x.ramax(&gsh[1], lmax);
   }
   x.sync();
   if (gsh[4]) {  // unknown access id in a caller plan (access.cpp:8-10)
@@ -1473,7 +1474,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     const JobDev& J = g.jobs[jb + b];
     int64_t fp = 0;
     for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.res_init[t]) fp += J.t_size[t];
-    if (fp) x.aadd(&sh[b * NF + F_INIT], fp);
+    x.radd(&sh[b * NF + F_INIT], fp);
     const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
     const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
     int64_t c = 0;
@@ -1723,7 +1724,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
         cmx = imax(cmx, fp);
       }
     }
-    if (cb >= 0) x.amax(&sh[cb * NF + F_MAXFP], cmx);
+    if (nb == 1) x.ramax(&sh[F_MAXFP], cb >= 0 ? cmx : INT64_MIN);
+    else if (cb >= 0) x.amax(&sh[cb * NF + F_MAXFP], cmx);
   }
   x.sync();
   etick(5);
@@ -1749,7 +1751,8 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       }
       if (pp != INT64_MAX && m <= pp && (E_x_type[slot] & 7) == EV_TUA && !(E_x_type[slot] & 16)) cl = m;
     }
-    if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
+    if (nb == 1) x.ramax(&sh[F_LUA], cl);
+    else if (cl >= 0) x.amax(&sh[cb * NF + F_LUA], cl);
   }
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
@@ -1921,7 +1924,7 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
     {
       int64_t mx = 0;
       for (int32_t i = x.tid; i < nn; i += x.nthr) mx = imax(mx, J.ev_start[S0 + i]);
-      x.amax(&gsh[14], mx);
+      x.ramax(&gsh[14], mx);
     }
     x.sync();
     const int tbits = nbits(uint64_t(gsh[14]));
@@ -1978,7 +1981,7 @@ TSL_HD void rebuild_busy(X& x, GroupDev& g) {
       const JobDev& J = g.jobs[j];
       int64_t mx = 0;
       for (int32_t i = x.tid; i < g.st[j].S; i += x.nthr) mx = imax(mx, J.ev_start[i]);
-      x.amax(&gsh[14], mx);
+      x.ramax(&gsh[14], mx);
     }
     x.sync();
     const int jbits = nbits(uint64_t(j1 - j0 - 1));

@@ -36,6 +36,9 @@ struct HostX {
   int32_t aadd32(int32_t* p, int32_t v) { int32_t o = *p; *p += v; return o; }
   void amin(int64_t* p, int64_t v) { if (v < *p) *p = v; }
   void amax(int64_t* p, int64_t v) { if (v > *p) *p = v; }
+  void radd(int64_t* p, int64_t v) { *p += v; }
+  void ramin(int64_t* p, int64_t v) { if (v < *p) *p = v; }
+  void ramax(int64_t* p, int64_t v) { if (v > *p) *p = v; }
   void amax32(int32_t* p, int32_t v) { if (v > *p) *p = v; }
   void aor32(int32_t* p, int32_t v) { *p |= v; }
   void amin32(int32_t* p, int32_t v) { if (v < *p) *p = v; }

@@ -463,6 +463,7 @@ struct DevX {
       else if (type == COOP_CONF) coop_conf(cta);
       else if (type == COOP_SPEC) coop_spec(cta);
       else if (type == COOP_A2) coop_a2(cta);
+      else if (type == COOP_SEQ) coop_seq(cta);
       else if (type == COOP_FOLD) coop_fold(cta);
       else coop_pass(cta, c->ks, c->vs, c->kd, c->vd, c->n, c->sh, c->nb);
     }
@@ -473,6 +474,7 @@ struct DevX {
   __device__ void coop_conf(int cta);                  // all CTAs: find_conflicts() on the grid (below)
   __device__ void coop_spec(int cta);                  // all CTAs: spec_phase() on the grid (below)
   __device__ void coop_a2(int cta);                    // all CTAs: component_speculation() on the grid (below)
+  __device__ void coop_seq(int cta);                   // all CTAs: build_sequence() on the grid (below)
   GroupDev* coop_group = nullptr;                      // the launch's (single) group, global
 
   // CTA 0 at the end of the kernel: release the workers, reset the block.
@@ -854,6 +856,28 @@ __device__ inline void spec_batch<DevX>(DevX& x, GroupDev& g, int64_t w0, int64_
   if (x.tid == 0) { gsh[GS_PPOOL] = __ldcg(&ggsh[GS_PPOOL]); gsh[GS_WPOOL] = __ldcg(&ggsh[GS_WPOOL]); }
   for (int j = x.tid; j < g.n_jobs; j += x.nthr) gsh[GS_PCAP + j] = __ldcg(&ggsh[GS_PCAP + j]);
   __syncthreads();
+}
+
+// The timeline builder on a cooperative launch: C4's 990,518 accesses and
+// ~4e5 tensors were ~4k strided iterations per thread of CTA 0 alone.
+__device__ void DevX::coop_seq(int cta) {
+  GridX gx = grid_ctx(*this, cta);
+  build_sequence(gx, *coop_group, coop->jb);
+}
+
+template <>
+__device__ inline void seq_batch<DevX>(DevX& x, GroupDev& g, int j) {
+  if (!x.coop || x.grid < 2) { build_sequence(x, g, j); return; }
+  __syncthreads();
+  if (x.tid == 0) {
+    volatile CoopCtl* c = x.coop;
+    c->jb = j; c->type = COOP_SEQ;
+    __threadfence();
+    atomicAdd(&x.coop->epoch, 1);
+  }
+  __syncthreads();
+  GridX gx = grid_ctx(x, 0);
+  build_sequence(gx, g, j);  // ends with a grid barrier (the index builds)
 }
 
 // Phase A2 on a cooperative launch: the union-find rounds, the member lists

@@ -1004,6 +1004,13 @@ TSL_HD void build_sequence(X& x, GroupDev& g, int j) {
   build_busy_index(x, g, j);
 }
 
+// The timeline builder of one job; an execution context may route it
+// elsewhere (the CUDA build runs it on every CTA of a cooperative launch).
+template <class X>
+TSL_HD void seq_batch(X& x, GroupDev& g, int j) {
+  build_sequence(x, g, j);
+}
+
 // ----------------------------------------------------------------------------
 // Stage 2: footprint evaluator for jobs [jb, je) (analyze_job, peak.cpp:246-250)
 // ----------------------------------------------------------------------------
@@ -3745,7 +3752,7 @@ TSL_HD void plan_group(X& x, GroupDev& g) {
   int64_t c0 = x.clock(), c1;
   const int64_t cstart = c0;
   auto lap = [&](int k) { c1 = x.clock(); if (x.tid == 0) g.stats.cyc[k] += c1 - c0; c0 = c1; };
-  for (int j = 0; j < g.n_jobs; ++j) build_sequence(x, g, j);
+  for (int j = 0; j < g.n_jobs; ++j) seq_batch(x, g, j);
   lap(0);
   if (!refresh(x, g, 0, g.n_jobs, true)) return;  // make_job_context's refresh
   lap(1);
@@ -3804,7 +3811,7 @@ TSL_HD void analyze_group(X& x, GroupDev& g) {
   for (int j = 0; j < g.n_jobs; ++j) {
     // keep the caller's plan (events/flags were uploaded into the job arrays)
     const JobState keep = g.st[j];
-    build_sequence(x, g, j);
+    seq_batch(x, g, j);
     const JobDev& J = g.jobs[j];
     for (int32_t a = x.tid; a < J.A; a += x.nthr) J.a_flag[a] = J.a_inflag[a];
     if (x.tid == 0) {

@@ -216,7 +216,7 @@ struct CoopCtl {
   int32_t abort;                 // a spin timed out: every CTA leaves (the group reports E_INTERNAL)
 };
 enum : int32_t { COOP_PASS = 1, COOP_EVAL = 2, COOP_FOLD = 3, COOP_REBUILD = 4, COOP_COMP = 5, COOP_CONF = 6, COOP_SPEC = 7,
-                 COOP_A2 = 8,
+                 COOP_A2 = 8, COOP_SEQ = 10,
                  COOP_EXIT = 9 };
 
 struct GroupDev {

@@ -1269,10 +1269,22 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
     for (int64_t i = x.tid; i < nn; i += x.nthr) { nw_g[i] = kv[i]; nw_gi[i] = ins_gr(kv[i]); }
   }
   // (the scan arrays' initial values: active base entries)
-  for (int64_t i = x.tid; i < NB; i += x.nthr) {
-    const int64_t a = active(bs[i]);
-    sc[i] = a;
-    sc2[ginv[i]] = a;
+  {
+    // (restrict-qualified views and unrolled strides: the loads of several
+    // iterations in flight -- these loops are latency-bound at 8 warps per SM)
+    const int32_t* __restrict__ r_bs = bs;
+    const int32_t* __restrict__ r_ginv = ginv;
+    const uint8_t* __restrict__ r_flag = a_flag;
+    const uint8_t* __restrict__ r_own = a_owned;
+    int64_t* __restrict__ r_sc = sc;
+    int64_t* __restrict__ r_sc2 = sc2;
+#pragma unroll 4
+    for (int64_t i = x.tid; i < NB; i += x.nthr) {
+      const int32_t b = r_bs[i];
+      const int64_t a = b < A ? 1 : ((r_flag[b - A] && !r_own[b - A]) ? 1 : 0);
+      r_sc[i] = a;
+      r_sc2[r_ginv[i]] = a;
+    }
   }
   if (x.tid == 0) { sc[NB] = 0; sc2[NB] = 0; }
   x.sync();
@@ -1292,12 +1304,22 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
   x.scan(sc2, int32_t(NB + 1));
   itick(4);
   constexpr int64_t LOW = 0xffffffffLL;
-  for (int64_t p = x.tid; p < NB; p += x.nthr) {
-    const int64_t e = p > 0 ? sc[p - 1] : 0;
-    if (!((sc[p] - e) & LOW)) continue;  // inactive release
-    const int64_t pos = (e & LOW) + (sc[p] >> 32);
-    g.x_order[pos] = int32_t(acc0 + bs[p]);
-    posb[ginv[p]] = int32_t(pos);
+  {
+    const int64_t* __restrict__ r_sc = sc;
+    const int32_t* __restrict__ r_bs = bs;
+    const int32_t* __restrict__ r_ginv = ginv;
+    int32_t* __restrict__ r_ord = g.x_order;
+    int32_t* __restrict__ r_posb = posb;
+#pragma unroll 4
+    for (int64_t p = x.tid; p < NB; p += x.nthr) {
+      const int64_t e = p > 0 ? r_sc[p - 1] : 0;
+      const int64_t c = r_sc[p];
+      const int32_t b = r_bs[p], gi = r_ginv[p];
+      if (!((c - e) & LOW)) continue;  // inactive release
+      const int64_t pos = (e & LOW) + (c >> 32);
+      r_ord[pos] = int32_t(acc0 + b);
+      r_posb[gi] = int32_t(pos);
+    }
   }
   for (int64_t k = x.tid; k < nD; k += x.nthr) {
     const int64_t e = dins[k] > 0 ? sc[dins[k] - 1] : 0;
@@ -1307,13 +1329,26 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
   }
   x.sync();
   itick(5);
-  for (int64_t q = x.tid; q < NB; q += x.nthr) {
-    const int64_t e = q > 0 ? sc2[q - 1] : 0;
-    if (!((sc2[q] - e) & LOW)) continue;
-    const int64_t gpos = (e & LOW) + (sc2[q] >> 32);
-    g.x_seq2[gpos] = posb[q];
-    g.x_key2[gpos] = lo_rank(gl[q]);
-    kv[gpos] = int32_t(acc0 + gb[q]);
+  {
+    const int64_t* __restrict__ r_sc = sc2;
+    const int32_t* __restrict__ r_posb = posb;
+    const uint32_t* __restrict__ r_gl = gl;
+    const int32_t* __restrict__ r_gb = gb;
+    int32_t* __restrict__ r_seq = g.x_seq2;
+    uint64_t* __restrict__ r_key = g.x_key2;
+    int32_t* __restrict__ r_kv = kv;
+#pragma unroll 4
+    for (int64_t q = x.tid; q < NB; q += x.nthr) {
+      const int64_t e = q > 0 ? r_sc[q - 1] : 0;
+      const int64_t c = r_sc[q];
+      const int32_t pb = r_posb[q], b = r_gb[q];
+      const uint32_t l = r_gl[q];
+      if (!((c - e) & LOW)) continue;
+      const int64_t gpos = (e & LOW) + (c >> 32);
+      r_seq[gpos] = pb;
+      r_key[gpos] = lo_rank(l);
+      r_kv[gpos] = int32_t(acc0 + b);
+    }
   }
   for (int64_t r = x.tid; r < nD; r += x.nthr) {
     const int64_t e = gins[r] > 0 ? sc2[gins[r] - 1] : 0;
@@ -1649,12 +1684,66 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // to the same storage iff its group key matches.
   {
     int64_t* chg = reinterpret_cast<int64_t*>(E_k_key);  // free after sort 1
-    for (int64_t m = x.tid; m < n; m += x.nthr) {
-      const int ty = E_x_type[E_gslot[m]] & 7;
-      chg[m] = ty == EV_TUA ? -1 : m;
+    {
+      // (restrict-qualified views and unrolled strides keep several
+      // iterations' loads in flight: these loops are latency-bound)
+      const int32_t* __restrict__ r_gs = E_gslot;
+      const int8_t* __restrict__ r_type = E_x_type;
+      int64_t* __restrict__ r_chg = chg;
+#pragma unroll 4
+      for (int64_t m = x.tid; m < n; m += x.nthr) r_chg[m] = (r_type[r_gs[m]] & 7) == EV_TUA ? -1 : m;
     }
     x.sync();
     x.scan_max(chg, int32_t(n));
+    if (nb == 1) {  // one job: no per-event job lookup
+      const uint8_t* __restrict__ c_res = g.jobs[jb].res_init;
+      const int64_t* __restrict__ c_size = g.jobs[jb].t_size;
+      const int32_t* __restrict__ r_seq = E_x_seq2;
+      const int32_t* __restrict__ r_gs = E_gslot;
+      const int32_t* __restrict__ r_store = E_x_store;
+      const int8_t* __restrict__ r_type = E_x_type;
+      const int64_t* __restrict__ r_chg = chg;
+      const uint64_t* __restrict__ r_key = E_x_key2;
+      int64_t* __restrict__ r_fp = E_x_fp;
+      uint8_t* __restrict__ r_state = E_x_state;
+#pragma unroll 2
+      for (int64_t m = x.tid; m < n; m += x.nthr) {
+        const int32_t pos = r_seq[m];
+        const int32_t slot = r_gs[m];
+        const int64_t prev = m > 0 ? r_chg[m - 1] : -1;
+        const int32_t s = r_store[slot];
+        const int tyf = r_type[slot];
+        const int ty = tyf & 7;
+        uint8_t res;
+        if (prev >= 0 && r_key[prev] == r_key[m]) {
+          const int pt = r_type[r_gs[prev]] & 7;
+          res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
+        } else {
+          res = c_res[s];
+        }
+        const int64_t size = c_size[s];
+        int64_t eff = 0;
+        int errc = 0;
+        switch (ty) {
+          case EV_TGA:
+            if (!res) { eff = (tyf & 8) ? 0 : size; res = 1; }
+            break;
+          case EV_TUA: break;
+          case EV_REL:
+          case EV_SOUT:
+            if (!res) errc = E_DOUBLE_RELEASE;
+            eff = -size; res = 0;
+            break;
+          default:  // EV_SIN
+            if (res) errc = E_SWAPIN_RESIDENT;
+            eff = size; res = 1;
+            break;
+        }
+        r_fp[pos] = eff;
+        r_state[pos] = res;
+        if (errc) x.amin(&sh[F_ERR], (int64_t(pos) << 3) | errc);
+      }
+    } else {
     int cb = -1;
     const uint8_t* c_res = nullptr;
     const int64_t* c_size = nullptr;
@@ -1699,6 +1788,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       E_x_state[pos] = res;
       if (errc) x.amin(&sh[b * NF + F_ERR], (int64_t(pos) << 3) | errc);
     }
+    }
     x.sync();
   }
   etick(4);
@@ -1711,7 +1801,20 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     }
   }
   x.sync();
-  {
+  if (nb == 1) {  // one job: the offset fix-up fused with the maximum, no job lookup
+    const int64_t off = sh[F_OFF];
+    int64_t* __restrict__ r_fp = E_x_fp;
+    int64_t cmx = INT64_MIN, neg = INT64_MAX;
+#pragma unroll 4
+    for (int64_t m = x.tid; m < n; m += x.nthr) {
+      const int64_t fp = r_fp[m] + off;
+      r_fp[m] = fp;
+      cmx = imax(cmx, fp);
+      if (fp < 0 && neg == INT64_MAX) neg = m;
+    }
+    if (neg != INT64_MAX) x.amin(&sh[F_ERR], (neg << 3) | E_NEG_FOOTPRINT);
+    x.ramax(&sh[F_MAXFP], cmx);
+  } else {
     // offset fix-up fused with the per-job maximum: jobs occupy contiguous
     // position ranges, so each thread folds its strided elements locally and
     // issues one atomic per job it touched.
@@ -1737,6 +1840,14 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   x.sync();
   etick(5);
   // 9. first strict maximum (analyze_peak, peak.cpp:236-241)
+  if (nb == 1) {  // each thread's first match is its only candidate
+    const int64_t mx = sh[F_MAXFP];
+    if (mx > sh[F_INIT]) {
+      const int64_t* __restrict__ r_fp = E_x_fp;
+      for (int64_t m = x.tid; m < n; m += x.nthr)
+        if (r_fp[m] == mx) { x.amin(&sh[F_PPOS], m); break; }
+    }
+  } else
   for (int64_t m = x.tid; m < n; m += x.nthr) {
     const int b = E_x_job[E_x_order[m]];
     int64_t* f = sh + b * NF;
@@ -1744,7 +1855,20 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   }
   x.sync();
   // 10. last_input_access at the peak; residency at the peak
-  {
+  if (nb == 1) {  // one job: only positions up to the peak matter
+    const int64_t pp = sh[F_PPOS];
+    int64_t cl = -1;
+    if (pp != INT64_MAX) {
+      const int32_t* __restrict__ r_ord = E_x_order;
+      const int8_t* __restrict__ r_type = E_x_type;
+#pragma unroll 4
+      for (int64_t m = x.tid; m <= pp; m += x.nthr) {
+        const int ty = r_type[r_ord[m]];
+        if ((ty & 7) == EV_TUA && !(ty & 16)) cl = m;
+      }
+    }
+    x.ramax(&sh[F_LUA], cl);
+  } else {
     int cb = -1;
     int64_t cl = -1;
     for (int64_t m = x.tid; m < n; m += x.nthr) {
@@ -1772,6 +1896,24 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // A storage's residency at the peak is its state after its last event at or
   // before the peak position: within a (job, storage) group positions ascend,
   // so that event is the one whose successor leaves the group or the prefix.
+  if (nb == 1) {
+    const int64_t pp = sh[F_PPOS];
+    if (pp != INT64_MAX) {
+      const int32_t* __restrict__ r_seq = E_x_seq2;
+      const int32_t* __restrict__ r_gs = E_gslot;
+      const uint64_t* __restrict__ r_key = E_x_key2;
+      const int32_t* __restrict__ r_store = E_x_store;
+      const uint8_t* __restrict__ r_state = E_x_state;
+      uint8_t* __restrict__ r_peak = g.jobs[jb].in_peak;
+#pragma unroll 4
+      for (int64_t m = x.tid; m < n; m += x.nthr) {
+        const int32_t pos = r_seq[m];
+        if (pos > pp) continue;
+        if (m + 1 < n && r_key[m + 1] == r_key[m] && r_seq[m + 1] <= pp) continue;
+        r_peak[r_store[r_gs[m]]] = r_state[pos];
+      }
+    }
+  } else
   for (int64_t m = x.tid; m < n; m += x.nthr) {
     const int32_t pos = E_x_seq2[m];
     const int32_t slot = E_gslot[m];
@@ -1793,9 +1935,17 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       if (J.in_peak[t]) pk_list[x.aadd(&f[F_NPEAK], 1)] = t;
     const int64_t base = f[F_BASE], nn = f[F_N];
     if (x.tid == 0) { J.curve_t[0] = 0; J.curve_b[0] = f[F_INIT]; }
-    for (int64_t m = x.tid; m < nn; m += x.nthr) {
-      J.curve_t[m + 1] = E_x_time[E_x_order[base + m]];
-      J.curve_b[m + 1] = E_x_fp[base + m];
+    {
+      const int64_t* __restrict__ r_time = E_x_time;
+      const int32_t* __restrict__ r_ord = E_x_order + base;
+      const int64_t* __restrict__ r_fp = E_x_fp + base;
+      int64_t* __restrict__ r_ct = J.curve_t + 1;
+      int64_t* __restrict__ r_cb = J.curve_b + 1;
+#pragma unroll 4
+      for (int64_t m = x.tid; m < nn; m += x.nthr) {
+        r_ct[m] = r_time[r_ord[m]];
+        r_cb[m] = r_fp[m];
+      }
     }
   }
   x.sync();

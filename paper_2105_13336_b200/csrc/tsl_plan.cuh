@@ -1511,19 +1511,33 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
   // 2. initial footprint; releases counted per contiguous access chunk of
   // each thread and scanned over (job, thread), so release slots are numbered
   // in access order (the scan's per-job totals are the release counts).
+  // (one-job big builds order the timeline incrementally, inc_order: events
+  // keep fixed slots -- a release at acc0 + A + a -- so only the count is
+  // needed, and no sort keys)
+  const bool inc = g.ec_bt != nullptr && nb == 1 && g.n_jobs == 1;
   int64_t* rcnt = E_x_fp;  // [nb * nthr] release counts -> offsets (free until step 7)
   for (int b = 0; b < nb; ++b) {
     const JobDev& J = g.jobs[jb + b];
     int64_t fp = 0;
     for (int32_t t = x.tid; t < J.T; t += x.nthr) if (J.res_init[t]) fp += J.t_size[t];
     x.radd(&sh[b * NF + F_INIT], fp);
+    if (inc) {
+      const uint8_t* __restrict__ r_flag = J.a_flag;
+      const uint8_t* __restrict__ r_own = J.a_owned;
+      int64_t c = 0;
+#pragma unroll 4
+      for (int32_t a = x.tid; a < J.A; a += x.nthr) c += (r_flag[a] && !r_own[a]) ? 1 : 0;
+      x.radd(&sh[b * NF + F_REL], c);
+      continue;
+    }
     const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
     const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
     int64_t c = 0;
     for (int32_t a = a0; a < a1; ++a) c += (J.a_flag[a] && !J.a_owned[a]) ? 1 : 0;
     rcnt[int64_t(b) * x.nthr + x.tid] = c;
   }
-  x.scan(rcnt, nb * x.nthr);  // inclusive; barriers on both sides
+  if (inc) x.sync();
+  else x.scan(rcnt, nb * x.nthr);  // inclusive; barriers on both sides
   // 3. bases and key geometry
   if (x.tid == 0) {
     int64_t base = 0, maxT = 1;
@@ -1531,7 +1545,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const JobDev& J = g.jobs[jb + b];
       const JobState& st = g.st[jb + b];
       int64_t* f = sh + b * NF;
-      f[F_REL] = rcnt[int64_t(b + 1) * x.nthr - 1] - (b > 0 ? rcnt[int64_t(b) * x.nthr - 1] : 0);
+      if (!inc) f[F_REL] = rcnt[int64_t(b + 1) * x.nthr - 1] - (b > 0 ? rcnt[int64_t(b) * x.nthr - 1] : 0);
       f[F_BASE] = base;
       f[F_N] = J.A + f[F_REL] + st.S + st.R;
       base += f[F_N];
@@ -1571,9 +1585,6 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     return k;
   };
   etick(0);
-  // one-job big builds order the timeline incrementally (inc_order): events
-  // keep fixed slots (a release at acc0 + A + a) and need no sort keys
-  const bool inc = g.ec_bt != nullptr && nb == 1 && g.n_jobs == 1;
   uint32_t* const E_dl = g.ec_dl;
   // 4. emit events (build_timeline, peak.cpp:66-174); release slots from the
   // step-2 scan.
@@ -1583,6 +1594,36 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
     int64_t* f = sh + b * NF;
     const int64_t base = f[F_BASE];
     const int64_t acc0 = base + st.S + st.R;  // first access slot
+    if (inc) {  // fixed slots: a coalesced strided walk
+      const int32_t* __restrict__ a_store = J.a_store;
+      const int32_t* __restrict__ a_tensor = J.a_tensor;
+      const uint8_t* __restrict__ a_flag = J.a_flag;
+      const uint8_t* __restrict__ a_owned = J.a_owned;
+      const int8_t* __restrict__ a_type = J.a_type;
+      const int64_t* __restrict__ a_start = J.a_start;
+      const int64_t* __restrict__ a_end = J.a_end;
+      int64_t* __restrict__ r_time = E_x_time + acc0;
+      int8_t* __restrict__ r_type = E_x_type + acc0;
+      int32_t* __restrict__ r_store = E_x_store + acc0;
+      int32_t* __restrict__ r_aid = E_x_aid + acc0;
+      int8_t* __restrict__ r_job = E_x_job + acc0;
+      const int32_t A = J.A;
+#pragma unroll 4
+      for (int32_t a = x.tid; a < A; a += x.nthr) {
+        const int32_t s = a_store[a];
+        const bool flagged = a_flag[a] != 0;
+        const bool owned = a_owned[a] != 0;
+        const bool tga = a_type[a] == ACC_TGA;
+        const int64_t te = a_end[a];
+        const int64_t ts = a_start[a];
+        r_time[a] = tga ? ts : te;
+        r_type[a] = tga ? int8_t(EV_TGA | (a_tensor[a] != s ? 8 : 0)) : int8_t(EV_TUA | (flagged ? 16 : 0));
+        r_store[a] = s; r_aid[a] = a; r_job[a] = int8_t(b);
+        if (flagged && !owned) {
+          r_time[A + a] = te; r_type[A + a] = EV_REL; r_store[A + a] = s; r_aid[A + a] = a; r_job[A + a] = int8_t(b);
+        }
+      }
+    } else {
     const int32_t ch = (J.A + x.nthr - 1) / x.nthr;
     const int32_t a0 = imin(J.A, int64_t(x.tid) * ch), a1 = imin(J.A, int64_t(a0) + ch);
     const int64_t idx = int64_t(b) * x.nthr + x.tid;
@@ -1622,6 +1663,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
           if (!inc) { E_k_val[rs] = int32_t(rs); E_k_key[rs] = key(b, te, EV_REL, rk); }
         }
       }
+    }
     }
     for (int32_t i = x.tid; i < st.S; i += x.nthr) {
       const int32_t s = J.t_store[J.ev_tensor[i]];

@@ -342,6 +342,8 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       // only 7 % faster re-score queries on C4 -- the bisection steps after
       // the coarse index mostly hit L1 -- and made index rebuilds costlier)
       p.ti_nb = tsl::TI_NB_HOST;
+      if (P->big)
+        if (const char* e = std::getenv("TSL_TI_NB")) p.ti_nb = std::max(16, std::min(1 << 20, std::atoi(e)));
       P->n_accesses += g.A;
       P->jp[gi].push_back(p);
     }

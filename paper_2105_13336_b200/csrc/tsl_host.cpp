@@ -104,7 +104,7 @@ struct GroupPlace {
   // incremental timeline order (one-job big builds)
   bool ec = false;
   int64_t ec_dcap = 0;
-  size_t ec_bt, ec_bl, ec_bs, ec_gt, ec_gl, ec_gb, ec_ginv, ec_posb, ec_sc, ec_dord, ec_dins, ec_dgrp, ec_gins, ec_nw, ec_posd, ec_dl;
+  size_t ec_gbt, ec_gbst, ec_gty, ec_gst, ec_bt, ec_bl, ec_bs, ec_gt, ec_gl, ec_gb, ec_ginv, ec_posb, ec_sc, ec_dord, ec_dins, ec_dgrp, ec_gins, ec_nw, ec_posd, ec_dl;
 };
 
 }  // namespace
@@ -513,6 +513,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       q.ec_nw = L.take<int32_t>(4 * D);
       q.ec_posd = L.take<int32_t>(D);
       q.ec_dl = L.take<uint32_t>(D);
+      q.ec_gbt = L.take<int8_t>(NB);
+      q.ec_gbst = L.take<int32_t>(NB);
+      q.ec_gty = L.take<int8_t>(E);
+      q.ec_gst = L.take<int32_t>(E);
     }
   }
   const size_t total = L.off;
@@ -613,6 +617,10 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       G->ec_nw = dp<int32_t>(ctx, q.ec_nw);
       G->ec_posd = dp<int32_t>(ctx, q.ec_posd);
       G->ec_dl = dp<uint32_t>(ctx, q.ec_dl);
+      G->ec_gbt = dp<int8_t>(ctx, q.ec_gbt);
+      G->ec_gbst = dp<int32_t>(ctx, q.ec_gbst);
+      G->ec_gty = dp<int8_t>(ctx, q.ec_gty);
+      G->ec_gst = dp<int32_t>(ctx, q.ec_gst);
     }
     for (size_t k = 0; k < gs.size(); ++k, ++jglob) {
       const Graph& g = *gs[k];
@@ -784,10 +792,12 @@ void launch(tsl_plan* P, int repeats, bool timed) {
   if (timed) cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
 }
 
-// Results to the host. Small builds: the whole output region in one copy.
-// Large ones (C4: ~250 MB of capacity-sized arrays): the headers first, then
-// only the used prefix of every output array (events, recomputes, history,
-// curve), one extra round trip for ~4x fewer bytes.
+// Results to the host. Builds of small jobs: the whole output region in one
+// copy (a C5 launch's 120 builds would otherwise need thousands of small
+// copies). Builds with jobs above one sort tile (C4: ~250 MB of
+// capacity-sized arrays): the headers first, then only the used prefix of
+// every output array (events, recomputes, history, curve) -- one extra round
+// trip for ~4x fewer bytes.
 void download(tsl_plan* P, cudaStream_t s) {
   Buffers* b = P->buf;
   size_t moved = 0;
@@ -797,7 +807,7 @@ void download(tsl_plan* P, cudaStream_t s) {
                "D2H");
     moved += n;
   };
-  if (P->d2h_bytes <= (size_t(8) << 20) || P->mode != 0) {
+  if (!P->big || P->d2h_bytes <= (size_t(8) << 20) || P->mode != 0) {
     d2h(P->d2h_off, P->d2h_bytes);
     cuda_check(cudaStreamSynchronize(s), "sync");
     P->d2h_done = moved;

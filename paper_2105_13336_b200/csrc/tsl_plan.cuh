@@ -1157,7 +1157,13 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
     x.sort(kk, kv, int32_t(NB), rbits);
     for (int64_t q = x.tid; q < NB; q += x.nthr) {
       const int32_t p = kv[q];
-      gb[q] = bs[p]; gt[q] = bt[p]; gl[q] = bl[p]; ginv[p] = int32_t(q);
+      const int32_t i = bs[p];
+      gb[q] = i; gt[q] = bt[p]; gl[q] = bl[p]; ginv[p] = int32_t(q);
+      const int32_t a = i < A ? i : i - A;
+      const int32_t s = a_store[a];
+      g.ec_gbst[q] = s;
+      g.ec_gbt[q] = i >= A ? int8_t(EV_REL)
+                  : J.a_type[a] == ACC_TGA ? int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0)) : int8_t(EV_TUA);
     }
     x.sync();
     if (x.tid == 0) { g.ec_ok = 1; g.ec_S0 = -1; }
@@ -1223,10 +1229,13 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
       const uint32_t l = dl[u];
       int32_t ct = 0, cg = 0;
       const int64_t v1 = imin(nn, (sl + 1) * ss);
+      const int64_t* __restrict__ r_xt = xt;
+      const uint32_t* __restrict__ r_dl = dl;
+#pragma unroll 4
       for (int64_t iv = sl * ss; iv < v1; ++iv) {
         const int32_t v = int32_t(n0 + iv);
-        const int64_t tv = xt[v];
-        const uint32_t lv = dl[v];
+        const int64_t tv = r_xt[v];
+        const uint32_t lv = r_dl[v];
         const bool same = tv == t && lv == l;
         ct += (same ? v < u : tl_less(tv, lv, t, l)) ? 1 : 0;
         cg += (same ? v < u : gr_less(tv, lv, t, l)) ? 1 : 0;
@@ -1334,20 +1343,27 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
     const int32_t* __restrict__ r_posb = posb;
     const uint32_t* __restrict__ r_gl = gl;
     const int32_t* __restrict__ r_gb = gb;
+    const int8_t* __restrict__ r_gbt = g.ec_gbt;
+    const int32_t* __restrict__ r_gbst = g.ec_gbst;
     int32_t* __restrict__ r_seq = g.x_seq2;
     uint64_t* __restrict__ r_key = g.x_key2;
     int32_t* __restrict__ r_kv = kv;
+    int8_t* __restrict__ r_gty = g.ec_gty;
+    int32_t* __restrict__ r_gst = g.ec_gst;
 #pragma unroll 4
     for (int64_t q = x.tid; q < NB; q += x.nthr) {
       const int64_t e = q > 0 ? r_sc[q - 1] : 0;
       const int64_t c = r_sc[q];
-      const int32_t pb = r_posb[q], b = r_gb[q];
+      const int32_t pb = r_posb[q], b = r_gb[q], st0 = r_gbst[q];
       const uint32_t l = r_gl[q];
+      const int8_t ty = r_gbt[q];
       if (!((c - e) & LOW)) continue;
       const int64_t gpos = (e & LOW) + (c >> 32);
       r_seq[gpos] = pb;
       r_key[gpos] = lo_rank(l);
       r_kv[gpos] = int32_t(acc0 + b);
+      r_gty[gpos] = ty;
+      r_gst[gpos] = st0;
     }
   }
   for (int64_t r = x.tid; r < nD; r += x.nthr) {
@@ -1357,6 +1373,8 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
     g.x_seq2[gpos] = posd[u];
     g.x_key2[gpos] = lo_rank(dl[u]);
     kv[gpos] = u;
+    g.ec_gty[gpos] = g.x_type[u];
+    g.ec_gst[gpos] = g.x_store[u];
   }
   x.sync();
   itick(6);
@@ -1732,8 +1750,14 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const int32_t* __restrict__ r_gs = E_gslot;
       const int8_t* __restrict__ r_type = E_x_type;
       int64_t* __restrict__ r_chg = chg;
+      if (inc) {  // (types already laid out in grouped order)
+        const int8_t* __restrict__ r_gty = g.ec_gty;
 #pragma unroll 4
-      for (int64_t m = x.tid; m < n; m += x.nthr) r_chg[m] = (r_type[r_gs[m]] & 7) == EV_TUA ? -1 : m;
+        for (int64_t m = x.tid; m < n; m += x.nthr) r_chg[m] = (r_gty[m] & 7) == EV_TUA ? -1 : m;
+      } else {
+#pragma unroll 4
+        for (int64_t m = x.tid; m < n; m += x.nthr) r_chg[m] = (r_type[r_gs[m]] & 7) == EV_TUA ? -1 : m;
+      }
     }
     x.sync();
     x.scan_max(chg, int32_t(n));
@@ -1748,17 +1772,20 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
       const uint64_t* __restrict__ r_key = E_x_key2;
       int64_t* __restrict__ r_fp = E_x_fp;
       uint8_t* __restrict__ r_state = E_x_state;
+      const int8_t* __restrict__ r_gty = inc ? g.ec_gty : nullptr;  // (grouped-order types / storages)
+      const int32_t* __restrict__ r_gst = inc ? g.ec_gst : nullptr;
 #pragma unroll 2
       for (int64_t m = x.tid; m < n; m += x.nthr) {
         const int32_t pos = r_seq[m];
-        const int32_t slot = r_gs[m];
         const int64_t prev = m > 0 ? r_chg[m - 1] : -1;
-        const int32_t s = r_store[slot];
-        const int tyf = r_type[slot];
+        int32_t s;
+        int tyf;
+        if (r_gty) { s = r_gst[m]; tyf = r_gty[m]; }
+        else { const int32_t slot = r_gs[m]; s = r_store[slot]; tyf = r_type[slot]; }
         const int ty = tyf & 7;
         uint8_t res;
         if (prev >= 0 && r_key[prev] == r_key[m]) {
-          const int pt = r_type[r_gs[prev]] & 7;
+          const int pt = (r_gty ? r_gty[prev] : r_type[r_gs[prev]]) & 7;
           res = (pt == EV_TGA || pt == EV_SIN) ? 1 : 0;
         } else {
           res = c_res[s];
@@ -1952,7 +1979,7 @@ TSL_HD bool evaluate(X& x, GroupDev& g, int jb, int je) {
         const int32_t pos = r_seq[m];
         if (pos > pp) continue;
         if (m + 1 < n && r_key[m + 1] == r_key[m] && r_seq[m + 1] <= pp) continue;
-        r_peak[r_store[r_gs[m]]] = r_state[pos];
+        r_peak[inc ? g.ec_gst[m] : r_store[r_gs[m]]] = r_state[pos];
       }
     }
   } else

@@ -301,6 +301,10 @@ struct GroupDev {
   int32_t* ec_nw;      // [4 * dcap] an evaluation's new D entries, ordered, with insertion points
   int32_t* ec_posd;    // [dcap] merged timeline position of each D slot
   uint32_t* ec_dl;     // [dcap] key low word of each D slot
+  int8_t* ec_gbt;      // [2A] grouped base entry: event type (| 8: an aliased TGA)
+  int32_t* ec_gbst;    // [2A] grouped base entry: storage
+  int8_t* ec_gty;      // [ecap] an evaluation's events in grouped order: type
+  int32_t* ec_gst;     // [ecap] storage
 };
 
 }  // namespace tsl

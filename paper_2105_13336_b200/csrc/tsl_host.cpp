@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -855,6 +857,27 @@ std::string err_text(const GroupDev& G, const std::vector<GraphP>& gs) {
   }
 }
 
+void cp64_now(Buffers* c, std::vector<int64_t>& v, size_t off, int32_t n) {
+  v.assign(hp<int64_t>(c, off), hp<int64_t>(c, off) + n);
+}
+
+// Runs independent tasks in order, or on up to 8 host threads when `par`.
+void run_tasks(std::vector<std::function<void()>>& tasks, bool par) {
+  if (!par) {
+    for (auto& t : tasks) t();
+    return;
+  }
+  const size_t nt = std::min<size_t>({8, tasks.size(), std::max(1u, std::thread::hardware_concurrency())});
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < tasks.size();) tasks[i]();
+  };
+  std::vector<std::thread> th;
+  for (size_t k = 1; k < nt; ++k) th.emplace_back(worker);
+  worker();
+  for (auto& t : th) t.join();
+}
+
 tsl_result* collect_group(tsl_plan* P, int gi) {
   Buffers* c = P->buf;
   const GroupDev& G = hp<GroupDev>(c, P->groups_off)[gi];
@@ -876,13 +899,18 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
     JobOut o;
     o.g = R->graphs[k].get();
     o.st = st;
+    // the copies out of the pinned buffer are independent: a big job's
+    // (C4: ~60 MB of events and curve) run on a few host threads
+    std::vector<std::function<void()>> tasks;
     auto cp64 = [&](std::vector<int64_t>& v, size_t off, int32_t n) {
-      v.assign(hp<int64_t>(c, off), hp<int64_t>(c, off) + n);
+      tasks.push_back([&v, c, off, n] { v.assign(hp<int64_t>(c, off), hp<int64_t>(c, off) + n); });
     };
     cp64(o.ev_id, p.ev[0], st.S);
-    o.ev_tensor.assign(hp<int32_t>(c, p.ev[1]), hp<int32_t>(c, p.ev[1]) + st.S);
-    o.ev_dir.assign(hp<int8_t>(c, p.ev[2]), hp<int8_t>(c, p.ev[2]) + st.S);
-    o.ev_wraps.assign(hp<int8_t>(c, p.ev[3]), hp<int8_t>(c, p.ev[3]) + st.S);
+    tasks.push_back([&] {
+      o.ev_tensor.assign(hp<int32_t>(c, p.ev[1]), hp<int32_t>(c, p.ev[1]) + st.S);
+      o.ev_dir.assign(hp<int8_t>(c, p.ev[2]), hp<int8_t>(c, p.ev[2]) + st.S);
+      o.ev_wraps.assign(hp<int8_t>(c, p.ev[3]), hp<int8_t>(c, p.ev[3]) + st.S);
+    });
     cp64(o.ev_trig, p.ev[4], st.S);
     cp64(o.ev_delta, p.ev[5], st.S);
     cp64(o.ev_start, p.ev[6], st.S);
@@ -891,25 +919,30 @@ tsl_result* collect_group(tsl_plan* P, int gi) {
     cp64(o.ev_late, p.ev[9], st.S);
     cp64(o.ev_pair, p.ev[10], st.S);
     cp64(o.ev_serves, p.ev[11], st.S);
-    cp64(o.rc_id, p.rc[0], st.R);
-    o.rc_tensor.assign(hp<int32_t>(c, p.rc[1]), hp<int32_t>(c, p.rc[1]) + st.R);
-    cp64(o.rc_target, p.rc[2], st.R);
-    o.rc_regen.assign(hp<int32_t>(c, p.rc[3]), hp<int32_t>(c, p.rc[3]) + st.R);
-    cp64(o.rc_lat, p.rc[4], st.R);
-    cp64(o.rc_saving, p.rc[5], st.R);
-    const uint8_t* fl = hp<uint8_t>(c, p.a_flag);
-    for (int32_t a = 0; a < g.A; ++a)
-      if (fl[a]) o.flags.push_back(a);
-    if (P->mode == 1) {  // caller flags outside [0, A) are kept verbatim
-      o.flags.clear();
-    }
-    const uint8_t* pk = hp<uint8_t>(c, p.in_peak);
-    std::vector<int32_t> byr(g.T);
-    for (int32_t t = 0; t < g.T; ++t) byr[g.trank[t]] = t;
-    for (int32_t r = 0; r < g.T; ++r)
-      if (pk[byr[r]]) o.peak_tensors.push_back(byr[r]);
+    tasks.push_back([&] {
+      cp64_now(c, o.rc_id, p.rc[0], st.R);
+      o.rc_tensor.assign(hp<int32_t>(c, p.rc[1]), hp<int32_t>(c, p.rc[1]) + st.R);
+      cp64_now(c, o.rc_target, p.rc[2], st.R);
+      o.rc_regen.assign(hp<int32_t>(c, p.rc[3]), hp<int32_t>(c, p.rc[3]) + st.R);
+      cp64_now(c, o.rc_lat, p.rc[4], st.R);
+      cp64_now(c, o.rc_saving, p.rc[5], st.R);
+    });
+    tasks.push_back([&] {
+      const uint8_t* fl = hp<uint8_t>(c, p.a_flag);
+      for (int32_t a = 0; a < g.A; ++a)
+        if (fl[a]) o.flags.push_back(a);
+      if (P->mode == 1) o.flags.clear();  // caller flags outside [0, A) are kept verbatim
+    });
+    tasks.push_back([&] {
+      const uint8_t* pk = hp<uint8_t>(c, p.in_peak);
+      std::vector<int32_t> byr(g.T);
+      for (int32_t t = 0; t < g.T; ++t) byr[g.trank[t]] = t;
+      for (int32_t r = 0; r < g.T; ++r)
+        if (pk[byr[r]]) o.peak_tensors.push_back(byr[r]);
+    });
     cp64(o.curve_t, p.curve_t, st.n_curve);
     cp64(o.curve_b, p.curve_b, st.n_curve);
+    run_tasks(tasks, size_t(st.S) + size_t(st.n_curve) + size_t(g.A) > (size_t(1) << 20));
     R->jobs.push_back(std::move(o));
   }
   R->history.assign(hp<int64_t>(c, P->gp[gi].hist), hp<int64_t>(c, P->gp[gi].hist) + std::min(G.n_hist, G.hist_cap));

@@ -66,6 +66,19 @@ inline void par_sort(std::vector<T>& v, Cmp cmp) {
   if (src != &v) v.swap(*src);
 }
 
+// fn(i) for i in [0, n), on up to 8 host threads for large n (contiguous ranges).
+template <class F>
+inline void par_for(size_t n, F fn) {
+  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t parts = n >= 65536 ? std::min<size_t>(8, hw) : 1;
+  if (parts <= 1) { for (size_t i = 0; i < n; ++i) fn(i); return; }
+  std::vector<std::thread> th;
+  for (size_t p = 1; p < parts; ++p)
+    th.emplace_back([&, p] { for (size_t i = n * p / parts; i < n * (p + 1) / parts; ++i) fn(i); });
+  for (size_t i = 0; i < n / parts; ++i) fn(i);
+  for (auto& t : th) t.join();
+}
+
 // Rank of every id in std::string order, ties by index (a stable sort). The
 // sort compares a 16-byte big-endian prefix held inline (ids of one job share
 // long prefixes, but rarely 16 bytes) and only then the strings.
@@ -80,7 +93,7 @@ inline std::vector<int32_t> lex_rank(const std::vector<std::string>& ids) {
     return v;
   };
   std::vector<K> keys(ids.size());
-  for (size_t i = 0; i < ids.size(); ++i) keys[i] = K{be(ids[i], 0), be(ids[i], 8), int32_t(i)};
+  par_for(ids.size(), [&](size_t i) { keys[i] = K{be(ids[i], 0), be(ids[i], 8), int32_t(i)}; });
   par_sort(keys, [&](const K& a, const K& b) {
     if (a.k0 != b.k0) return a.k0 < b.k0;
     if (a.k1 != b.k1) return a.k1 < b.k1;
@@ -91,7 +104,7 @@ inline std::vector<int32_t> lex_rank(const std::vector<std::string>& ids) {
     return c != 0 ? c < 0 : a.i < b.i;
   });
   std::vector<int32_t> rank(ids.size());
-  for (size_t r = 0; r < keys.size(); ++r) rank[keys[r].i] = static_cast<int32_t>(r);
+  par_for(keys.size(), [&](size_t r) { rank[keys[r].i] = static_cast<int32_t>(r); });
   return rank;
 }
 
@@ -143,8 +156,8 @@ inline Graph load_graph(const tsl_job_desc& d) {
   std::vector<int8_t> phase(g.O, 0);
   std::string phase_err;
   auto op_side = [&] {
-    g.oid.reserve(g.O);
-    for (int o = 0; o < g.O; ++o) g.oid.emplace_back(d.op_ids[o] ? d.op_ids[o] : "");
+    g.oid.resize(g.O);
+    par_for(size_t(g.O), [&](size_t o) { g.oid[o] = d.op_ids[o] ? d.op_ids[o] : ""; });
     orank = lex_rank(g.oid);
     std::vector<int32_t> by(g.O);
     for (int i = 0; i < g.O; ++i) by[orank[i]] = i;
@@ -164,13 +177,12 @@ inline Graph load_graph(const tsl_job_desc& d) {
   } join_on_exit{op_thread};
   if (g.O > 4096) op_thread = std::thread(op_side);
   else op_side();
-  g.tid.reserve(g.T);
   g.size.assign(d.tensor_sizes, d.tensor_sizes + g.T);
   g.kind.assign(d.tensor_kinds, d.tensor_kinds + g.T);
-  for (int i = 0; i < g.T; ++i) {
-    g.tid.emplace_back(d.tensor_ids[i] ? d.tensor_ids[i] : "");
+  for (int i = 0; i < g.T; ++i)
     if (g.kind[i] < 0 || g.kind[i] > 4) fail(TSL_ERR_VALIDATION, "unknown tensor kind: #" + std::to_string(g.kind[i]));
-  }
+  g.tid.resize(g.T);
+  par_for(size_t(g.T), [&](size_t i) { g.tid[i] = d.tensor_ids[i] ? d.tensor_ids[i] : ""; });
   lap("tid");
   g.trank = lex_rank(g.tid);
   lap("lexrank");
@@ -296,17 +308,41 @@ inline Graph load_graph(const tsl_job_desc& d) {
   }
   for (auto& e : edges) indeg[e.second]++;
   lap("sort-edges");
-  auto cmp = [&](int32_t a, int32_t b) { return orank[a] > orank[b]; };
-  std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
+  // the min-heap on the op id is a three-level bitset over the (unique) id
+  // ranks: insert and extract-min in a few word operations
+  std::vector<int32_t> by_rank(g.O);
+  for (int o = 0; o < g.O; ++o) by_rank[orank[o]] = o;
+  std::vector<uint64_t> b0((size_t(g.O) + 63) / 64, 0), b1((b0.size() + 63) / 64, 0), b2((b1.size() + 63) / 64, 0);
+  int64_t n_ready = 0;
+  auto push = [&](int32_t o) {
+    const uint32_t r = uint32_t(orank[o]);
+    b0[r >> 6] |= uint64_t(1) << (r & 63);
+    b1[r >> 12] |= uint64_t(1) << ((r >> 6) & 63);
+    b2[r >> 18] |= uint64_t(1) << ((r >> 12) & 63);
+    ++n_ready;
+  };
+  auto pop_min = [&]() -> int32_t {
+    size_t w2 = 0;
+    while (!b2[w2]) ++w2;
+    const size_t w1 = w2 * 64 + size_t(__builtin_ctzll(b2[w2]));
+    const size_t w0 = w1 * 64 + size_t(__builtin_ctzll(b1[w1]));
+    const uint32_t r = uint32_t(w0 * 64 + size_t(__builtin_ctzll(b0[w0])));
+    b0[w0] &= b0[w0] - 1;
+    if (!b0[w0]) {
+      b1[w1] &= ~(uint64_t(1) << (w0 & 63));
+      if (!b1[w1]) b2[w2] &= ~(uint64_t(1) << (w1 & 63));
+    }
+    --n_ready;
+    return by_rank[r];
+  };
   for (int o = 0; o < g.O; ++o)
-    if (indeg[o] == 0) ready.push(o);
+    if (indeg[o] == 0) push(o);
   g.topo.reserve(g.O);
-  while (!ready.empty()) {
-    int32_t o = ready.top();
-    ready.pop();
+  while (n_ready > 0) {
+    const int32_t o = pop_min();
     g.topo.push_back(o);
     for (int32_t k = soff[o]; k < soff[o + 1]; ++k)
-      if (--indeg[edges[k].second] == 0) ready.push(edges[k].second);
+      if (--indeg[edges[k].second] == 0) push(edges[k].second);
   }
   if (static_cast<int32_t>(g.topo.size()) != g.O) fail(TSL_ERR_VALIDATION, "cycle detected in graph of job " + g.job_id);
   lap("topo");

@@ -106,7 +106,7 @@ struct GroupPlace {
   // incremental timeline order (one-job big builds)
   bool ec = false;
   int64_t ec_dcap = 0;
-  size_t ec_gbt, ec_gbst, ec_gty, ec_gst, ec_bt, ec_bl, ec_bs, ec_gt, ec_gl, ec_gb, ec_ginv, ec_posb, ec_sc, ec_dord, ec_dins, ec_dgrp, ec_gins, ec_nw, ec_posd, ec_dl;
+  size_t ec_act, ec_ract, ec_rpos, ec_gbt, ec_gbst, ec_gty, ec_gst, ec_bt, ec_bl, ec_bs, ec_gt, ec_gl, ec_gb, ec_ginv, ec_posb, ec_sc, ec_dord, ec_dins, ec_dgrp, ec_gins, ec_nw, ec_posd, ec_dl;
 };
 
 }  // namespace
@@ -517,6 +517,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       q.ec_dl = L.take<uint32_t>(D);
       q.ec_gbt = L.take<int8_t>(NB);
       q.ec_gbst = L.take<int32_t>(NB);
+      q.ec_act = L.take<uint8_t>(2 * NB);
+      q.ec_ract = L.take<uint8_t>(NB / 2);
+      q.ec_rpos = L.take<int32_t>(NB);
       q.ec_gty = L.take<int8_t>(E);
       q.ec_gst = L.take<int32_t>(E);
     }
@@ -621,6 +624,9 @@ tsl_plan* prepare(tsl_ctx* cx, const tsl_job_desc* jobs, const int32_t* offs, in
       G->ec_dl = dp<uint32_t>(ctx, q.ec_dl);
       G->ec_gbt = dp<int8_t>(ctx, q.ec_gbt);
       G->ec_gbst = dp<int32_t>(ctx, q.ec_gbst);
+      G->ec_act = dp<uint8_t>(ctx, q.ec_act);
+      G->ec_ract = dp<uint8_t>(ctx, q.ec_ract);
+      G->ec_rpos = dp<int32_t>(ctx, q.ec_rpos);
       G->ec_gty = dp<int8_t>(ctx, q.ec_gty);
       G->ec_gst = dp<int32_t>(ctx, q.ec_gst);
     }

@@ -1164,6 +1164,10 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
       g.ec_gbst[q] = s;
       g.ec_gbt[q] = i >= A ? int8_t(EV_REL)
                   : J.a_type[a] == ACC_TGA ? int8_t(EV_TGA | (J.a_tensor[a] != s ? 8 : 0)) : int8_t(EV_TUA);
+      const uint8_t act = uint8_t(active(i));
+      g.ec_act[p] = act;
+      g.ec_act[NB + q] = act;
+      if (i >= A) { g.ec_ract[a] = act; g.ec_rpos[a] = p; g.ec_rpos[A + a] = int32_t(q); }
     }
     x.sync();
     if (x.tid == 0) { g.ec_ok = 1; g.ec_S0 = -1; }
@@ -1279,20 +1283,35 @@ TSL_HD void inc_order(X& x, GroupDev& g, int j, int64_t n, int rbits, int64_t ac
   }
   // (the scan arrays' initial values: active base entries)
   {
-    // (restrict-qualified views and unrolled strides: the loads of several
-    // iterations in flight -- these loops are latency-bound at 8 warps per SM)
-    const int32_t* __restrict__ r_bs = bs;
-    const int32_t* __restrict__ r_ginv = ginv;
+    // activity of the base entries, kept across evaluations in both orders:
+    // only releases whose activity changed since the last evaluation are
+    // rewritten, then both scan inputs expand from the bytes (coalesced).
+    // (restrict-qualified views and unrolled strides: several iterations'
+    // loads in flight -- these loops are latency-bound at 8 warps per SM)
     const uint8_t* __restrict__ r_flag = a_flag;
     const uint8_t* __restrict__ r_own = a_owned;
+    uint8_t* __restrict__ r_ract = g.ec_ract;
+    uint8_t* __restrict__ r_act = g.ec_act;
+    const int32_t* __restrict__ r_rpos = g.ec_rpos;
+#pragma unroll 4
+    for (int32_t a = x.tid; a < A; a += x.nthr) {
+      const uint8_t now = (r_flag[a] && !r_own[a]) ? 1 : 0;
+      if (now != r_ract[a]) {
+        r_ract[a] = now;
+        r_act[r_rpos[a]] = now;
+        r_act[NB + r_rpos[A + a]] = now;
+      }
+    }
+  }
+  x.sync();
+  {
+    const uint8_t* __restrict__ r_act = g.ec_act;
     int64_t* __restrict__ r_sc = sc;
     int64_t* __restrict__ r_sc2 = sc2;
 #pragma unroll 4
     for (int64_t i = x.tid; i < NB; i += x.nthr) {
-      const int32_t b = r_bs[i];
-      const int64_t a = b < A ? 1 : ((r_flag[b - A] && !r_own[b - A]) ? 1 : 0);
-      r_sc[i] = a;
-      r_sc2[r_ginv[i]] = a;
+      r_sc[i] = r_act[i];
+      r_sc2[i] = r_act[NB + i];
     }
   }
   if (x.tid == 0) { sc[NB] = 0; sc2[NB] = 0; }

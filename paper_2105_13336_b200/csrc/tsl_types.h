@@ -303,6 +303,9 @@ struct GroupDev {
   uint32_t* ec_dl;     // [dcap] key low word of each D slot
   int8_t* ec_gbt;      // [2A] grouped base entry: event type (| 8: an aliased TGA)
   int32_t* ec_gbst;    // [2A] grouped base entry: storage
+  uint8_t* ec_act;     // [2 x 2A] activity of each base entry, timeline then grouped order
+  uint8_t* ec_ract;    // [A] activity of access a's release as last recorded
+  int32_t* ec_rpos;    // [2 x A] positions of access a's release entry in the two orders
   int8_t* ec_gty;      // [ecap] an evaluation's events in grouped order: type
   int32_t* ec_gst;     // [ecap] storage
 };

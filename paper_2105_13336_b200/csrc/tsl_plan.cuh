@@ -2430,7 +2430,7 @@ TSL_HD int32_t rescore_candidate(X& x, GroupDev& g, int j, int32_t s, int64_t m,
 // attention candidate and everything before it is decided in bulk (a warp
 // prefix sum assigns event slots and ids in plan order).
 constexpr int32_t CS_HIT = 16;
-constexpr int64_t COMP_MIN_CANDIDATES = 512;
+constexpr int64_t COMP_MIN_CANDIDATES = 64;
 constexpr int32_t CS_DIFF = 32;  // decided by a re-score whose result differs from the speculation
 constexpr int32_t CS_BRK = 64;   // an earlier member of the candidate's component has CS_DIFF
 
@@ -3315,8 +3315,8 @@ TSL_HD bool swap_pass(X& x, GroupDev& g) {
   x.sort(g.k_key, g.k_val, int32_t(nc), jbits + sbits + rbits);
   ptick(13);
   // component speculation (phase A2): spec_comp 2 always, 1 for passes of
-  // at least COMP_MIN_CANDIDATES candidates (below that the extra phase costs
-  // more than the few re-scores it saves), 0 never
+  // at least COMP_MIN_CANDIDATES candidates (below that -- C1's ~40 -- the
+  // extra phase costs more than the few re-scores it saves), 0 never
   const bool comp_on = !coupled && (g.spec_comp == 2 || (g.spec_comp == 1 && nc >= COMP_MIN_CANDIDATES));
   // Candidate records live in shared memory when they fit (the sort scratch
   // is free until phase E): the in-order decisions read them back-to-back.

@@ -167,7 +167,7 @@ typedef struct tsl_stats {
   int64_t stageprof[24];  /* SM cycles: [0..6] incremental timeline order phases, [7..10] its new-entry ordering,
                              [11..14] swap-pass prologue (peak sizes, candidates, sort, rest), [15] phase A,
                              [16..20] component runs: sum of per-pass longest run, members, runs,
-                             sum of per-pass slowest run cycles, run cycles */
+                             sum of per-pass slowest run cycles, run cycles, [23] union-find rounds */
 } tsl_stats;
 
 typedef struct tsl_ctx tsl_ctx;

@@ -3146,6 +3146,7 @@ TSL_HD void component_speculation(X& x, GroupDev& g, int64_t w0, int64_t w1, con
     x.sync();
     const bool again = gsh[GS_CCHG] != 0;
     x.sync();  // (every thread has read the flag before the next round resets it)
+    if (x.tid == 0) g.stats.sprof[23] += 1;  // union-find rounds (stageprof)
     if (!again) break;
   }
   // members of each component in candidate order: sort (root, index)

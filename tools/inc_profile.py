@@ -15,3 +15,4 @@ print("inc phases base/new+init/merges/atomics/scans/scatter1/scatter2:", list(s
 sp = list(s["stageprof"])
 print(f"component runs: {sp[18]} runs, {sp[17]} members, sum of per-pass longest run {sp[16]} members, "
       f"sum of per-pass slowest run {sp[19]} cyc, all runs {sp[20]} cyc; A2 total {s['cyc_spec'] - sp[15]} cyc")
+print("union-find rounds", sp[23])
